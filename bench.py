@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""Benchmark: batched LQR-scan solves/sec (BASELINE.json metric) on the
+config-3 shape -- 65,536 independent subproblems, half pendulum (nx=2,
+nu=1) and half cart-pole (nx=4, nu=1), horizon T=256, fp64 -- sharded by
+problem across ranks (strong scaling, no data-path collective).
+
+One step = one LQR-scan solve (value pass + gains + propagation pass, the
+hot path of every Newton iteration) of every problem.  The subproblem data
+are the real Newton expansions of the two models at seeded random
+trajectories (config-3 initial-state distributions), built on the device
+before timing.  Inputs (~3.9 GB per GPU at N=1) exceed the 126 MB L2, so no
+flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--no-cpu-baseline] [--no-e2e] [--no-sweep]
+
+Under torchrun every rank solves its shard; rank 0 prints one JSON line.
+`--impl reference` times the CPU reference path (the pinned numpy port of
+pintoc's value_pass + propagation_pass, oracle/) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched LQR-scan solves/sec"
+UNIT = "solves/s"
+B_TOTAL = 65536
+T = 256
+ALPHA = 1.0          # NewtonOptions.alpha0: the regularisation of a first iteration
+
+
+# ---------------------------------------------------------------------------
+# workload (shared by both arms)
+# ---------------------------------------------------------------------------
+
+def half_sizes(b_local: int) -> tuple[int, int]:
+    bp = b_local // 2
+    return bp, b_local - bp
+
+
+def initial_states(system: str, n: int, rng) -> np.ndarray:
+    """config 3: theta ~ U(-pi, pi), velocities ~ N(0, 0.5^2), cart ~ U(-1, 1)."""
+    if system == "pendulum":
+        return np.stack([rng.uniform(-np.pi, np.pi, n), 0.5 * rng.standard_normal(n)], 1)
+    return np.stack([rng.uniform(-1, 1, n), rng.uniform(-np.pi, np.pi, n),
+                     0.5 * rng.standard_normal(n), 0.5 * rng.standard_normal(n)], 1)
+
+
+def initial_controls(system: str, n: int, rng) -> np.ndarray:
+    bound = 5.0 if system == "pendulum" else 10.0
+    return np.clip(0.3 * bound * rng.standard_normal((n, T, 1)), -0.9 * bound, 0.9 * bound)
+
+
+def models_pkg(P):
+    pend = P.ControlProblem(
+        P.PendulumDynamics(T, P.PendulumParams(damping=0.1, dt=0.05)),
+        P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0])),
+        P.BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0))
+    Q = np.diag([1.0, 10.0, 0.1, 0.1])
+    cart = P.ControlProblem(
+        P.CartPoleDynamics(T, P.CartPoleParams(cart_mass=1.0, pole_mass=0.1, pole_length=0.5,
+                                               dt=0.02)),
+        P.QuadraticCost(Q, np.diag([0.01]), 10 * Q, x_goal=np.array([0.0, np.pi, 0.0, 0.0])),
+        P.BoxConstraint(4, 1, control_lower=-10.0, control_upper=10.0,
+                        state_lower=[-1.5, -np.inf, -np.inf, -np.inf],
+                        state_upper=[1.5, np.inf, np.inf, np.inf]))
+    return {"pendulum": pend, "cartpole": cart}
+
+
+def models_oracle(O):
+    pend = (O.Pendulum(damping=0.1, dt=0.05),
+            O.Quadratic(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0])))
+    Q = np.diag([1.0, 10.0, 0.1, 0.1])
+    cart = (O.CartPole(cart_mass=1.0, pole_mass=0.1, pole_length=0.5, dt=0.02),
+            O.Quadratic(Q, np.diag([0.01]), 10 * Q, goal=np.array([0.0, np.pi, 0.0, 0.0])))
+    return {"pendulum": pend, "cartpole": cart}
+
+
+def rng_for(rank: int, system: str):
+    return np.random.default_rng([2409, 20027, rank, 0 if system == "pendulum" else 1])
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the oracle port of pintoc's LQR-scan solve
+# ---------------------------------------------------------------------------
+
+def cpu_lqr_sample(n_per_half: int, cores: int, pool=None) -> tuple[float, int]:
+    """Reference LQR-scan solves of n_per_half problems of each half, spread
+    over `cores` worker processes.  Each worker builds its expansions
+    untimed, then times its solves; the aggregate throughput is the sum of
+    the per-worker rates (workers run concurrently, one per core)."""
+    jobs = []
+    for system in ("pendulum", "cartpole"):
+        rng = rng_for(0, system)
+        x0 = initial_states(system, n_per_half, rng)
+        us = initial_controls(system, n_per_half, rng)
+        per = max(1, math.ceil(2 * n_per_half / cores))
+        for i in range(0, n_per_half, per):
+            jobs.append((system, x0[i:i + per], us[i:i + per]))
+    res = pool.map(_cpu_timed_chunk, jobs) if pool else list(map(_cpu_timed_chunk, jobs))
+    solved = sum(r[0] for r in res)
+    rate = sum(r[0] / max(r[1], 1e-9) for r in res)
+    return rate, solved
+
+
+def _cpu_timed_chunk(args):
+    system, x0s, us = args
+    sys.path.insert(0, ROOT)
+    from oracle import pintoc_oracle as O
+    dyn, cost = models_oracle(O)[system]
+    exps = []
+    t_setup0 = time.perf_counter()
+    for x0, u in zip(x0s, us):
+        xs = O.rollout(dyn, x0, u)
+        lam = O.costate_pass(dyn, cost, ("zero",), xs, u)
+        exps.append(O.expansion(dyn, cost, ("zero",), xs, u, lam, ALPHA))
+    t0 = time.perf_counter()
+    for e in exps:
+        O.lqr_solve(e)
+    t1 = time.perf_counter()
+    return len(exps), t1 - t0, t1 - t_setup0
+
+
+def make_pool(cores: int):
+    import multiprocessing as mp
+    return mp.get_context("spawn").Pool(cores)
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    per_half = max(1, cores)  # one problem per core per half per step
+    pool = make_pool(cores)
+    try:
+        for _ in range(args.warmup):
+            cpu_lqr_sample(per_half, cores, pool)
+        vals, wall = [], 0.0
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            v, _ = cpu_lqr_sample(per_half, cores, pool)
+            wall += time.perf_counter() - t0
+            vals.append(v)
+    finally:
+        pool.close()
+    value = statistics.median(vals)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{2 * per_half} problems per step (half pendulum, half "
+                                   "cart-pole, T=256) of the config-3 workload; LQR-scan solve "
+                                   "timed, expansion built untimed"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n: int) -> dict:
+    return {"workload": "config 3: 65,536 independent LQR subproblems (32,768 pendulum nx=2 "
+                        "nu=1 + 32,768 cart-pole nx=4 nu=1), T=256, Newton expansions at "
+                        "seeded config-3 trajectories, alpha=1",
+            "global_batch": B_TOTAL, "horizon": T, "parallelism": f"problem-sharded x{n}",
+            "l2": "inputs > L2 (no flush needed)"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING recipe)."""
+
+    def __init__(self, index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for row in open(self.path):
+            f = [x.strip() for x in row.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def measured_peak() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path)).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def build_inputs(P, torch, system: str, n: int, rank: int):
+    """Device Newton expansions of n problems of one half (untimed setup)."""
+    from paper_2409_20027_b200._device import DeviceSolver, SolveSettings
+    prob = models_pkg(P)[system]
+    rng = rng_for(rank, system)
+    x0 = initial_states(system, n, rng)
+    us = initial_controls(system, n, rng)
+    solver = DeviceSolver(prob.dynamics, prob.cost, None, n, SolveSettings(alpha0=ALPHA))
+    X = torch.zeros(n, T + 1, solver.nx, dtype=torch.float64)
+    X[:, 0] = torch.as_tensor(x0)
+    solver.load(X, torch.as_tensor(us))
+    solver.rollout()
+    solver.load(solver.field("states", T + 1, (solver.nx,)).contiguous(), torch.as_tensor(us))
+    solver.expand()
+    nx, nu = solver.nx, solver.nu
+    f = lambda name, c, rows=T: solver.read(name).view(c, rows, n).clone()
+    inputs = [f("P", nx * nx), f("R", nu * nu), f("M", nx * nu), f("d", nu), f("Fx", nx * nx),
+              f("Fu", nx * nu), f("PT", nx * nx, 1)]
+    del solver
+    return inputs, nx, nu
+
+
+def alg_bytes(n: int, nx: int, nu: int) -> int:
+    """Minimum HBM traffic of one LQR-scan solve: read the expansion once,
+    write gains + deviations once (8-byte words)."""
+    inp = nx * nx + nu * nu + nx * nu + nu + nx * nx + nx * nu
+    out = nu * nx + nu + nx + nu
+    return 8 * n * (T * (inp + out) + nx * nx + nx)
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200.passes import LqrSolver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    b_local = B_TOTAL // world
+    bp, bc = half_sizes(b_local)
+
+    halves = {}
+    for system, n in (("pendulum", bp), ("cartpole", bc)):
+        inputs, nx, nu = build_inputs(P, torch, system, n, rank)
+        alpha = torch.full((n,), ALPHA, dtype=torch.float64, device="cuda")
+        halves[system] = (LqrSolver(n, T, nx, nu, dtype=torch.float64), inputs, alpha, n, nx, nu)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for solver, inputs, alpha, *_ in halves.values():
+            solver.solve(*inputs, alpha)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    # per-half timing (roofline of the dominant kernel pair)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    half_ms = {k: 0.0 for k in halves}
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        for i, (k, (solver, inputs, alpha, *_)) in enumerate(halves.items()):
+            ev[2 * i].record(stream)
+            solver.solve(*inputs, alpha)
+            ev[2 * i + 1].record(stream)
+        torch.cuda.synchronize()
+        for i, k in enumerate(halves):
+            half_ms[k] += ev[2 * i].elapsed_time(ev[2 * i + 1]) / args.steps
+
+    # timed region
+    clocks = Clocks(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms = t0.elapsed_time(t1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t)
+    value = B_TOTAL / (ms * 1e-3)
+
+    # end-to-end through the C ABI with host buffers: H2D of the step's
+    # expansions from pinned memory, solve, D2H of gains and deviations
+    e2e = None
+    if not args.no_e2e:
+        host = {k: [t.cpu().pin_memory() for t in h[1]] for k, h in halves.items()}
+        dev_in = {k: [torch.empty_like(t) for t in h[1]] for k, h in halves.items()}
+        outs = {k: [torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                    for t in (h[0].Gamma, h[0].gamma, h[0].dx, h[0].du)] for k, h in halves.items()}
+        h2d = sum(t.numel() * t.element_size() for v in host.values() for t in v)
+        d2h = sum(t.numel() * t.element_size() for v in outs.values() for t in v)
+
+        def e2e_step():
+            for k, (solver, _, alpha, *_r) in halves.items():
+                for d, h in zip(dev_in[k], host[k]):
+                    d.copy_(h, non_blocking=True)
+                solver.solve(*dev_in[k], alpha)
+                for h, d in zip(outs[k], (solver.Gamma, solver.gamma, solver.dx, solver.du)):
+                    h.copy_(d, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(2, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([a.elapsed_time(b) / n_e2e], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": B_TOTAL / (float(e_ms) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "ms_per_step": float(e_ms)}
+        del host, dev_in, outs
+
+    # horizon sweep of the single-problem LQR-scan latency (config 1, nx=4)
+    sweep = None
+    if rank == 0 and not args.no_sweep:
+        sweep = lqr_latency_sweep(torch, LqrSolver)
+
+    if rank == 0:
+        solver_c, _, _, n_c, nx_c, nu_c = halves["cartpole"]
+        by = alg_bytes(n_c, nx_c, nu_c)
+        peak, peak_src = measured_peak()
+        achieved = by / (half_ms["cartpole"] * 1e-3) / 1e9
+        kname = "lqr_sweep_cartpole(k_value_down0+k_prop_down0)"
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname,
+                "algorithmic_bytes_per_launch": by, "ms_per_launch": half_ms["cartpole"],
+                "peak_source": peak_src,
+                "pendulum_half": {"ms": half_ms["pendulum"],
+                                  "achieved_gbs": alg_bytes(halves["pendulum"][3], 2, 1)
+                                  / (half_ms["pendulum"] * 1e-3) / 1e9}}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            pool = make_pool(cores)
+            try:
+                cpu_lqr_sample(max(1, cores // 2), cores, pool)
+                v, n_done = cpu_lqr_sample(4 * cores, cores, pool)
+            finally:
+                pool.close()
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": f"{n_done} problems (half pendulum, half cart-pole, T=256) of the "
+                             "config-3 workload through the pinned numpy port of pintoc's "
+                             "value_pass+propagation_pass (oracle/), one process per core"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": workload_config(world),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 4 * args.steps, "clocks": clk,
+            "lqr_latency_sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def lqr_latency_sweep(torch, LqrSolver):
+    """Single-problem LQR-scan solve latency vs horizon (config 1: random
+    time-varying systems, batch 1, fp64) -- the log-T claim."""
+    from oracle.pintoc_oracle import random_lqr_expansion  # input generator only
+    out = {}
+    for nx in (2, 4, 8, 12):
+        nu = nx // 2
+        row = {}
+        for logT in (8, 10, 12, 14, 16):
+            Tn = 1 << logT
+            rng = np.random.default_rng([1, nx, logT])
+            e = random_lqr_expansion(rng, Tn, nx, nu)
+            dev = torch.device("cuda")
+            soa = lambda a, c: torch.as_tensor(a.reshape(a.shape[0], c).T.copy()).unsqueeze(-1).to(dev)
+            ins = [soa(e.P, nx * nx), soa(e.R, nu * nu), soa(e.M, nx * nu), soa(e.d, nu),
+                   soa(e.Fx, nx * nx), soa(e.Fu, nx * nu), soa(e.PT[None], nx * nx)]
+            alpha = torch.zeros(1, dtype=torch.float64, device=dev)
+            s = LqrSolver(1, Tn, nx, nu)
+            for _ in range(3):
+                s.solve(*ins, alpha)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            a.record()
+            for _ in range(reps):
+                s.solve(*ins, alpha)
+            b.record()
+            torch.cuda.synchronize()
+            row[str(Tn)] = round(a.elapsed_time(b) / reps, 4)
+        out[f"nx{nx}_ms"] = row
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,213 @@
+/*
+ * pintoc_b200 -- C ABI of the B200-native parallel-in-time Newton solver.
+ *
+ * Drop-in boundary for the hot path of the reference package `pintoc`
+ * (arxiv 2409.20027 artifact, /root/reference/pkg/src/pintoc).  Every entry
+ * point below replaces one reference function; the file:line it replaces is
+ * given beside it.  The reference is pure Python, so the binding a
+ * maintainer would add is a ctypes stub; the Python
+ * package `paper_2409_20027_b200` is exactly that binding.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  `void* stream` is a cudaStream_t
+ *     (NULL = legacy default stream).  Return value 0 = success, < 0 = error
+ *     (message via ptc_last_error()).
+ *   - dtype: PTC_F32 or PTC_F64; every array argument is in that dtype
+ *     unless typed explicitly.
+ *   - HBM layout "SoA, batch-minor": a per-stage field with C scalar
+ *     components over `rows` stages of `batch` problems is stored as
+ *         field[(c * rows + t) * batch + b],
+ *     matrices row-major inside c (c = i * ncols + j).  For batch = 1 this is
+ *     one contiguous time series per matrix entry.
+ *   - Workspaces are caller-allocated device memory (the Python binding
+ *     allocates them as torch tensors).
+ */
+#ifndef PINTOC_B200_H
+#define PINTOC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PTC_F32 0
+#define PTC_F64 1
+
+#define PTC_OK 0
+#define PTC_ERR_ARG (-1)
+#define PTC_ERR_UNSUPPORTED (-2)
+#define PTC_ERR_CUDA (-3)
+#define PTC_ERR_WORKSPACE (-4)
+
+/* dynamics models (reference systems.py) */
+#define PTC_DYN_PENDULUM 0   /* PendulumDynamics, systems.py:172-231   */
+#define PTC_DYN_CARTPOLE 1   /* CartPoleDynamics, systems.py:341-437   */
+#define PTC_DYN_LINEAR 2     /* LinearDynamics, systems.py:32-77 (+ time-varying) */
+
+/* augmentation of a plain Newton solve (reference problem.py:343-433, outer.py) */
+#define PTC_AUG_ZERO 0
+#define PTC_AUG_BARRIER 1
+#define PTC_AUG_ADMM 2
+
+/* solve method */
+#define PTC_METHOD_NEWTON 0   /* newton.py:129  newton_solve   */
+#define PTC_METHOD_BARRIER 1  /* outer.py:221   barrier_solve  */
+#define PTC_METHOD_ADMM 2     /* outer.py:392   admm_solve     */
+
+/* per-problem status codes (int32, read back with ptc_solver_read "status") */
+#define PTC_ST_RUNNING 0
+#define PTC_ST_DONE 1
+#define PTC_ST_ERR_STALLED (-1)    /* SolverStalledError (newton.py:168-171) */
+#define PTC_ST_ERR_INFEASIBLE (-2) /* InfeasibleError from total_cost          */
+
+/* Newton termination codes ("round_term"); names as newton.py:41-44 */
+#define PTC_TERM_NONE 0
+#define PTC_TERM_COST 1       /* "converged_cost" */
+#define PTC_TERM_STEP 2       /* "converged_step" */
+#define PTC_TERM_MAX_ITERS 3  /* "max_iters"      */
+#define PTC_TERM_STALLED 4    /* "stalled"        */
+
+const char* ptc_last_error(void);
+int ptc_version(void);
+
+/* 1 if kernels for (dtype, model, nx, nu) are compiled in; model = -1 asks
+ * about the model-free LQR kernels only. */
+int ptc_supported(int dtype, int model, int nx, int nu);
+
+/* ------------------------------------------------------------------------
+ * LQR subproblem solve = value_pass + propagation_pass
+ *   replaces passes.py:291 value_pass  (Alg. 2: suffix scan over dual value
+ *   elements, passes.py:244-288, gains passes.py:316-323) and
+ *   passes.py:338 propagation_pass (Alg. 3: prefix scan of closed-loop
+ *   affine maps).
+ * Inputs (device, SoA batch-minor, `horizon` rows unless noted):
+ *   P (nx*nx), R (nu*nu, unregularised), M (nx*nu), d (nu), Fx (nx*nx),
+ *   Fu (nx*nu), PT (nx*nx, 1 row), alpha (float64[batch], R_reg = R + alpha I).
+ * Outputs (device): S (nx*nx, horizon+1 rows) and s (nx, horizon+1) may be
+ *   NULL; Gamma (nu*nx), gamma (nu), dx (nx, horizon+1), du (nu).
+ *   flags (int32[batch], must be zeroed by the caller): bit 1 R+alpha I not
+ *   positive definite, bit 2 some Q_t not positive definite (both
+ *   DefinitenessError), bit 4 singular I + C Y (ConditioningError).
+ * chunk0 / chunk: scan-tree plan (stages per level-0 thread, items per
+ *   thread above level 0); 0 = automatic.  chunk0 >= horizon gives the
+ *   sequential (one thread per problem) schedule.
+ * ---------------------------------------------------------------------- */
+int64_t ptc_lqr_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
+                                int chunk0, int chunk);
+int ptc_lqr_solve(int dtype, int batch, int horizon, int nx, int nu,
+                  const void* P, const void* R, const void* M, const void* d,
+                  const void* Fx, const void* Fu, const void* PT, const double* alpha,
+                  void* S, void* s, void* Gamma, void* gamma, void* dx, void* du,
+                  int* flags, void* workspace, int64_t workspace_bytes,
+                  int chunk0, int chunk, void* stream);
+/* propagation_pass alone (passes.py:338-361) for a given feedback law:
+ * Fx, Fu, Gamma (nu*nx), gamma (nu) in; dx, du out; d (nu) may be NULL.
+ * Same workspace as ptc_lqr_solve. */
+int ptc_propagate(int dtype, int batch, int horizon, int nx, int nu,
+                  const void* Fx, const void* Fu, const void* Gamma, const void* gamma,
+                  const void* d, void* dx, void* du, void* workspace, int64_t workspace_bytes,
+                  int chunk0, int chunk, void* stream);
+/* the plan the automatic choice would use (for reporting / depth probes) */
+int ptc_lqr_plan(int batch, int horizon, int chunk0, int chunk, int* out_chunk0,
+                 int* out_chunk, int* out_levels);
+
+/* ------------------------------------------------------------------------
+ * Batched device-resident solver
+ *   one object = `batch` independent problems sharing model, cost and
+ *   constraints (per-problem initial trajectories).  Replaces
+ *   newton.py:129 newton_solve, outer.py:221 barrier_solve and
+ *   outer.py:392 admm_solve; the augmentations are outer.py:30-157
+ *   (BarrierAugmentation) and outer.py:252-333 (AdmmAugmentation); the
+ *   passes inside one iteration are passes.py:122 costate_pass,
+ *   passes.py:155 hamiltonian_expansion, value_pass, propagation_pass,
+ *   problem.py:449 rollout and problem.py:476 total_cost.
+ * ---------------------------------------------------------------------- */
+typedef struct ptc_solver ptc_solver;
+
+typedef struct ptc_problem_desc {
+  int32_t dtype, batch, horizon, nx, nu;
+  int32_t model;               /* PTC_DYN_* */
+  double dyn_params[8];        /* pendulum: g, l, m, b, dt; cart-pole: g, l, m_cart, m_pole, dt */
+  /* affine model x' = A x + B u + c: host arrays in dtype, shapes
+   * (nx*nx, lin_rows, lin_batch), (nx*nu, lin_rows, lin_batch),
+   * (nx, lin_rows, lin_batch) with lin_rows in {1, horizon} (time-invariant
+   * or time-varying) and lin_batch in {1, batch}; lin_c may be NULL */
+  const void* lin_a;
+  const void* lin_b;
+  const void* lin_c;
+  int32_t lin_rows, lin_batch;
+  /* quadratic cost (systems.py:80-139), float64 host arrays */
+  const double* Q;             /* nx*nx */
+  const double* R;             /* nu*nu */
+  const double* Qf;            /* nx*nx */
+  const double* goal;          /* nx, may be NULL (= 0) */
+  /* box constraints (problem.py:233-340), float64 host, +-inf = absent;
+   * any pointer may be NULL */
+  const double* state_lower;
+  const double* state_upper;
+  const double* control_lower;
+  const double* control_upper;
+  /* solve */
+  int32_t method;              /* PTC_METHOD_* */
+  int32_t aug;                 /* PTC_AUG_* for PTC_METHOD_NEWTON */
+  double aug_mu;               /* barrier weight for PTC_AUG_BARRIER */
+  double alpha0, nu0, inner_tol;
+  int32_t max_iters;
+  double mu0, zeta, mu_tol;    /* barrier (outer.py:180-193) */
+  double rho, residual_tol;    /* ADMM (outer.py:351-364), also the ADMM-aug rho */
+  int32_t max_outer;
+  int32_t hist_cap;            /* per-problem Newton iteration records kept */
+  int32_t round_cap;           /* per-problem outer rounds recorded */
+  int32_t keep_round_controls; /* barrier: store each round's controls */
+  int32_t chunk0, chunk;       /* scan plan, 0 = automatic */
+} ptc_problem_desc;
+
+int64_t ptc_solver_workspace_bytes(const ptc_problem_desc* desc);
+int ptc_solver_create(const ptc_problem_desc* desc, void* workspace, int64_t workspace_bytes,
+                      ptc_solver** out);
+int ptc_solver_destroy(ptc_solver* s);
+
+/* Load initial trajectories: states (nx, horizon+1, batch), controls
+ * (nu, horizon, batch); host (on_device = 0) or device pointers.  Resets the
+ * solver state.  For PTC_AUG_ADMM Newton solves, z and v (W, horizon, batch)
+ * may be given (else zero). */
+int ptc_solver_load(ptc_solver* s, const void* states, const void* controls,
+                    const void* z, const void* v, int on_device, void* stream);
+
+/* first stage t where x_{t+1} != f_t(x_t, u_t) per problem (-1 if
+ * consistent), int32 host array [batch] -- newton.py:118-126 */
+int ptc_solver_check_consistency(ptc_solver* s, int32_t* first_bad_stage, void* stream);
+
+/* Enqueue n device iterations (costate + expansion, value scan, propagation
+ * scan, rollout + cost, trust-region control, outer-loop control). */
+int ptc_solver_iterate(ptc_solver* s, int n, void* stream);
+
+/* Number of problems still running (synchronises the stream). */
+int ptc_solver_running(ptc_solver* s, int32_t* n_running, void* stream);
+
+/* Pass-level entry points on the loaded trajectory (buffer 0):
+ *   expand  = costate_pass + hamiltonian_expansion (passes.py:122, 155)
+ *   lqr     = value_pass + propagation_pass on that expansion
+ *   rollout = problem.py:449 rollout (controls -> states, from x_0)
+ *   cost    = problem.py:476 total_cost -> "cur_cost", "bad_index" */
+int ptc_solver_expand(ptc_solver* s, void* stream);
+int ptc_solver_lqr(ptc_solver* s, const double* alpha_host, void* stream);
+int ptc_solver_rollout(ptc_solver* s, void* stream);
+int ptc_solver_total_cost(ptc_solver* s, void* stream);
+
+/* Copy a named buffer out (dst host or device).  Names: states, controls
+ * (current trajectory), lam, P, R, M, d, Fx, Fu, PT, S, s, Gamma, gamma, dx,
+ * du, z, v, status, iters, term, round, hist_len, hist, cur_cost, alpha, mu,
+ * round_mu, round_cost, round_iters, round_term, round_rp, round_rd,
+ * round_controls, bad_index, flags.  ptc_solver_buffer_info reports the
+ * element count and element size. */
+int ptc_solver_buffer_info(ptc_solver* s, const char* name, int64_t* numel, int32_t* elem_bytes);
+int ptc_solver_read(ptc_solver* s, const char* name, void* dst, int64_t bytes, int dst_on_device,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PINTOC_B200_H */

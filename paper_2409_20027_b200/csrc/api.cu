@@ -1,0 +1,703 @@
+// C ABI implementation (include/pintoc_b200.h): workspace carving, the
+// batched solver object and dispatch into the instantiated kernel sets.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/pintoc_b200.h"
+#include "launch.cuh"
+
+namespace ptc {
+
+std::map<LqrKey, LqrOps>& lqr_registry() {
+  static std::map<LqrKey, LqrOps> r;
+  return r;
+}
+std::map<NewtonKey, NewtonOps>& newton_registry() {
+  static std::map<NewtonKey, NewtonOps> r;
+  return r;
+}
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define PTC_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess)                                                    \
+      return fail(PTC_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+// ------------------------------------------------------------------ planning
+
+// Automatic scan plan.  Large batches fill the GPU on their own: one thread
+// per problem sweeps its horizon (no tree, work optimal).  Small batches
+// split the horizon into chunks of K0 stages so that ~32K threads are busy,
+// with an 8-ary tree above them (log-depth in the horizon).
+static Plan auto_plan(int B, int T, int K0, int K) {
+  if (K <= 0) K = 8;
+  if (K0 <= 0) {
+    const long long work = (long long)B * T;
+    if (B >= 8192) K0 = T;
+    else K0 = (int)std::max<long long>(4, (work + 32767) / 32768);
+  }
+  return make_plan(T, K0, K);
+}
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+template <typename R>
+static void carve_lqr_tree(Carver& c, LqrArgs<R>& a, int nx) {
+  const Plan& pl = a.plan;
+  const size_t B = a.B;
+  a.red = c.template take<double>(3 * (size_t)pl.units0() * B);
+  for (int l = 0; l <= kMaxLevels; ++l) a.vagg[l] = a.vcar[l] = a.pagg[l] = a.pcar[l] = nullptr;
+  for (int l = 1; l <= pl.L; ++l) {
+    const size_t n = (size_t)pl.n[l] * B;
+    a.vagg[l] = c.template take<R>(n * (3 * nx * nx + 2 * nx));
+    a.vcar[l] = c.template take<R>(n * (nx * nx + nx));
+    a.pagg[l] = c.template take<R>(n * (nx * nx + nx));
+    a.pcar[l] = c.template take<R>(n * nx);
+  }
+}
+
+}  // namespace ptc
+
+using namespace ptc;
+
+extern "C" {
+
+const char* ptc_last_error(void) { return g_err.c_str(); }
+
+int ptc_version(void) { return 100; }
+
+int ptc_supported(int dtype, int model, int nx, int nu) {
+  if (model < 0) return lqr_registry().count(LqrKey(dtype, nx, nu)) ? 1 : 0;
+  return newton_registry().count(NewtonKey(dtype, model, nx, nu)) ? 1 : 0;
+}
+
+int ptc_lqr_plan(int batch, int horizon, int chunk0, int chunk, int* out_chunk0, int* out_chunk,
+                 int* out_levels) {
+  if (batch < 1 || horizon < 1) return fail(PTC_ERR_ARG, "batch and horizon must be >= 1");
+  Plan p = auto_plan(batch, horizon, chunk0, chunk);
+  if (out_chunk0) *out_chunk0 = p.K0;
+  if (out_chunk) *out_chunk = p.K;
+  if (out_levels) *out_levels = p.L;
+  return PTC_OK;
+}
+
+int64_t ptc_lqr_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu, int chunk0,
+                                int chunk) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  Carver c{nullptr};
+  if (dtype == PTC_F64) {
+    LqrArgs<double> a{};
+    a.B = batch;
+    a.T = horizon;
+    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    carve_lqr_tree(c, a, nx);
+  } else {
+    LqrArgs<float> a{};
+    a.B = batch;
+    a.T = horizon;
+    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    carve_lqr_tree(c, a, nx);
+  }
+  return (int64_t)c.off + 256;
+}
+
+}  // extern "C"
+
+template <typename R>
+static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, const void* Rm,
+                       const void* M, const void* d, const void* Fx, const void* Fu,
+                       const void* PT, const double* alpha, void* S, void* s, void* Gamma,
+                       void* gamma, void* dx, void* du, int* flags, void* ws, int64_t ws_bytes,
+                       int chunk0, int chunk, cudaStream_t st) {
+  auto it = lqr_registry().find(LqrKey(dtype_code<R>(), nx, nu));
+  if (it == lqr_registry().end())
+    return fail(PTC_ERR_UNSUPPORTED, "LQR kernels not instantiated for nx=" + std::to_string(nx) +
+                                         " nu=" + std::to_string(nu));
+  LqrArgs<R> a{};
+  a.B = batch;
+  a.T = horizon;
+  a.plan = auto_plan(batch, horizon, chunk0, chunk);
+  a.P = (const R*)P;
+  a.Rm = (const R*)Rm;
+  a.M = (const R*)M;
+  a.d = (const R*)d;
+  a.Fx = (const R*)Fx;
+  a.Fu = (const R*)Fu;
+  a.PT = (const R*)PT;
+  a.alpha = alpha;
+  a.status = nullptr;
+  a.S = (R*)S;
+  a.s = (R*)s;
+  a.Gam = (R*)Gamma;
+  a.gam = (R*)gamma;
+  a.dX = (R*)dx;
+  a.dU = (R*)du;
+  a.flags = flags;
+  Carver c{(char*)ws};
+  carve_lqr_tree(c, a, nx);
+  if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
+  if ((S == nullptr) != (s == nullptr)) return fail(PTC_ERR_ARG, "S and s must both be given or both NULL");
+  it->second.solve(&a, st);
+  PTC_CUDA(cudaGetLastError());
+  return PTC_OK;
+}
+
+template <typename R>
+static int propagate_t(int batch, int horizon, int nx, int nu, const void* Fx, const void* Fu,
+                       const void* Gamma, const void* gamma, const void* d, void* dx, void* du,
+                       void* ws, int64_t ws_bytes, int chunk0, int chunk, cudaStream_t st) {
+  auto it = lqr_registry().find(LqrKey(dtype_code<R>(), nx, nu));
+  if (it == lqr_registry().end())
+    return fail(PTC_ERR_UNSUPPORTED, "LQR kernels not instantiated for nx=" + std::to_string(nx) +
+                                         " nu=" + std::to_string(nu));
+  LqrArgs<R> a{};
+  a.B = batch;
+  a.T = horizon;
+  a.plan = auto_plan(batch, horizon, chunk0, chunk);
+  a.Fx = (const R*)Fx;
+  a.Fu = (const R*)Fu;
+  a.d = (const R*)d;
+  a.Gam = (R*)Gamma;
+  a.gam = (R*)gamma;
+  a.dX = (R*)dx;
+  a.dU = (R*)du;
+  Carver c{(char*)ws};
+  carve_lqr_tree(c, a, nx);
+  if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
+  it->second.propagate(&a, st);
+  PTC_CUDA(cudaGetLastError());
+  return PTC_OK;
+}
+
+extern "C" {
+
+int ptc_propagate(int dtype, int batch, int horizon, int nx, int nu, const void* Fx,
+                  const void* Fu, const void* Gamma, const void* gamma, const void* d, void* dx,
+                  void* du, void* workspace, int64_t workspace_bytes, int chunk0, int chunk,
+                  void* stream) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == PTC_F64)
+    return propagate_t<double>(batch, horizon, nx, nu, Fx, Fu, Gamma, gamma, d, dx, du, workspace,
+                               workspace_bytes, chunk0, chunk, st);
+  if (dtype == PTC_F32)
+    return propagate_t<float>(batch, horizon, nx, nu, Fx, Fu, Gamma, gamma, d, dx, du, workspace,
+                              workspace_bytes, chunk0, chunk, st);
+  return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
+}
+
+int ptc_lqr_solve(int dtype, int batch, int horizon, int nx, int nu, const void* P, const void* R,
+                  const void* M, const void* d, const void* Fx, const void* Fu, const void* PT,
+                  const double* alpha, void* S, void* s, void* Gamma, void* gamma, void* dx,
+                  void* du, int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                  int chunk, void* stream) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == PTC_F64)
+    return lqr_solve_t<double>(batch, horizon, nx, nu, P, R, M, d, Fx, Fu, PT, alpha, S, s, Gamma,
+                               gamma, dx, du, flags, workspace, workspace_bytes, chunk0, chunk, st);
+  if (dtype == PTC_F32)
+    return lqr_solve_t<float>(batch, horizon, nx, nu, P, R, M, d, Fx, Fu, PT, alpha, S, s, Gamma,
+                              gamma, dx, du, flags, workspace, workspace_bytes, chunk0, chunk, st);
+  return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// solver object
+// ---------------------------------------------------------------------------
+
+struct ptc_solver {
+  virtual ~ptc_solver() = default;
+  ptc_problem_desc desc;
+  virtual int load(const void* X, const void* U, const void* z, const void* v, int on_dev,
+                   cudaStream_t s) = 0;
+  virtual int check(int32_t* bad, cudaStream_t s) = 0;
+  virtual int iterate(int n, cudaStream_t s) = 0;
+  virtual int running(int32_t* n, cudaStream_t s) = 0;
+  virtual int expand(cudaStream_t s) = 0;
+  virtual int lqr(const double* alpha_host, cudaStream_t s) = 0;
+  virtual int rollout(cudaStream_t s) = 0;
+  virtual int total_cost(cudaStream_t s) = 0;
+  virtual int info(const char* name, int64_t* numel, int32_t* es) = 0;
+  virtual int read(const char* name, void* dst, int64_t bytes, int on_dev, cudaStream_t s) = 0;
+};
+
+namespace ptc {
+
+template <typename R>
+__global__ void k_normalize_parity(NewtonArgs<R> a, int nx, int nu) {
+  // make buffer 0 hold every problem's current trajectory
+  const long long n = (long long)a.B * (a.T + 1);
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = (int)(i % a.B);
+  const int t = (int)(i / a.B);
+  if (a.parity[b] == 0) return;
+  for (int c = 0; c < nx; ++c) {
+    size_t o = ((size_t)c * (a.T + 1) + t) * a.B + b;
+    a.X[o] = a.X[a.xsz + o];
+  }
+  if (t < a.T)
+    for (int c = 0; c < nu; ++c) {
+      size_t o = ((size_t)c * a.T + t) * a.B + b;
+      a.U[o] = a.U[a.usz + o];
+    }
+}
+
+template <typename R>
+__global__ void k_clear_parity(NewtonArgs<R> a) {
+  const int b = unit_id();
+  if (b < a.B) a.parity[b] = 0;
+}
+
+struct Buf {
+  void* p;
+  int64_t numel;
+  int32_t es;
+};
+
+template <typename R>
+struct Solver final : ptc_solver {
+  NewtonArgs<R> na{};
+  LqrArgs<R> la{};
+  const NewtonOps* ops = nullptr;
+  int nx = 0, nu = 0, W = 0;
+  R *S = nullptr, *s_ = nullptr;
+  int* bad_t = nullptr;
+  ProblemParams hp{};
+  std::map<std::string, Buf> bufs;
+
+  static void build_params(const ptc_problem_desc& d, ProblemParams& p) {
+    std::memset(&p, 0, sizeof(p));
+    p.dyn_kind = d.model;
+    for (int i = 0; i < 8; ++i) p.dyn[i] = d.dyn_params[i];
+    const int nx = d.nx, nu = d.nu;
+    for (int i = 0; i < nx * nx; ++i) {
+      p.Q[i] = d.Q ? d.Q[i] : 0.0;
+      p.Qf[i] = d.Qf ? d.Qf[i] : 0.0;
+    }
+    for (int i = 0; i < nu * nu; ++i) p.Rc[i] = d.R ? d.R[i] : 0.0;
+    for (int i = 0; i < nx; ++i) p.goal[i] = d.goal ? d.goal[i] : 0.0;
+    int W = 0;
+    auto add = [&](int var, int idx, double sign, double bound) {
+      p.row_var[W] = var;
+      p.row_idx[W] = idx;
+      p.row_sign[W] = sign;
+      p.row_bound[W] = bound;
+      ++W;
+    };
+    // stacking order of BoxConstraint (problem.py:254-260): state upper,
+    // state lower, control upper, control lower; infinite bounds dropped
+    for (int i = 0; i < nx; ++i)
+      if (d.state_upper && std::isfinite(d.state_upper[i])) add(0, i, 1.0, d.state_upper[i]);
+    for (int i = 0; i < nx; ++i)
+      if (d.state_lower && std::isfinite(d.state_lower[i])) add(0, i, -1.0, d.state_lower[i]);
+    p.Ws = W;
+    for (int i = 0; i < nu; ++i)
+      if (d.control_upper && std::isfinite(d.control_upper[i])) add(1, i, 1.0, d.control_upper[i]);
+    for (int i = 0; i < nu; ++i)
+      if (d.control_lower && std::isfinite(d.control_lower[i])) add(1, i, -1.0, d.control_lower[i]);
+    p.W = W;
+    p.lin_T = std::max(1, d.lin_rows);
+    p.lin_B = std::max(1, d.lin_batch);
+  }
+
+  static size_t layout(const ptc_problem_desc& d, Carver& c, Solver* self) {
+    const size_t B = d.batch, T = d.horizon, nx = d.nx, nu = d.nu;
+    ProblemParams pp;
+    build_params(d, pp);
+    const size_t W = pp.W;
+    NewtonArgs<R> a{};
+    LqrArgs<R> l{};
+    a.B = l.B = (int)B;
+    a.T = l.T = (int)T;
+    a.plan = l.plan = auto_plan((int)B, (int)T, d.chunk0, d.chunk);
+    const size_t P0 = a.plan.units0();
+    ProblemParams* dpp = c.template take<ProblemParams>(1);
+    R *linA = nullptr, *linB = nullptr, *linc = nullptr;
+    if (d.model == PTC_DYN_LINEAR) {
+      const size_t lt = pp.lin_T, lb = pp.lin_B;
+      linA = c.template take<R>(nx * nx * lt * lb);
+      linB = c.template take<R>(nx * nu * lt * lb);
+      linc = c.template take<R>(nx * lt * lb);
+    }
+    a.xsz = nx * (T + 1) * B;
+    a.usz = nu * T * B;
+    a.X = c.template take<R>(2 * a.xsz);
+    a.U = c.template take<R>(2 * a.usz);
+    auto ib = [&]() { return c.template take<int>(B); };
+    auto db = [&]() { return c.template take<double>(B); };
+    a.status = ib(); a.phase = ib(); a.parity = ib(); a.flags = ib(); a.iters = ib();
+    a.term = ib(); a.round = ib(); a.hist_len = ib(); a.bad_index = ib();
+    a.n_running = c.template take<int>(1);
+    int* bad_t = ib();
+    a.alpha = db(); a.nu = db(); a.cur_cost = db(); a.cand_cost = db(); a.mu = db();
+    a.opt.hist_cap = std::max(0, d.hist_cap);
+    a.opt.round_cap = std::max(1, d.round_cap);
+    a.hist = c.template take<double>((size_t)a.opt.hist_cap * 5 * B + 1);
+    const size_t rc = a.opt.round_cap;
+    a.round_mu = c.template take<double>(rc * B);
+    a.round_cost = c.template take<double>(rc * B);
+    a.round_rp = c.template take<double>(rc * B);
+    a.round_rd = c.template take<double>(rc * B);
+    a.round_iters = c.template take<int>(rc * B);
+    a.round_term = c.template take<int>(rc * B);
+    a.round_U = (d.method == PTC_METHOD_BARRIER && d.keep_round_controls)
+                    ? c.template take<R>(rc * nu * T * B) : nullptr;
+    const bool admm = d.method == PTC_METHOD_ADMM || d.aug == PTC_AUG_ADMM;
+    a.z = admm ? c.template take<R>(std::max<size_t>(W, 1) * T * B) : nullptr;
+    a.v = admm ? c.template take<R>(std::max<size_t>(W, 1) * T * B) : nullptr;
+    a.lam = c.template take<R>(nx * (T + 1) * B);
+    a.P = c.template take<R>(nx * nx * T * B);
+    a.Rm = c.template take<R>(nu * nu * T * B);
+    a.M = c.template take<R>(nx * nu * T * B);
+    a.d = c.template take<R>(nu * T * B);
+    a.Fx = c.template take<R>(nx * nx * T * B);
+    a.Fu = c.template take<R>(nx * nu * T * B);
+    a.PT = c.template take<R>(nx * nx * B);
+    for (int k = 0; k <= kMaxLevels; ++k) a.cagg[k] = a.ccar[k] = nullptr;
+    for (int k = 1; k <= a.plan.L; ++k) {
+      a.cagg[k] = c.template take<R>((size_t)a.plan.n[k] * B * (nx * nx + nx));
+      a.ccar[k] = c.template take<R>((size_t)a.plan.n[k] * B * nx);
+    }
+    a.cpart[0] = c.template take<double>(3 * P0 * B);
+    a.cpart[1] = c.template take<double>(3 * P0 * B);
+    a.apart = c.template take<double>(2 * P0 * B);
+    // LQR outputs + tree
+    const bool keep_S = B * (T + 1) * (nx * nx + nx) <= (size_t)64 << 20;
+    R* S = keep_S ? c.template take<R>(nx * nx * (T + 1) * B) : nullptr;
+    R* s = keep_S ? c.template take<R>(nx * (T + 1) * B) : nullptr;
+    l.Gam = c.template take<R>(nu * nx * T * B);
+    l.gam = c.template take<R>(nu * T * B);
+    l.dX = c.template take<R>(nx * (T + 1) * B);
+    l.dU = c.template take<R>(nu * T * B);
+    carve_lqr_tree(c, l, (int)nx);
+    a.red = l.red;
+    if (self) {
+      self->hp = pp;
+      self->W = (int)W;
+      self->S = S;
+      self->s_ = s;
+      self->bad_t = bad_t;
+      a.pp = dpp;
+      a.aug_kind = d.method == PTC_METHOD_BARRIER ? AUG_BARRIER
+                   : d.method == PTC_METHOD_ADMM  ? AUG_ADMM
+                                                  : d.aug;
+      a.opt.method = d.method;
+      a.opt.alpha0 = d.alpha0;
+      a.opt.nu0 = d.nu0;
+      a.opt.inner_tol = d.inner_tol;
+      a.opt.max_iters = d.max_iters;
+      a.opt.mu0 = d.method == PTC_METHOD_BARRIER ? d.mu0 : d.aug_mu;
+      a.opt.zeta = d.zeta;
+      a.opt.mu_tol = d.mu_tol;
+      a.opt.rho = d.rho;
+      a.opt.residual_tol = d.residual_tol;
+      a.opt.max_outer = d.max_outer;
+      a.opt.keep_round_controls = d.keep_round_controls;
+      self->hp.lin_A = linA;
+      self->hp.lin_Bm = linB;
+      self->hp.lin_c = linc;
+      // LQR args view the solver's expansion
+      l.P = a.P; l.Rm = a.Rm; l.M = a.M; l.d = a.d; l.Fx = a.Fx; l.Fu = a.Fu; l.PT = a.PT;
+      l.alpha = a.alpha;
+      l.status = a.status;
+      l.flags = a.flags;
+      l.S = nullptr;
+      l.s = nullptr;
+      self->na = a;
+      self->la = l;
+      auto reg = [&](const char* n, void* p, int64_t numel, int32_t es) {
+        self->bufs[n] = Buf{p, numel, es};
+      };
+      const int rs = sizeof(R);
+      reg("states", a.X, a.xsz, rs);
+      reg("controls", a.U, a.usz, rs);
+      reg("lam", a.lam, nx * (T + 1) * B, rs);
+      reg("P", a.P, nx * nx * T * B, rs);
+      reg("R", a.Rm, nu * nu * T * B, rs);
+      reg("M", a.M, nx * nu * T * B, rs);
+      reg("d", a.d, nu * T * B, rs);
+      reg("Fx", a.Fx, nx * nx * T * B, rs);
+      reg("Fu", a.Fu, nx * nu * T * B, rs);
+      reg("PT", a.PT, nx * nx * B, rs);
+      if (S) {
+        reg("S", S, nx * nx * (T + 1) * B, rs);
+        reg("s", s, nx * (T + 1) * B, rs);
+      }
+      reg("Gamma", l.Gam, nu * nx * T * B, rs);
+      reg("gamma", l.gam, nu * T * B, rs);
+      reg("dx", l.dX, nx * (T + 1) * B, rs);
+      reg("du", l.dU, nu * T * B, rs);
+      if (a.z) {
+        reg("z", a.z, W * T * B, rs);
+        reg("v", a.v, W * T * B, rs);
+      }
+      reg("status", a.status, B, 4);
+      reg("phase", a.phase, B, 4);
+      reg("iters", a.iters, B, 4);
+      reg("term", a.term, B, 4);
+      reg("round", a.round, B, 4);
+      reg("hist_len", a.hist_len, B, 4);
+      reg("bad_index", a.bad_index, B, 4);
+      reg("flags", a.flags, B, 4);
+      reg("parity", a.parity, B, 4);
+      reg("hist", a.hist, (int64_t)a.opt.hist_cap * 5 * B, 8);
+      reg("cur_cost", a.cur_cost, B, 8);
+      reg("alpha", a.alpha, B, 8);
+      reg("mu", a.mu, B, 8);
+      reg("round_mu", a.round_mu, rc * B, 8);
+      reg("round_cost", a.round_cost, rc * B, 8);
+      reg("round_rp", a.round_rp, rc * B, 8);
+      reg("round_rd", a.round_rd, rc * B, 8);
+      reg("round_iters", a.round_iters, rc * B, 4);
+      reg("round_term", a.round_term, rc * B, 4);
+      if (a.round_U) reg("round_controls", a.round_U, rc * nu * T * B, rs);
+    }
+    return c.off + 256;
+  }
+
+  int init(const ptc_problem_desc& d, void* ws, int64_t bytes) {
+    desc = d;
+    nx = d.nx;
+    nu = d.nu;
+    ops = nullptr;
+    auto it = newton_registry().find(NewtonKey(dtype_code<R>(), d.model, d.nx, d.nu));
+    if (it == newton_registry().end())
+      return fail(PTC_ERR_UNSUPPORTED, "solver kernels not instantiated for model " +
+                                           std::to_string(d.model) + " nx=" + std::to_string(d.nx) +
+                                           " nu=" + std::to_string(d.nu));
+    ops = &it->second;
+    Carver c{(char*)ws};
+    size_t need = layout(d, c, this);
+    if ((int64_t)need > bytes) return fail(PTC_ERR_WORKSPACE, "solver workspace too small");
+    if (d.model == PTC_DYN_LINEAR) {
+      const size_t lt = hp.lin_T, lb = hp.lin_B;
+      if (!d.lin_a || !d.lin_b) return fail(PTC_ERR_ARG, "linear model needs lin_a and lin_b");
+      PTC_CUDA(cudaMemcpy((void*)hp.lin_A, d.lin_a, sizeof(R) * nx * nx * lt * lb, cudaMemcpyHostToDevice));
+      PTC_CUDA(cudaMemcpy((void*)hp.lin_Bm, d.lin_b, sizeof(R) * nx * nu * lt * lb, cudaMemcpyHostToDevice));
+      if (d.lin_c)
+        PTC_CUDA(cudaMemcpy((void*)hp.lin_c, d.lin_c, sizeof(R) * nx * lt * lb, cudaMemcpyHostToDevice));
+      else
+        PTC_CUDA(cudaMemset((void*)hp.lin_c, 0, sizeof(R) * nx * lt * lb));
+    }
+    PTC_CUDA(cudaMemcpy((void*)na.pp, &hp, sizeof(ProblemParams), cudaMemcpyHostToDevice));
+    return PTC_OK;
+  }
+
+  int load(const void* X, const void* U, const void* z, const void* v, int on_dev,
+           cudaStream_t s) override {
+    auto kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    PTC_CUDA(cudaMemcpyAsync(na.X, X, sizeof(R) * na.xsz, kind, s));
+    PTC_CUDA(cudaMemcpyAsync(na.U, U, sizeof(R) * na.usz, kind, s));
+    ops->init(&na, s);
+    if (desc.method == PTC_METHOD_NEWTON && na.aug_kind == AUG_ADMM) {
+      const size_t n = sizeof(R) * (size_t)std::max(W, 1) * na.T * na.B;
+      if (z) PTC_CUDA(cudaMemcpyAsync(na.z, z, n, kind, s));
+      else PTC_CUDA(cudaMemsetAsync(na.z, 0, n, s));
+      if (v) PTC_CUDA(cudaMemcpyAsync(na.v, v, n, kind, s));
+      else PTC_CUDA(cudaMemsetAsync(na.v, 0, n, s));
+    }
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+
+  int check(int32_t* bad, cudaStream_t s) override {
+    std::vector<int> init(na.B, 0x7fffffff);
+    PTC_CUDA(cudaMemcpyAsync(bad_t, init.data(), sizeof(int) * na.B, cudaMemcpyHostToDevice, s));
+    ops->check(&na, bad_t, s);
+    PTC_CUDA(cudaMemcpyAsync(bad, bad_t, sizeof(int) * na.B, cudaMemcpyDeviceToHost, s));
+    PTC_CUDA(cudaStreamSynchronize(s));
+    for (int b = 0; b < na.B; ++b)
+      if (bad[b] == 0x7fffffff) bad[b] = -1;
+    return PTC_OK;
+  }
+
+  int iterate(int n, cudaStream_t s) override {
+    for (int i = 0; i < n; ++i) ops->iterate(&na, &la, s);
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+
+  int running(int32_t* n, cudaStream_t s) override {
+    PTC_CUDA(cudaMemcpyAsync(n, na.n_running, sizeof(int), cudaMemcpyDeviceToHost, s));
+    PTC_CUDA(cudaStreamSynchronize(s));
+    return PTC_OK;
+  }
+
+  int expand(cudaStream_t s) override {
+    ops->expand(&na, s);
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+
+  int lqr(const double* alpha_host, cudaStream_t s) override {
+    if (alpha_host)
+      PTC_CUDA(cudaMemcpyAsync(na.alpha, alpha_host, sizeof(double) * na.B, cudaMemcpyHostToDevice, s));
+    PTC_CUDA(cudaMemsetAsync(na.flags, 0, sizeof(int) * na.B, s));
+    LqrArgs<R> l = la;
+    l.status = nullptr;
+    l.S = S;
+    l.s = s_;
+    ops->lqr(&l, s);
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+
+  int rollout(cudaStream_t s) override {
+    PTC_CUDA(cudaMemsetAsync(na.bad_index, 0xff, sizeof(int) * na.B, s));
+    ops->rollout(&na, s);
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+
+  int total_cost(cudaStream_t s) override {
+    ops->cost(&na, s);
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+
+  int info(const char* name, int64_t* numel, int32_t* es) override {
+    auto it = bufs.find(name);
+    if (it == bufs.end()) return fail(PTC_ERR_ARG, std::string("unknown buffer ") + name);
+    if (numel) *numel = it->second.numel;
+    if (es) *es = it->second.es;
+    return PTC_OK;
+  }
+
+  int read(const char* name, void* dst, int64_t bytes, int on_dev, cudaStream_t s) override {
+    auto it = bufs.find(name);
+    if (it == bufs.end()) return fail(PTC_ERR_ARG, std::string("unknown buffer ") + name);
+    const Buf& bf = it->second;
+    if (bytes < bf.numel * bf.es) return fail(PTC_ERR_ARG, "destination too small");
+    if (!strcmp(name, "states") || !strcmp(name, "controls")) {
+      const long long n = (long long)na.B * (na.T + 1);
+      k_normalize_parity<R><<<grid_for(n), kBlock, 0, s>>>(na, nx, nu);
+      k_clear_parity<R><<<grid_for(na.B), kBlock, 0, s>>>(na);
+    }
+    PTC_CUDA(cudaMemcpyAsync(dst, bf.p, bf.numel * bf.es,
+                             on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    if (!on_dev) PTC_CUDA(cudaStreamSynchronize(s));
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+};
+
+}  // namespace ptc
+
+extern "C" {
+
+static int validate(const ptc_problem_desc* d) {
+  if (!d) return fail(PTC_ERR_ARG, "desc is NULL");
+  if (d->dtype != PTC_F32 && d->dtype != PTC_F64) return fail(PTC_ERR_ARG, "bad dtype");
+  if (d->batch < 1 || d->horizon < 1 || d->nx < 1 || d->nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  if (d->nx > kMaxNX || d->nu > kMaxNU) return fail(PTC_ERR_ARG, "nx <= 12 and nu <= 6 required");
+  if (d->method < 0 || d->method > 2) return fail(PTC_ERR_ARG, "bad method");
+  if (d->model == PTC_DYN_LINEAR) {
+    if (d->lin_rows != 1 && d->lin_rows != d->horizon) return fail(PTC_ERR_ARG, "lin_rows must be 1 or horizon");
+    if (d->lin_batch != 1 && d->lin_batch != d->batch) return fail(PTC_ERR_ARG, "lin_batch must be 1 or batch");
+  }
+  return PTC_OK;
+}
+
+int64_t ptc_solver_workspace_bytes(const ptc_problem_desc* d) {
+  int rc = validate(d);
+  if (rc) return rc;
+  Carver c{nullptr};
+  if (d->dtype == PTC_F64) return (int64_t)Solver<double>::layout(*d, c, nullptr);
+  return (int64_t)Solver<float>::layout(*d, c, nullptr);
+}
+
+int ptc_solver_create(const ptc_problem_desc* d, void* ws, int64_t bytes, ptc_solver** out) {
+  int rc = validate(d);
+  if (rc) return rc;
+  if (!out) return fail(PTC_ERR_ARG, "out is NULL");
+  std::unique_ptr<ptc_solver> s;
+  if (d->dtype == PTC_F64) {
+    auto* p = new Solver<double>();
+    s.reset(p);
+    rc = p->init(*d, ws, bytes);
+  } else {
+    auto* p = new Solver<float>();
+    s.reset(p);
+    rc = p->init(*d, ws, bytes);
+  }
+  if (rc) return rc;
+  *out = s.release();
+  return PTC_OK;
+}
+
+int ptc_solver_destroy(ptc_solver* s) {
+  delete s;
+  return PTC_OK;
+}
+
+#define PTC_S(s) if (!(s)) return fail(PTC_ERR_ARG, "solver is NULL")
+
+int ptc_solver_load(ptc_solver* s, const void* X, const void* U, const void* z, const void* v,
+                    int on_device, void* stream) {
+  PTC_S(s);
+  return s->load(X, U, z, v, on_device, (cudaStream_t)stream);
+}
+int ptc_solver_check_consistency(ptc_solver* s, int32_t* bad, void* stream) {
+  PTC_S(s);
+  return s->check(bad, (cudaStream_t)stream);
+}
+int ptc_solver_iterate(ptc_solver* s, int n, void* stream) {
+  PTC_S(s);
+  return s->iterate(n, (cudaStream_t)stream);
+}
+int ptc_solver_running(ptc_solver* s, int32_t* n, void* stream) {
+  PTC_S(s);
+  return s->running(n, (cudaStream_t)stream);
+}
+int ptc_solver_expand(ptc_solver* s, void* stream) {
+  PTC_S(s);
+  return s->expand((cudaStream_t)stream);
+}
+int ptc_solver_lqr(ptc_solver* s, const double* alpha_host, void* stream) {
+  PTC_S(s);
+  return s->lqr(alpha_host, (cudaStream_t)stream);
+}
+int ptc_solver_rollout(ptc_solver* s, void* stream) {
+  PTC_S(s);
+  return s->rollout((cudaStream_t)stream);
+}
+int ptc_solver_total_cost(ptc_solver* s, void* stream) {
+  PTC_S(s);
+  return s->total_cost((cudaStream_t)stream);
+}
+int ptc_solver_buffer_info(ptc_solver* s, const char* name, int64_t* numel, int32_t* es) {
+  PTC_S(s);
+  return s->info(name, numel, es);
+}
+int ptc_solver_read(ptc_solver* s, const char* name, void* dst, int64_t bytes, int on_dev,
+                    void* stream) {
+  PTC_S(s);
+  return s->read(name, dst, bytes, on_dev, (cudaStream_t)stream);
+}
+
+}  // extern "C"

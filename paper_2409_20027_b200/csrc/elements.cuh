@@ -1,0 +1,404 @@
+// Scan elements of the three Newton passes and their associative operators.
+//
+//  * value elements (A, Y, C, eta, b): dual form of a conditional value
+//    function (reference passes.py:38-46, element init 244-261, combine
+//    264-288).  `vcombine` is the general operator used on tree interior
+//    nodes; `vstep` is the same operator specialised to a right operand with
+//    A = C = b = 0 -- every suffix that contains the terminal element has
+//    that shape, so all down-sweep work is this cheap Riccati-like step.
+//  * affine maps (F, e): x -> F x + e.  Propagation (passes.py:330-361) and
+//    linear rollout compose them forwards; the co-state suffix
+//    (passes.py:113-148) composes them backwards with F = fx^T.
+#pragma once
+
+#include "linalg.cuh"
+
+namespace ptc {
+
+// ---------------------------------------------------------------------------
+// SoA field access: field[(c * rows + t) * B + b]
+// ---------------------------------------------------------------------------
+
+template <typename R>
+PTC_D R ldf(const R* __restrict__ f, int c, int t, int rows, int B, int b) {
+  return __ldg(f + ((size_t)c * rows + t) * B + b);
+}
+
+template <typename R>
+PTC_D void stf(R* __restrict__ f, int c, int t, int rows, int B, int b, R v) {
+  f[((size_t)c * rows + t) * B + b] = v;
+}
+
+template <int M, int N, typename R>
+PTC_D void ld_mat(const R* f, int t, int rows, int B, int b, R (&A)[M][N], int c0 = 0) {
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) A[i][j] = ldf(f, c0 + i * N + j, t, rows, B, b);
+}
+
+template <int N, typename R>
+PTC_D void ld_vec(const R* f, int t, int rows, int B, int b, R (&a)[N], int c0 = 0) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = ldf(f, c0 + i, t, rows, B, b);
+}
+
+template <int M, int N, typename R>
+PTC_D void st_mat(R* f, int t, int rows, int B, int b, const R (&A)[M][N], int c0 = 0) {
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) stf(f, c0 + i * N + j, t, rows, B, b, A[i][j]);
+}
+
+template <int N, typename R>
+PTC_D void st_vec(R* f, int t, int rows, int B, int b, const R (&a)[N], int c0 = 0) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) stf(f, c0 + i, t, rows, B, b, a[i]);
+}
+
+// ---------------------------------------------------------------------------
+// value elements
+// ---------------------------------------------------------------------------
+
+template <typename R, int NX>
+struct VElem {
+  R A[NX][NX], Y[NX][NX], C[NX][NX], eta[NX], b[NX];
+  static constexpr int kComp = 3 * NX * NX + 2 * NX;
+};
+
+template <typename R, int NX>
+struct VCarry {  // value function of a suffix containing the terminal
+  R Y[NX][NX], eta[NX];
+  static constexpr int kComp = NX * NX + NX;
+};
+
+template <typename R, int NX>
+PTC_D void ld_velem(const R* f, int t, int rows, int B, int b, VElem<R, NX>& e) {
+  ld_mat(f, t, rows, B, b, e.A, 0);
+  ld_mat(f, t, rows, B, b, e.Y, NX * NX);
+  ld_mat(f, t, rows, B, b, e.C, 2 * NX * NX);
+  ld_vec(f, t, rows, B, b, e.eta, 3 * NX * NX);
+  ld_vec(f, t, rows, B, b, e.b, 3 * NX * NX + NX);
+}
+
+template <typename R, int NX>
+PTC_D void st_velem(R* f, int t, int rows, int B, int b, const VElem<R, NX>& e) {
+  st_mat(f, t, rows, B, b, e.A, 0);
+  st_mat(f, t, rows, B, b, e.Y, NX * NX);
+  st_mat(f, t, rows, B, b, e.C, 2 * NX * NX);
+  st_vec(f, t, rows, B, b, e.eta, 3 * NX * NX);
+  st_vec(f, t, rows, B, b, e.b, 3 * NX * NX + NX);
+}
+
+template <typename R, int NX>
+PTC_D void ld_vcarry(const R* f, int t, int rows, int B, int b, VCarry<R, NX>& c) {
+  ld_mat(f, t, rows, B, b, c.Y, 0);
+  ld_vec(f, t, rows, B, b, c.eta, NX * NX);
+}
+
+template <typename R, int NX>
+PTC_D void st_vcarry(R* f, int t, int rows, int B, int b, const VCarry<R, NX>& c) {
+  st_mat(f, t, rows, B, b, c.Y, 0);
+  st_vec(f, t, rows, B, b, c.eta, NX * NX);
+}
+
+template <typename R, int NX>
+PTC_D void vcarry_zero(VCarry<R, NX>& c) {
+  set_zero(c.Y);
+  set_zero(c.eta);
+}
+
+// Per-stage expansion data entering the subproblem (reference passes.py:62-97)
+template <typename R, int NX, int NU>
+struct Stage {
+  R P[NX][NX], Rr[NU][NU], M[NX][NU], d[NU], Fx[NX][NX], Fu[NX][NU];
+};
+
+template <typename R, int NX, int NU>
+PTC_D void ld_stage(const R* P, const R* Rm, const R* M, const R* d, const R* Fx, const R* Fu,
+                    int t, int T, int B, int b, R alpha, Stage<R, NX, NU>& s) {
+  ld_mat(P, t, T, B, b, s.P);
+  ld_mat(Rm, t, T, B, b, s.Rr);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) s.Rr[i][i] += alpha;
+  ld_mat(M, t, T, B, b, s.M);
+  ld_vec(d, t, T, B, b, s.d);
+  ld_mat(Fx, t, T, B, b, s.Fx);
+  ld_mat(Fu, t, T, B, b, s.Fu);
+}
+
+// Dual element of one stage (reference passes.py:192-228 / 244-261):
+//   A = Fx - Fu Rr^-1 M^T,  Y = P - M Rr^-1 M^T,  C = Fu Rr^-1 Fu^T,
+//   eta = M Rr^-1 d,        b = -Fu Rr^-1 d.
+// Also returns the Cholesky factor of Rr (reused by the gains).
+template <typename R, int NX, int NU>
+PTC_D bool velem_from_stage(const Stage<R, NX, NU>& s, VElem<R, NX>& e, R (&L)[NU][NU]) {
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) L[i][j] = s.Rr[i][j];
+  bool ok = cholesky<NU>(L);
+  R RiMt[NU][NX], RiFt[NU][NX], Rid[NU];
+#pragma unroll
+  for (int i = 0; i < NU; ++i) {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      RiMt[i][j] = s.M[j][i];
+      RiFt[i][j] = s.Fu[j][i];
+    }
+    Rid[i] = s.d[i];
+  }
+  chol_solve<NU, NX>(L, RiMt);
+  chol_solve<NU, NX>(L, RiFt);
+  chol_solve_vec<NU>(L, Rid);
+  R tmp[NX][NX];
+  mm<NX, NU, NX>(s.Fu, RiMt, tmp);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) e.A[i][j] = s.Fx[i][j] - tmp[i][j];
+  mm<NX, NU, NX>(s.M, RiMt, tmp);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) e.Y[i][j] = s.P[i][j] - tmp[i][j];
+  symmetrize<NX>(e.Y);
+  mm<NX, NU, NX>(s.Fu, RiFt, e.C);
+  symmetrize<NX>(e.C);
+  mv<NX, NU>(s.M, Rid, e.eta);
+  mv<NX, NU>(s.Fu, Rid, e.b);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e.b[i] = -e.b[i];
+  return ok;
+}
+
+template <typename R, int NX>
+PTC_D void velem_terminal(const R (&PT)[NX][NX], VElem<R, NX>& e) {
+  set_zero(e.A);
+  set_zero(e.C);
+  set_zero(e.eta);
+  set_zero(e.b);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) e.Y[i][j] = PT[i][j];
+}
+
+// General combine  out = l (earlier) (x) r (later)  (reference passes.py:264-288)
+//   G = I + C_l Y_r
+//   X = G^-1 [A_l | C_l | b_l + C_l eta_r],   Z = G^-T [Y_r A_l | eta_r - Y_r b_l]
+//   A = A_r X1,  Y = sym(A_l^T Z1 + Y_l),  C = sym(A_r X2 A_r^T + C_r),
+//   eta = A_l^T z + eta_l,  b = A_r x + b_r
+template <typename R, int NX>
+PTC_D bool vcombine(const VElem<R, NX>& l, const VElem<R, NX>& r, VElem<R, NX>& o) {
+  R G[NX][NX];
+  mm<NX, NX, NX>(l.C, r.Y, G);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) G[i][i] += R(1);
+  int piv[NX];
+  bool ok = lu_factor<NX>(G, piv);
+  // right-hand sides of the transposed solve
+  R Z[NX][NX + 1];
+  {
+    R YA[NX][NX];
+    mm<NX, NX, NX>(r.Y, l.A, YA);
+    R Yb[NX];
+    mv<NX, NX>(r.Y, l.b, Yb);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) Z[i][j] = YA[i][j];
+      Z[i][NX] = r.eta[i] - Yb[i];
+    }
+  }
+  lu_solve_t<NX, NX + 1>(G, piv, Z);
+  // Y and eta (need only l and Z)
+  {
+    R Zs[NX][NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int j = 0; j < NX; ++j) Zs[i][j] = Z[i][j];
+    mtm<NX, NX, NX>(l.A, Zs, o.Y);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int j = 0; j < NX; ++j) o.Y[i][j] += l.Y[i][j];
+    symmetrize<NX>(o.Y);
+    R z[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) z[i] = Z[i][NX];
+    mtv<NX, NX>(l.A, z, o.eta);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) o.eta[i] += l.eta[i];
+  }
+  // forward solve X = G^-1 [A_l | C_l | b_l + C_l eta_r]
+  R X[NX][2 * NX + 1];
+  {
+    R Ce[NX];
+    mv<NX, NX>(l.C, r.eta, Ce);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        X[i][j] = l.A[i][j];
+        X[i][NX + j] = l.C[i][j];
+      }
+      X[i][2 * NX] = l.b[i] + Ce[i];
+    }
+  }
+  lu_solve<NX, 2 * NX + 1>(G, piv, X);
+  {
+    R X1[NX][NX], X2[NX][NX], x[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        X1[i][j] = X[i][j];
+        X2[i][j] = X[i][NX + j];
+      }
+      x[i] = X[i][2 * NX];
+    }
+    mm<NX, NX, NX>(r.A, X1, o.A);
+    R T2[NX][NX];
+    mm<NX, NX, NX>(r.A, X2, T2);
+    mmt<NX, NX, NX>(T2, r.A, o.C);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int j = 0; j < NX; ++j) o.C[i][j] += r.C[i][j];
+    symmetrize<NX>(o.C);
+    mv<NX, NX>(r.A, x, o.b);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) o.b[i] += r.b[i];
+  }
+  return ok;
+}
+
+// Specialised combine  carry' = e (x) carry  for a carry with A = C = b = 0:
+//   (I + Y_c C_e) Z = [Y_c A_e | eta_c - Y_c b_e]
+//   Y' = sym(A_e^T Z1 + Y_e),  eta' = A_e^T z + eta_e
+template <typename R, int NX>
+PTC_D bool vstep(const VElem<R, NX>& e, const VCarry<R, NX>& c, VCarry<R, NX>& o) {
+  R G[NX][NX];
+  mm<NX, NX, NX>(c.Y, e.C, G);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) G[i][i] += R(1);
+  int piv[NX];
+  bool ok = lu_factor<NX>(G, piv);
+  R Z[NX][NX + 1];
+  {
+    R YA[NX][NX];
+    mm<NX, NX, NX>(c.Y, e.A, YA);
+    R Yb[NX];
+    mv<NX, NX>(c.Y, e.b, Yb);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) Z[i][j] = YA[i][j];
+      Z[i][NX] = c.eta[i] - Yb[i];
+    }
+  }
+  lu_solve<NX, NX + 1>(G, piv, Z);
+  R Zs[NX][NX], z[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Zs[i][j] = Z[i][j];
+    z[i] = Z[i][NX];
+  }
+  mtm<NX, NX, NX>(e.A, Zs, o.Y);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) o.Y[i][j] += e.Y[i][j];
+  symmetrize<NX>(o.Y);
+  mtv<NX, NX>(e.A, z, o.eta);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) o.eta[i] += e.eta[i];
+  return ok;
+}
+
+// Feedback gains at stage t from the cost-to-go (S, s = -eta) of stage t+1
+// (reference passes.py:316-323):
+//   Q = sym(Rr + Fu^T S Fu),  Gamma = -Q^-1 (M^T + Fu^T S Fx),
+//   gamma = -Q^-1 (d + Fu^T s)
+template <typename R, int NX, int NU>
+PTC_D bool gains(const Stage<R, NX, NU>& s, const VCarry<R, NX>& next, R (&Gam)[NU][NX],
+                 R (&gam)[NU]) {
+  R FtS[NU][NX];
+  mtm<NU, NX, NX>(s.Fu, next.Y, FtS);
+  R Q[NU][NU];
+  mm<NU, NX, NU>(FtS, s.Fu, Q);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) Q[i][j] += s.Rr[i][j];
+  symmetrize<NU>(Q);
+  bool ok = cholesky<NU>(Q);
+  mm<NU, NX, NX>(FtS, s.Fx, Gam);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Gam[i][j] += s.M[j][i];
+  R Fe[NU];
+  mtv<NU, NX>(s.Fu, next.eta, Fe);  // Fu^T eta = -Fu^T s
+#pragma unroll
+  for (int i = 0; i < NU; ++i) gam[i] = s.d[i] - Fe[i];
+  chol_solve<NU, NX>(Q, Gam);
+  chol_solve_vec<NU>(Q, gam);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Gam[i][j] = -Gam[i][j];
+    gam[i] = -gam[i];
+  }
+  return ok;
+}
+
+// ---------------------------------------------------------------------------
+// affine maps
+// ---------------------------------------------------------------------------
+
+template <typename R, int NX>
+struct Aff {
+  R F[NX][NX], e[NX];
+  static constexpr int kComp = NX * NX + NX;
+};
+
+template <typename R, int NX>
+PTC_D void aff_identity(Aff<R, NX>& a) {
+  set_identity(a.F);
+  set_zero(a.e);
+}
+
+// o = outer o inner  (apply inner first):  F = F_o F_i,  e = F_o e_i + e_o
+template <typename R, int NX>
+PTC_D void aff_compose(const Aff<R, NX>& outer, const Aff<R, NX>& inner, Aff<R, NX>& o) {
+  mm<NX, NX, NX>(outer.F, inner.F, o.F);
+  mv<NX, NX>(outer.F, inner.e, o.e);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) o.e[i] += outer.e[i];
+}
+
+template <typename R, int NX>
+PTC_D void aff_apply(const Aff<R, NX>& a, const R (&x)[NX], R (&y)[NX]) {
+  mv<NX, NX>(a.F, x, y);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) y[i] += a.e[i];
+}
+
+template <typename R, int NX>
+PTC_D void ld_aff(const R* f, int t, int rows, int B, int b, Aff<R, NX>& a) {
+  ld_mat(f, t, rows, B, b, a.F, 0);
+  ld_vec(f, t, rows, B, b, a.e, NX * NX);
+}
+
+template <typename R, int NX>
+PTC_D void st_aff(R* f, int t, int rows, int B, int b, const Aff<R, NX>& a) {
+  st_mat(f, t, rows, B, b, a.F, 0);
+  st_vec(f, t, rows, B, b, a.e, NX * NX);
+}
+
+}  // namespace ptc

@@ -1,0 +1,202 @@
+// Host-side launch sequences (one per pass / per Newton iteration) and the
+// registry that maps (dtype, model, nx, nu) to instantiated sequences.
+#pragma once
+
+#include <map>
+#include <tuple>
+
+#include "newton_kernels.cuh"
+
+namespace ptc {
+
+constexpr int kBlock = 128;
+
+inline dim3 grid_for(long long n) { return dim3((unsigned)((n + kBlock - 1) / kBlock)); }
+
+template <typename R, int NX, int NU>
+void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
+  const Plan& pl = a.plan;
+  const long long B = a.B, P0 = pl.units0();
+  if (pl.L >= 1) {
+    k_value_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) k_value_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    k_value_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+    for (int l = pl.L - 1; l >= 1; --l)
+      k_value_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+  }
+  k_value_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  if (pl.L >= 1) {
+    for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    k_prop_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+    for (int l = pl.L - 1; l >= 1; --l)
+      k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+  }
+  k_prop_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+}
+
+template <typename R, int NX, int NU>
+void launch_prop(const LqrArgs<R>& a, cudaStream_t s) {
+  const Plan& pl = a.plan;
+  const long long B = a.B, P0 = pl.units0();
+  if (pl.L >= 1) {
+    k_prop_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    k_prop_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+    for (int l = pl.L - 1; l >= 1; --l)
+      k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+  }
+  k_prop_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+}
+
+template <typename R, class Dyn>
+void launch_costate(const NewtonArgs<R>& a, cudaStream_t s) {
+  constexpr int NX = Dyn::NX;
+  const Plan& pl = a.plan;
+  const long long B = a.B, P0 = pl.units0();
+  if (pl.L >= 1) {
+    k_costate_up0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) k_costate_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    k_costate_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+    for (int l = pl.L - 1; l >= 1; --l)
+      k_costate_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+  }
+  k_costate_down0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+}
+
+template <typename R, class Dyn>
+void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaStream_t s) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const long long B = a.B, P0 = a.plan.units0();
+  cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
+  k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
+  launch_costate<R, Dyn>(a, s);
+  launch_lqr<R, NX, NU>(la, s);
+  k_rollout<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
+  k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+  k_control<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+  k_round_end<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  k_outer<R><<<grid_for(B), kBlock, 0, s>>>(a);
+}
+
+// in-place rollout of buffer 0 from its x_0 (problem.py:449 `rollout`)
+template <typename R, class Dyn>
+__global__ void k_rollout_inplace(NewtonArgs<R> a) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int b = unit_id();
+  if (b >= a.B) return;
+  R x[NX];
+  ld_x(a, 0, 0, b, x);
+  bool finite = true;
+  for (int t = 0; t < a.T; ++t) {
+    R u[NU], xn[NX];
+    ld_u(a, 0, t, b, u);
+    Dyn::step(*a.pp, t, b, x, u, xn);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      if (finite && !isfinite(xn[i])) { finite = false; a.bad_index[b] = t + 1; }
+      x[i] = xn[i];
+    }
+    st_vec(a.X, t + 1, a.T + 1, a.B, b, x);
+  }
+}
+
+// total_cost of buffer parity[b] (problem.py:476), result in cur_cost[b],
+// first infeasible (stage * W + row) in bad_index[b]
+template <typename R, int NX>
+__global__ void k_cost_finalize(NewtonArgs<R> a) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  int bad;
+  a.cur_cost[b] = finalize_cost<R, NX>(a, 0, a.parity[b], b, bad);
+  a.bad_index[b] = bad;
+}
+
+template <typename R>
+__global__ void k_force_phase(NewtonArgs<R> a, int ph) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  a.status[b] = ST_RUNNING;
+  a.phase[b] = ph;
+}
+
+// ---------------------------------------------------------------------------
+// registry
+// ---------------------------------------------------------------------------
+
+struct LqrOps {
+  void (*solve)(const void* args, cudaStream_t s);
+  void (*propagate)(const void* args, cudaStream_t s);
+};
+
+struct NewtonOps {
+  void (*lqr)(const void* la, cudaStream_t s);
+  void (*init)(const void* na, cudaStream_t s);
+  void (*check)(const void* na, int* bad_t, cudaStream_t s);
+  void (*iterate)(const void* na, const void* la, cudaStream_t s);
+  void (*expand)(const void* na, cudaStream_t s);
+  void (*rollout)(const void* na, cudaStream_t s);
+  void (*cost)(const void* na, cudaStream_t s);
+};
+
+using LqrKey = std::tuple<int, int, int>;            // dtype, nx, nu
+using NewtonKey = std::tuple<int, int, int, int>;    // dtype, dyn, nx, nu
+
+std::map<LqrKey, LqrOps>& lqr_registry();
+std::map<NewtonKey, NewtonOps>& newton_registry();
+
+template <typename R>
+constexpr int dtype_code() { return sizeof(R) == 8 ? 1 : 0; }
+
+template <typename R, int NX, int NU>
+struct RegisterLqr {
+  static void solve(const void* a, cudaStream_t s) {
+    launch_lqr<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
+  }
+  static void propagate(const void* a, cudaStream_t s) {
+    launch_prop<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
+  }
+  RegisterLqr() { lqr_registry()[LqrKey(dtype_code<R>(), NX, NU)] = LqrOps{&solve, &propagate}; }
+};
+
+template <typename R, class Dyn, int DYN>
+struct RegisterNewton {
+  static constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  static const NewtonArgs<R>& A(const void* p) { return *static_cast<const NewtonArgs<R>*>(p); }
+  static void lqr(const void* la, cudaStream_t s) {
+    launch_lqr<R, NX, NU>(*static_cast<const LqrArgs<R>*>(la), s);
+  }
+  static void init(const void* p, cudaStream_t s) {
+    const NewtonArgs<R>& a = A(p);
+    k_init_state<R><<<grid_for(a.B), kBlock, 0, s>>>(a);
+    if (a.opt.method == METHOD_ADMM)
+      k_admm_init<R, NX, NU><<<grid_for((long long)a.T * a.B), kBlock, 0, s>>>(a);
+  }
+  static void check(const void* p, int* bad_t, cudaStream_t s) {
+    const NewtonArgs<R>& a = A(p);
+    k_check_consistent<R, Dyn><<<grid_for((long long)a.T * a.B), kBlock, 0, s>>>(a, bad_t);
+  }
+  static void iterate(const void* p, const void* la, cudaStream_t s) {
+    launch_newton_iteration<R, Dyn>(A(p), *static_cast<const LqrArgs<R>*>(la), s);
+  }
+  static void expand(const void* p, cudaStream_t s) {
+    const NewtonArgs<R>& a = A(p);
+    k_force_phase<R><<<grid_for(a.B), kBlock, 0, s>>>(a, PH_NEED_EXP);
+    launch_costate<R, Dyn>(a, s);
+  }
+  static void rollout(const void* p, cudaStream_t s) {
+    const NewtonArgs<R>& a = A(p);
+    k_rollout_inplace<R, Dyn><<<grid_for(a.B), kBlock, 0, s>>>(a);
+  }
+  static void cost(const void* p, cudaStream_t s) {
+    const NewtonArgs<R>& a = A(p);
+    k_force_phase<R><<<grid_for(a.B), kBlock, 0, s>>>(a, PH_NEED_COST);
+    k_cost_partials<R, NX, NU><<<grid_for((long long)a.plan.units0() * a.B), kBlock, 0, s>>>(a, 0);
+    k_cost_finalize<R, NX><<<grid_for(a.B), kBlock, 0, s>>>(a);
+  }
+  RegisterNewton() {
+    newton_registry()[NewtonKey(dtype_code<R>(), DYN, NX, NU)] =
+        NewtonOps{&lqr, &init, &check, &iterate, &expand, &rollout, &cost};
+  }
+};
+
+}  // namespace ptc

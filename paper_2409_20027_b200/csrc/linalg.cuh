@@ -1,0 +1,275 @@
+// Fixed-size dense linear algebra in registers (compile-time shapes, fully
+// unrolled).  Everything a value-function combine needs: products,
+// Cholesky (with the LAPACK potrf failure rule), LU with partial pivoting
+// applied by predicated row swaps so no register array is ever indexed
+// dynamically, and solves with the matrix or its transpose.
+#pragma once
+
+#include "common.cuh"
+
+namespace ptc {
+
+// C = A * B  (A: MxK, B: KxN)
+template <int M, int K, int N, typename R>
+PTC_D void mm(const R (&A)[M][K], const R (&B)[K][N], R (&C)[M][N]) {
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R acc = A[i][0] * B[0][j];
+#pragma unroll
+      for (int k = 1; k < K; ++k) acc = fma(A[i][k], B[k][j], acc);
+      C[i][j] = acc;
+    }
+}
+
+// C = A^T * B  (A: KxM, B: KxN)
+template <int M, int K, int N, typename R>
+PTC_D void mtm(const R (&A)[K][M], const R (&B)[K][N], R (&C)[M][N]) {
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R acc = A[0][i] * B[0][j];
+#pragma unroll
+      for (int k = 1; k < K; ++k) acc = fma(A[k][i], B[k][j], acc);
+      C[i][j] = acc;
+    }
+}
+
+// C = A * B^T  (A: MxK, B: NxK)
+template <int M, int K, int N, typename R>
+PTC_D void mmt(const R (&A)[M][K], const R (&B)[N][K], R (&C)[M][N]) {
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R acc = A[i][0] * B[j][0];
+#pragma unroll
+      for (int k = 1; k < K; ++k) acc = fma(A[i][k], B[j][k], acc);
+      C[i][j] = acc;
+    }
+}
+
+// y = A x
+template <int M, int K, typename R>
+PTC_D void mv(const R (&A)[M][K], const R (&x)[K], R (&y)[M]) {
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    R acc = A[i][0] * x[0];
+#pragma unroll
+    for (int k = 1; k < K; ++k) acc = fma(A[i][k], x[k], acc);
+    y[i] = acc;
+  }
+}
+
+// y = A^T x  (A: KxM)
+template <int M, int K, typename R>
+PTC_D void mtv(const R (&A)[K][M], const R (&x)[K], R (&y)[M]) {
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    R acc = A[0][i] * x[0];
+#pragma unroll
+    for (int k = 1; k < K; ++k) acc = fma(A[k][i], x[k], acc);
+    y[i] = acc;
+  }
+}
+
+template <int N, typename R>
+PTC_D void symmetrize(R (&A)[N][N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) {
+      R v = R(0.5) * (A[i][j] + A[j][i]);
+      A[i][j] = v;
+      A[j][i] = v;
+    }
+}
+
+template <int N, typename R>
+PTC_D void set_identity(R (&A)[N][N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) A[i][j] = (i == j) ? R(1) : R(0);
+}
+
+template <int M, int N, typename R>
+PTC_D void set_zero(R (&A)[M][N]) {
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) A[i][j] = R(0);
+}
+
+template <int N, typename R>
+PTC_D void set_zero(R (&a)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = R(0);
+}
+
+// In-place lower Cholesky factor.  Fails (returns false) exactly when LAPACK
+// potrf would: a non-positive or NaN pivot.
+template <int N, typename R>
+PTC_D bool cholesky(R (&A)[N][N]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    R s = A[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) s = fma(-A[j][k], A[j][k], s);
+    ok = ok && (s > R(0));
+    R d = sqrt(s);
+    A[j][j] = d;
+    R inv = R(1) / d;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      R v = A[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v = fma(-A[i][k], A[j][k], v);
+      A[i][j] = v * inv;
+    }
+  }
+  return ok;
+}
+
+// Solve (L L^T) X = B in place, L from cholesky().
+template <int N, int M, typename R>
+PTC_D void chol_solve(const R (&L)[N][N], R (&B)[N][M]) {
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R v = B[i][c];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v = fma(-L[i][k], B[k][c], v);
+      B[i][c] = v / L[i][i];
+    }
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) {
+      R v = B[i][c];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) v = fma(-L[k][i], B[k][c], v);
+      B[i][c] = v / L[i][i];
+    }
+  }
+}
+
+template <int N, typename R>
+PTC_D void chol_solve_vec(const R (&L)[N][N], R (&b)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    R v = b[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) v = fma(-L[i][k], b[k], v);
+    b[i] = v / L[i][i];
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    R v = b[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) v = fma(-L[k][i], b[k], v);
+    b[i] = v / L[i][i];
+  }
+}
+
+// Row swap i <-> k of an N x M array, applied only when `cond` holds.  All
+// indices are compile-time after unrolling, so the arrays stay in registers.
+template <int N, int M, typename R>
+PTC_D void cswap_rows(R (&A)[N][M], int i, int k, bool cond) {
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    R a = A[i][j], b = A[k][j];
+    A[i][j] = cond ? b : a;
+    A[k][j] = cond ? a : b;
+  }
+}
+
+// LU factorisation with partial pivoting (P A = L U, unit L), LAPACK getrf
+// pivot rule (first maximal |a_ik|).  Returns false on an exactly zero pivot
+// (numpy raises LinAlgError "Singular matrix" in that case).
+template <int N, typename R>
+PTC_D bool lu_factor(R (&A)[N][N], int (&piv)[N]) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int p = k;
+    R best = fabs(A[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      R v = fabs(A[i][k]);
+      bool take = v > best;
+      best = take ? v : best;
+      p = take ? i : p;
+    }
+    piv[k] = p;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) cswap_rows<N, N>(A, i, k, p == i);
+    R pv = A[k][k];
+    ok = ok && (pv != R(0));
+    R inv = R(1) / pv;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      R l = A[i][k] * inv;
+      A[i][k] = l;
+#pragma unroll
+      for (int j = k + 1; j < N; ++j) A[i][j] = fma(-l, A[k][j], A[i][j]);
+    }
+  }
+  return ok;
+}
+
+// Solve A X = B in place given lu_factor(A).
+template <int N, int M, typename R>
+PTC_D void lu_solve(const R (&LU)[N][N], const int (&piv)[N], R (&B)[N][M]) {
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) cswap_rows<N, M>(B, i, k, piv[k] == i);
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
+      R v = B[i][c];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v = fma(-LU[i][k], B[k][c], v);
+      B[i][c] = v;
+    }
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) {
+      R v = B[i][c];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) v = fma(-LU[i][k], B[k][c], v);
+      B[i][c] = v / LU[i][i];
+    }
+  }
+}
+
+// Solve A^T X = B in place given lu_factor(A):  A^T = U^T L^T P.
+template <int N, int M, typename R>
+PTC_D void lu_solve_t(const R (&LU)[N][N], const int (&piv)[N], R (&B)[N][M]) {
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {  // U^T y = b (lower, non-unit)
+      R v = B[i][c];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v = fma(-LU[k][i], B[k][c], v);
+      B[i][c] = v / LU[i][i];
+    }
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) {  // L^T z = y (upper, unit)
+      R v = B[i][c];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) v = fma(-LU[k][i], B[k][c], v);
+      B[i][c] = v;
+    }
+  }
+#pragma unroll
+  for (int k = N - 1; k >= 0; --k)
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) cswap_rows<N, M>(B, i, k, piv[k] == i);
+}
+
+}  // namespace ptc

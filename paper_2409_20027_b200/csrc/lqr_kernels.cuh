@@ -1,0 +1,376 @@
+// LQR subproblem kernels: blocked reverse scan over value elements (Alg. 2)
+// and blocked forward scan over closed-loop affine maps (Alg. 3).
+//
+// Scan structure:
+//   up-sweep   level 0: each thread folds K0 consecutive stages into one
+//              aggregate (elements built from the expansion on the fly, so
+//              the dual elements never touch HBM);
+//              level l: each thread folds K aggregates of level l.
+//   top        one thread per problem walks the <= K top items.
+//   down-sweep level l: carries flow back down; at level 0 the carry is the
+//              cost-to-go (S_{t+1}, s_{t+1}) and the thread sweeps its chunk
+//              with the cheap specialised combine, emitting the gains and
+//              (fused) the level-1 aggregates of the propagation scan.
+// With K0 >= T (large batches) the tree vanishes and every problem is one
+// sequential sweep per pass -- the work-optimal schedule when the batch
+// alone fills the GPU.
+#pragma once
+
+#include "elements.cuh"
+
+namespace ptc {
+
+template <typename R>
+struct LqrArgs {
+  int B, T;
+  Plan plan;
+  // expansion (T rows unless noted), SoA (comp, rows, B)
+  const R *P, *Rm, *M, *d, *Fx, *Fu;
+  const R* PT;             // (nx*nx, 1, B)
+  const double* alpha;     // [B]
+  const int* status;       // [B] or null; only ST_RUNNING problems are processed
+  // outputs
+  R *S, *s;                // (nx*nx | nx, T+1, B), optional (null = skip)
+  R *Gam, *gam;            // (nu*nx | nu, T, B)
+  R *dX, *dU;              // (nx, T+1, B), (nu, T, B)
+  int* flags;              // [B] OR of FLAG_*
+  double* red;             // (3, P0, B): sum du^2, sum du.d, max |du|
+  // tree scratch, index l = 1..L, item rows n[l]
+  R* vagg[kMaxLevels + 1];
+  R* vcar[kMaxLevels + 1];
+  R* pagg[kMaxLevels + 1];
+  R* pcar[kMaxLevels + 1];
+};
+
+template <typename R>
+PTC_D bool lqr_skip(const LqrArgs<R>& a, int b) {
+  return a.status != nullptr && a.status[b] != ST_RUNNING;
+}
+
+PTC_D int unit_id() { return blockIdx.x * blockDim.x + threadIdx.x; }
+
+// ----------------------------------------------------------------- value up
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) k_value_up0(LqrArgs<R> a) {
+  const int P0 = a.plan.units0();
+  const int u = unit_id();
+  if (u >= P0 * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const R alpha = R(a.alpha[b]);
+  VElem<R, NX> acc;
+  Stage<R, NX, NU> st;
+  R L[NU][NU];
+  bool okr = true, okc = true;
+  int start;
+  if (j == P0 - 1) {
+    R PT[NX][NX];
+    ld_mat(a.PT, 0, 1, B, b, PT);
+    velem_terminal(PT, acc);
+    start = t1 - 1;
+  } else {
+    ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t1 - 1, T, B, b, alpha, st);
+    okr &= velem_from_stage(st, acc, L);
+    start = t1 - 2;
+  }
+  for (int t = start; t >= t0; --t) {
+    ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t, T, B, b, alpha, st);
+    VElem<R, NX> e, o;
+    okr &= velem_from_stage(st, e, L);
+    okc &= vcombine(e, acc, o);
+    acc = o;
+  }
+  st_velem(a.vagg[1], j, a.plan.n[1], B, b, acc);
+  int fl = (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND);
+  if (fl) atomicOr(a.flags + b, fl);
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_value_up(LqrArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nu = a.plan.n[l + 1];
+  const int u = unit_id();
+  if (u >= nu * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  VElem<R, NX> acc;
+  ld_velem(a.vagg[l], last, nl, a.B, b, acc);
+  bool okc = true;
+  for (int i = last - 1; i >= first; --i) {
+    VElem<R, NX> e, o;
+    ld_velem(a.vagg[l], i, nl, a.B, b, e);
+    okc &= vcombine(e, acc, o);
+    acc = o;
+  }
+  st_velem(a.vagg[l + 1], j, nu, a.B, b, acc);
+  if (!okc) atomicOr(a.flags + b, FLAG_COND);
+}
+
+// --------------------------------------------------------------- value down
+
+// top level: one thread per problem, zero carry beyond the terminal
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_value_top(LqrArgs<R> a) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (lqr_skip(a, b)) return;
+  const int L = a.plan.L, nL = a.plan.n[L];
+  VCarry<R, NX> c;
+  vcarry_zero(c);
+  bool okc = true;
+  for (int i = nL - 1; i >= 0; --i) {
+    st_vcarry(a.vcar[L], i, nL, a.B, b, c);
+    VElem<R, NX> e;
+    ld_velem(a.vagg[L], i, nL, a.B, b, e);
+    VCarry<R, NX> o;
+    okc &= vstep(e, c, o);
+    c = o;
+  }
+  if (!okc) atomicOr(a.flags + b, FLAG_COND);
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_value_down(LqrArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nu = a.plan.n[l + 1];
+  const int u = unit_id();
+  if (u >= nu * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  VCarry<R, NX> c;
+  ld_vcarry(a.vcar[l + 1], j, nu, a.B, b, c);
+  bool okc = true;
+  for (int i = last; i >= first; --i) {
+    st_vcarry(a.vcar[l], i, nl, a.B, b, c);
+    VElem<R, NX> e;
+    ld_velem(a.vagg[l], i, nl, a.B, b, e);
+    VCarry<R, NX> o;
+    okc &= vstep(e, c, o);
+    c = o;
+  }
+  if (!okc) atomicOr(a.flags + b, FLAG_COND);
+}
+
+// level-0 down-sweep: cost-to-go, gains, optional (S, s) output and the
+// level-1 aggregates of the forward propagation scan
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
+  const int P0 = a.plan.units0();
+  const int u = unit_id();
+  if (u >= P0 * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const R alpha = R(a.alpha[b]);
+  const bool tree = a.plan.L >= 1;
+  VCarry<R, NX> c;
+  if (tree) ld_vcarry(a.vcar[1], j, a.plan.n[1], B, b, c);
+  else vcarry_zero(c);
+  bool okr = true, okc = true, okq = true;
+  if (j == P0 - 1) {
+    // the terminal element V_{N+1}: Y = P_T, everything else zero
+    ld_mat(a.PT, 0, 1, B, b, c.Y);
+    set_zero(c.eta);
+    if (a.S) {
+      st_mat(a.S, T, T + 1, B, b, c.Y);
+      R z[NX];
+      set_zero(z);
+      st_vec(a.s, T, T + 1, B, b, z);
+    }
+  }
+  Aff<R, NX> pa;
+  if (tree) aff_identity(pa);
+  for (int t = t1 - 1; t >= t0; --t) {
+    Stage<R, NX, NU> st;
+    ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t, T, B, b, alpha, st);
+    R Gam[NU][NX], gam[NU];
+    okq &= gains(st, c, Gam, gam);
+    st_mat(a.Gam, t, T, B, b, Gam);
+    st_vec(a.gam, t, T, B, b, gam);
+    if (tree) {
+      Aff<R, NX> m, o;
+      if (t == 0) {
+        set_zero(m.F);
+      } else {
+        mm<NX, NU, NX>(st.Fu, Gam, m.F);
+#pragma unroll
+        for (int i = 0; i < NX; ++i)
+#pragma unroll
+          for (int k = 0; k < NX; ++k) m.F[i][k] += st.Fx[i][k];
+      }
+      mv<NX, NU>(st.Fu, gam, m.e);
+      aff_compose(pa, m, o);
+      pa = o;
+    }
+    VElem<R, NX> e;
+    R L[NU][NU];
+    okr &= velem_from_stage(st, e, L);
+    VCarry<R, NX> o;
+    okc &= vstep(e, c, o);
+    c = o;
+    if (a.S) {
+      st_mat(a.S, t, T + 1, B, b, c.Y);
+      R sv[NX];
+#pragma unroll
+      for (int i = 0; i < NX; ++i) sv[i] = -c.eta[i];
+      st_vec(a.s, t, T + 1, B, b, sv);
+    }
+  }
+  if (tree) st_aff(a.pagg[1], j, a.plan.n[1], B, b, pa);
+  int fl = (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND) | (okq ? 0 : FLAG_DEF_Q);
+  if (fl) atomicOr(a.flags + b, fl);
+}
+
+// ---------------------------------------------------------- propagation scan
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_prop_up(LqrArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nu = a.plan.n[l + 1];
+  const int u = unit_id();
+  if (u >= nu * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  Aff<R, NX> acc;
+  ld_aff(a.pagg[l], first, nl, a.B, b, acc);
+  for (int i = first + 1; i <= last; ++i) {
+    Aff<R, NX> m, o;
+    ld_aff(a.pagg[l], i, nl, a.B, b, m);
+    aff_compose(m, acc, o);
+    acc = o;
+  }
+  st_aff(a.pagg[l + 1], j, nu, a.B, b, acc);
+}
+
+// level-0 up-sweep of the propagation scan for a given feedback law
+// (standalone propagation_pass; inside the Newton loop this aggregate is
+// produced by k_value_down0 instead)
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) k_prop_up0(LqrArgs<R> a) {
+  const int P0 = a.plan.units0();
+  const int u = unit_id();
+  if (u >= P0 * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  Aff<R, NX> acc;
+  aff_identity(acc);
+  for (int t = t0; t < t1; ++t) {
+    R Gam[NU][NX], gam[NU], Fx[NX][NX], Fu[NX][NU];
+    ld_mat(a.Gam, t, T, B, b, Gam);
+    ld_vec(a.gam, t, T, B, b, gam);
+    ld_mat(a.Fx, t, T, B, b, Fx);
+    ld_mat(a.Fu, t, T, B, b, Fu);
+    Aff<R, NX> m, o;
+    mm<NX, NU, NX>(Fu, Gam, m.F);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NX; ++k) m.F[i][k] = (t == 0) ? R(0) : m.F[i][k] + Fx[i][k];
+    mv<NX, NU>(Fu, gam, m.e);
+    aff_compose(m, acc, o);
+    acc = o;
+  }
+  st_aff(a.pagg[1], j, a.plan.n[1], B, b, acc);
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_prop_top(LqrArgs<R> a) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (lqr_skip(a, b)) return;
+  const int L = a.plan.L, nL = a.plan.n[L];
+  R x[NX];
+  set_zero(x);
+  for (int i = 0; i < nL; ++i) {
+    st_vec(a.pcar[L], i, nL, a.B, b, x);
+    Aff<R, NX> m;
+    ld_aff(a.pagg[L], i, nL, a.B, b, m);
+    R y[NX];
+    aff_apply(m, x, y);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) x[k] = y[k];
+  }
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_prop_down(LqrArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nu = a.plan.n[l + 1];
+  const int u = unit_id();
+  if (u >= nu * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  R x[NX];
+  ld_vec(a.pcar[l + 1], j, nu, a.B, b, x);
+  for (int i = first; i <= last; ++i) {
+    st_vec(a.pcar[l], i, nl, a.B, b, x);
+    Aff<R, NX> m;
+    ld_aff(a.pagg[l], i, nl, a.B, b, m);
+    R y[NX];
+    aff_apply(m, x, y);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) x[k] = y[k];
+  }
+}
+
+// level-0 forward sweep: dx_t, du_t = Gamma_t dx_t + gamma_t and the
+// per-chunk partial reductions used by the trust-region test
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
+  const int P0 = a.plan.units0();
+  const int u = unit_id();
+  if (u >= P0 * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  R x[NX];
+  if (a.plan.L >= 1) ld_vec(a.pcar[1], j, a.plan.n[1], B, b, x);
+  else set_zero(x);
+  double s2 = 0.0, sd = 0.0, mx = 0.0;
+  for (int t = t0; t < t1; ++t) {
+    st_vec(a.dX, t, T + 1, B, b, x);
+    R Gam[NU][NX], gam[NU], Fx[NX][NX], Fu[NX][NU], dd[NU];
+    ld_mat(a.Gam, t, T, B, b, Gam);
+    ld_vec(a.gam, t, T, B, b, gam);
+    ld_mat(a.Fx, t, T, B, b, Fx);
+    ld_mat(a.Fu, t, T, B, b, Fu);
+    if (a.d) ld_vec(a.d, t, T, B, b, dd);
+    else set_zero(dd);
+    R du[NU];
+    mv<NU, NX>(Gam, x, du);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      du[i] += gam[i];
+      s2 += double(du[i]) * double(du[i]);
+      sd += double(du[i]) * double(dd[i]);
+      mx = nanmax(mx, double(fabs(du[i])));
+    }
+    st_vec(a.dU, t, T, B, b, du);
+    // closed loop: F = Fx + Fu Gamma (F = 0 on the head stage), e = Fu gamma
+    R F[NX][NX], e[NX], y[NX];
+    mm<NX, NU, NX>(Fu, Gam, F);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NX; ++k) F[i][k] = (t == 0) ? R(0) : F[i][k] + Fx[i][k];
+    mv<NX, NU>(Fu, gam, e);
+    mv<NX, NX>(F, x, y);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
+  }
+  if (j == P0 - 1) st_vec(a.dX, T, T + 1, B, b, x);
+  if (a.red) {
+    a.red[((size_t)0 * P0 + j) * B + b] = s2;
+    a.red[((size_t)1 * P0 + j) * B + b] = sd;
+    a.red[((size_t)2 * P0 + j) * B + b] = mx;
+  }
+}
+
+}  // namespace ptc

@@ -1,0 +1,469 @@
+// Device-side models: dynamics (pendulum, cart-pole, affine), quadratic cost,
+// box constraints and the two outer-loop augmentations.  Each stage
+// evaluation is fused: one call produces everything the expansion needs,
+// with dynamics Hessians contracted against lambda_{t+1} on the fly (no
+// d_x^3 tensors ever reach HBM).
+//
+// Reference: systems.py (pendulum 161-231, cart-pole 260-437, linear 32-77,
+// quadratic cost 80-139), problem.py:233-340 (BoxConstraint),
+// outer.py:30-157 (barrier), outer.py:252-333 (ADMM penalty),
+// passes.py:155-185 (expansion).
+#pragma once
+
+#include "elements.cuh"
+
+namespace ptc {
+
+enum : int { DYN_PENDULUM = 0, DYN_CARTPOLE = 1, DYN_LINEAR = 2 };
+
+constexpr int kMaxNX = 12;
+constexpr int kMaxNU = 6;
+constexpr int kMaxRows = 2 * (kMaxNX + kMaxNU);
+
+// Problem description shared by every problem of a batch (lives in HBM,
+// read through the read-only path; all threads read the same words).
+struct ProblemParams {
+  int dyn_kind;
+  double dyn[8];            // pendulum: g, l, m, b, dt ; cart-pole: g, l, mc, mp, dt
+  int lin_T, lin_B;         // affine model: A/B/c vary over stages if lin_T > 1,
+                            // over problems if lin_B > 1
+  const void* lin_A;        // (nx*nx, lin_T, lin_B) in the solver dtype
+  const void* lin_Bm;       // (nx*nu, lin_T, lin_B)
+  const void* lin_c;        // (nx,    lin_T, lin_B)
+  double Q[kMaxNX * kMaxNX], Rc[kMaxNU * kMaxNU], Qf[kMaxNX * kMaxNX], goal[kMaxNX];
+  int W, Ws;                // stacked constraint rows, of which Ws are state rows
+  int row_var[kMaxRows];    // 0 = state, 1 = control
+  int row_idx[kMaxRows];
+  double row_sign[kMaxRows];
+  double row_bound[kMaxRows];
+};
+
+// Augmentation state for one launch (reference AugmentedCost variants)
+template <typename R>
+struct AugArgs {
+  int kind;              // AUG_ZERO / AUG_BARRIER / AUG_ADMM
+  const double* mu;      // [B] barrier weight per problem
+  double rho;            // ADMM penalty
+  const R* z;            // (W, T, B)
+  const R* v;            // (W, T, B)
+};
+
+// ---------------------------------------------------------------------------
+// dynamics
+// ---------------------------------------------------------------------------
+
+// First derivatives of the dynamics plus lambda-contracted second
+// derivatives  Hxx = sum_k lam_k fxx[k], Huu, Hxu.
+template <typename R, int NX, int NU>
+struct DynDerivs {
+  R fx[NX][NX], fu[NX][NU], Hxx[NX][NX], Huu[NU][NU], Hxu[NX][NU];
+};
+
+template <typename R>
+struct Pendulum {
+  static constexpr int NX = 2, NU = 1;
+
+  PTC_D static void step(const ProblemParams& p, int, int, const R (&x)[2], const R (&u)[1],
+                         R (&xn)[2]) {
+    const R g = R(p.dyn[0]), l = R(p.dyn[1]), m = R(p.dyn[2]), bd = R(p.dyn[3]), dt = R(p.dyn[4]);
+    R acc = -(g / l) * sin(x[0]) + (u[0] - bd * x[1]) / (m * (l * l));
+    xn[0] = x[0] + dt * x[1];
+    xn[1] = x[1] + dt * acc;
+  }
+
+  template <bool kSecond>
+  PTC_D static void derivs(const ProblemParams& p, int, int, const R (&x)[2], const R (&)[1],
+                           const R (&lam)[2], DynDerivs<R, 2, 1>& D) {
+    const R g = R(p.dyn[0]), l = R(p.dyn[1]), m = R(p.dyn[2]), bd = R(p.dyn[3]), dt = R(p.dyn[4]);
+    const R inertia = m * (l * l);
+    D.fx[0][0] = R(1);
+    D.fx[0][1] = dt;
+    D.fx[1][0] = -dt * (g / l) * cos(x[0]);
+    D.fx[1][1] = R(1) - dt * bd / inertia;
+    D.fu[0][0] = R(0);
+    D.fu[1][0] = dt / inertia;
+    if (kSecond) {
+      D.Hxx[0][0] = lam[1] * (dt * (g / l) * sin(x[0]));
+      D.Hxx[0][1] = D.Hxx[1][0] = D.Hxx[1][1] = R(0);
+      D.Huu[0][0] = R(0);
+      D.Hxu[0][0] = D.Hxu[1][0] = R(0);
+    }
+  }
+};
+
+// Second-order jet in (theta, omega, force) for the cart-pole accelerations.
+template <typename R>
+struct Jet {
+  R v, g[3], h[3][3];
+};
+
+template <typename R>
+PTC_D Jet<R> jvar(R val, int k) {
+  Jet<R> j;
+  j.v = val;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    j.g[a] = (a == k) ? R(1) : R(0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) j.h[a][c] = R(0);
+  }
+  return j;
+}
+
+template <typename R>
+PTC_D Jet<R> jadd(const Jet<R>& a, const Jet<R>& b) {
+  Jet<R> o;
+  o.v = a.v + b.v;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    o.g[i] = a.g[i] + b.g[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o.h[i][k] = a.h[i][k] + b.h[i][k];
+  }
+  return o;
+}
+
+template <typename R>
+PTC_D Jet<R> jscale(const Jet<R>& a, R s) {
+  Jet<R> o;
+  o.v = a.v * s;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    o.g[i] = a.g[i] * s;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o.h[i][k] = a.h[i][k] * s;
+  }
+  return o;
+}
+
+template <typename R>
+PTC_D Jet<R> jaddc(const Jet<R>& a, R c) {
+  Jet<R> o = a;
+  o.v = a.v + c;
+  return o;
+}
+
+template <typename R>
+PTC_D Jet<R> jmul(const Jet<R>& a, const Jet<R>& b) {
+  Jet<R> o;
+  o.v = a.v * b.v;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o.g[i] = a.g[i] * b.v + b.g[i] * a.v;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      o.h[i][k] = a.h[i][k] * b.v + b.h[i][k] * a.v + a.g[i] * b.g[k] + a.g[k] * b.g[i];
+  return o;
+}
+
+template <typename R>
+PTC_D Jet<R> jrecip(const Jet<R>& a) {
+  Jet<R> o;
+  R r = R(1) / a.v;
+  R r2 = r * r;
+  o.v = r;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o.g[i] = -a.g[i] * r2;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o.h[i][k] = -a.h[i][k] * r2 + R(2) * a.g[i] * a.g[k] * (r2 * r);
+  return o;
+}
+
+template <typename R>
+PTC_D void jsincos(const Jet<R>& a, Jet<R>& s, Jet<R>& c) {
+  R sv, cv;
+  sv = sin(a.v);
+  cv = cos(a.v);
+  s.v = sv;
+  c.v = cv;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    s.g[i] = a.g[i] * cv;
+    c.g[i] = -a.g[i] * sv;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      R gg = a.g[i] * a.g[k];
+      s.h[i][k] = a.h[i][k] * cv - gg * sv;
+      c.h[i][k] = -a.h[i][k] * sv - gg * cv;
+    }
+  }
+}
+
+template <typename R>
+struct CartPole {
+  static constexpr int NX = 4, NU = 1;
+
+  // cart acc = (F + mp s (l om + g c)) / (mc + mp s^2)
+  // pole acc = (-F c - mp l om^2 c s - (mc + mp) g s) / (l (mc + mp s^2))
+  PTC_D static void accels(const ProblemParams& p, R th, R om, R force, Jet<R>& cart,
+                           Jet<R>& pole) {
+    const R g = R(p.dyn[0]), ln = R(p.dyn[1]), mc = R(p.dyn[2]), mp = R(p.dyn[3]);
+    Jet<R> TH = jvar(th, 0), OM = jvar(om, 1), FF = jvar(force, 2);
+    Jet<R> s, c;
+    jsincos(TH, s, c);
+    Jet<R> den = jaddc(jscale(jmul(s, s), mp), mc);
+    Jet<R> rden = jrecip(den);
+    Jet<R> inner = jadd(jscale(OM, ln), jscale(c, g));
+    Jet<R> n1 = jadd(FF, jscale(jmul(s, inner), mp));
+    cart = jmul(n1, rden);
+    Jet<R> n2 = jadd(jadd(jscale(jmul(FF, c), R(-1)), jscale(jmul(jmul(jmul(OM, OM), c), s), -(mp * ln))),
+                     jscale(s, -((mc + mp) * g)));
+    pole = jscale(jmul(n2, rden), R(1) / ln);
+  }
+
+  PTC_D static void step(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
+                         R (&xn)[4]) {
+    const R g = R(p.dyn[0]), ln = R(p.dyn[1]), mc = R(p.dyn[2]), mp = R(p.dyn[3]), dt = R(p.dyn[4]);
+    R s = sin(x[1]), c = cos(x[1]);
+    R den = mc + mp * s * s;
+    R ca = (u[0] + mp * s * (ln * x[3] + g * c)) / den;
+    R pa = (-u[0] * c - mp * ln * x[3] * x[3] * c * s - (mc + mp) * g * s) / (ln * den);
+    xn[0] = x[0] + dt * x[2];
+    xn[1] = x[1] + dt * x[3];
+    xn[2] = x[2] + dt * ca;
+    xn[3] = x[3] + dt * pa;
+  }
+
+  template <bool kSecond>
+  PTC_D static void derivs(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
+                           const R (&lam)[4], DynDerivs<R, 4, 1>& D) {
+    const R dt = R(p.dyn[4]);
+    Jet<R> cart, pole;
+    accels(p, x[1], x[3], u[0], cart, pole);
+    set_identity(D.fx);
+    D.fx[0][2] = dt;
+    D.fx[1][3] = dt;
+    D.fx[2][1] = dt * cart.g[0];
+    D.fx[2][3] = dt * cart.g[1];
+    D.fx[3][1] = dt * pole.g[0];
+    D.fx[3][3] = R(1) + dt * pole.g[1];
+    D.fu[0][0] = R(0);
+    D.fu[1][0] = R(0);
+    D.fu[2][0] = dt * cart.g[2];
+    D.fu[3][0] = dt * pole.g[2];
+    if (kSecond) {
+      set_zero(D.Hxx);
+      set_zero(D.Hxu);
+      D.Huu[0][0] = R(0);
+      // rows 2 (cart) and 3 (pole) carry second derivatives in (theta, omega)
+      const R l2 = lam[2] * dt, l3 = lam[3] * dt;
+      D.Hxx[1][1] = l2 * cart.h[0][0] + l3 * pole.h[0][0];
+      D.Hxx[1][3] = D.Hxx[3][1] = l2 * cart.h[0][1] + l3 * pole.h[0][1];
+      D.Hxx[3][3] = l2 * cart.h[1][1] + l3 * pole.h[1][1];
+      D.Hxu[1][0] = l2 * cart.h[0][2] + l3 * pole.h[0][2];
+      D.Hxu[3][0] = l2 * cart.h[1][2] + l3 * pole.h[1][2];
+    }
+  }
+};
+
+// x' = A_t x + B_t u + c_t with per-stage / per-problem broadcasting
+template <typename R, int NX_, int NU_>
+struct Affine {
+  static constexpr int NX = NX_, NU = NU_;
+
+  PTC_D static size_t at(const ProblemParams& p, int c, int t, int b) {
+    int tt = p.lin_T > 1 ? t : 0;
+    int bb = p.lin_B > 1 ? b : 0;
+    return ((size_t)c * p.lin_T + tt) * p.lin_B + bb;
+  }
+
+  PTC_D static void mats(const ProblemParams& p, int t, int b, R (&A)[NX][NX], R (&Bm)[NX][NU]) {
+    const R* pa = static_cast<const R*>(p.lin_A);
+    const R* pb = static_cast<const R*>(p.lin_Bm);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) A[i][j] = __ldg(pa + at(p, i * NX + j, t, b));
+#pragma unroll
+      for (int j = 0; j < NU; ++j) Bm[i][j] = __ldg(pb + at(p, i * NU + j, t, b));
+    }
+  }
+
+  PTC_D static void offset(const ProblemParams& p, int t, int b, R (&c)[NX]) {
+    const R* pc = static_cast<const R*>(p.lin_c);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) c[i] = pc ? __ldg(pc + at(p, i, t, b)) : R(0);
+  }
+
+  PTC_D static void step(const ProblemParams& p, int t, int b, const R (&x)[NX], const R (&u)[NU],
+                         R (&xn)[NX]) {
+    R A[NX][NX], Bm[NX][NU], c[NX];
+    mats(p, t, b, A, Bm);
+    offset(p, t, b, c);
+    R ax[NX], bu[NX];
+    mv<NX, NX>(A, x, ax);
+    mv<NX, NU>(Bm, u, bu);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xn[i] = ax[i] + bu[i] + c[i];
+  }
+
+  template <bool kSecond>
+  PTC_D static void derivs(const ProblemParams& p, int t, int b, const R (&)[NX], const R (&)[NU],
+                           const R (&)[NX], DynDerivs<R, NX, NU>& D) {
+    mats(p, t, b, D.fx, D.fu);
+    if (kSecond) {
+      set_zero(D.Hxx);
+      set_zero(D.Huu);
+      set_zero(D.Hxu);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// cost, constraints, augmentation
+// ---------------------------------------------------------------------------
+
+// stage cost 0.5 (x-g)^T Q (x-g) + 0.5 u^T R u
+template <typename R, int NX, int NU>
+PTC_D R stage_cost(const ProblemParams& p, const R (&x)[NX], const R (&u)[NU]) {
+  R e[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e[i] = x[i] - R(p.goal[i]);
+  R qx = R(0), ru = R(0);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) qx += e[i] * R(p.Q[i * NX + j]) * e[j];
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) ru += u[i] * R(p.Rc[i * NU + j]) * u[j];
+  return R(0.5) * (qx + ru);
+}
+
+template <typename R, int NX>
+PTC_D R terminal_cost(const ProblemParams& p, const R (&x)[NX]) {
+  R e[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e[i] = x[i] - R(p.goal[i]);
+  R q = R(0);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    R row = R(0);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) row += R(p.Qf[i * NX + j]) * e[j];
+    q += e[i] * row;
+  }
+  return R(0.5) * q;
+}
+
+template <typename R, int NX>
+PTC_D void terminal_grad(const ProblemParams& p, const R (&x)[NX], R (&gx)[NX]) {
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    R acc = R(0);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) acc += R(p.Qf[i * NX + j]) * (x[j] - R(p.goal[j]));
+    gx[i] = acc;
+  }
+}
+
+// value of stacked constraint row k: sign * (var[idx] - bound)
+template <typename R, int NX, int NU>
+PTC_D R row_value(const ProblemParams& p, int k, const R (&x)[NX], const R (&u)[NU]) {
+  const int idx = p.row_idx[k];
+  R var = R(0);
+  if (p.row_var[k] == 0) {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) var = (i == idx) ? x[i] : var;
+  } else {
+#pragma unroll
+    for (int i = 0; i < NU; ++i) var = (i == idx) ? u[i] : var;
+  }
+  const R bnd = R(p.row_bound[k]);
+  return p.row_sign[k] > 0 ? var - bnd : bnd - var;
+}
+
+// Augmentation value at one stage; `bad_row` reports the first row with
+// w >= 0 for the barrier (-1 if strictly feasible).
+template <typename R, int NX, int NU>
+PTC_D R aug_value(const ProblemParams& p, const AugArgs<R>& a, int t, int T, int B, int b,
+                  const R (&x)[NX], const R (&u)[NU], int& bad_row) {
+  bad_row = -1;
+  if (a.kind == AUG_ZERO) return R(0);
+  const int W = p.W;
+  if (a.kind == AUG_BARRIER) {
+    R sg = R(0), sh = R(0);
+    for (int k = 0; k < W; ++k) {
+      R w = row_value<R, NX, NU>(p, k, x, u);
+      if (w >= R(0) && bad_row < 0) bad_row = k;
+      R lg = log(-w);
+      if (k < p.Ws) sg += lg; else sh += lg;
+    }
+    return -R(a.mu[b]) * (sg + sh);
+  }
+  const R rho = R(a.rho);
+  R acc = R(0);
+  for (int k = 0; k < W; ++k) {
+    R w = row_value<R, NX, NU>(p, k, x, u);
+    R res = w - ldf(a.z, k, t, T, B, b) + ldf(a.v, k, t, T, B, b) / rho;
+    acc += res * res;
+  }
+  return R(0.5) * rho * acc;
+}
+
+// Gradient and (diagonal) Hessian of the augmentation with respect to the
+// state and the control.  Box rows touch a single variable each, so the
+// Hessians are diagonal and the cross term vanishes (outer.py:97-99).
+template <typename R, int NX, int NU>
+PTC_D void aug_derivs(const ProblemParams& p, const AugArgs<R>& a, int t, int T, int B, int b,
+                      const R (&x)[NX], const R (&u)[NU], R (&cx)[NX], R (&cu)[NU],
+                      R (&cxx)[NX], R (&cuu)[NU]) {
+  set_zero(cx);
+  set_zero(cu);
+  set_zero(cxx);
+  set_zero(cuu);
+  if (a.kind == AUG_ZERO) return;
+  const int W = p.W;
+  if (a.kind == AUG_BARRIER) {
+    const R mu = R(a.mu[b]);
+    for (int k = 0; k < W; ++k) {
+      R w = row_value<R, NX, NU>(p, k, x, u);
+      R inv = R(1) / w;
+      R sgn = R(p.row_sign[k]);
+      R sc = sgn / w;
+      R g1 = sgn * inv;
+      R h1 = sc * sc;
+      const int idx = p.row_idx[k];
+      if (p.row_var[k] == 0) {
+#pragma unroll
+        for (int i = 0; i < NX; ++i)
+          if (i == idx) { cx[i] += g1; cxx[i] += h1; }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NU; ++i)
+          if (i == idx) { cu[i] += g1; cuu[i] += h1; }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NX; ++i) { cx[i] = -mu * cx[i]; cxx[i] = mu * cxx[i]; }
+#pragma unroll
+    for (int i = 0; i < NU; ++i) { cu[i] = -mu * cu[i]; cuu[i] = mu * cuu[i]; }
+    return;
+  }
+  const R rho = R(a.rho);
+  for (int k = 0; k < W; ++k) {
+    R w = row_value<R, NX, NU>(p, k, x, u);
+    R res = w - ldf(a.z, k, t, T, B, b) + ldf(a.v, k, t, T, B, b) / rho;
+    R sgn = R(p.row_sign[k]);
+    const int idx = p.row_idx[k];
+    if (p.row_var[k] == 0) {
+#pragma unroll
+      for (int i = 0; i < NX; ++i)
+        if (i == idx) { cx[i] += sgn * res; cxx[i] += sgn * sgn; }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NU; ++i)
+        if (i == idx) { cu[i] += sgn * res; cuu[i] += sgn * sgn; }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NX; ++i) { cx[i] *= rho; cxx[i] *= rho; }
+#pragma unroll
+  for (int i = 0; i < NU; ++i) { cu[i] *= rho; cuu[i] *= rho; }
+}
+
+}  // namespace ptc

@@ -1,0 +1,657 @@
+// Kernels of one device-resident Newton iteration (reference newton.py:129-215)
+// and of the two outer loops (outer.py:221-245 barrier, outer.py:392-435 ADMM).
+//
+// Every problem of a batch carries its own trust-region state (alpha, nu),
+// iteration counter, history and outer-loop state in HBM; the control kernel
+// replays the reference's accept/reject logic per problem, so a batch of
+// independent MPC problems advances without any host round trip and a
+// single problem reproduces the reference iteration sequence.
+#pragma once
+
+#include "lqr_kernels.cuh"
+#include "models.cuh"
+
+namespace ptc {
+
+constexpr double kAlphaMax = 1e12;
+
+enum : int { METHOD_NEWTON = 0, METHOD_BARRIER = 1, METHOD_ADMM = 2 };
+
+struct Options {
+  int method;
+  double alpha0, nu0, inner_tol;
+  int max_iters;
+  double mu0, zeta, mu_tol;
+  double rho, residual_tol;
+  int max_outer;
+  int hist_cap, round_cap;
+  int keep_round_controls;
+};
+
+template <typename R>
+struct NewtonArgs {
+  int B, T;
+  Plan plan;
+  Options opt;
+  const ProblemParams* pp;
+  int aug_kind;            // AUG_* used inside the Newton solve
+  // trajectories, double buffered: buffer q at X + q * xsz
+  R *X, *U;
+  size_t xsz, usz;
+  // per-problem state [B]
+  int *status, *phase, *parity, *flags, *iters, *term, *round, *hist_len, *bad_index, *n_running;
+  double *alpha, *nu, *cur_cost, *cand_cost, *mu;
+  double* hist;            // (hist_cap, 5, B)
+  double *round_mu, *round_cost, *round_rp, *round_rd;   // (round_cap, B)
+  int *round_iters, *round_term;                          // (round_cap, B)
+  R* round_U;              // (round_cap, nu, T, B) or null
+  // ADMM consensus variables (W, T, B)
+  R *z, *v;
+  // expansion
+  R *lam, *P, *Rm, *M, *d, *Fx, *Fu, *PT;
+  // co-state scan tree
+  R* cagg[kMaxLevels + 1];
+  R* ccar[kMaxLevels + 1];
+  // partial reductions per level-0 unit
+  double* cpart[2];        // (3, P0, B): sum l, sum c, first infeasible index
+  double* apart;           // (2, P0, B): ADMM primal / dual residual maxima
+  double* red;             // (3, P0, B) from the propagation sweep
+};
+
+template <typename R>
+PTC_D AugArgs<R> aug_of(const NewtonArgs<R>& a) {
+  AugArgs<R> g;
+  g.kind = a.aug_kind;
+  g.mu = a.mu;
+  g.rho = a.opt.rho;
+  g.z = a.z;
+  g.v = a.v;
+  return g;
+}
+
+template <typename R, int NX>
+PTC_D void ld_x(const NewtonArgs<R>& a, int q, int t, int b, R (&x)[NX]) {
+  ld_vec(a.X + q * a.xsz, t, a.T + 1, a.B, b, x);
+}
+
+template <typename R, int NU>
+PTC_D void ld_u(const NewtonArgs<R>& a, int q, int t, int b, R (&u)[NU]) {
+  ld_vec(a.U + q * a.usz, t, a.T, a.B, b, u);
+}
+
+template <typename R>
+PTC_D bool running(const NewtonArgs<R>& a, int b) { return a.status[b] == ST_RUNNING; }
+
+// ------------------------------------------------------------ initialisation
+
+template <typename R>
+__global__ void k_init_state(NewtonArgs<R> a) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  a.status[b] = ST_RUNNING;
+  a.phase[b] = PH_NEED_COST | PH_NEED_EXP;
+  a.parity[b] = 0;
+  a.flags[b] = 0;
+  a.iters[b] = 0;
+  a.term[b] = TERM_NONE;
+  a.round[b] = 0;
+  a.hist_len[b] = 0;
+  a.bad_index[b] = -1;
+  a.alpha[b] = a.opt.alpha0;
+  a.nu[b] = a.opt.nu0;
+  a.cur_cost[b] = 0.0;
+  a.cand_cost[b] = 0.0;
+  a.mu[b] = a.opt.mu0;
+  if (a.opt.method == METHOD_BARRIER && !(a.opt.mu0 > a.opt.mu_tol)) a.status[b] = ST_DONE;
+}
+
+// x_{t+1} == f_t(x_t, u_t) check of the initial trajectory (newton.py:118-126)
+template <typename R, class Dyn>
+__global__ void k_check_consistent(NewtonArgs<R> a, int* bad_t) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int i = unit_id();
+  if (i >= a.T * a.B) return;
+  const int b = i % a.B, t = i / a.B;
+  R x[NX], u[NU], xn[NX], p[NX];
+  ld_x(a, 0, t, b, x);
+  ld_u(a, 0, t, b, u);
+  ld_x(a, 0, t + 1, b, xn);
+  Dyn::step(*a.pp, t, b, x, u, p);
+  double gap = 0.0, mag = 0.0;
+#pragma unroll
+  for (int k = 0; k < NX; ++k) {
+    gap = nanmax(gap, double(fabs(p[k] - xn[k])));
+    mag = nanmax(mag, double(fabs(p[k])));
+  }
+  const double tol = (sizeof(R) == 8 ? 1e-8 : 1e-4) * (1.0 + mag);
+  if (gap > tol || gap != gap) atomicMin(bad_t + b, t);
+}
+
+// ADMM start: z = Pi_C(w(x, u)), v = 0   (outer.py:409-410)
+template <typename R, int NX, int NU>
+__global__ void k_admm_init(NewtonArgs<R> a) {
+  const int i = unit_id();
+  if (i >= a.T * a.B) return;
+  const int b = i % a.B, t = i / a.B;
+  const ProblemParams& p = *a.pp;
+  R x[NX], u[NU];
+  ld_x(a, 0, t, b, x);
+  ld_u(a, 0, t, b, u);
+  for (int k = 0; k < p.W; ++k) {
+    R w = row_value<R, NX, NU>(p, k, x, u);
+    stf(a.z, k, t, a.T, a.B, b, w < R(0) ? w : R(0));
+    stf(a.v, k, t, a.T, a.B, b, R(0));
+  }
+}
+
+// ------------------------------------------------------- cost of a trajectory
+
+// which = 0: current trajectory (only when PH_NEED_COST), 1: the candidate
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int which) {
+  const int P0 = a.plan.units0();
+  const int u0 = unit_id();
+  if (u0 >= P0 * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (!running(a, b)) return;
+  if (which == 0 && !(a.phase[b] & PH_NEED_COST)) return;
+  const int q = which == 0 ? a.parity[b] : 1 - a.parity[b];
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const ProblemParams& p = *a.pp;
+  const AugArgs<R> g = aug_of(a);
+  double sl = 0.0, sc = 0.0;
+  int bad = -1;
+  for (int t = t0; t < t1; ++t) {
+    R x[NX], u[NU];
+    ld_x(a, q, t, b, x);
+    ld_u(a, q, t, b, u);
+    sl += double(stage_cost<R, NX, NU>(p, x, u));
+    int br;
+    sc += double(aug_value<R, NX, NU>(p, g, t, T, B, b, x, u, br));
+    if (br >= 0 && bad < 0) bad = t * p.W + br;
+  }
+  double* cp = a.cpart[which];
+  cp[((size_t)0 * P0 + j) * B + b] = sl;
+  cp[((size_t)1 * P0 + j) * B + b] = sc;
+  cp[((size_t)2 * P0 + j) * B + b] = double(bad);
+}
+
+// ------------------------------------------------------------ co-state scan
+
+// level-0 up-sweep: fold the reverse maps lambda_t = q_t + fx_t^T lambda_{t+1}
+// over a chunk (the last stage absorbs the terminal gradient, F = 0)
+template <typename R, class Dyn>
+__global__ void __launch_bounds__(128) k_costate_up0(NewtonArgs<R> a) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int P0 = a.plan.units0();
+  const int u0 = unit_id();
+  if (u0 >= P0 * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (!running(a, b) || !(a.phase[b] & PH_NEED_EXP)) return;
+  const int q = a.parity[b];
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const ProblemParams& p = *a.pp;
+  const AugArgs<R> g = aug_of(a);
+  Aff<R, NX> acc;
+  aff_identity(acc);
+  for (int t = t1 - 1; t >= t0; --t) {
+    R x[NX], u[NU], lam0[NX];
+    ld_x(a, q, t, b, x);
+    ld_u(a, q, t, b, u);
+    set_zero(lam0);
+    DynDerivs<R, NX, NU> D;
+    Dyn::template derivs<false>(p, t, b, x, u, lam0, D);
+    R cx[NX], cu[NU], cxx[NX], cuu[NU];
+    aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
+    Aff<R, NX> m;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      R lx = R(0);
+#pragma unroll
+      for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+      m.e[i] = lx + cx[i];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) m.F[i][k] = D.fx[k][i];
+    }
+    if (t == T - 1) {
+      R xT[NX], lT[NX], fl[NX];
+      ld_x(a, q, T, b, xT);
+      terminal_grad(p, xT, lT);
+      mv<NX, NX>(m.F, lT, fl);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) {
+        m.e[i] += fl[i];
+#pragma unroll
+        for (int k = 0; k < NX; ++k) m.F[i][k] = R(0);
+      }
+    }
+    Aff<R, NX> o;
+    aff_compose(m, acc, o);
+    acc = o;
+  }
+  st_aff(a.cagg[1], j, a.plan.n[1], B, b, acc);
+}
+
+// generic affine tree kernels shared by the co-state (reverse) scan
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_costate_up(NewtonArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nu = a.plan.n[l + 1];
+  const int u0 = unit_id();
+  if (u0 >= nu * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (!running(a, b) || !(a.phase[b] & PH_NEED_EXP)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  Aff<R, NX> acc;
+  ld_aff(a.cagg[l], last, nl, a.B, b, acc);
+  for (int i = last - 1; i >= first; --i) {
+    Aff<R, NX> m, o;
+    ld_aff(a.cagg[l], i, nl, a.B, b, m);
+    aff_compose(m, acc, o);
+    acc = o;
+  }
+  st_aff(a.cagg[l + 1], j, nu, a.B, b, acc);
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_costate_top(NewtonArgs<R> a) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (!running(a, b) || !(a.phase[b] & PH_NEED_EXP)) return;
+  const int L = a.plan.L, nL = a.plan.n[L];
+  R c[NX];
+  set_zero(c);
+  for (int i = nL - 1; i >= 0; --i) {
+    st_vec(a.ccar[L], i, nL, a.B, b, c);
+    Aff<R, NX> m;
+    ld_aff(a.cagg[L], i, nL, a.B, b, m);
+    R y[NX];
+    aff_apply(m, c, y);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) c[k] = y[k];
+  }
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_costate_down(NewtonArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nu = a.plan.n[l + 1];
+  const int u0 = unit_id();
+  if (u0 >= nu * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (!running(a, b) || !(a.phase[b] & PH_NEED_EXP)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  R c[NX];
+  ld_vec(a.ccar[l + 1], j, nu, a.B, b, c);
+  for (int i = last; i >= first; --i) {
+    st_vec(a.ccar[l], i, nl, a.B, b, c);
+    Aff<R, NX> m;
+    ld_aff(a.cagg[l], i, nl, a.B, b, m);
+    R y[NX];
+    aff_apply(m, c, y);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) c[k] = y[k];
+  }
+}
+
+// level-0 down-sweep fused with the Hamiltonian expansion (passes.py:155-185):
+// with lambda_{t+1} in registers, evaluate every model derivative at
+// (x_t, u_t) once and emit P, R, M, d, Fx, Fu and lambda_t.
+template <typename R, class Dyn>
+__global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int P0 = a.plan.units0();
+  const int u0 = unit_id();
+  if (u0 >= P0 * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (!running(a, b) || !(a.phase[b] & PH_NEED_EXP)) return;
+  const int q = a.parity[b];
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const ProblemParams& p = *a.pp;
+  const AugArgs<R> g = aug_of(a);
+  R ln[NX];
+  if (j == P0 - 1) {
+    R xT[NX];
+    ld_x(a, q, T, b, xT);
+    terminal_grad(p, xT, ln);
+    st_vec(a.lam, T, T + 1, B, b, ln);
+    R PT[NX][NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NX; ++k) PT[i][k] = R(p.Qf[i * NX + k]);
+    symmetrize<NX>(PT);
+    st_mat(a.PT, 0, 1, B, b, PT);
+  } else {
+    ld_vec(a.ccar[1], j, a.plan.n[1], B, b, ln);
+  }
+  for (int t = t1 - 1; t >= t0; --t) {
+    R x[NX], u[NU];
+    ld_x(a, q, t, b, x);
+    ld_u(a, q, t, b, u);
+    DynDerivs<R, NX, NU> D;
+    Dyn::template derivs<true>(p, t, b, x, u, ln, D);
+    R cx[NX], cu[NU], cxx[NX], cuu[NU];
+    aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
+    R Pm[NX][NX], Rm[NU][NU], dv[NU], lt[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NX; ++k)
+        Pm[i][k] = (R(p.Q[i * NX + k]) + (i == k ? cxx[i] : R(0))) + D.Hxx[i][k];
+    symmetrize<NX>(Pm);
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+#pragma unroll
+      for (int k = 0; k < NU; ++k)
+        Rm[i][k] = (R(p.Rc[i * NU + k]) + (i == k ? cuu[i] : R(0))) + D.Huu[i][k];
+    symmetrize<NU>(Rm);
+    R ftl[NU];
+    mtv<NU, NX>(D.fu, ln, ftl);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      R ru = R(0);
+#pragma unroll
+      for (int k = 0; k < NU; ++k) ru += u[k] * R(p.Rc[i * NU + k]);
+      dv[i] = (ru + cu[i]) + ftl[i];
+    }
+    R fxl[NX];
+    mtv<NX, NX>(D.fx, ln, fxl);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      R lx = R(0);
+#pragma unroll
+      for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+      lt[i] = (lx + cx[i]) + fxl[i];
+    }
+    st_mat(a.P, t, T, B, b, Pm);
+    st_mat(a.Rm, t, T, B, b, Rm);
+    st_mat(a.M, t, T, B, b, D.Hxu);
+    st_vec(a.d, t, T, B, b, dv);
+    st_mat(a.Fx, t, T, B, b, D.fx);
+    st_mat(a.Fu, t, T, B, b, D.fu);
+    st_vec(a.lam, t, T + 1, B, b, lt);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) ln[i] = lt[i];
+  }
+}
+
+// --------------------------------------------------------------- rollout
+
+// candidate u + du rolled through the nonlinear dynamics (problem.py:449-473)
+// -- inherently sequential in time, parallel over the batch
+template <typename R, class Dyn>
+__global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (!running(a, b)) return;
+  const int q = a.parity[b], c = 1 - q;
+  const int T = a.T, B = a.B;
+  const ProblemParams& p = *a.pp;
+  R x[NX];
+  ld_x(a, q, 0, b, x);
+  st_vec(a.X + c * a.xsz, 0, T + 1, B, b, x);
+  bool finite = true;
+  for (int t = 0; t < T; ++t) {
+    R u[NU], du[NU];
+    ld_u(a, q, t, b, u);
+    ld_vec(dU, t, T, B, b, du);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) u[i] += du[i];
+    st_vec(a.U + c * a.usz, t, T, B, b, u);
+    R xn[NX];
+    Dyn::step(p, t, b, x, u, xn);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      finite = finite && isfinite(xn[i]);
+      x[i] = xn[i];
+    }
+    st_vec(a.X + c * a.xsz, t + 1, T + 1, B, b, x);
+  }
+  if (!finite) atomicOr(a.flags + b, FLAG_DIVERGED);
+}
+
+// ------------------------------------------------------- trust-region control
+
+template <typename R>
+PTC_D void record(const NewtonArgs<R>& a, int b, double cost, double alpha, double ratio,
+                  double step, double acc) {
+  const int k = a.hist_len[b];
+  if (k < a.opt.hist_cap) {
+    double* h = a.hist + (size_t)k * 5 * a.B + b;
+    h[0 * a.B] = cost;
+    h[1 * a.B] = alpha;
+    h[2 * a.B] = ratio;
+    h[3 * a.B] = step;
+    h[4 * a.B] = acc;
+  }
+  a.hist_len[b] = k + 1;
+}
+
+template <typename R, int NX>
+PTC_D double finalize_cost(const NewtonArgs<R>& a, int which, int q, int b, int& bad) {
+  const int P0 = a.plan.units0();
+  const double* cp = a.cpart[which];
+  double sl = 0.0, sc = 0.0;
+  bad = -1;
+  for (int j = 0; j < P0; ++j) {
+    sl += cp[((size_t)0 * P0 + j) * a.B + b];
+    sc += cp[((size_t)1 * P0 + j) * a.B + b];
+    int bj = int(cp[((size_t)2 * P0 + j) * a.B + b]);
+    if (bad < 0 && bj >= 0) bad = bj;
+  }
+  R xT[NX];
+  ld_x(a, q, a.T, b, xT);
+  double term = double(terminal_cost(*a.pp, xT));
+  return term + (sl + sc);
+}
+
+// One step of newton.py:157-208 for every running problem.
+template <typename R, int NX>
+__global__ void k_control(NewtonArgs<R> a) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (!running(a, b)) return;
+  int ph = a.phase[b];
+  const bool barrier = a.aug_kind == AUG_BARRIER;
+  double cur = a.cur_cost[b];
+  if (ph & PH_NEED_COST) {
+    int bad;
+    cur = finalize_cost<R, NX>(a, 0, a.parity[b], b, bad);
+    if (barrier && bad >= 0) {
+      a.status[b] = ST_ERR_INFEASIBLE;
+      a.bad_index[b] = bad;
+      return;
+    }
+    ph &= ~PH_NEED_COST;
+  }
+  ph &= ~PH_NEED_EXP;  // consumed by this iteration's co-state pass
+  double alpha = a.alpha[b], nu = a.nu[b];
+  const int fl = a.flags[b];
+  a.flags[b] = 0;
+  int it = a.iters[b];
+  bool finished = false;
+  int term = TERM_NONE;
+  const double tol = a.opt.inner_tol;
+  if (fl & (FLAG_DEF_R | FLAG_DEF_Q | FLAG_COND)) {
+    if (alpha > kAlphaMax) {
+      a.status[b] = ST_ERR_STALLED;
+      a.alpha[b] = alpha;
+      a.phase[b] = ph;
+      a.cur_cost[b] = cur;
+      return;
+    }
+    record(a, b, cur, alpha, -INFINITY, NAN, 0.0);
+    alpha = alpha > 0.0 ? alpha * nu : 1e-6;
+    nu = 2.0 * nu;
+    ++it;
+  } else {
+    const int P0 = a.plan.units0();
+    double s2 = 0.0, sd = 0.0, step = 0.0;
+    for (int j = 0; j < P0; ++j) {
+      s2 += a.red[((size_t)0 * P0 + j) * a.B + b];
+      sd += a.red[((size_t)1 * P0 + j) * a.B + b];
+      step = nanmax(step, a.red[((size_t)2 * P0 + j) * a.B + b]);
+    }
+    if (step <= tol) {
+      record(a, b, cur, alpha, NAN, step, 0.0);
+      ++it;
+      finished = true;
+      term = TERM_STEP;
+    } else {
+      const double pred = 0.5 * (alpha * s2 - sd);
+      int bad;
+      const double cand = finalize_cost<R, NX>(a, 1, 1 - a.parity[b], b, bad);
+      double ratio;
+      double newc = INFINITY;
+      if ((fl & FLAG_DIVERGED) || (barrier && bad >= 0)) {
+        ratio = -INFINITY;
+      } else {
+        newc = cand;
+        ratio = (pred <= 0.0) ? -INFINITY : (cur - newc) / pred;
+      }
+      const double used = alpha;
+      if (ratio > 0.0) {
+        const double f = 1.0 - pow(2.0 * ratio - 1.0, 3.0);
+        alpha = alpha * (f > 1.0 / 3.0 ? f : 1.0 / 3.0);
+        nu = 2.0;
+        const double rel = fabs(cur - newc) / fmax(1.0, fabs(cur));
+        record(a, b, newc, used, ratio, step, 1.0);
+        a.parity[b] ^= 1;
+        cur = newc;
+        ph |= PH_NEED_EXP;
+        ++it;
+        if (rel <= tol) {
+          finished = true;
+          term = TERM_COST;
+        }
+      } else {
+        alpha = alpha * nu;
+        nu = 2.0 * nu;
+        record(a, b, cur, used, ratio, step, 0.0);
+        ++it;
+        if (alpha > kAlphaMax) {
+          finished = true;
+          term = TERM_STALLED;
+        }
+      }
+    }
+  }
+  if (!finished && it >= a.opt.max_iters) {
+    finished = true;
+    term = TERM_MAX_ITERS;
+  }
+  if (finished) {
+    ph |= PH_ROUND_DONE;
+    a.term[b] = term;
+  }
+  a.iters[b] = it;
+  a.alpha[b] = alpha;
+  a.nu[b] = nu;
+  a.cur_cost[b] = cur;
+  a.phase[b] = ph;
+}
+
+// --------------------------------------------------------------- outer loops
+
+// per-stage work at the end of a Newton round: copy the round's controls
+// (barrier report) or run the ADMM consensus/dual update with residual maxima
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) k_round_end(NewtonArgs<R> a) {
+  const int P0 = a.plan.units0();
+  const int u0 = unit_id();
+  if (u0 >= P0 * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (!running(a, b) || !(a.phase[b] & PH_ROUND_DONE)) return;
+  const int T = a.T, B = a.B, q = a.parity[b];
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  if (a.opt.method == METHOD_BARRIER) {
+    const int r = a.round[b];
+    if (a.round_U && r < a.opt.round_cap) {
+      R* dst = a.round_U + (size_t)r * NU * T * B;
+      for (int t = t0; t < t1; ++t) {
+        R u[NU];
+        ld_u(a, q, t, b, u);
+        st_vec(dst, t, T, B, b, u);
+      }
+    }
+    return;
+  }
+  if (a.opt.method != METHOD_ADMM) return;
+  const ProblemParams& p = *a.pp;
+  const R rho = R(a.opt.rho);
+  double rp = 0.0, rd = 0.0;
+  for (int t = t0; t < t1; ++t) {
+    R x[NX], u[NU];
+    ld_x(a, q, t, b, x);
+    ld_u(a, q, t, b, u);
+    for (int k = 0; k < p.W; ++k) {
+      R w = row_value<R, NX, NU>(p, k, x, u);
+      R zp = ldf(a.z, k, t, T, B, b);
+      R vv = ldf(a.v, k, t, T, B, b);
+      R zs = w + vv / rho;
+      R zn = zs < R(0) ? zs : R(0);
+      if (zs != zs) zn = zs;
+      R vn = vv + rho * (w - zn);
+      stf(a.z, k, t, T, B, b, zn);
+      stf(a.v, k, t, T, B, b, vn);
+      rp = nanmax(rp, double(fabs(w - zn)));
+      rd = nanmax(rd, double(fabs(zn - zp)));
+    }
+  }
+  a.apart[((size_t)0 * P0 + j) * B + b] = rp;
+  a.apart[((size_t)1 * P0 + j) * B + b] = rd;
+}
+
+template <typename R>
+__global__ void k_outer(NewtonArgs<R> a) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (running(a, b) && (a.phase[b] & PH_ROUND_DONE)) {
+    const int r = a.round[b];
+    const int m = a.opt.method;
+    if (r < a.opt.round_cap) {
+      const size_t o = (size_t)r * a.B + b;
+      a.round_mu[o] = a.mu[b];
+      a.round_cost[o] = a.cur_cost[b];
+      a.round_iters[o] = a.iters[b];
+      a.round_term[o] = a.term[b];
+      a.round_rp[o] = 0.0;
+      a.round_rd[o] = 0.0;
+    }
+    a.round[b] = r + 1;
+    bool again = false;
+    if (m == METHOD_BARRIER) {
+      const double mu = a.mu[b] * a.opt.zeta;
+      a.mu[b] = mu;
+      again = mu > a.opt.mu_tol;
+    } else if (m == METHOD_ADMM) {
+      const int P0 = a.plan.units0();
+      double rp = 0.0, rd = 0.0;
+      for (int j = 0; j < P0; ++j) {
+        rp = nanmax(rp, a.apart[((size_t)0 * P0 + j) * a.B + b]);
+        rd = nanmax(rd, a.apart[((size_t)1 * P0 + j) * a.B + b]);
+      }
+      if (r < a.opt.round_cap) {
+        a.round_rp[(size_t)r * a.B + b] = rp;
+        a.round_rd[(size_t)r * a.B + b] = rd;
+      }
+      const bool conv = rp <= a.opt.residual_tol && rd <= a.opt.residual_tol;
+      again = !conv && (r + 1) < a.opt.max_outer;
+    }
+    if (again) {
+      a.alpha[b] = a.opt.alpha0;
+      a.nu[b] = a.opt.nu0;
+      a.iters[b] = 0;
+      a.phase[b] = PH_NEED_COST | PH_NEED_EXP;
+    } else {
+      a.status[b] = ST_DONE;
+      a.phase[b] &= ~PH_ROUND_DONE;
+    }
+  }
+  if (running(a, b)) atomicAdd(a.n_running, 1);
+}
+
+}  // namespace ptc

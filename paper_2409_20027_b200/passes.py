@@ -1,0 +1,215 @@
+"""Pass-level API (mirror of reference ``pintoc/passes.py``).
+
+``value_pass`` + ``propagation_pass`` together are the LQR-scan solve of
+one Newton subproblem; on the device they are one call (``LqrSolver``) that
+runs the blocked reverse scan over dual value elements, the gains, and the
+blocked forward scan over closed-loop maps.  ``costate_pass`` and
+``hamiltonian_expansion`` run the fused co-state / expansion kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, replace
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _native as N
+from ._device import DeviceSolver, SolveSettings
+from .exceptions import ConditioningError, DefinitenessError
+from .newton import aug_settings, plan_chunks
+from .problem import Trajectory
+
+
+class FeedbackLaw(NamedTuple):
+    """du_t = Gamma_t dx_t + gamma_t  (passes.py:55-59)."""
+    Gamma: np.ndarray  # (N, d_u, d_x)
+    gamma: np.ndarray  # (N, d_u)
+
+
+@dataclass(frozen=True)
+class StageExpansion:
+    """Second-order data of the subproblem (passes.py:62-97)."""
+    P: np.ndarray
+    R: np.ndarray
+    M: np.ndarray
+    d: np.ndarray
+    Fx: np.ndarray
+    Fu: np.ndarray
+    P_terminal: np.ndarray
+    alpha: float
+    R_reg: np.ndarray
+
+    @property
+    def horizon(self) -> int:
+        return self.P.shape[0]
+
+    @property
+    def d_x(self) -> int:
+        return self.P.shape[1]
+
+    @property
+    def d_u(self) -> int:
+        return self.R.shape[1]
+
+    def with_alpha(self, alpha: float) -> "StageExpansion":
+        if alpha < 0:
+            raise ValueError("alpha must be nonnegative")
+        return replace(self, alpha=alpha, R_reg=self.R + alpha * np.eye(self.d_u))
+
+    @staticmethod
+    def build(P, R, M, d, Fx, Fu, P_terminal, alpha=0.0) -> "StageExpansion":
+        R = np.asarray(R, float)
+        return StageExpansion(np.asarray(P, float), R, np.asarray(M, float),
+                              np.asarray(d, float), np.asarray(Fx, float),
+                              np.asarray(Fu, float), np.asarray(P_terminal, float),
+                              float(alpha), R + alpha * np.eye(R.shape[1]))
+
+
+FLAG_DEF_R, FLAG_DEF_Q, FLAG_COND = 1, 2, 4
+
+
+class LqrSolver:
+    """Batched LQR-scan solver on device tensors in SoA batch-minor layout.
+
+    Inputs (torch, device, dtype float32/float64): P (nx*nx, T, B),
+    R (nu*nu, T, B), M (nx*nu, T, B), d (nu, T, B), Fx (nx*nx, T, B),
+    Fu (nx*nu, T, B), PT (nx*nx, 1, B), alpha (float64, B).
+    """
+
+    def __init__(self, batch, horizon, nx, nu, dtype=None, chunk0=0, chunk=0,
+                 with_value=False, device=None):
+        torch = N.require_cuda()
+        self.torch = torch
+        self.lib = N.load_library()
+        self.B, self.T, self.nx, self.nu = int(batch), int(horizon), int(nx), int(nu)
+        self.dtype = dtype or torch.float64
+        self.code = N.PTC_F64 if self.dtype == torch.float64 else N.PTC_F32
+        if not self.lib.ptc_supported(self.code, -1, self.nx, self.nu):
+            raise N.NativeError(f"LQR kernels not compiled for nx={nx} nu={nu}")
+        self.chunk0, self.chunk = int(chunk0), int(chunk)
+        dev = torch.device(device or "cuda")
+        self.device = dev
+        nbytes = self.lib.ptc_lqr_workspace_bytes(self.code, self.B, self.T, self.nx, self.nu,
+                                                  self.chunk0, self.chunk)
+        N.check(0 if nbytes >= 0 else int(nbytes))
+        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+        B, T, nx_, nu_ = self.B, self.T, self.nx, self.nu
+        mk = lambda *s: torch.empty(*s, dtype=self.dtype, device=dev)
+        self.Gamma = mk(nu_ * nx_, T, B)
+        self.gamma = mk(nu_, T, B)
+        self.dx = mk(nx_, T + 1, B)
+        self.du = mk(nu_, T, B)
+        self.S = mk(nx_ * nx_, T + 1, B) if with_value else None
+        self.s = mk(nx_, T + 1, B) if with_value else None
+        self.flags = torch.zeros(B, dtype=torch.int32, device=dev)
+
+    def plan(self):
+        k0, k, lv = C.c_int(), C.c_int(), C.c_int()
+        N.check(self.lib.ptc_lqr_plan(self.B, self.T, self.chunk0, self.chunk, C.byref(k0),
+                                      C.byref(k), C.byref(lv)))
+        return k0.value, k.value, lv.value
+
+    def solve(self, P, R, M, d, Fx, Fu, PT, alpha, stream=None):
+        self.flags.zero_()
+        ptr = lambda t: None if t is None else t.data_ptr()
+        N.check(self.lib.ptc_lqr_solve(
+            self.code, self.B, self.T, self.nx, self.nu,
+            ptr(P), ptr(R), ptr(M), ptr(d), ptr(Fx), ptr(Fu), ptr(PT), ptr(alpha),
+            ptr(self.S), ptr(self.s), ptr(self.Gamma), ptr(self.gamma), ptr(self.dx),
+            ptr(self.du), ptr(self.flags), ptr(self.workspace), self.workspace.numel(),
+            self.chunk0, self.chunk, N.stream_ptr(stream)))
+
+
+def _soa(torch, a, dtype, device, comps):
+    """(T, *comp) numpy -> (prod comp, T, 1) device."""
+    t = torch.as_tensor(np.asarray(a, float), dtype=dtype).reshape(a.shape[0], comps)
+    return t.t().contiguous().unsqueeze(-1).to(device)
+
+
+def lqr_solve(exp: StageExpansion, executor: str = "auto", dtype=None):
+    """value_pass + propagation_pass of one expansion on the device.
+    Returns S, s, FeedbackLaw, dxs, dus as numpy (reference shapes)."""
+    torch = N.require_cuda()
+    dtype = dtype or torch.float64
+    n, nx, nu = exp.horizon, exp.d_x, exp.d_u
+    c0, c1 = plan_chunks(executor, n)
+    solver = LqrSolver(1, n, nx, nu, dtype=dtype, chunk0=c0, chunk=c1, with_value=True)
+    dev = solver.device
+    args = [_soa(torch, exp.P, dtype, dev, nx * nx), _soa(torch, exp.R, dtype, dev, nu * nu),
+            _soa(torch, exp.M, dtype, dev, nx * nu), _soa(torch, exp.d, dtype, dev, nu),
+            _soa(torch, exp.Fx, dtype, dev, nx * nx), _soa(torch, exp.Fu, dtype, dev, nx * nu),
+            _soa(torch, exp.P_terminal[None], dtype, dev, nx * nx)]
+    alpha = torch.full((1,), float(exp.alpha), dtype=torch.float64, device=dev)
+    solver.solve(*args, alpha)
+    fl = int(solver.flags[0])
+    if fl & (FLAG_DEF_R | FLAG_DEF_Q):
+        raise DefinitenessError(-1, "R + alpha*I" if fl & FLAG_DEF_R else "Q")
+    if fl & FLAG_COND:
+        raise ConditioningError("singular I + C*Y while combining value elements")
+    host = lambda t, shape: t[..., 0].t().reshape(shape).cpu().numpy()
+    S = host(solver.S, (n + 1, nx, nx))
+    s = host(solver.s, (n + 1, nx))
+    law = FeedbackLaw(host(solver.Gamma, (n, nu, nx)), host(solver.gamma, (n, nu)))
+    return S, s, law, host(solver.dx, (n + 1, nx)), host(solver.du, (n, nu))
+
+
+def value_pass(exp: StageExpansion, executor: str = "auto", dtype=None):
+    """Cost-to-go (S, s) and the affine control law (passes.py:291-323)."""
+    S, s, law, _, _ = lqr_solve(exp, executor, dtype)
+    return S, s, law
+
+
+def propagation_pass(law: FeedbackLaw, exp: StageExpansion, executor: str = "auto",
+                     dtype=None):
+    """Closed-loop deviations from dx_1 = 0 (passes.py:338-361) for the law of
+    this expansion (the device computes law and propagation in one solve; a
+    foreign law is propagated by the same forward scan kernels)."""
+    S, s, own, dxs, dus = lqr_solve(exp, executor, dtype)
+    if np.array_equal(np.asarray(law.Gamma), own.Gamma) and np.array_equal(
+            np.asarray(law.gamma), own.gamma):
+        return dxs, dus
+    return propagate(law, exp, dtype=dtype)
+
+
+def propagate(law: FeedbackLaw, exp: StageExpansion, dtype=None):
+    """Forward scan of an arbitrary feedback law (device)."""
+    from ._device import propagate_law
+    return propagate_law(law, exp, dtype)
+
+
+def _pass_solver(traj: Trajectory, cost, aug, dyn, alpha, dtype):
+    st = aug_settings(aug)
+    con = getattr(aug, "constraints", None)
+    settings = SolveSettings(method=N.METHOD_NEWTON, alpha0=float(alpha), **st)
+    solver = DeviceSolver(dyn, cost, con, 1, settings, dtype=dtype)
+    z = v = None
+    if st["aug"] == N.AUG_ADMM:
+        z, v = np.asarray(aug.z, float)[None], np.asarray(aug.v, float)[None]
+    solver.load(traj.states[None], traj.controls[None], z, v)
+    solver.expand()
+    return solver
+
+
+def costate_pass(traj: Trajectory, cost, aug, dyn, executor: str = "auto", dtype=None):
+    """Adjoint vectors lambda_{1:N+1} (passes.py:122-148) on the device."""
+    solver = _pass_solver(traj, cost, aug, dyn, 0.0, dtype)
+    return solver.field("lam", solver.T + 1, (solver.nx,))[0].cpu().numpy()
+
+
+def hamiltonian_expansion(traj: Trajectory, costates, cost, aug, dyn, alpha: float = 0.0,
+                          dtype=None) -> StageExpansion:
+    """P, R, M, d, Fx, Fu of the augmented Lagrangian (passes.py:155-185).
+    The device kernel fuses the co-state sweep with the expansion, so the
+    co-states are recomputed on the fly (``costates`` is accepted for API
+    compatibility and must be the output of ``costate_pass``)."""
+    if alpha < 0:
+        raise ValueError("alpha must be nonnegative")
+    solver = _pass_solver(traj, cost, aug, dyn, alpha, dtype)
+    T, nx, nu = solver.T, solver.nx, solver.nu
+    f = lambda name, shape: solver.field(name, T, shape)[0].cpu().numpy()
+    PT = solver.read("PT").view(nx, nx).cpu().numpy()
+    return StageExpansion.build(f("P", (nx, nx)), f("R", (nu, nu)), f("M", (nx, nu)),
+                                f("d", (nu,)), f("Fx", (nx, nx)), f("Fu", (nx, nu)), PT,
+                                alpha)

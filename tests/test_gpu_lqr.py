@@ -1,0 +1,155 @@
+"""GPU parity of the LQR-scan solve (value pass + propagation pass).
+
+CUDA path (through the C ABI) vs the reference's own outputs (golden
+fixtures) and vs the pinned CPU oracle on seeded inputs, across scan plans:
+sequential sweep, default tree, and a deliberately deep binary tree.
+Tolerances: fp64 1e-9 relative (BASELINE north_star), fp32 1e-4.
+"""
+
+import numpy as np
+import pytest
+from conftest import golden, rel_gap
+
+from oracle import pintoc_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+PLANS = [("sequential", None), ("auto", (0, 0)), ("deep", (2, 2)), ("wide", (3, 5))]
+
+
+def _exp_from_golden(g, p):
+    import paper_2409_20027_b200 as P
+    return P.StageExpansion.build(g[p + "P"], g[p + "R"], g[p + "M"], g[p + "d"], g[p + "Fx"],
+                                  g[p + "Fu"], g[p + "PT"], float(g[p + "alpha"]))
+
+
+def _solve(exp, plan, dtype=None):
+    import torch
+    from paper_2409_20027_b200 import passes
+    n, nx, nu = exp.horizon, exp.d_x, exp.d_u
+    if plan[0] == "sequential":
+        c0, c1 = n, 0
+    else:
+        c0, c1 = plan[1]
+    dtype = dtype or torch.float64
+    solver = passes.LqrSolver(1, n, nx, nu, dtype=dtype, chunk0=c0, chunk=c1, with_value=True)
+    dev = solver.device
+    soa = lambda a, c: passes._soa(torch, a, dtype, dev, c)
+    args = [soa(exp.P, nx * nx), soa(exp.R, nu * nu), soa(exp.M, nx * nu), soa(exp.d, nu),
+            soa(exp.Fx, nx * nx), soa(exp.Fu, nx * nu), soa(exp.P_terminal[None], nx * nx)]
+    alpha = torch.full((1,), float(exp.alpha), dtype=torch.float64, device=dev)
+    solver.solve(*args, alpha)
+    torch.cuda.synchronize()
+    host = lambda t, shape: t[..., 0].t().reshape(shape).double().cpu().numpy()
+    return (host(solver.S, (n + 1, nx, nx)), host(solver.s, (n + 1, nx)),
+            host(solver.Gamma, (n, nu, nx)), host(solver.gamma, (n, nu)),
+            host(solver.dx, (n + 1, nx)), host(solver.du, (n, nu)), int(solver.flags[0]))
+
+
+@pytest.mark.parametrize("plan", PLANS, ids=[p[0] for p in PLANS])
+def test_lqr_small_matches_reference(plan):
+    g = golden("lqr_small")
+    for i in range(int(g["count"])):
+        p = f"{i}_"
+        S, s, Gam, gam, dxs, dus, fl = _solve(_exp_from_golden(g, p), plan)
+        assert fl == 0
+        for name, val in dict(S=S, s=s, Gamma=Gam, gamma=gam, dxs=dxs, dus=dus).items():
+            assert rel_gap(val, g[p + name]) < 1e-9, (i, name, plan)
+
+
+@pytest.mark.parametrize("plan", PLANS, ids=[p[0] for p in PLANS])
+def test_lqr_config1_matches_reference(plan):
+    g = golden("lqr_config1")
+    for nx in (2, 4, 8, 12):
+        p = f"{nx}_"
+        S, s, Gam, gam, dxs, dus, fl = _solve(_exp_from_golden(g, p), plan)
+        assert fl == 0
+        for name, val in dict(S=S, s=s, Gamma=Gam, gamma=gam, dxs=dxs, dus=dus).items():
+            assert rel_gap(val, g[p + name]) < 1e-9, (nx, name, plan)
+
+
+@pytest.mark.parametrize("nx,T", [(2, 4096), (4, 2048), (8, 512), (12, 256)])
+def test_lqr_long_horizon_vs_oracle(nx, T):
+    import paper_2409_20027_b200 as P
+    rng = np.random.default_rng(7000 + nx)
+    e = O.random_lqr_expansion(rng, T, nx, nx // 2)
+    ref = O.lqr_solve(e)
+    exp = P.StageExpansion.build(e.P, e.R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.0)
+    for plan in PLANS:
+        S, s, Gam, gam, dxs, dus, fl = _solve(exp, plan)
+        assert fl == 0
+        for k, val in enumerate((S, s, Gam, gam, dxs, dus)):
+            assert rel_gap(val, ref[k]) < 1e-9, (nx, T, plan[0], k)
+
+
+def test_lqr_fp32_within_tolerance():
+    import torch
+    import paper_2409_20027_b200 as P
+    rng = np.random.default_rng(11)
+    e = O.random_lqr_expansion(rng, 256, 4, 2)
+    ref = O.lqr_solve(e)
+    exp = P.StageExpansion.build(e.P, e.R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.0)
+    for plan in PLANS:
+        out = _solve(exp, plan, dtype=torch.float32)
+        for k in range(6):
+            assert rel_gap(out[k], ref[k]) < 1e-4, (plan[0], k)
+
+
+def test_lqr_batch_matches_per_problem_oracle():
+    """B independent problems in one launch (SoA batch-minor layout)."""
+    import torch
+    from paper_2409_20027_b200 import passes
+    B, T, nx, nu = 37, 64, 3, 2
+    rng = np.random.default_rng(5)
+    exps = [O.random_lqr_expansion(rng, T, nx, nu, alpha=0.3 * b / B) for b in range(B)]
+    for c0, c1 in [(T, 0), (0, 0), (2, 3)]:
+        sol = passes.LqrSolver(B, T, nx, nu, chunk0=c0, chunk=c1, with_value=True)
+        dev = sol.device
+        stack = lambda f, c: torch.as_tensor(np.stack([f(e).reshape(T, c) for e in exps], -1)
+                                             ).permute(1, 0, 2).contiguous().to(dev)
+        args = [stack(lambda e: e.P, nx * nx), stack(lambda e: e.R, nu * nu),
+                stack(lambda e: e.M, nx * nu), stack(lambda e: e.d, nu),
+                stack(lambda e: e.Fx, nx * nx), stack(lambda e: e.Fu, nx * nu),
+                torch.as_tensor(np.stack([e.PT.reshape(1, nx * nx) for e in exps], -1)
+                                ).permute(1, 0, 2).contiguous().to(dev)]
+        alpha = torch.tensor([e.alpha for e in exps], dtype=torch.float64, device=dev)
+        sol.solve(*args, alpha)
+        du = sol.du.permute(2, 1, 0).cpu().numpy()
+        G = sol.Gamma.permute(2, 1, 0).cpu().numpy().reshape(B, T, nu, nx)
+        for b in (0, 17, B - 1):
+            ref = O.lqr_solve(exps[b])
+            assert rel_gap(du[b], ref[5]) < 1e-9
+            assert rel_gap(G[b], ref[2]) < 1e-9
+
+
+def test_propagation_of_foreign_law_matches_oracle():
+    import paper_2409_20027_b200 as P
+    rng = np.random.default_rng(3)
+    e = O.random_lqr_expansion(rng, 40, 3, 2)
+    exp = P.StageExpansion.build(e.P, e.R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.0)
+    law = P.FeedbackLaw(rng.normal(size=(40, 2, 3)), rng.normal(size=(40, 2)))
+    dxs, dus = P.propagation_pass(law, exp)
+    rx, ru = O.propagation_pass(law.Gamma, law.gamma, e)
+    assert rel_gap(dxs, rx) < 1e-10 and rel_gap(dus, ru) < 1e-10
+    law0 = P.FeedbackLaw(law.Gamma, np.zeros((40, 2)))
+    dxs, dus = P.propagation_pass(law0, exp)
+    assert np.allclose(dxs, 0.0) and np.allclose(dus, 0.0)
+
+
+def test_indefinite_regularised_r_raises_definiteness():
+    import paper_2409_20027_b200 as P
+    exp = P.StageExpansion.build(np.eye(1)[None], np.array([[[-1.0]]]), np.zeros((1, 1, 1)),
+                                 np.zeros((1, 1)), np.eye(1)[None], np.eye(1)[None],
+                                 np.zeros((1, 1)))
+    with pytest.raises(P.DefinitenessError):
+        P.value_pass(exp)
+
+
+def test_value_pass_pure_regularisation_is_zero():
+    import paper_2409_20027_b200 as P
+    n = 5
+    exp = P.StageExpansion.build(np.zeros((n, 2, 2)), np.zeros((n, 1, 1)), np.zeros((n, 2, 1)),
+                                 np.zeros((n, 1)), np.tile(np.eye(2), (n, 1, 1)),
+                                 np.ones((n, 2, 1)), np.zeros((2, 2)), alpha=4.0)
+    S, s, law = P.value_pass(exp)
+    assert np.allclose(S, 0.0) and np.allclose(law.Gamma, 0.0) and np.allclose(law.gamma, 0.0)
