@@ -132,6 +132,8 @@ class DeviceSolver:
     def to_soa(self, arr, rows: int, comps: int):
         """(B, rows, comps) array/tensor -> device (comps, rows, B) contiguous."""
         torch = self.torch
+        if isinstance(arr, np.ndarray) and not arr.flags.writeable:
+            arr = arr.copy()
         t = torch.as_tensor(arr, dtype=self.dtype)
         if t.dim() == 2:
             t = t.unsqueeze(0)

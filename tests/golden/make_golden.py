@@ -87,6 +87,28 @@ def save(name, **arrays):
     print(f"wrote {path} ({os.path.getsize(path) / 1024:.1f} KiB)")
 
 
+def ulp_nudges(x0, u0):
+    """Two copies of the inputs moved by one ulp (up / down)."""
+    return [(np.nextafter(x0, np.inf), np.nextafter(u0, np.inf)),
+            (np.nextafter(x0, -np.inf), np.nextafter(u0, -np.inf))]
+
+
+def noise_floor(solve, x0, u0, traj, counts):
+    """The reference's own reproducibility: rerun it with the inputs moved by
+    one ulp and record how far its final trajectory moves and whether its
+    iteration counts change.  GPU parity is judged against this floor."""
+    fu = fx = 0.0
+    stable = True
+    for xp, up in ulp_nudges(x0, u0):
+        t2, c2 = solve(xp, up)
+        fu = max(fu, float(np.abs(t2.controls - traj.controls).max()
+                           / max(1.0, np.abs(traj.controls).max())))
+        fx = max(fx, float(np.abs(t2.states - traj.states).max()
+                           / max(1.0, np.abs(traj.states).max())))
+        stable = stable and list(c2) == list(counts)
+    return dict(floor_u=np.array(fu), floor_x=np.array(fx), stable=np.array(stable))
+
+
 def newton_hist(rep):
     h = np.array([(r.cost, r.alpha, r.gain_ratio, r.step_norm, float(r.accepted))
                   for r in rep.history]).reshape(-1, 5)
@@ -196,6 +218,14 @@ def case_newton_lq():
         init = rollout(dyn, x0, np.zeros((n, du)))
         alpha0 = [0.0, 1.0][i % 2]
         traj, rep = newton_solve(dyn, cost, None, init, NewtonOptions(alpha0=alpha0))
+
+        def solve(xp, up, dyn=dyn, cost=cost, alpha0=alpha0, n=n, du=du):
+            t, r = newton_solve(dyn, cost, None, rollout(dyn, xp, up),
+                                NewtonOptions(alpha0=alpha0))
+            return t, [r.iterations]
+        fl = noise_floor(solve, x0, np.zeros((n, du)), traj, [rep.iterations])
+        for k, v in fl.items():
+            out[f"{i}_{k}"] = v
         for k, v in dict(A=A, B=B, Q=Q, R=R, Qf=Qf, goal=goal, x0=x0,
                          alpha0=np.array(alpha0), xs=traj.states, us=traj.controls,
                          hist=newton_hist(rep),
@@ -233,7 +263,34 @@ def case_barrier_pendulum_cfg0():
     wall = time.perf_counter() - t0
     out = dict(x0=x0, u0=u0, wall_s=np.array(wall))
     _barrier_record("sol", traj, rep, out)
+
+    def solve(xp, up):
+        t, r = barrier_solve(prob, rollout(dyn, xp, up), opts)
+        return t, [q.newton.iterations for q in r.rounds]
+    out.update({"sol_" + k: v for k, v in noise_floor(
+        solve, x0, u0, traj, [q.newton.iterations for q in rep.rounds]).items()})
     save("barrier_pendulum_cfg0", **out)
+
+
+def case_barrier_pendulum_conv():
+    """A converging swing-up (reference defaults, N=40, dt=0.05, 300 max
+    iterations): every round terminates on the cost test."""
+    T = 40
+    prob = pintoc.make_swingup_problem("pendulum", T, 0.05)
+    rng = np.random.default_rng(42)
+    u0 = np.clip(rng.standard_normal((T, 1)), -4.5, 4.5)
+    x0 = np.array([math.pi, 0.0])
+    opts = BarrierOptions(newton=NewtonOptions(max_iters=300))
+    traj, rep = barrier_solve(prob, rollout(prob.dynamics, x0, u0), opts)
+    out = dict(x0=x0, u0=u0)
+    _barrier_record("sol", traj, rep, out)
+
+    def solve(xp, up):
+        t, r = barrier_solve(prob, rollout(prob.dynamics, xp, up), opts)
+        return t, [q.newton.iterations for q in r.rounds]
+    out.update({"sol_" + k: v for k, v in noise_floor(
+        solve, x0, u0, traj, [q.newton.iterations for q in rep.rounds]).items()})
+    save("barrier_pendulum_conv", **out)
 
 
 def case_barrier_tvlinear():
@@ -254,6 +311,13 @@ def case_barrier_tvlinear():
     traj, rep = barrier_solve(ControlProblem(dyn, cost, box), init, BarrierOptions())
     out = dict(A=A, B=B, c=c, Q=Q, x0=x0, u0=u0)
     _barrier_record("sol", traj, rep, out)
+
+    def solve(xp, up):
+        t, r = barrier_solve(ControlProblem(dyn, cost, box), rollout(dyn, xp, up),
+                             BarrierOptions())
+        return t, [q.newton.iterations for q in r.rounds]
+    out.update({"sol_" + k: v for k, v in noise_floor(
+        solve, x0, u0, traj, [q.newton.iterations for q in rep.rounds]).items()})
     save("barrier_tvlinear", **out)
 
 
@@ -278,6 +342,12 @@ def case_admm_small():
     traj, rep = admm_solve(prob, init, AdmmOptions(rho=1.0, max_outer=150))
     out.update(pend_x0=x0, pend_u0=u0)
     _admm_record("pend", traj, rep, out)
+
+    def solve(xp, up):
+        t, r = admm_solve(prob, rollout(prob.dynamics, xp, up), AdmmOptions(rho=1.0, max_outer=150))
+        return t, [q.iterations for q in r.newton_reports]
+    out.update({"pend_" + k: v for k, v in noise_floor(
+        solve, x0, u0, traj, [q.iterations for q in rep.newton_reports]).items()})
     # cart-pole, config-2 parameters, short horizon
     T = 60
     dyn = CartPoleDynamics(T, CartPoleParams(cart_mass=1.0, pole_mass=0.1,
@@ -293,6 +363,13 @@ def case_admm_small():
     traj, rep = admm_solve(ControlProblem(dyn, cost, box), init, AdmmOptions(rho=1.0, max_outer=40))
     out.update(cp_x0=x0, cp_u0=u0)
     _admm_record("cp", traj, rep, out)
+
+    def solve2(xp, up):
+        t, r = admm_solve(ControlProblem(dyn, cost, box), rollout(dyn, xp, up),
+                          AdmmOptions(rho=1.0, max_outer=40))
+        return t, [q.iterations for q in r.newton_reports]
+    out.update({"cp_" + k: v for k, v in noise_floor(
+        solve2, x0, u0, traj, [q.iterations for q in rep.newton_reports]).items()})
     save("admm_small", **out)
 
 
@@ -319,7 +396,7 @@ def case_admm_cartpole_cfg2():
 
 
 FAST = [case_lqr_small, case_lqr_config1, case_passes_models, case_newton_lq,
-        case_barrier_pendulum_cfg0, case_barrier_tvlinear, case_admm_small]
+        case_barrier_pendulum_cfg0, case_barrier_pendulum_conv, case_barrier_tvlinear, case_admm_small]
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
