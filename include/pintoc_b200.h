@@ -113,6 +113,38 @@ int ptc_lqr_plan(int batch, int horizon, int chunk0, int chunk, int* out_chunk0,
                  int* out_chunk, int* out_levels);
 
 /* ------------------------------------------------------------------------
+ * Time-sharded LQR solve (BASELINE config 4): the horizon is split into
+ * contiguous blocks, one per rank; same math as ptc_lqr_solve (value_pass +
+ * propagation_pass, passes.py:291 / 338) with the scans' block-boundary
+ * carries exchanged by the caller (one all-gather per scan).  Per rank:
+ *   phase 0: value up-sweep of the local block -> block_out = block value
+ *            aggregate (value_comps, 1, batch)
+ *   [caller all-gathers block_out of every rank, rank-major:
+ *    blocks_in = (world, value_comps, 1, batch)]
+ *   phase 1: carry from the later blocks, value down-sweep, gains (and S, s
+ *            if given; row `horizon` = the cost-to-go handed in), then the
+ *            propagation up-sweep -> block_out = block affine aggregate
+ *            (prop_comps, 1, batch)
+ *   [caller all-gathers: blocks_in = (world, prop_comps, 1, batch)]
+ *   phase 2: deviation entering the block from the earlier blocks, forward
+ *            sweep -> dx (nx, horizon+1, batch; row `horizon` = the next
+ *            block's first deviation), du.
+ * Inputs are the local block's stages (global stages t_base ..
+ * t_base+horizon-1); PT is read only when is_last.  The same workspace
+ * (ptc_lqr_block_workspace_bytes) must be passed to all three phases.
+ * ---------------------------------------------------------------------- */
+int ptc_lqr_block_comps(int nx, int* value_comps, int* prop_comps);
+int64_t ptc_lqr_block_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
+                                      int chunk0, int chunk);
+int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, int nu, int t_base,
+                        int is_last, int rank, int world, const void* P, const void* R,
+                        const void* M, const void* d, const void* Fx, const void* Fu,
+                        const void* PT, const double* alpha, const void* blocks_in,
+                        void* block_out, void* S, void* s, void* Gamma, void* gamma, void* dx,
+                        void* du, int* flags, void* workspace, int64_t workspace_bytes,
+                        int chunk0, int chunk, void* stream);
+
+/* ------------------------------------------------------------------------
  * Batched device-resident solver
  *   one object = `batch` independent problems sharing model, cost and
  *   constraints (per-problem initial trajectories).  Replaces

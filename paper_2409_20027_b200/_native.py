@@ -67,6 +67,10 @@ _SIGS = {
     "ptc_lqr_plan": (C.c_int, [C.c_int] * 4 + [C.POINTER(C.c_int)] * 3),
     "ptc_propagate": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7
                       + [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]),
+    "ptc_lqr_block_comps": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ptc_lqr_block_workspace_bytes": (C.c_int64, [C.c_int] * 7),
+    "ptc_lqr_block_solve": (C.c_int, [C.c_int] * 10 + [C.c_void_p] * 16
+                            + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]),
     "ptc_solver_workspace_bytes": (C.c_int64, [C.POINTER(ProblemDesc)]),
     "ptc_solver_create": (C.c_int, [C.POINTER(ProblemDesc), C.c_void_p, C.c_int64,
                                     C.POINTER(C.c_void_p)]),

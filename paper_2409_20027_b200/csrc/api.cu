@@ -68,7 +68,13 @@ static void carve_lqr_tree(Carver& c, LqrArgs<R>& a, int nx) {
   const size_t B = a.B;
   a.red = c.template take<double>(3 * (size_t)pl.units0() * B);
   for (int l = 0; l <= kMaxLevels; ++l) a.vagg[l] = a.vcar[l] = a.pagg[l] = a.pcar[l] = nullptr;
-  for (int l = 1; l <= pl.L; ++l) {
+  a.vcin_buf = a.xin_buf = nullptr;
+  if (a.block_mode) {
+    a.vcin_buf = c.template take<R>(B * (nx * nx + nx));
+    a.xin_buf = c.template take<R>(B * nx);
+  }
+  const int top = (a.block_mode && pl.L == 0) ? 1 : pl.L;
+  for (int l = 1; l <= top; ++l) {
     const size_t n = (size_t)pl.n[l] * B;
     a.vagg[l] = c.template take<R>(n * (3 * nx * nx + 2 * nx));
     a.vcar[l] = c.template take<R>(n * (nx * nx + nx));
@@ -204,6 +210,91 @@ int ptc_propagate(int dtype, int batch, int horizon, int nx, int nu, const void*
   if (dtype == PTC_F32)
     return propagate_t<float>(batch, horizon, nx, nu, Fx, Fu, Gamma, gamma, d, dx, du, workspace,
                               workspace_bytes, chunk0, chunk, st);
+  return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
+}
+
+int ptc_lqr_block_comps(int nx, int* value_comps, int* prop_comps) {
+  if (nx < 1) return fail(PTC_ERR_ARG, "nx must be >= 1");
+  if (value_comps) *value_comps = 3 * nx * nx + 2 * nx;
+  if (prop_comps) *prop_comps = nx * nx + nx;
+  return PTC_OK;
+}
+
+int64_t ptc_lqr_block_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
+                                      int chunk0, int chunk) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  Carver c{nullptr};
+  if (dtype == PTC_F64) {
+    LqrArgs<double> a{};
+    a.B = batch;
+    a.T = horizon;
+    a.block_mode = 1;
+    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    carve_lqr_tree(c, a, nx);
+  } else {
+    LqrArgs<float> a{};
+    a.B = batch;
+    a.T = horizon;
+    a.block_mode = 1;
+    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    carve_lqr_tree(c, a, nx);
+  }
+  return (int64_t)c.off + 256;
+}
+
+int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, int nu, int t_base,
+                        int is_last, int rank, int world, const void* P, const void* R,
+                        const void* M, const void* d, const void* Fx, const void* Fu,
+                        const void* PT, const double* alpha, const void* blocks_in,
+                        void* block_out, void* S, void* s, void* Gamma, void* gamma, void* dx,
+                        void* du, int* flags, void* workspace, int64_t workspace_bytes,
+                        int chunk0, int chunk, void* stream) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  if (phase < 0 || phase > 2) return fail(PTC_ERR_ARG, "phase must be 0, 1 or 2");
+  if (world < 1 || rank < 0 || rank >= world) return fail(PTC_ERR_ARG, "bad rank / world");
+  if (t_base < 0) return fail(PTC_ERR_ARG, "t_base must be >= 0");
+  if (phase > 0 && blocks_in == nullptr) return fail(PTC_ERR_ARG, "phase 1/2 need blocks_in");
+  if (phase < 2 && block_out == nullptr) return fail(PTC_ERR_ARG, "phase 0/1 need block_out");
+  if (is_last && PT == nullptr) return fail(PTC_ERR_ARG, "the last block needs PT");
+  if ((S == nullptr) != (s == nullptr)) return fail(PTC_ERR_ARG, "S and s must both be given or both NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  auto run = [&](auto zero) -> int {
+    using Rt = decltype(zero);
+    auto it = lqr_registry().find(LqrKey(dtype_code<Rt>(), nx, nu));
+    if (it == lqr_registry().end())
+      return fail(PTC_ERR_UNSUPPORTED, "LQR kernels not instantiated for nx=" +
+                                           std::to_string(nx) + " nu=" + std::to_string(nu));
+    LqrArgs<Rt> a{};
+    a.B = batch;
+    a.T = horizon;
+    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    a.block_mode = 1;
+    a.t_base = t_base;
+    a.no_terminal = is_last ? 0 : 1;
+    a.P = (const Rt*)P;
+    a.Rm = (const Rt*)R;
+    a.M = (const Rt*)M;
+    a.d = (const Rt*)d;
+    a.Fx = (const Rt*)Fx;
+    a.Fu = (const Rt*)Fu;
+    a.PT = (const Rt*)PT;
+    a.alpha = alpha;
+    a.S = (Rt*)S;
+    a.s = (Rt*)s;
+    a.Gam = (Rt*)Gamma;
+    a.gam = (Rt*)gamma;
+    a.dX = (Rt*)dx;
+    a.dU = (Rt*)du;
+    a.flags = flags;
+    Carver c{(char*)workspace};
+    carve_lqr_tree(c, a, nx);
+    if ((int64_t)c.off > workspace_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
+    it->second.block(&a, phase, blocks_in, block_out, rank, world, st);
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  };
+  if (dtype == PTC_F64) return run(0.0);
+  if (dtype == PTC_F32) return run(0.0f);
   return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
 }
 

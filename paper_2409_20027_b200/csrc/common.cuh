@@ -69,9 +69,9 @@ inline Plan make_plan(int T, int K0, int K) {
   p.K = K;
   p.n[0] = T;
   int n1 = (T + K0 - 1) / K0;
+  p.n[1] = n1;  // level-1 rows also serve the block aggregates when L == 0
   if (n1 <= 1) { p.L = 0; return p; }
   int l = 1;
-  p.n[1] = n1;
   while (p.n[l] > K && l < kMaxLevels) {
     p.n[l + 1] = (p.n[l] + K - 1) / K;
     ++l;

@@ -48,6 +48,45 @@ void launch_prop(const LqrArgs<R>& a, cudaStream_t s) {
   k_prop_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
 }
 
+// Time-block phases (horizon sharded across ranks; sharded.py drives them
+// with an all-gather of the block aggregates between phases):
+//   0  value up-sweep            -> block value aggregate (VElem) in `out`
+//   1  carry from gathered value aggregates, value down-sweep + gains,
+//      propagation up-sweep      -> block affine aggregate (Aff) in `out`
+//   2  carry from gathered affine aggregates, propagation down-sweep
+template <typename R, int NX, int NU>
+void launch_lqr_block(const LqrArgs<R>& a0, int phase, const void* blocks, void* out, int rank,
+                      int world, cudaStream_t s) {
+  LqrArgs<R> a = a0;
+  const Plan& pl = a.plan;
+  const long long B = a.B, P0 = pl.units0();
+  if (phase == 0) {
+    k_value_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) k_value_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    k_value_block<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, static_cast<R*>(out));
+  } else if (phase == 1) {
+    k_value_carry<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, static_cast<const R*>(blocks), rank, world);
+    a.vcarry_in = a.vcin_buf;
+    if (pl.L >= 1) {
+      k_value_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+      for (int l = pl.L - 1; l >= 1; --l)
+        k_value_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    }
+    k_value_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    k_prop_block<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, static_cast<R*>(out));
+  } else {
+    k_prop_carry<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, static_cast<const R*>(blocks), rank);
+    a.x_in = a.xin_buf;
+    if (pl.L >= 1) {
+      k_prop_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+      for (int l = pl.L - 1; l >= 1; --l)
+        k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+    }
+    k_prop_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  }
+}
+
 template <typename R, class Dyn>
 void launch_costate(const NewtonArgs<R>& a, cudaStream_t s) {
   constexpr int NX = Dyn::NX;
@@ -126,6 +165,8 @@ __global__ void k_force_phase(NewtonArgs<R> a, int ph) {
 struct LqrOps {
   void (*solve)(const void* args, cudaStream_t s);
   void (*propagate)(const void* args, cudaStream_t s);
+  void (*block)(const void* args, int phase, const void* blocks, void* out, int rank, int world,
+                cudaStream_t s);
 };
 
 struct NewtonOps {
@@ -155,7 +196,14 @@ struct RegisterLqr {
   static void propagate(const void* a, cudaStream_t s) {
     launch_prop<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
   }
-  RegisterLqr() { lqr_registry()[LqrKey(dtype_code<R>(), NX, NU)] = LqrOps{&solve, &propagate}; }
+  static void block(const void* a, int phase, const void* blocks, void* out, int rank, int world,
+                    cudaStream_t s) {
+    launch_lqr_block<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), phase, blocks, out, rank,
+                                world, s);
+  }
+  RegisterLqr() {
+    lqr_registry()[LqrKey(dtype_code<R>(), NX, NU)] = LqrOps{&solve, &propagate, &block};
+  }
 };
 
 template <typename R, class Dyn, int DYN>

@@ -35,6 +35,19 @@ struct LqrArgs {
   R *dX, *dU;              // (nx, T+1, B), (nu, T, B)
   int* flags;              // [B] OR of FLAG_*
   double* red;             // (3, P0, B): sum du^2, sum du.d, max |du|
+  // time-block mode (horizon sharded across ranks, see sharded.py):
+  //   t_base       global index of local stage 0 (the head element of the
+  //                propagation scan, F = 0, exists only at global stage 0)
+  //   no_terminal  this block does not end with the terminal element
+  //   vcarry_in    (nx*nx + nx, 1, B) cost-to-go (Y, eta) entering the block
+  //                from the later blocks, or null (= zero)
+  //   x_in         (nx, 1, B) deviation dx at the block's first stage, or null
+  //   block_mode   emit block aggregates (level-1 scratch always carved)
+  int t_base, no_terminal, block_mode;
+  const R* vcarry_in;
+  const R* x_in;
+  R* vcin_buf;             // workspace for vcarry_in   (nx*nx + nx, 1, B)
+  R* xin_buf;              // workspace for x_in        (nx, 1, B)
   // tree scratch, index l = 1..L, item rows n[l]
   R* vagg[kMaxLevels + 1];
   R* vcar[kMaxLevels + 1];
@@ -66,7 +79,7 @@ __global__ void __launch_bounds__(128) k_value_up0(LqrArgs<R> a) {
   R L[NU][NU];
   bool okr = true, okc = true;
   int start;
-  if (j == P0 - 1) {
+  if (j == P0 - 1 && !a.no_terminal) {
     R PT[NX][NX];
     ld_mat(a.PT, 0, 1, B, b, PT);
     velem_terminal(PT, acc);
@@ -119,7 +132,8 @@ __global__ void __launch_bounds__(128) k_value_top(LqrArgs<R> a) {
   if (lqr_skip(a, b)) return;
   const int L = a.plan.L, nL = a.plan.n[L];
   VCarry<R, NX> c;
-  vcarry_zero(c);
+  if (a.vcarry_in) ld_vcarry(a.vcarry_in, 0, 1, a.B, b, c);
+  else vcarry_zero(c);
   bool okc = true;
   for (int i = nL - 1; i >= 0; --i) {
     st_vcarry(a.vcar[L], i, nL, a.B, b, c);
@@ -167,11 +181,21 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   const R alpha = R(a.alpha[b]);
   const bool tree = a.plan.L >= 1;
+  const bool emit_pagg = tree || a.block_mode;
   VCarry<R, NX> c;
   if (tree) ld_vcarry(a.vcar[1], j, a.plan.n[1], B, b, c);
+  else if (a.vcarry_in) ld_vcarry(a.vcarry_in, 0, 1, B, b, c);
   else vcarry_zero(c);
   bool okr = true, okc = true, okq = true;
-  if (j == P0 - 1) {
+  if (j == P0 - 1 && a.no_terminal && a.S) {
+    // block end: the cost-to-go handed in by the later blocks
+    st_mat(a.S, T, T + 1, B, b, c.Y);
+    R sv[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) sv[i] = -c.eta[i];
+    st_vec(a.s, T, T + 1, B, b, sv);
+  }
+  if (j == P0 - 1 && !a.no_terminal) {
     // the terminal element V_{N+1}: Y = P_T, everything else zero
     ld_mat(a.PT, 0, 1, B, b, c.Y);
     set_zero(c.eta);
@@ -183,7 +207,7 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
     }
   }
   Aff<R, NX> pa;
-  if (tree) aff_identity(pa);
+  if (emit_pagg) aff_identity(pa);
   for (int t = t1 - 1; t >= t0; --t) {
     Stage<R, NX, NU> st;
     ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t, T, B, b, alpha, st);
@@ -191,9 +215,9 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
     okq &= gains(st, c, Gam, gam);
     st_mat(a.Gam, t, T, B, b, Gam);
     st_vec(a.gam, t, T, B, b, gam);
-    if (tree) {
+    if (emit_pagg) {
       Aff<R, NX> m, o;
-      if (t == 0) {
+      if (t + a.t_base == 0) {
         set_zero(m.F);
       } else {
         mm<NX, NU, NX>(st.Fu, Gam, m.F);
@@ -220,7 +244,7 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
       st_vec(a.s, t, T + 1, B, b, sv);
     }
   }
-  if (tree) st_aff(a.pagg[1], j, a.plan.n[1], B, b, pa);
+  if (emit_pagg) st_aff(a.pagg[1], j, a.plan.n[1], B, b, pa);
   int fl = (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND) | (okq ? 0 : FLAG_DEF_Q);
   if (fl) atomicOr(a.flags + b, fl);
 }
@@ -271,7 +295,7 @@ __global__ void __launch_bounds__(128) k_prop_up0(LqrArgs<R> a) {
 #pragma unroll
     for (int i = 0; i < NX; ++i)
 #pragma unroll
-      for (int k = 0; k < NX; ++k) m.F[i][k] = (t == 0) ? R(0) : m.F[i][k] + Fx[i][k];
+      for (int k = 0; k < NX; ++k) m.F[i][k] = (t + a.t_base == 0) ? R(0) : m.F[i][k] + Fx[i][k];
     mv<NX, NU>(Fu, gam, m.e);
     aff_compose(m, acc, o);
     acc = o;
@@ -286,7 +310,8 @@ __global__ void __launch_bounds__(128) k_prop_top(LqrArgs<R> a) {
   if (lqr_skip(a, b)) return;
   const int L = a.plan.L, nL = a.plan.n[L];
   R x[NX];
-  set_zero(x);
+  if (a.x_in) ld_vec(a.x_in, 0, 1, a.B, b, x);
+  else set_zero(x);
   for (int i = 0; i < nL; ++i) {
     st_vec(a.pcar[L], i, nL, a.B, b, x);
     Aff<R, NX> m;
@@ -332,6 +357,7 @@ __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   R x[NX];
   if (a.plan.L >= 1) ld_vec(a.pcar[1], j, a.plan.n[1], B, b, x);
+  else if (a.x_in) ld_vec(a.x_in, 0, 1, B, b, x);
   else set_zero(x);
   double s2 = 0.0, sd = 0.0, mx = 0.0;
   for (int t = t0; t < t1; ++t) {
@@ -359,7 +385,7 @@ __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
 #pragma unroll
     for (int i = 0; i < NX; ++i)
 #pragma unroll
-      for (int k = 0; k < NX; ++k) F[i][k] = (t == 0) ? R(0) : F[i][k] + Fx[i][k];
+      for (int k = 0; k < NX; ++k) F[i][k] = (t + a.t_base == 0) ? R(0) : F[i][k] + Fx[i][k];
     mv<NX, NU>(Fu, gam, e);
     mv<NX, NX>(F, x, y);
 #pragma unroll
@@ -371,6 +397,90 @@ __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
     a.red[((size_t)1 * P0 + j) * B + b] = sd;
     a.red[((size_t)2 * P0 + j) * B + b] = mx;
   }
+}
+
+// ------------------------------------------------------------ time blocks
+// Horizon sharded into contiguous blocks, one per rank (BASELINE config 4).
+// Each rank folds its block into one aggregate per scan; the aggregates are
+// all-gathered (NCCL) and every rank turns the gathered list into the carry
+// entering its block, then finishes its block locally.
+// Gathered layout: rank-major, blocks[(r * comps + c) * B + b].
+
+// value aggregate of the whole block: fold of the top-level items
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_value_block(LqrArgs<R> a, R* out) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int L = a.plan.L > 0 ? a.plan.L : 1, nL = a.plan.n[L];
+  VElem<R, NX> acc;
+  ld_velem(a.vagg[L], nL - 1, nL, a.B, b, acc);
+  bool okc = true;
+  for (int i = nL - 2; i >= 0; --i) {
+    VElem<R, NX> e, o;
+    ld_velem(a.vagg[L], i, nL, a.B, b, e);
+    okc &= vcombine(e, acc, o);
+    acc = o;
+  }
+  st_velem(out, 0, 1, a.B, b, acc);
+  if (!okc) atomicOr(a.flags + b, FLAG_COND);
+}
+
+// cost-to-go entering block `rank`: the later blocks' aggregates applied to
+// a zero carry (the last block holds the terminal element)
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_value_carry(LqrArgs<R> a, const R* blocks, int rank,
+                                                     int world) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  constexpr int kC = VElem<R, NX>::kComp;
+  VCarry<R, NX> c;
+  vcarry_zero(c);
+  bool okc = true;
+  for (int r = world - 1; r > rank; --r) {
+    VElem<R, NX> e;
+    ld_velem(blocks + (size_t)r * kC * a.B, 0, 1, a.B, b, e);
+    VCarry<R, NX> o;
+    okc &= vstep(e, c, o);
+    c = o;
+  }
+  st_vcarry(a.vcin_buf, 0, 1, a.B, b, c);
+  if (!okc) atomicOr(a.flags + b, FLAG_COND);
+}
+
+// propagation aggregate of the whole block (first item applied first)
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_prop_block(LqrArgs<R> a, R* out) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int L = a.plan.L > 0 ? a.plan.L : 1, nL = a.plan.n[L];
+  Aff<R, NX> acc;
+  ld_aff(a.pagg[L], 0, nL, a.B, b, acc);
+  for (int i = 1; i < nL; ++i) {
+    Aff<R, NX> m, o;
+    ld_aff(a.pagg[L], i, nL, a.B, b, m);
+    aff_compose(m, acc, o);
+    acc = o;
+  }
+  st_aff(out, 0, 1, a.B, b, acc);
+}
+
+// deviation entering block `rank`: the earlier blocks' maps applied to dx_1 = 0
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_prop_carry(LqrArgs<R> a, const R* blocks, int rank) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  constexpr int kC = Aff<R, NX>::kComp;
+  R x[NX];
+  set_zero(x);
+  for (int r = 0; r < rank; ++r) {
+    Aff<R, NX> m;
+    ld_aff(blocks + (size_t)r * kC * a.B, 0, 1, a.B, b, m);
+    R y[NX];
+    aff_apply(m, x, y);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) x[k] = y[k];
+  }
+  st_vec(a.xin_buf, 0, 1, a.B, b, x);
 }
 
 }  // namespace ptc

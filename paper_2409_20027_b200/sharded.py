@@ -1,0 +1,169 @@
+"""Multi-GPU decompositions of the LQR-scan solve (BASELINE configs 3 and 4).
+
+* ``shard_problems``: independent problems split across ranks (config 3).
+  No data-path collective -- each rank solves its slice.
+* ``TimeShardedLqr``: one long horizon split into contiguous time blocks,
+  one per rank (config 4).  The two scans of the LQR subproblem
+  (value_pass, reference ``passes.py:291-323``, and propagation_pass,
+  ``passes.py:338-361``) are associative, so each rank folds its block into
+  one aggregate per scan, the aggregates are all-gathered (one NCCL
+  all-gather per scan over NVLink), and every rank combines the gathered
+  list into the carry entering its block and finishes the block locally:
+
+      phase 0  local value up-sweep            -> block value aggregate
+      gather   (world, 3nx^2+2nx, 1, B)
+      phase 1  carry from later blocks, local value down-sweep + gains,
+               local propagation up-sweep      -> block affine aggregate
+      gather   (world, nx^2+nx, 1, B)
+      phase 2  carry from earlier blocks, local forward sweep -> dx, du
+
+The block arithmetic is behind a small ops interface so the same driver runs
+the CUDA kernels (``CudaBlockOps``, the product) and, in the CPU tests, a
+numpy stand-in with a gloo process group (test infrastructure only).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _native as N
+
+
+def block_bounds(horizon: int, world: int, rank: int) -> tuple[int, int]:
+    """(t_base, length) of rank's contiguous block; lengths differ by <= 1."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world")
+    if horizon < world:
+        raise ValueError(f"horizon {horizon} shorter than world size {world}")
+    q, r = divmod(horizon, world)
+    t0 = rank * q + min(rank, r)
+    return t0, q + (1 if rank < r else 0)
+
+
+def shard_problems(batch: int, world: int, rank: int) -> slice:
+    """Contiguous slice of a problem batch owned by rank (config 3)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world")
+    q, r = divmod(batch, world)
+    b0 = rank * q + min(rank, r)
+    return slice(b0, b0 + q + (1 if rank < r else 0))
+
+
+def block_comps(nx: int) -> tuple[int, int]:
+    """Components of one value aggregate (A, Y, C, eta, b) and one affine
+    aggregate (F, e)."""
+    return 3 * nx * nx + 2 * nx, nx * nx + nx
+
+
+# ---------------------------------------------------------------- gathers
+
+def nccl_gather(group=None):
+    """All-gather over a torch.distributed group into one rank-major tensor."""
+    import torch
+    import torch.distributed as dist
+
+    def gather(t):
+        world = dist.get_world_size(group)
+        out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+        else:  # gloo has no all_gather_into_tensor
+            parts = list(out.unbind(0))
+            dist.all_gather(parts, t.contiguous(), group=group)
+            out = torch.stack(parts)
+        return out
+    return gather
+
+
+# ------------------------------------------------------------------ driver
+
+class TimeShardedLqr:
+    """Drives the three block phases of one rank with a gather between them."""
+
+    def __init__(self, ops, gather):
+        self.ops = ops
+        self.gather = gather
+
+    def solve(self):
+        vblk = self.ops.value_up()
+        pblk = self.ops.value_down(self.gather(vblk))
+        self.ops.propagate(self.gather(pblk))
+        return self.ops
+
+
+def emulate_ranks(ops_list):
+    """Run the block phases of `world` ranks in one process, in rank order,
+    with the all-gather replaced by a stack (single-device parity tests and
+    the N=1 bench; no kernel ever waits on another)."""
+    import torch
+    vs = [o.value_up() for o in ops_list]
+    V = torch.stack(vs)
+    ps = [o.value_down(V) for o in ops_list]
+    Pg = torch.stack(ps)
+    for o in ops_list:
+        o.propagate(Pg)
+    return ops_list
+
+
+class CudaBlockOps:
+    """One rank's block of a time-sharded LQR-scan solve on the device.
+
+    Inputs are the block's stages in SoA batch-minor layout (see
+    include/pintoc_b200.h): P (nx*nx, T, B), R (nu*nu, T, B), M, d, Fx, Fu;
+    PT (nx*nx, 1, B) on the last block; alpha float64 [B].  Outputs after
+    ``propagate``: Gamma, gamma, dx (nx, T+1, B), du; S, s when requested.
+    """
+
+    def __init__(self, rank, world, t_base, P, R, M, d, Fx, Fu, PT, alpha, nx, nu,
+                 with_value=False, chunk0=0, chunk=0):
+        torch = N.require_cuda()
+        self.torch = torch
+        self.lib = N.load_library()
+        self.rank, self.world, self.t_base = int(rank), int(world), int(t_base)
+        self.nx, self.nu = int(nx), int(nu)
+        self.T, self.B = int(P.shape[1]), int(P.shape[2])
+        self.dtype = P.dtype
+        self.code = N.PTC_F64 if P.dtype == torch.float64 else N.PTC_F32
+        self.inputs = (P, R, M, d, Fx, Fu, PT if rank == world - 1 else None, alpha)
+        self.chunk0, self.chunk = int(chunk0), int(chunk)
+        dev = P.device
+        nbytes = self.lib.ptc_lqr_block_workspace_bytes(self.code, self.B, self.T, self.nx,
+                                                        self.nu, self.chunk0, self.chunk)
+        N.check(0 if nbytes >= 0 else int(nbytes))
+        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+        vc, pc = block_comps(self.nx)
+        mk = lambda *s: torch.empty(*s, dtype=self.dtype, device=dev)
+        self.vblock = mk(vc, 1, self.B)
+        self.pblock = mk(pc, 1, self.B)
+        T, B = self.T, self.B
+        self.Gamma = mk(self.nu * self.nx, T, B)
+        self.gamma = mk(self.nu, T, B)
+        self.dx = mk(self.nx, T + 1, B)
+        self.du = mk(self.nu, T, B)
+        self.S = mk(self.nx * self.nx, T + 1, B) if with_value else None
+        self.s = mk(self.nx, T + 1, B) if with_value else None
+        self.flags = torch.zeros(B, dtype=torch.int32, device=dev)
+
+    def _run(self, phase, blocks_in, block_out):
+        ptr = lambda t: None if t is None else t.data_ptr()
+        P, R, M, d, Fx, Fu, PT, alpha = self.inputs
+        N.check(self.lib.ptc_lqr_block_solve(
+            phase, self.code, self.B, self.T, self.nx, self.nu, self.t_base,
+            int(self.rank == self.world - 1), self.rank, self.world,
+            ptr(P), ptr(R), ptr(M), ptr(d), ptr(Fx), ptr(Fu), ptr(PT), ptr(alpha),
+            ptr(blocks_in), ptr(block_out), ptr(self.S), ptr(self.s), ptr(self.Gamma),
+            ptr(self.gamma), ptr(self.dx), ptr(self.du), ptr(self.flags),
+            ptr(self.workspace), self.workspace.numel(), self.chunk0, self.chunk,
+            N.stream_ptr()))
+
+    def value_up(self):
+        self.flags.zero_()
+        self._run(0, None, self.vblock)
+        return self.vblock
+
+    def value_down(self, gathered):
+        self._run(1, gathered.contiguous(), self.pblock)
+        return self.pblock
+
+    def propagate(self, gathered):
+        self._run(2, gathered.contiguous(), None)
