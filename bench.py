@@ -117,6 +117,20 @@ def cpu_lqr_sample(n_per_half: int, cores: int, pool=None) -> tuple[float, int]:
     return rate, solved
 
 
+def lm_alpha_oracle(O, e, alpha0=ALPHA, nu0=2.0):
+    """First regularisation of the reference's LM escalation (newton.py:166-176:
+    alpha <- alpha * nu, nu <- 2 nu on a failed subproblem) at which the
+    LQR subproblem is solvable."""
+    alpha, nu = alpha0, nu0
+    while alpha <= 1e12:
+        try:
+            O.lqr_solve(e.with_alpha(alpha))
+            return alpha
+        except O.OracleError:
+            alpha, nu = alpha * nu, 2.0 * nu
+    return alpha
+
+
 def _cpu_timed_chunk(args):
     system, x0s, us = args
     sys.path.insert(0, ROOT)
@@ -127,7 +141,8 @@ def _cpu_timed_chunk(args):
     for x0, u in zip(x0s, us):
         xs = O.rollout(dyn, x0, u)
         lam = O.costate_pass(dyn, cost, ("zero",), xs, u)
-        exps.append(O.expansion(dyn, cost, ("zero",), xs, u, lam, ALPHA))
+        e = O.expansion(dyn, cost, ("zero",), xs, u, lam, ALPHA)
+        exps.append(e.with_alpha(lm_alpha_oracle(O, e)))
     t0 = time.perf_counter()
     for e in exps:
         O.lqr_solve(e)
@@ -177,7 +192,9 @@ def run_reference(args) -> None:
 def workload_config(n: int) -> dict:
     return {"workload": "config 3: 65,536 independent LQR subproblems (32,768 pendulum nx=2 "
                         "nu=1 + 32,768 cart-pole nx=4 nu=1), T=256, Newton expansions at "
-                        "seeded config-3 trajectories, alpha=1",
+                        "seeded config-3 trajectories",
+            "alpha": "per problem, first solvable value of the reference LM escalation "
+                     "1, 2, 8, 64, ... (newton.py:166-176)",
             "global_batch": B_TOTAL, "horizon": T, "parallelism": f"problem-sharded x{n}",
             "l2": "inputs > L2 (no flush needed)"}
 
@@ -264,6 +281,23 @@ def build_inputs(P, torch, system: str, n: int, rank: int):
     return inputs, nx, nu
 
 
+def lm_alpha_device(torch, solver, inputs, n, alpha0=ALPHA, nu0=2.0):
+    """Per-problem regularisation: the first alpha of the reference's LM
+    escalation (alpha <- alpha nu, nu <- 2 nu; newton.py:166-176) at which
+    the subproblem is solvable -- the subproblem its Newton loop actually
+    solves (untimed setup; mirrors lm_alpha_oracle of the CPU arm)."""
+    alpha = torch.full((n,), alpha0, dtype=torch.float64, device="cuda")
+    nu = torch.full((n,), nu0, dtype=torch.float64, device="cuda")
+    for _ in range(64):
+        solver.solve(*inputs, alpha)
+        bad = solver.flags != 0
+        if not bool(bad.any()) or float(alpha.max()) > 1e12:
+            break
+        alpha = torch.where(bad, alpha * nu, alpha)
+        nu = torch.where(bad, 2.0 * nu, nu)
+    return alpha
+
+
 def alg_bytes(n: int, nx: int, nu: int) -> int:
     """Minimum HBM traffic of one LQR-scan solve: read the expansion once,
     write gains + deviations once (8-byte words)."""
@@ -289,17 +323,28 @@ def run_ours(args) -> None:
     bp, bc = half_sizes(b_local)
 
     halves = {}
+    ill_posed = 0
     for system, n in (("pendulum", bp), ("cartpole", bc)):
         inputs, nx, nu = build_inputs(P, torch, system, n, rank)
-        alpha = torch.full((n,), ALPHA, dtype=torch.float64, device="cuda")
-        halves[system] = (LqrSolver(n, T, nx, nu, dtype=torch.float64), inputs, alpha, n, nx, nu)
+        solver = LqrSolver(n, T, nx, nu, dtype=torch.float64)
+        alpha = lm_alpha_device(torch, solver, inputs, n)
+        ill_posed += int((solver.flags != 0).sum())
+        halves[system] = (solver, inputs, alpha, n, nx, nu)
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
 
+    # the two halves are independent: run them concurrently on two streams
+    side = [torch.cuda.Stream() for _ in halves]
+
     def step():
-        for solver, inputs, alpha, *_ in halves.values():
-            solver.solve(*inputs, alpha)
+        for st in side:
+            st.wait_stream(stream)
+        for (solver, inputs, alpha, *_), st in zip(halves.values(), side):
+            with torch.cuda.stream(st):
+                solver.solve(*inputs, alpha, stream=st)
+        for st in side:
+            stream.wait_stream(st)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -375,11 +420,7 @@ def run_ours(args) -> None:
                "ms_per_step": float(e_ms)}
         del host, dev_in, outs
 
-    # horizon sweep of the single-problem LQR-scan latency (config 1, nx=4)
-    sweep = None
-    if rank == 0 and not args.no_sweep:
-        sweep = lqr_latency_sweep(torch, LqrSolver)
-
+    roof = None
     if rank == 0:
         solver_c, _, _, n_c, nx_c, nu_c = halves["cartpole"]
         by = alg_bytes(n_c, nx_c, nu_c)
@@ -393,6 +434,20 @@ def run_ours(args) -> None:
                 "pendulum_half": {"ms": half_ms["pendulum"],
                                   "achieved_gbs": alg_bytes(halves["pendulum"][3], 2, 1)
                                   / (half_ms["pendulum"] * 1e-3) / 1e9}}
+
+    # horizon sweep of the single-problem LQR-scan latency (config 1, nx=4)
+    sweep = nsweep = None
+    if rank == 0 and not args.no_sweep:
+        sweep = lqr_latency_sweep(torch, LqrSolver)
+    if rank == 0 and not args.no_newton_sweep:
+        nsweep = newton_latency_sweep(torch, P)
+    longh = None
+    if not args.no_long:
+        del halves
+        torch.cuda.empty_cache()
+        longh = long_horizon_leg(torch, world, rank)
+
+    if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
@@ -412,8 +467,9 @@ def run_ours(args) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": workload_config(world),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": 4 * args.steps, "clocks": clk,
-            "lqr_latency_sweep": sweep,
+            "gpu_launches": 4 * args.steps, "clocks": clk, "ill_posed_subproblems": ill_posed,
+            "lqr_latency_sweep": sweep, "newton_latency_sweep": nsweep,
+            "long_horizon": longh,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -453,6 +509,104 @@ def lqr_latency_sweep(torch, LqrSolver):
     return out
 
 
+def newton_latency_sweep(torch, P):
+    """Per-Newton-iteration latency vs horizon (pendulum, batch 1, fp64, zero
+    augmentation): costate scan + expansion, value + propagation scans,
+    nonlinear rollout, cost, trust-region control -- one ptc_solver_iterate.
+    Timed over the first iterations from a seeded random start (every
+    iteration does full work), reloaded between repetitions."""
+    from paper_2409_20027_b200 import _native as N
+    from paper_2409_20027_b200._device import DeviceSolver, SolveSettings
+    out = {}
+    for logT in (8, 10, 12, 14, 16):
+        Tn = 1 << logT
+        dyn = P.PendulumDynamics(Tn, P.PendulumParams(damping=0.1, dt=0.05))
+        cost = P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0]))
+        s = DeviceSolver(dyn, cost, None, 1, SolveSettings(method=N.METHOD_NEWTON, max_iters=1000,
+                                                            inner_tol=1e-300))
+        rng = np.random.default_rng([3, logT])
+        us = torch.as_tensor(0.5 * rng.standard_normal((1, Tn, 1)))
+        X = torch.zeros(1, Tn + 1, 2, dtype=torch.float64)
+        X[0, 0, 0] = np.pi
+        s.load(X, us)
+        s.rollout()
+        X = s.field("states", Tn + 1, (2,)).contiguous()
+        iters, reps, per = 4, 3, []
+        for _ in range(reps):
+            s.load(X, us)
+            s.iterate(1)  # first iteration also evaluates the start cost
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            s.iterate(iters)
+            b.record()
+            torch.cuda.synchronize()
+            per.append(a.elapsed_time(b) / iters)
+        out[str(Tn)] = round(statistics.median(per), 4)
+        del s
+    return {"pendulum_ms_per_iteration": out}
+
+
+def long_horizon_leg(torch, world: int, rank: int, steps: int = 5):
+    """Config 4: one T = 2^20 LQR-scan solve, nx=12, nu=4, fp64, horizon split
+    into `world` contiguous time blocks (one per rank) with an NCCL
+    all-gather of the block aggregates per scan.  Random time-varying
+    linearised-quadrotor-like data generated on the device (seeded per
+    rank): A_k = I + dt F_k (dt = 0.01, F_k ~ N(0, 0.2) on a 3x3-block
+    band), B_k ~ N(0, 0.1), Q = diag U(0.1, 10), R = 0.1 I, d = B_k^T c_k
+    with c_k ~ N(0, 0.01)."""
+    import torch.distributed as dist
+    from paper_2409_20027_b200.sharded import (CudaBlockOps, TimeShardedLqr, block_bounds,
+                                               nccl_gather)
+    T_all, nx, nu = 1 << 20, 12, 4
+    t0, Tl = block_bounds(T_all, world, rank)
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(20027 + rank)
+    f64 = torch.float64
+    band = torch.zeros(nx, nx, dtype=f64, device=dev)
+    for i in range(4):
+        for j in (i, i + 1):
+            if j < 4:
+                band[3 * i:3 * i + 3, 3 * j:3 * j + 3] = 1.0
+    F = torch.randn(Tl, nx, nx, generator=g, device=dev, dtype=f64) * (0.2 ** 0.5) * band
+    A = torch.eye(nx, dtype=f64, device=dev) + 0.01 * F
+    Bm = torch.randn(Tl, nx, nu, generator=g, device=dev, dtype=f64) * (0.1 ** 0.5)
+    qd = torch.empty(nx, dtype=f64, device=dev).uniform_(0.1, 10.0, generator=g)
+    c = torch.randn(Tl, nx, generator=g, device=dev, dtype=f64) * 0.1
+    soa = lambda t, comps: t.reshape(Tl, comps).t().contiguous().unsqueeze(-1)
+    Pm = soa(torch.diag(qd).expand(Tl, nx, nx), nx * nx)
+    Rm = soa((0.1 * torch.eye(nu, dtype=f64, device=dev)).expand(Tl, nu, nu), nu * nu)
+    Mm = torch.zeros(nx * nu, Tl, 1, dtype=f64, device=dev)
+    dm = soa(torch.einsum("tij,ti->tj", Bm, c), nu)
+    Fx, Fu = soa(A, nx * nx), soa(Bm, nx * nu)
+    PT = (10.0 * torch.diag(qd)).reshape(nx * nx, 1, 1).contiguous()
+    alpha = torch.zeros(1, dtype=f64, device=dev)
+    del F, A, Bm, c
+    ops = CudaBlockOps(rank, world, t0, Pm, Rm, Mm, dm, Fx, Fu, PT, alpha, nx, nu)
+    drv = TimeShardedLqr(ops, nccl_gather() if world > 1 else (lambda t: t.unsqueeze(0)))
+    for _ in range(2):
+        drv.solve()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        drv.solve()
+    b.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b) / steps], dtype=f64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    flags = int(ops.flags.max())
+    in_bytes = 8 * T_all * (nx * nx * 2 + nu * nu + nx * nu * 2 + nu)
+    out_bytes = 8 * T_all * (nu * nx + nu + nx + nu)
+    return {"config": "config 4: T=2^20, nx=12, nu=4, fp64, batch 1, time blocks x%d" % world,
+            "ms_per_solve": float(ms), "flags": flags,
+            "achieved_gbs": (in_bytes + out_bytes) / (float(ms) * 1e-3) / 1e9,
+            "algorithmic_bytes": in_bytes + out_bytes}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -462,6 +616,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-newton-sweep", action="store_true")
+    ap.add_argument("--no-long", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -49,17 +49,26 @@ class Divergence(OracleError):
         self.step = step
         super().__init__(f"non-finite state at rollout step {step}")
 
+    def __reduce__(self):  # picklable across the CPU baseline's worker pool
+        return (type(self), (self.step,))
+
 
 class Infeasible(OracleError):
     def __init__(self, stage, component, value):
         self.stage, self.component, self.value = stage, component, value
         super().__init__(f"stage {stage} component {component} value {value}")
 
+    def __reduce__(self):
+        return (type(self), (self.stage, self.component, self.value))
+
 
 class Definiteness(OracleError):
     def __init__(self, stage, what):
         self.stage, self.what = stage, what
         super().__init__(f"{what} not positive definite at stage {stage}")
+
+    def __reduce__(self):
+        return (type(self), (self.stage, self.what))
 
 
 class Conditioning(OracleError):

@@ -581,6 +581,9 @@ struct Solver final : ptc_solver {
       return fail(PTC_ERR_UNSUPPORTED, "solver kernels not instantiated for model " +
                                            std::to_string(d.model) + " nx=" + std::to_string(d.nx) +
                                            " nu=" + std::to_string(d.nu));
+    if (!lqr_registry().count(LqrKey(dtype_code<R>(), d.nx, d.nu)))
+      return fail(PTC_ERR_UNSUPPORTED, "LQR kernels not instantiated for nx=" +
+                                           std::to_string(d.nx) + " nu=" + std::to_string(d.nu));
     ops = &it->second;
     Carver c{(char*)ws};
     size_t need = layout(d, c, this);

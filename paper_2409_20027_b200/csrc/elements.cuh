@@ -118,8 +118,16 @@ struct Stage {
 template <typename R, int NX, int NU>
 PTC_D void ld_stage(const R* P, const R* Rm, const R* M, const R* d, const R* Fx, const R* Fu,
                     int t, int T, int B, int b, R alpha, Stage<R, NX, NU>& s) {
-  ld_mat(P, t, T, B, b, s.P);
-  ld_mat(Rm, t, T, B, b, s.Rr);
+  // P and R are symmetric (reference passes.py:178-179 symmetrises them; the
+  // StageExpansion invariant): load the upper triangles and mirror
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = i; j < NX; ++j) s.P[i][j] = s.P[j][i] = ldf(P, i * NX + j, t, T, B, b);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = i; j < NU; ++j) s.Rr[i][j] = s.Rr[j][i] = ldf(Rm, i * NU + j, t, T, B, b);
 #pragma unroll
   for (int i = 0; i < NU; ++i) s.Rr[i][i] += alpha;
   ld_mat(M, t, T, B, b, s.M);
@@ -355,6 +363,83 @@ PTC_D bool gains(const Stage<R, NX, NU>& s, const VCarry<R, NX>& next, R (&Gam)[
     gam[i] = -gam[i];
   }
   return ok;
+}
+
+// One stage element folded into a terminal-containing suffix, fused with the
+// gains of that stage: the composition  gains(st, c)  +  vstep(velem(st), c)
+// of the reference's value pass (passes.py:192-228 element, 264-288 combine,
+// 316-323 gains) written without forming the dual element.  With
+//   Q = sym(Rr + Fu^T S Fu),  Qux = M^T + Fu^T S Fx,  qu = d + Fu^T s
+// the push-through identity  (I + S C)^-1 S = S - S Fu Q^-1 Fu^T S  (C =
+// Fu Rr^-1 Fu^T) turns the combine into
+//   Gamma = -Q^-1 Qux,  gamma = -Q^-1 qu,
+//   S' = sym(P + Fx^T S Fx + Qux^T Gamma),  s' = Fx^T s + Qux^T gamma,
+// exactly the suffix value of the dual scan (Y' = S', eta' = -s').  Since
+// det(I + C S) = det(Q) / det(Rr), a singular combine is a Q that fails its
+// Cholesky, so the two definiteness flags cover the conditioning case.
+// Returns FLAG_DEF_R / FLAG_DEF_Q bits.
+template <typename R, int NX, int NU>
+PTC_D int riccati_step(const Stage<R, NX, NU>& st, const VCarry<R, NX>& c, R (&Gam)[NU][NX],
+                       R (&gam)[NU], VCarry<R, NX>& o) {
+  int fl = 0;
+  {
+    R L[NU][NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+#pragma unroll
+      for (int j = 0; j < NU; ++j) L[i][j] = st.Rr[i][j];
+    if (!cholesky<NU>(L)) fl |= FLAG_DEF_R;
+  }
+  R FtS[NU][NX];
+  mtm<NU, NX, NX>(st.Fu, c.Y, FtS);
+  R Q[NU][NU];
+  mm<NU, NX, NU>(FtS, st.Fu, Q);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) Q[i][j] += st.Rr[i][j];
+  symmetrize<NU>(Q);
+  if (!cholesky<NU>(Q)) fl |= FLAG_DEF_Q;
+  R Qux[NU][NX];
+  mm<NU, NX, NX>(FtS, st.Fx, Qux);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Qux[i][j] += st.M[j][i];
+  R Fe[NU];
+  mtv<NU, NX>(st.Fu, c.eta, Fe);  // Fu^T eta = -Fu^T s
+#pragma unroll
+  for (int i = 0; i < NU; ++i) gam[i] = st.d[i] - Fe[i];
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Gam[i][j] = Qux[i][j];
+  chol_solve<NU, NX>(Q, Gam);
+  chol_solve_vec<NU>(Q, gam);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Gam[i][j] = -Gam[i][j];
+    gam[i] = -gam[i];
+  }
+  // S' = P + Fx^T (S Fx) + Qux^T Gamma
+  R SF[NX][NX];
+  mm<NX, NX, NX>(c.Y, st.Fx, SF);
+  mtm<NX, NX, NX>(st.Fx, SF, o.Y);
+  R QG[NX][NX];
+  mtm<NX, NU, NX>(Qux, Gam, QG);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) o.Y[i][j] += st.P[i][j] + QG[i][j];
+  symmetrize<NX>(o.Y);
+  // eta' = -s' = Fx^T eta - Qux^T gamma
+  R Fte[NX], Qg[NX];
+  mtv<NX, NX>(st.Fx, c.eta, Fte);
+  mtv<NX, NU>(Qux, gam, Qg);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) o.eta[i] = Fte[i] - Qg[i];
+  return fl;
 }
 
 // ---------------------------------------------------------------------------

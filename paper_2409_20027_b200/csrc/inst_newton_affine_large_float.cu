@@ -1,4 +1,3 @@
-// nx = 12 kernel sets, float
+// Newton kernel sets of affine models nx = 12, float
 #include "inst_common.cuh"
-PTC_REG_LQR(float, 12, 4) PTC_REG_LQR(float, 12, 6)
 PTC_REG_AFFINE(float, 12, 4) PTC_REG_AFFINE(float, 12, 6)

@@ -24,7 +24,10 @@ void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
     for (int l = pl.L - 1; l >= 1; --l)
       k_value_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
   }
-  k_value_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  if (pl.L >= 1 || a.block_mode)
+    k_value_down0<R, NX, NU, true><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  else
+    k_value_down0<R, NX, NU, false><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
   if (pl.L >= 1) {
     for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_prop_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
@@ -72,7 +75,7 @@ void launch_lqr_block(const LqrArgs<R>& a0, int phase, const void* blocks, void*
       for (int l = pl.L - 1; l >= 1; --l)
         k_value_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     }
-    k_value_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_value_down0<R, NX, NU, true><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_prop_block<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, static_cast<R*>(out));
   } else {
@@ -102,6 +105,37 @@ void launch_costate(const NewtonArgs<R>& a, cudaStream_t s) {
   k_costate_down0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
 }
 
+// ---------------------------------------------------------------------------
+// registry (declared before the Newton sequence, which dispatches its LQR
+// solve through it so Newton and LQR kernel sets compile in separate units)
+// ---------------------------------------------------------------------------
+
+struct LqrOps {
+  void (*solve)(const void* args, cudaStream_t s);
+  void (*propagate)(const void* args, cudaStream_t s);
+  void (*block)(const void* args, int phase, const void* blocks, void* out, int rank, int world,
+                cudaStream_t s);
+};
+
+struct NewtonOps {
+  void (*lqr)(const void* la, cudaStream_t s);
+  void (*init)(const void* na, cudaStream_t s);
+  void (*check)(const void* na, int* bad_t, cudaStream_t s);
+  void (*iterate)(const void* na, const void* la, cudaStream_t s);
+  void (*expand)(const void* na, cudaStream_t s);
+  void (*rollout)(const void* na, cudaStream_t s);
+  void (*cost)(const void* na, cudaStream_t s);
+};
+
+using LqrKey = std::tuple<int, int, int>;            // dtype, nx, nu
+using NewtonKey = std::tuple<int, int, int, int>;    // dtype, dyn, nx, nu
+
+std::map<LqrKey, LqrOps>& lqr_registry();
+std::map<NewtonKey, NewtonOps>& newton_registry();
+
+template <typename R>
+constexpr int dtype_code() { return sizeof(R) == 8 ? 1 : 0; }
+
 template <typename R, class Dyn>
 void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaStream_t s) {
   constexpr int NX = Dyn::NX, NU = Dyn::NU;
@@ -109,7 +143,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
   k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
   launch_costate<R, Dyn>(a, s);
-  launch_lqr<R, NX, NU>(la, s);
+  lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&la, s);
   k_rollout<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
   k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
   k_control<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
@@ -162,32 +196,6 @@ __global__ void k_force_phase(NewtonArgs<R> a, int ph) {
 // registry
 // ---------------------------------------------------------------------------
 
-struct LqrOps {
-  void (*solve)(const void* args, cudaStream_t s);
-  void (*propagate)(const void* args, cudaStream_t s);
-  void (*block)(const void* args, int phase, const void* blocks, void* out, int rank, int world,
-                cudaStream_t s);
-};
-
-struct NewtonOps {
-  void (*lqr)(const void* la, cudaStream_t s);
-  void (*init)(const void* na, cudaStream_t s);
-  void (*check)(const void* na, int* bad_t, cudaStream_t s);
-  void (*iterate)(const void* na, const void* la, cudaStream_t s);
-  void (*expand)(const void* na, cudaStream_t s);
-  void (*rollout)(const void* na, cudaStream_t s);
-  void (*cost)(const void* na, cudaStream_t s);
-};
-
-using LqrKey = std::tuple<int, int, int>;            // dtype, nx, nu
-using NewtonKey = std::tuple<int, int, int, int>;    // dtype, dyn, nx, nu
-
-std::map<LqrKey, LqrOps>& lqr_registry();
-std::map<NewtonKey, NewtonOps>& newton_registry();
-
-template <typename R>
-constexpr int dtype_code() { return sizeof(R) == 8 ? 1 : 0; }
-
 template <typename R, int NX, int NU>
 struct RegisterLqr {
   static void solve(const void* a, cudaStream_t s) {
@@ -211,7 +219,7 @@ struct RegisterNewton {
   static constexpr int NX = Dyn::NX, NU = Dyn::NU;
   static const NewtonArgs<R>& A(const void* p) { return *static_cast<const NewtonArgs<R>*>(p); }
   static void lqr(const void* la, cudaStream_t s) {
-    launch_lqr<R, NX, NU>(*static_cast<const LqrArgs<R>*>(la), s);
+    lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(la, s);
   }
   static void init(const void* p, cudaStream_t s) {
     const NewtonArgs<R>& a = A(p);

@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(128) k_value_down(LqrArgs<R> a, int l) {
 
 // level-0 down-sweep: cost-to-go, gains, optional (S, s) output and the
 // level-1 aggregates of the forward propagation scan
-template <typename R, int NX, int NU>
+// kAgg: emit the level-1 aggregates of the propagation scan (tree or block
+// mode); the single-sweep schedule instantiates it without, saving registers
+template <typename R, int NX, int NU, bool kAgg>
 __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
   const int P0 = a.plan.units0();
   const int u = unit_id();
@@ -181,12 +183,11 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   const R alpha = R(a.alpha[b]);
   const bool tree = a.plan.L >= 1;
-  const bool emit_pagg = tree || a.block_mode;
+  constexpr bool emit_pagg = kAgg;
   VCarry<R, NX> c;
   if (tree) ld_vcarry(a.vcar[1], j, a.plan.n[1], B, b, c);
   else if (a.vcarry_in) ld_vcarry(a.vcarry_in, 0, 1, B, b, c);
   else vcarry_zero(c);
-  bool okr = true, okc = true, okq = true;
   if (j == P0 - 1 && a.no_terminal && a.S) {
     // block end: the cost-to-go handed in by the later blocks
     st_mat(a.S, T, T + 1, B, b, c.Y);
@@ -207,16 +208,21 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
     }
   }
   Aff<R, NX> pa;
-  if (emit_pagg) aff_identity(pa);
+  if constexpr (emit_pagg) aff_identity(pa);
+  int fl = 0;
+  // software pipeline: stage t-1 is loaded while stage t is folded
+  Stage<R, NX, NU> st;
+  if (t1 - 1 >= t0) ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t1 - 1, T, B, b, alpha, st);
   for (int t = t1 - 1; t >= t0; --t) {
-    Stage<R, NX, NU> st;
-    ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t, T, B, b, alpha, st);
+    Stage<R, NX, NU> nst;
+    if (t > t0) ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t - 1, T, B, b, alpha, nst);
     R Gam[NU][NX], gam[NU];
-    okq &= gains(st, c, Gam, gam);
+    VCarry<R, NX> o;
+    fl |= riccati_step(st, c, Gam, gam, o);
     st_mat(a.Gam, t, T, B, b, Gam);
     st_vec(a.gam, t, T, B, b, gam);
-    if (emit_pagg) {
-      Aff<R, NX> m, o;
+    if constexpr (emit_pagg) {
+      Aff<R, NX> m, ao;
       if (t + a.t_base == 0) {
         set_zero(m.F);
       } else {
@@ -227,14 +233,9 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
           for (int k = 0; k < NX; ++k) m.F[i][k] += st.Fx[i][k];
       }
       mv<NX, NU>(st.Fu, gam, m.e);
-      aff_compose(pa, m, o);
-      pa = o;
+      aff_compose(pa, m, ao);
+      pa = ao;
     }
-    VElem<R, NX> e;
-    R L[NU][NU];
-    okr &= velem_from_stage(st, e, L);
-    VCarry<R, NX> o;
-    okc &= vstep(e, c, o);
     c = o;
     if (a.S) {
       st_mat(a.S, t, T + 1, B, b, c.Y);
@@ -243,9 +244,9 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
       for (int i = 0; i < NX; ++i) sv[i] = -c.eta[i];
       st_vec(a.s, t, T + 1, B, b, sv);
     }
+    if (t > t0) st = nst;
   }
-  if (emit_pagg) st_aff(a.pagg[1], j, a.plan.n[1], B, b, pa);
-  int fl = (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND) | (okq ? 0 : FLAG_DEF_Q);
+  if constexpr (emit_pagg) st_aff(a.pagg[1], j, a.plan.n[1], B, b, pa);
   if (fl) atomicOr(a.flags + b, fl);
 }
 
@@ -344,6 +345,21 @@ __global__ void __launch_bounds__(128) k_prop_down(LqrArgs<R> a, int l) {
   }
 }
 
+template <typename R, int NX, int NU>
+struct PropStage {
+  R Gam[NU][NX], gam[NU], Fx[NX][NX], Fu[NX][NU], dd[NU];
+};
+
+template <typename R, int NX, int NU>
+PTC_D void ld_prop_stage(const LqrArgs<R>& a, int t, int b, PropStage<R, NX, NU>& p) {
+  ld_mat(a.Gam, t, a.T, a.B, b, p.Gam);
+  ld_vec(a.gam, t, a.T, a.B, b, p.gam);
+  ld_mat(a.Fx, t, a.T, a.B, b, p.Fx);
+  ld_mat(a.Fu, t, a.T, a.B, b, p.Fu);
+  if (a.d) ld_vec(a.d, t, a.T, a.B, b, p.dd);
+  else set_zero(p.dd);
+}
+
 // level-0 forward sweep: dx_t, du_t = Gamma_t dx_t + gamma_t and the
 // per-chunk partial reductions used by the trust-region test
 template <typename R, int NX, int NU>
@@ -360,36 +376,35 @@ __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
   else if (a.x_in) ld_vec(a.x_in, 0, 1, B, b, x);
   else set_zero(x);
   double s2 = 0.0, sd = 0.0, mx = 0.0;
+  // software pipeline: stage t+1's law and Jacobians load while stage t runs
+  PropStage<R, NX, NU> ps;
+  if (t0 < t1) ld_prop_stage(a, t0, b, ps);
   for (int t = t0; t < t1; ++t) {
+    PropStage<R, NX, NU> nps;
+    if (t + 1 < t1) ld_prop_stage(a, t + 1, b, nps);
     st_vec(a.dX, t, T + 1, B, b, x);
-    R Gam[NU][NX], gam[NU], Fx[NX][NX], Fu[NX][NU], dd[NU];
-    ld_mat(a.Gam, t, T, B, b, Gam);
-    ld_vec(a.gam, t, T, B, b, gam);
-    ld_mat(a.Fx, t, T, B, b, Fx);
-    ld_mat(a.Fu, t, T, B, b, Fu);
-    if (a.d) ld_vec(a.d, t, T, B, b, dd);
-    else set_zero(dd);
     R du[NU];
-    mv<NU, NX>(Gam, x, du);
+    mv<NU, NX>(ps.Gam, x, du);
 #pragma unroll
     for (int i = 0; i < NU; ++i) {
-      du[i] += gam[i];
+      du[i] += ps.gam[i];
       s2 += double(du[i]) * double(du[i]);
-      sd += double(du[i]) * double(dd[i]);
+      sd += double(du[i]) * double(ps.dd[i]);
       mx = nanmax(mx, double(fabs(du[i])));
     }
     st_vec(a.dU, t, T, B, b, du);
     // closed loop: F = Fx + Fu Gamma (F = 0 on the head stage), e = Fu gamma
     R F[NX][NX], e[NX], y[NX];
-    mm<NX, NU, NX>(Fu, Gam, F);
+    mm<NX, NU, NX>(ps.Fu, ps.Gam, F);
 #pragma unroll
     for (int i = 0; i < NX; ++i)
 #pragma unroll
-      for (int k = 0; k < NX; ++k) F[i][k] = (t + a.t_base == 0) ? R(0) : F[i][k] + Fx[i][k];
-    mv<NX, NU>(Fu, gam, e);
+      for (int k = 0; k < NX; ++k) F[i][k] = (t + a.t_base == 0) ? R(0) : F[i][k] + ps.Fx[i][k];
+    mv<NX, NU>(ps.Fu, ps.gam, e);
     mv<NX, NX>(F, x, y);
 #pragma unroll
     for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
+    if (t + 1 < t1) ps = nps;
   }
   if (j == P0 - 1) st_vec(a.dX, T, T + 1, B, b, x);
   if (a.red) {
