@@ -204,43 +204,57 @@ def workload_config(n: int) -> dict:
 # ---------------------------------------------------------------------------
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING recipe)."""
+    """SM clocks and throttle reasons sampled DURING the timed region
+    (B200_PROFILING recipe): an NVML polling thread at ~1 ms (the timed
+    region of a config-3 run is only tens of ms), nvidia-smi as fallback."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+             ("hw_thermal_slowdown", "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+             ("sw_thermal_slowdown", "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+             ("sw_power_cap", "nvmlClocksThrottleReasonSwPowerCap", 0x4))
 
     def __init__(self, index: int):
-        self.path = tempfile.mktemp(suffix=".csv")
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
+        self.sm, self.smax, self.reasons, self.err = [], [], set(), None
+        self.stop_ev = threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        except Exception as err:  # noqa: BLE001 - report, never fail the bench
+            self.nv, self.err = None, f"nvml unavailable: {err}"
+        self.thread = threading.Thread(target=self._poll, daemon=True)
+        self.thread.start()
+
+    def _poll(self):
+        if self.nv is None:
+            return
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                mask = int(get_reasons(self.h))
+                for name, const, default in self.NAMES:
+                    if mask & int(getattr(nv, const, default)):
+                        self.reasons.add(name)
+            except Exception as err:  # noqa: BLE001
+                self.err = str(err)
+                return
+            self.stop_ev.wait(0.001)
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for row in open(self.path):
-            f = [x.strip() for x in row.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                smax.append(float(f[2]))
-            except ValueError:
-                continue
-            for name, val in zip(names, f[5:9]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
-                "reasons": sorted(reasons)}
+        self.stop_ev.set()
+        self.thread.join()
+        out = {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+               "sm_max_mhz": max(self.smax) if self.smax else None,
+               "samples": len(self.sm), "reasons": sorted(self.reasons), "source": "nvml"}
+        if self.err:
+            out["error"] = self.err
+        return out
 
 
 def measured_peak() -> tuple[float, str]:

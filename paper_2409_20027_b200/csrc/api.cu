@@ -1,6 +1,7 @@
 // C ABI implementation (include/pintoc_b200.h): workspace carving, the
 // batched solver object and dispatch into the instantiated kernel sets.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -130,6 +131,47 @@ int64_t ptc_lqr_workspace_bytes(int dtype, int batch, int horizon, int nx, int n
 
 }  // extern "C"
 
+// Graph cache of LQR launch sequences keyed by the full argument block
+// (plain-old-data, zero-initialised so padding compares equal).
+struct LqrGraph {
+  std::vector<unsigned char> key;
+  cudaGraphExec_t exec;
+};
+
+template <typename R>
+static cudaGraphExec_t lqr_graph_for(const LqrArgs<R>& a, const LqrOps& ops, cudaStream_t) {
+  static thread_local std::vector<LqrGraph> cache;
+  static thread_local cudaStream_t cap = nullptr;
+  const unsigned char* kb = reinterpret_cast<const unsigned char*>(&a);
+  std::vector<unsigned char> key(kb, kb + sizeof(a));
+  key.push_back((unsigned char)sizeof(R));
+  for (auto& g : cache)
+    if (g.key == key) return g.exec;
+  if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    ops.solve(&a, cap);
+    ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && g != nullptr;
+  }
+  if (ok) ok = cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+  if (g) cudaGraphDestroy(g);
+  if (!ok) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  if (cache.size() >= 32) {
+    cudaGraphExecDestroy(cache.front().exec);
+    cache.erase(cache.begin());
+  }
+  cache.push_back(LqrGraph{std::move(key), ex});
+  return ex;
+}
+
 template <typename R>
 static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, const void* Rm,
                        const void* M, const void* d, const void* Fx, const void* Fu,
@@ -140,7 +182,8 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
   if (it == lqr_registry().end())
     return fail(PTC_ERR_UNSUPPORTED, "LQR kernels not instantiated for nx=" + std::to_string(nx) +
                                          " nu=" + std::to_string(nu));
-  LqrArgs<R> a{};
+  LqrArgs<R> a;
+  std::memset(&a, 0, sizeof(a));  // padding too: the graph cache keys on the bytes
   a.B = batch;
   a.T = horizon;
   a.plan = auto_plan(batch, horizon, chunk0, chunk);
@@ -164,6 +207,15 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
   carve_lqr_tree(c, a, nx);
   if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
   if ((S == nullptr) != (s == nullptr)) return fail(PTC_ERR_ARG, "S and s must both be given or both NULL");
+  if (a.plan.L >= 1 && !getenv("PTC_NO_GRAPH")) {
+    // a tree plan is 4L+4 short launches: replay them as one CUDA graph,
+    // cached per argument set (same buffers -> same graph)
+    cudaGraphExec_t ex = lqr_graph_for(a, it->second, st);
+    if (ex) {
+      PTC_CUDA(cudaGraphLaunch(ex, st));
+      return PTC_OK;
+    }
+  }
   it->second.solve(&a, st);
   PTC_CUDA(cudaGetLastError());
   return PTC_OK;
@@ -630,8 +682,41 @@ struct Solver final : ptc_solver {
     return PTC_OK;
   }
 
+  // One Newton iteration is a fixed launch sequence over fixed buffers, so
+  // it is captured once into a CUDA graph (on a private stream: the legacy
+  // default stream cannot be captured) and replayed on the caller's stream.
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t iter_exec = nullptr;
+  bool graph_off = false;
+
+  void build_iteration_graph() {
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      ops->iterate(&na, &la, cap_stream);
+      ok = cudaStreamEndCapture(cap_stream, &g) == cudaSuccess && g != nullptr;
+    }
+    if (ok) ok = cudaGraphInstantiate(&iter_exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      iter_exec = nullptr;
+      graph_off = true;
+      (void)cudaGetLastError();
+    }
+  }
+
+  ~Solver() override {
+    if (iter_exec) cudaGraphExecDestroy(iter_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+  }
+
   int iterate(int n, cudaStream_t s) override {
-    for (int i = 0; i < n; ++i) ops->iterate(&na, &la, s);
+    if (n > 0 && !iter_exec && !graph_off && !getenv("PTC_NO_GRAPH")) build_iteration_graph();
+    for (int i = 0; i < n; ++i) {
+      if (iter_exec) PTC_CUDA(cudaGraphLaunch(iter_exec, s));
+      else ops->iterate(&na, &la, s);
+    }
     PTC_CUDA(cudaGetLastError());
     return PTC_OK;
   }

@@ -6,6 +6,7 @@
 #include <tuple>
 
 #include "newton_kernels.cuh"
+#include "wide.cuh"
 
 namespace ptc {
 
@@ -198,16 +199,25 @@ __global__ void k_force_phase(NewtonArgs<R> a, int ph) {
 
 template <typename R, int NX, int NU>
 struct RegisterLqr {
+  // nx >= 8: warp-cooperative kernels (wide.cuh); smaller states keep one
+  // thread per scan unit with every operand in registers
+  static constexpr bool kWide = NX >= 8;
   static void solve(const void* a, cudaStream_t s) {
-    launch_lqr<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
+    if constexpr (kWide) launch_lqr_wide<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
+    else launch_lqr<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
   }
   static void propagate(const void* a, cudaStream_t s) {
-    launch_prop<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
+    if constexpr (kWide) launch_prop_wide<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
+    else launch_prop<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), s);
   }
   static void block(const void* a, int phase, const void* blocks, void* out, int rank, int world,
                     cudaStream_t s) {
-    launch_lqr_block<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), phase, blocks, out, rank,
-                                world, s);
+    if constexpr (kWide)
+      launch_lqr_block_wide<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), phase, blocks, out,
+                                       rank, world, s);
+    else
+      launch_lqr_block<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), phase, blocks, out, rank,
+                                  world, s);
   }
   RegisterLqr() {
     lqr_registry()[LqrKey(dtype_code<R>(), NX, NU)] = LqrOps{&solve, &propagate, &block};

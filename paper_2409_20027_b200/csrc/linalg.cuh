@@ -109,8 +109,10 @@ PTC_D void set_zero(R (&a)[N]) {
   for (int i = 0; i < N; ++i) a[i] = R(0);
 }
 
-// In-place lower Cholesky factor.  Fails (returns false) exactly when LAPACK
-// potrf would: a non-positive or NaN pivot.
+// In-place lower Cholesky factor L (A = L L^T) with the RECIPROCAL of the
+// diagonal stored on the diagonal, so the solves below multiply instead of
+// divide (one division per row instead of one per right-hand side).  Fails
+// (returns false) exactly when LAPACK potrf would: a non-positive or NaN pivot.
 template <int N, typename R>
 PTC_D bool cholesky(R (&A)[N][N]) {
   bool ok = true;
@@ -120,9 +122,8 @@ PTC_D bool cholesky(R (&A)[N][N]) {
 #pragma unroll
     for (int k = 0; k < j; ++k) s = fma(-A[j][k], A[j][k], s);
     ok = ok && (s > R(0));
-    R d = sqrt(s);
-    A[j][j] = d;
-    R inv = R(1) / d;
+    const R inv = R(1) / sqrt(s);
+    A[j][j] = inv;
 #pragma unroll
     for (int i = j + 1; i < N; ++i) {
       R v = A[i][j];
@@ -134,7 +135,7 @@ PTC_D bool cholesky(R (&A)[N][N]) {
   return ok;
 }
 
-// Solve (L L^T) X = B in place, L from cholesky().
+// Solve (L L^T) X = B in place, L from cholesky() (reciprocal diagonal).
 template <int N, int M, typename R>
 PTC_D void chol_solve(const R (&L)[N][N], R (&B)[N][M]) {
 #pragma unroll
@@ -144,14 +145,14 @@ PTC_D void chol_solve(const R (&L)[N][N], R (&B)[N][M]) {
       R v = B[i][c];
 #pragma unroll
       for (int k = 0; k < i; ++k) v = fma(-L[i][k], B[k][c], v);
-      B[i][c] = v / L[i][i];
+      B[i][c] = v * L[i][i];
     }
 #pragma unroll
     for (int i = N - 1; i >= 0; --i) {
       R v = B[i][c];
 #pragma unroll
       for (int k = i + 1; k < N; ++k) v = fma(-L[k][i], B[k][c], v);
-      B[i][c] = v / L[i][i];
+      B[i][c] = v * L[i][i];
     }
   }
 }
@@ -163,14 +164,14 @@ PTC_D void chol_solve_vec(const R (&L)[N][N], R (&b)[N]) {
     R v = b[i];
 #pragma unroll
     for (int k = 0; k < i; ++k) v = fma(-L[i][k], b[k], v);
-    b[i] = v / L[i][i];
+    b[i] = v * L[i][i];
   }
 #pragma unroll
   for (int i = N - 1; i >= 0; --i) {
     R v = b[i];
 #pragma unroll
     for (int k = i + 1; k < N; ++k) v = fma(-L[k][i], b[k], v);
-    b[i] = v / L[i][i];
+    b[i] = v * L[i][i];
   }
 }
 
@@ -209,6 +210,7 @@ PTC_D bool lu_factor(R (&A)[N][N], int (&piv)[N]) {
     R pv = A[k][k];
     ok = ok && (pv != R(0));
     R inv = R(1) / pv;
+    A[k][k] = inv;  // U's diagonal is kept as reciprocals (solves multiply)
 #pragma unroll
     for (int i = k + 1; i < N; ++i) {
       R l = A[i][k] * inv;
@@ -241,7 +243,7 @@ PTC_D void lu_solve(const R (&LU)[N][N], const int (&piv)[N], R (&B)[N][M]) {
       R v = B[i][c];
 #pragma unroll
       for (int k = i + 1; k < N; ++k) v = fma(-LU[i][k], B[k][c], v);
-      B[i][c] = v / LU[i][i];
+      B[i][c] = v * LU[i][i];
     }
   }
 }
@@ -256,7 +258,7 @@ PTC_D void lu_solve_t(const R (&LU)[N][N], const int (&piv)[N], R (&B)[N][M]) {
       R v = B[i][c];
 #pragma unroll
       for (int k = 0; k < i; ++k) v = fma(-LU[k][i], B[k][c], v);
-      B[i][c] = v / LU[i][i];
+      B[i][c] = v * LU[i][i];
     }
 #pragma unroll
     for (int i = N - 2; i >= 0; --i) {  // L^T z = y (upper, unit)

@@ -1,0 +1,1054 @@
+// Warp-cooperative LQR-scan kernels for wide states (nx >= 8).
+//
+// The thread-per-unit kernels of lqr_kernels.cuh keep every matrix of a
+// combine in registers; at nx = 12 a value element alone is 456 words and
+// the combines spill to local memory and run as one long serial chain per
+// thread.  Here one WARP owns one scan unit: its operands live in a
+// per-warp shared-memory slab and the 32 lanes split every product over
+// output entries, every LU step over rows, every triangular solve over
+// right-hand-side columns.  Same plan, same tree, same block phases, same
+// arithmetic as the thread kernels (dual combine, Riccati-form level-0 step,
+// affine compositions) -- only the execution mapping differs.
+#pragma once
+
+#include "lqr_kernels.cuh"
+
+namespace ptc {
+
+constexpr int kWarpsPerBlock = 4;
+
+PTC_D int lane_id() { return threadIdx.x & 31; }
+PTC_D int warp_unit() { return blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); }
+
+// ------------------------------------------------------------ primitives
+
+// C (MxN) = op(A) op(B); A stored row-major as (TA ? KxM : MxK), B as
+// (TB ? NxK : KxN).  MODE 0: C = AB, 1: C += AB, -1: C -= AB.  C must not
+// alias A or B.
+template <int M, int K, int N, bool TA, bool TB, int MODE, typename R>
+PTC_D void w_mm(const R* A, const R* B, R* C) {
+  for (int e = lane_id(); e < M * N; e += 32) {
+    const int i = e / N, j = e - (e / N) * N;
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const R av = TA ? A[k * M + i] : A[i * K + k];
+      const R bv = TB ? B[j * K + k] : B[k * N + j];
+      s = (k == 0) ? av * bv : fma(av, bv, s);
+    }
+    if (MODE == 0) C[e] = s;
+    else if (MODE > 0) C[e] += s;
+    else C[e] -= s;
+  }
+  __syncwarp();
+}
+
+// y (M) = op(A) x; A stored as (TA ? KxM : MxK).  MODE as w_mm.
+template <int M, int K, bool TA, int MODE, typename R>
+PTC_D void w_mv(const R* A, const R* x, R* y) {
+  for (int i = lane_id(); i < M; i += 32) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const R av = TA ? A[k * M + i] : A[i * K + k];
+      s = (k == 0) ? av * x[k] : fma(av, x[k], s);
+    }
+    if (MODE == 0) y[i] = s;
+    else if (MODE > 0) y[i] += s;
+    else y[i] -= s;
+  }
+  __syncwarp();
+}
+
+template <int N, typename R>
+PTC_D void w_sym(R* A) {
+  for (int e = lane_id(); e < N * N; e += 32) {
+    const int i = e / N, j = e - (e / N) * N;
+    if (j > i) {
+      const R v = R(0.5) * (A[i * N + j] + A[j * N + i]);
+      A[i * N + j] = v;
+      A[j * N + i] = v;
+    }
+  }
+  __syncwarp();
+}
+
+template <int N, typename R>
+PTC_D void w_copy(const R* src, R* dst) {
+  for (int e = lane_id(); e < N; e += 32) dst[e] = src[e];
+  __syncwarp();
+}
+
+template <int N, typename R>
+PTC_D void w_fill(R* dst, R v) {
+  for (int e = lane_id(); e < N; e += 32) dst[e] = v;
+  __syncwarp();
+}
+
+template <int N, typename R>
+PTC_D void w_identity(R* A) {
+  for (int e = lane_id(); e < N * N; e += 32) A[e] = (e / N == e - (e / N) * N) ? R(1) : R(0);
+  __syncwarp();
+}
+
+// LU with partial pivoting of G (NxN, in place), reciprocal pivots on the
+// diagonal, the same pivot rule as lu_factor (first row of maximal |.|).
+template <int N, typename R>
+PTC_D bool w_lu(R* G, int* piv) {
+  const int ln = lane_id();
+  bool ok = true;
+  for (int k = 0; k < N; ++k) {
+    R v = (ln >= k && ln < N) ? fabs(G[ln * N + k]) : R(-1);
+    int p = (ln >= k && ln < N) ? ln : N;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const R ov = __shfl_xor_sync(0xffffffffu, v, off);
+      const int op = __shfl_xor_sync(0xffffffffu, p, off);
+      if (ov > v || (ov == v && op < p)) {
+        v = ov;
+        p = op;
+      }
+    }
+    if (!(v == v)) p = k;  // NaN column: keep the diagonal, as lu_factor does
+    if (ln == 0) piv[k] = p;
+    if (p != k)
+      for (int j = ln; j < N; j += 32) {
+        const R t = G[k * N + j];
+        G[k * N + j] = G[p * N + j];
+        G[p * N + j] = t;
+      }
+    __syncwarp();
+    const R pv = G[k * N + k];
+    ok = ok && (pv != R(0));
+    const R inv = R(1) / pv;
+    __syncwarp();
+    if (ln == 0) G[k * N + k] = inv;
+    for (int i = k + 1 + ln; i < N; i += 32) G[i * N + k] *= inv;
+    __syncwarp();
+    for (int e = ln; e < (N - k - 1) * (N - k - 1); e += 32) {
+      const int i = k + 1 + e / (N - k - 1), j = k + 1 + e % (N - k - 1);
+      G[i * N + j] = fma(-G[i * N + k], G[k * N + j], G[i * N + j]);
+    }
+    __syncwarp();
+  }
+  return ok;
+}
+
+// Solve G X = B (B: N x M row-major, in place); lanes own columns.
+template <int N, int M, typename R>
+PTC_D void w_lu_solve(const R* LU, const int* piv, R* B) {
+  for (int c = lane_id(); c < M; c += 32) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int p = piv[k];
+      if (p != k) {
+        const R t = B[k * M + c];
+        B[k * M + c] = B[p * M + c];
+        B[p * M + c] = t;
+      }
+    }
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
+      R v = B[i * M + c];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v = fma(-LU[i * N + k], B[k * M + c], v);
+      B[i * M + c] = v;
+    }
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) {
+      R v = B[i * M + c];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) v = fma(-LU[i * N + k], B[k * M + c], v);
+      B[i * M + c] = v * LU[i * N + i];
+    }
+  }
+  __syncwarp();
+}
+
+// Small SPD matrices (nu <= 6): every lane factors its own register copy.
+template <int N, typename R>
+PTC_D bool w_chol_regs(const R* Q, R (&L)[N][N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) L[i][j] = Q[i * N + j];
+  return cholesky<N>(L);
+}
+
+// ------------------------------------------------------------ slab layout
+
+template <typename R, int NX, int NU>
+struct WSlab {
+  static constexpr int VC = 3 * NX * NX + 2 * NX;
+  static constexpr int SC = NX * NX + NU * NU + NX * NU + NU + NX * NX + NX * NU;
+  // offsets (in elements of R)
+  static constexpr int oL = 0, oRt = VC, oO = 2 * VC, oSt = 3 * VC;
+  static constexpr int oG = oSt + SC, oX = oG + NX * NX, oZ = oX + NX * (2 * NX + 1);
+  static constexpr int oT1 = oZ + NX * (NX + 1), oT2 = oT1 + NX * NX, oT3 = oT2 + NX * NX;
+  static constexpr int nR = oT3 + NX * NX;
+  static constexpr int bytes = nR * (int)sizeof(R) + 16 * (int)sizeof(int);
+  // stage sub-offsets
+  static constexpr int sP = 0, sR = NX * NX, sM = sR + NU * NU, sd = sM + NX * NU,
+                       sFx = sd + NU, sFu = sFx + NX * NX;
+  // value element sub-offsets (global component order)
+  static constexpr int eA = 0, eY = NX * NX, eC = 2 * NX * NX, eEta = 3 * NX * NX,
+                       eB = 3 * NX * NX + NX;
+};
+
+template <typename R, int NX, int NU>
+PTC_D R* warp_slab() {
+  extern __shared__ __align__(16) unsigned char w_smem[];
+  return reinterpret_cast<R*>(w_smem + (threadIdx.x >> 5) * WSlab<R, NX, NU>::bytes);
+}
+
+template <typename R, int NX, int NU>
+PTC_D int* warp_piv(R* slab) {
+  return reinterpret_cast<int*>(slab + WSlab<R, NX, NU>::nR);
+}
+
+// global <-> slab (component c of item t at f[(c * rows + t) * B + b])
+template <int C, typename R>
+PTC_D void w_ld(const R* f, int t, int rows, int B, int b, R* dst, int c0 = 0) {
+  for (int c = lane_id(); c < C; c += 32) dst[c] = __ldg(f + ((size_t)(c0 + c) * rows + t) * B + b);
+  __syncwarp();
+}
+
+template <int C, typename R>
+PTC_D void w_st(R* f, int t, int rows, int B, int b, const R* src, int c0 = 0) {
+  for (int c = lane_id(); c < C; c += 32) f[((size_t)(c0 + c) * rows + t) * B + b] = src[c];
+  __syncwarp();
+}
+
+template <typename R, int NX, int NU>
+PTC_D void w_ld_stage(const LqrArgs<R>& a, int t, int b, R alpha, R* st) {
+  using S = WSlab<R, NX, NU>;
+  const int T = a.T, B = a.B;
+  w_ld<NX * NX>(a.P, t, T, B, b, st + S::sP);
+  w_ld<NU * NU>(a.Rm, t, T, B, b, st + S::sR);
+  w_ld<NX * NU>(a.M, t, T, B, b, st + S::sM);
+  w_ld<NU>(a.d, t, T, B, b, st + S::sd);
+  w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
+  w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
+  for (int i = lane_id(); i < NU; i += 32) st[S::sR + i * NU + i] += alpha;
+  __syncwarp();
+}
+
+// --------------------------------------------------------- element algebra
+
+// dual element of a stage (velem_from_stage); returns false when Rr fails
+// its Cholesky.  Uses X as scratch for Rr^-1 [M^T | Fu^T | d].
+template <typename R, int NX, int NU>
+PTC_D bool w_velem(const R* st, R* e, R* X) {
+  using S = WSlab<R, NX, NU>;
+  constexpr int W = 2 * NX + 1;  // columns of X (NU rows used)
+  R L[NU][NU];
+  const bool ok = w_chol_regs<NU>(st + S::sR, L);
+  const int ln = lane_id();
+  if (ln < W) {
+    R v[NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+      v[i] = ln < NX ? st[S::sM + ln * NU + i]
+                     : (ln < 2 * NX ? st[S::sFu + (ln - NX) * NU + i] : st[S::sd + i]);
+    chol_solve_vec<NU>(L, v);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) X[i * W + ln] = v[i];
+  }
+  __syncwarp();
+  // A = Fx - Fu RiMt, Y = sym(P - M RiMt), C = sym(Fu RiFt), eta = M Rid, b = -Fu Rid
+  for (int q = ln; q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    R fa = R(0), my = R(0), fc = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      const R fu = st[S::sFu + i * NU + k], m = st[S::sM + i * NU + k];
+      fa = (k == 0) ? fu * X[k * W + j] : fma(fu, X[k * W + j], fa);
+      my = (k == 0) ? m * X[k * W + j] : fma(m, X[k * W + j], my);
+      fc = (k == 0) ? fu * X[k * W + NX + j] : fma(fu, X[k * W + NX + j], fc);
+    }
+    e[S::eA + q] = st[S::sFx + q] - fa;
+    e[S::eY + q] = st[S::sP + q] - my;
+    e[S::eC + q] = fc;
+  }
+  for (int i = ln; i < NX; i += 32) {
+    R me = R(0), fb = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      me = (k == 0) ? st[S::sM + i * NU + k] * X[k * W + 2 * NX]
+                    : fma(st[S::sM + i * NU + k], X[k * W + 2 * NX], me);
+      fb = (k == 0) ? st[S::sFu + i * NU + k] * X[k * W + 2 * NX]
+                    : fma(st[S::sFu + i * NU + k], X[k * W + 2 * NX], fb);
+    }
+    e[S::eEta + i] = me;
+    e[S::eB + i] = -fb;
+  }
+  __syncwarp();
+  w_sym<NX>(e + S::eY);
+  w_sym<NX>(e + S::eC);
+  return ok;
+}
+
+template <typename R, int NX, int NU>
+PTC_D void w_velem_terminal(const R* PT, R* e) {
+  using S = WSlab<R, NX, NU>;
+  for (int q = lane_id(); q < S::VC; q += 32)
+    e[q] = (q >= S::eY && q < S::eY + NX * NX) ? PT[q - S::eY] : R(0);
+  __syncwarp();
+}
+
+// general combine o = l (x) r (vcombine); slab scratch G, X, Z, T1
+template <typename R, int NX, int NU>
+PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* slab) {
+  using S = WSlab<R, NX, NU>;
+  R* G = slab + S::oG;
+  R* X = slab + S::oX;
+  R* Z = slab + S::oZ;
+  R* T1 = slab + S::oT1;
+  int* piv = warp_piv<R, NX, NU>(slab);
+  constexpr int WX = 2 * NX + 1, WZ = NX + 1;
+  // G = I + C_l Y_r ; G^T is what the Z solve needs, so factor G^T directly
+  // Z = G^-T [Y_r A_l | eta_r - Y_r b_l]   X = G^-1 [A_l | C_l | b_l + C_l eta_r]
+  w_mm<NX, NX, NX, false, false, 0>(l + S::eC, r + S::eY, G);
+  // X rhs, Z rhs (independent of the factorisation)
+  for (int q = lane_id(); q < NX * WX; q += 32) {
+    const int i = q / WX, j = q - (q / WX) * WX;
+    if (j < NX) X[q] = l[S::eA + i * NX + j];
+    else if (j < 2 * NX) X[q] = l[S::eC + i * NX + (j - NX)];
+    else {
+      R s = l[S::eB + i];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) s = fma(l[S::eC + i * NX + k], r[S::eEta + k], s);
+      X[q] = s;
+    }
+  }
+  for (int q = lane_id(); q < NX * WZ; q += 32) {
+    const int i = q / WZ, j = q - (q / WZ) * WZ;
+    R s = R(0);
+    if (j < NX) {
+#pragma unroll
+      for (int k = 0; k < NX; ++k)
+        s = (k == 0) ? r[S::eY + i * NX] * l[S::eA + j] : fma(r[S::eY + i * NX + k], l[S::eA + k * NX + j], s);
+    } else {
+      R yb = R(0);
+#pragma unroll
+      for (int k = 0; k < NX; ++k) yb = (k == 0) ? r[S::eY + i * NX] * l[S::eB] : fma(r[S::eY + i * NX + k], l[S::eB + k], yb);
+      s = r[S::eEta + i] - yb;
+    }
+    Z[q] = s;
+  }
+  for (int i = lane_id(); i < NX; i += 32) G[i * NX + i] += R(1);
+  __syncwarp();
+  // transposed copy for the G^T solve
+  for (int q = lane_id(); q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    T1[j * NX + i] = G[q];
+  }
+  __syncwarp();
+  bool ok = w_lu<NX>(G, piv);
+  w_lu_solve<NX, WX>(G, piv, X);
+  ok = w_lu<NX>(T1, piv) && ok;
+  w_lu_solve<NX, WZ>(T1, piv, Z);
+  // Y = sym(A_l^T Z1 + Y_l), eta = A_l^T z + eta_l
+  for (int q = lane_id(); q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? l[S::eA + i] * Z[j] : fma(l[S::eA + k * NX + i], Z[k * WZ + j], s);
+    o[S::eY + q] = s + l[S::eY + q];
+  }
+  for (int i = lane_id(); i < NX; i += 32) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? l[S::eA + i] * Z[NX] : fma(l[S::eA + k * NX + i], Z[k * WZ + NX], s);
+    o[S::eEta + i] = s + l[S::eEta + i];
+  }
+  // A = A_r X1, T1 = A_r X2, b = A_r x + b_r
+  for (int q = lane_id(); q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    R s1 = R(0), s2 = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) {
+      const R ar = r[S::eA + i * NX + k];
+      s1 = (k == 0) ? ar * X[j] : fma(ar, X[k * WX + j], s1);
+      s2 = (k == 0) ? ar * X[NX + j] : fma(ar, X[k * WX + NX + j], s2);
+    }
+    o[S::eA + q] = s1;
+    T1[q] = s2;
+  }
+  for (int i = lane_id(); i < NX; i += 32) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? r[S::eA + i * NX] * X[2 * NX] : fma(r[S::eA + i * NX + k], X[k * WX + 2 * NX], s);
+    o[S::eB + i] = s + r[S::eB + i];
+  }
+  __syncwarp();
+  // C = sym(T1 A_r^T + C_r)
+  for (int q = lane_id(); q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? T1[i * NX] * r[S::eA + j * NX] : fma(T1[i * NX + k], r[S::eA + j * NX + k], s);
+    o[S::eC + q] = s + r[S::eC + q];
+  }
+  __syncwarp();
+  w_sym<NX>(o + S::eY);
+  w_sym<NX>(o + S::eC);
+  return ok;
+}
+
+// carry step o = e (x) c for a carry (Y, eta) (vstep); c and o are carries
+// stored as [Y (NX*NX) | eta (NX)]
+template <typename R, int NX, int NU>
+PTC_D bool w_vstep(const R* e, const R* c, R* o, R* slab) {
+  using S = WSlab<R, NX, NU>;
+  R* G = slab + S::oG;
+  R* Z = slab + S::oZ;
+  int* piv = warp_piv<R, NX, NU>(slab);
+  constexpr int WZ = NX + 1;
+  // G = I + Y_c C_e ; Z = [Y_c A_e | eta_c - Y_c b_e] ; Z <- G^-1 Z
+  w_mm<NX, NX, NX, false, false, 0>(c, e + S::eC, G);
+  for (int q = lane_id(); q < NX * WZ; q += 32) {
+    const int i = q / WZ, j = q - (q / WZ) * WZ;
+    R s = R(0);
+    if (j < NX) {
+#pragma unroll
+      for (int k = 0; k < NX; ++k) s = (k == 0) ? c[i * NX] * e[S::eA + j] : fma(c[i * NX + k], e[S::eA + k * NX + j], s);
+    } else {
+      R yb = R(0);
+#pragma unroll
+      for (int k = 0; k < NX; ++k) yb = (k == 0) ? c[i * NX] * e[S::eB] : fma(c[i * NX + k], e[S::eB + k], yb);
+      s = c[NX * NX + i] - yb;
+    }
+    Z[q] = s;
+  }
+  for (int i = lane_id(); i < NX; i += 32) G[i * NX + i] += R(1);
+  __syncwarp();
+  const bool ok = w_lu<NX>(G, piv);
+  w_lu_solve<NX, WZ>(G, piv, Z);
+  for (int q = lane_id(); q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? e[S::eA + i] * Z[j] : fma(e[S::eA + k * NX + i], Z[k * WZ + j], s);
+    o[q] = s + e[S::eY + q];
+  }
+  for (int i = lane_id(); i < NX; i += 32) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? e[S::eA + i] * Z[NX] : fma(e[S::eA + k * NX + i], Z[k * WZ + NX], s);
+    o[NX * NX + i] = s + e[S::eEta + i];
+  }
+  __syncwarp();
+  w_sym<NX>(o);
+  return ok;
+}
+
+// Riccati-form level-0 step (riccati_step): stage st, carry c -> gains
+// (written to Gam (NU*NX) and gam (NU) in the slab) and carry o.
+template <typename R, int NX, int NU>
+PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* slab) {
+  using S = WSlab<R, NX, NU>;
+  R* FtS = slab + S::oX;                 // NU x NX
+  R* Qux = FtS + NU * NX;                // NU x NX
+  R* Qm = Qux + NU * NX;                 // NU x NU
+  R* SF = slab + S::oT1;                 // NX x NX
+  int fl = 0;
+  {
+    R L[NU][NU];
+    if (!w_chol_regs<NU>(st + S::sR, L)) fl |= FLAG_DEF_R;
+  }
+  w_mm<NU, NX, NX, true, false, 0>(st + S::sFu, c, FtS);
+  w_mm<NX, NX, NX, false, false, 0>(c, st + S::sFx, SF);
+  w_mm<NU, NX, NU, false, false, 0>(FtS, st + S::sFu, Qm);
+  w_mm<NU, NX, NX, false, false, 0>(FtS, st + S::sFx, Qux);
+  for (int q = lane_id(); q < NU * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    Qux[q] += st[S::sM + j * NU + i];
+  }
+  __syncwarp();
+  R L[NU][NU];
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j)
+      L[i][j] = R(0.5) * ((Qm[i * NU + j] + st[S::sR + i * NU + j]) +
+                          (Qm[j * NU + i] + st[S::sR + j * NU + i]));
+  if (!cholesky<NU>(L)) fl |= FLAG_DEF_Q;
+  const int ln = lane_id();
+  if (ln <= NX) {  // lanes 0..NX-1: columns of Gamma, lane NX: gamma
+    R v[NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      if (ln < NX) {
+        v[i] = Qux[i * NX + ln];
+      } else {
+        R fe = R(0);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) fe = (k == 0) ? st[S::sFu + i] * c[NX * NX] : fma(st[S::sFu + k * NU + i], c[NX * NX + k], fe);
+        v[i] = st[S::sd + i] - fe;
+      }
+    }
+    chol_solve_vec<NU>(L, v);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      if (ln < NX) Gam[i * NX + ln] = -v[i];
+      else gam[i] = -v[i];
+    }
+  }
+  __syncwarp();
+  // S' = sym(P + Fx^T SF + Qux^T Gam), eta' = Fx^T eta - Qux^T gam
+  for (int q = ln; q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? st[S::sFx + i] * SF[j] : fma(st[S::sFx + k * NX + i], SF[k * NX + j], s);
+    R g = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) g = (k == 0) ? Qux[i] * Gam[j] : fma(Qux[k * NX + i], Gam[k * NX + j], g);
+    o[q] = s + (st[S::sP + q] + g);
+  }
+  for (int i = ln; i < NX; i += 32) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) s = (k == 0) ? st[S::sFx + i] * c[NX * NX] : fma(st[S::sFx + k * NX + i], c[NX * NX + k], s);
+    R g = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) g = (k == 0) ? Qux[i] * gam[0] : fma(Qux[k * NX + i], gam[k], g);
+    o[NX * NX + i] = s - g;
+  }
+  __syncwarp();
+  w_sym<NX>(o);
+  return fl;
+}
+
+// affine maps [F (NX*NX) | e (NX)]: o = outer o inner
+template <typename R, int NX>
+PTC_D void w_aff_compose(const R* outer, const R* inner, R* o) {
+  w_mm<NX, NX, NX, false, false, 0>(outer, inner, o);
+  w_mv<NX, NX, false, 0>(outer, inner + NX * NX, o + NX * NX);
+  for (int i = lane_id(); i < NX; i += 32) o[NX * NX + i] += outer[NX * NX + i];
+  __syncwarp();
+}
+
+// closed-loop map of stage t: F = Fx + Fu Gamma (0 at global stage 0), e = Fu gamma
+template <typename R, int NX, int NU>
+PTC_D void w_closed_loop(const R* Fx, const R* Fu, const R* Gam, const R* gam, bool head, R* m) {
+  for (int q = lane_id(); q < NX * NX; q += 32) {
+    const int i = q / NX, j = q - (q / NX) * NX;
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) s = (k == 0) ? Fu[i * NU] * Gam[j] : fma(Fu[i * NU + k], Gam[k * NX + j], s);
+    m[q] = head ? R(0) : s + Fx[q];
+  }
+  for (int i = lane_id(); i < NX; i += 32) {
+    R s = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) s = (k == 0) ? Fu[i * NU] * gam[0] : fma(Fu[i * NU + k], gam[k], s);
+    m[NX * NX + i] = s;
+  }
+  __syncwarp();
+}
+
+#define PTC_WIDE_PROLOGUE(count)                     \
+  const int u = warp_unit();                         \
+  if (u >= (count) * a.B) return;                    \
+  const int b = u % a.B, j = u / a.B;                \
+  (void)j;                                           \
+  if (lqr_skip(a, b)) return;                        \
+  using S = WSlab<R, NX, NU>;                        \
+  R* slab = warp_slab<R, NX, NU>();                  \
+  (void)slab;
+
+// ------------------------------------------------------------ value scan
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_value_up0(LqrArgs<R> a) {
+  PTC_WIDE_PROLOGUE(a.plan.units0())
+  const int P0 = a.plan.units0(), T = a.T;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const R alpha = R(a.alpha[b]);
+  R* acc = slab + S::oL;
+  R* e = slab + S::oRt;
+  R* o = slab + S::oO;
+  R* st = slab + S::oSt;
+  bool okr = true, okc = true;
+  int start;
+  if (j == P0 - 1 && !a.no_terminal) {
+    w_ld<NX * NX>(a.PT, 0, 1, a.B, b, slab + S::oT2);
+    w_velem_terminal<R, NX, NU>(slab + S::oT2, acc);
+    start = t1 - 1;
+  } else {
+    w_ld_stage<R, NX, NU>(a, t1 - 1, b, alpha, st);
+    okr &= w_velem<R, NX, NU>(st, acc, slab + S::oX);
+    start = t1 - 2;
+  }
+  for (int t = start; t >= t0; --t) {
+    w_ld_stage<R, NX, NU>(a, t, b, alpha, st);
+    okr &= w_velem<R, NX, NU>(st, e, slab + S::oX);
+    okc &= w_vcombine<R, NX, NU>(e, acc, o, slab);
+    w_copy<S::VC>(o, acc);
+  }
+  w_st<S::VC>(a.vagg[1], j, a.plan.n[1], a.B, b, acc);
+  const int fl = (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND);
+  if (fl && lane_id() == 0) atomicOr(a.flags + b, fl);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_value_up(LqrArgs<R> a, int l) {
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  R* acc = slab + S::oL;
+  R* e = slab + S::oRt;
+  R* o = slab + S::oO;
+  w_ld<S::VC>(a.vagg[l], last, nl, a.B, b, acc);
+  bool okc = true;
+  for (int i = last - 1; i >= first; --i) {
+    w_ld<S::VC>(a.vagg[l], i, nl, a.B, b, e);
+    okc &= w_vcombine<R, NX, NU>(e, acc, o, slab);
+    w_copy<S::VC>(o, acc);
+  }
+  w_st<S::VC>(a.vagg[l + 1], j, nn, a.B, b, acc);
+  if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_value_top(LqrArgs<R> a) {
+  PTC_WIDE_PROLOGUE(1)
+  constexpr int CC = NX * NX + NX;
+  const int L = a.plan.L, nL = a.plan.n[L];
+  R* c = slab + S::oL;
+  R* e = slab + S::oRt;
+  R* o = slab + S::oO;
+  if (a.vcarry_in) w_ld<CC>(a.vcarry_in, 0, 1, a.B, b, c);
+  else w_fill<CC>(c, R(0));
+  bool okc = true;
+  for (int i = nL - 1; i >= 0; --i) {
+    w_st<CC>(a.vcar[L], i, nL, a.B, b, c);
+    w_ld<S::VC>(a.vagg[L], i, nL, a.B, b, e);
+    okc &= w_vstep<R, NX, NU>(e, c, o, slab);
+    w_copy<CC>(o, c);
+  }
+  if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_value_down(LqrArgs<R> a, int l) {
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
+  constexpr int CC = NX * NX + NX;
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  R* c = slab + S::oL;
+  R* e = slab + S::oRt;
+  R* o = slab + S::oO;
+  w_ld<CC>(a.vcar[l + 1], j, nn, a.B, b, c);
+  bool okc = true;
+  for (int i = last; i >= first; --i) {
+    w_st<CC>(a.vcar[l], i, nl, a.B, b, c);
+    w_ld<S::VC>(a.vagg[l], i, nl, a.B, b, e);
+    okc &= w_vstep<R, NX, NU>(e, c, o, slab);
+    w_copy<CC>(o, c);
+  }
+  if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
+}
+
+template <typename R, int NX, int NU, bool kAgg>
+__global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
+  PTC_WIDE_PROLOGUE(a.plan.units0())
+  constexpr int CC = NX * NX + NX;
+  const int P0 = a.plan.units0(), T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const R alpha = R(a.alpha[b]);
+  const bool tree = a.plan.L >= 1;
+  R* c = slab + S::oL;               // carry [Y | eta]
+  R* o = c + CC;                     // next carry
+  R* pa = slab + S::oRt;             // propagation aggregate [F | e]
+  R* m = pa + CC;                    // stage closed-loop map
+  R* pt = slab + S::oO;              // composition scratch
+  R* st = slab + S::oSt;
+  R* Gam = slab + S::oT2;            // NU x NX
+  R* gam = slab + S::oT3;            // NU
+  if (tree) w_ld<CC>(a.vcar[1], j, a.plan.n[1], B, b, c);
+  else if (a.vcarry_in) w_ld<CC>(a.vcarry_in, 0, 1, B, b, c);
+  else w_fill<CC>(c, R(0));
+  if (j == P0 - 1 && a.no_terminal && a.S) {
+    w_st<NX * NX>(a.S, T, T + 1, B, b, c);
+    for (int i = lane_id(); i < NX; i += 32) o[i] = -c[NX * NX + i];
+    __syncwarp();
+    w_st<NX>(a.s, T, T + 1, B, b, o);
+  }
+  if (j == P0 - 1 && !a.no_terminal) {
+    w_ld<NX * NX>(a.PT, 0, 1, B, b, c);
+    w_fill<NX>(c + NX * NX, R(0));
+    if (a.S) {
+      w_st<NX * NX>(a.S, T, T + 1, B, b, c);
+      w_st<NX>(a.s, T, T + 1, B, b, c + NX * NX);
+    }
+  }
+  if constexpr (kAgg) {
+    w_identity<NX>(pa);
+    w_fill<NX>(pa + NX * NX, R(0));
+  }
+  int fl = 0;
+  for (int t = t1 - 1; t >= t0; --t) {
+    w_ld_stage<R, NX, NU>(a, t, b, alpha, st);
+    fl |= w_riccati<R, NX, NU>(st, c, o, Gam, gam, slab);
+    w_st<NU * NX>(a.Gam, t, T, B, b, Gam);
+    w_st<NU>(a.gam, t, T, B, b, gam);
+    if constexpr (kAgg) {
+      w_closed_loop<R, NX, NU>(st + S::sFx, st + S::sFu, Gam, gam, t + a.t_base == 0, m);
+      w_aff_compose<R, NX>(pa, m, pt);
+      w_copy<CC>(pt, pa);
+    }
+    w_copy<CC>(o, c);
+    if (a.S) {
+      w_st<NX * NX>(a.S, t, T + 1, B, b, c);
+      for (int i = lane_id(); i < NX; i += 32) o[i] = -c[NX * NX + i];
+      __syncwarp();
+      w_st<NX>(a.s, t, T + 1, B, b, o);
+    }
+  }
+  if constexpr (kAgg) w_st<CC>(a.pagg[1], j, a.plan.n[1], B, b, pa);
+  if (fl && lane_id() == 0) atomicOr(a.flags + b, fl);
+}
+
+// ------------------------------------------------------ propagation scan
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_prop_up(LqrArgs<R> a, int l) {
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
+  constexpr int CC = NX * NX + NX;
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  R* acc = slab + S::oL;
+  R* m = slab + S::oRt;
+  R* o = slab + S::oO;
+  w_ld<CC>(a.pagg[l], first, nl, a.B, b, acc);
+  for (int i = first + 1; i <= last; ++i) {
+    w_ld<CC>(a.pagg[l], i, nl, a.B, b, m);
+    w_aff_compose<R, NX>(m, acc, o);
+    w_copy<CC>(o, acc);
+  }
+  w_st<CC>(a.pagg[l + 1], j, nn, a.B, b, acc);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_prop_up0(LqrArgs<R> a) {
+  PTC_WIDE_PROLOGUE(a.plan.units0())
+  constexpr int CC = NX * NX + NX;
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  R* acc = slab + S::oL;
+  R* m = slab + S::oRt;
+  R* o = slab + S::oO;
+  R* st = slab + S::oSt;
+  R* Gam = slab + S::oT2;
+  R* gam = slab + S::oT3;
+  w_identity<NX>(acc);
+  w_fill<NX>(acc + NX * NX, R(0));
+  for (int t = t0; t < t1; ++t) {
+    w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
+    w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
+    w_ld<NU * NX>(a.Gam, t, T, B, b, Gam);
+    w_ld<NU>(a.gam, t, T, B, b, gam);
+    w_closed_loop<R, NX, NU>(st + S::sFx, st + S::sFu, Gam, gam, t + a.t_base == 0, m);
+    w_aff_compose<R, NX>(m, acc, o);
+    w_copy<CC>(o, acc);
+  }
+  w_st<CC>(a.pagg[1], j, a.plan.n[1], B, b, acc);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_prop_top(LqrArgs<R> a) {
+  PTC_WIDE_PROLOGUE(1)
+  constexpr int CC = NX * NX + NX;
+  const int L = a.plan.L, nL = a.plan.n[L];
+  R* x = slab + S::oL;
+  R* m = slab + S::oRt;
+  R* y = slab + S::oO;
+  if (a.x_in) w_ld<NX>(a.x_in, 0, 1, a.B, b, x);
+  else w_fill<NX>(x, R(0));
+  for (int i = 0; i < nL; ++i) {
+    w_st<NX>(a.pcar[L], i, nL, a.B, b, x);
+    w_ld<CC>(a.pagg[L], i, nL, a.B, b, m);
+    w_mv<NX, NX, false, 0>(m, x, y);
+    for (int k = lane_id(); k < NX; k += 32) x[k] = y[k] + m[NX * NX + k];
+    __syncwarp();
+  }
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_prop_down(LqrArgs<R> a, int l) {
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
+  constexpr int CC = NX * NX + NX;
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  R* x = slab + S::oL;
+  R* m = slab + S::oRt;
+  R* y = slab + S::oO;
+  w_ld<NX>(a.pcar[l + 1], j, nn, a.B, b, x);
+  for (int i = first; i <= last; ++i) {
+    w_st<NX>(a.pcar[l], i, nl, a.B, b, x);
+    w_ld<CC>(a.pagg[l], i, nl, a.B, b, m);
+    w_mv<NX, NX, false, 0>(m, x, y);
+    for (int k = lane_id(); k < NX; k += 32) x[k] = y[k] + m[NX * NX + k];
+    __syncwarp();
+  }
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_prop_down0(LqrArgs<R> a) {
+  PTC_WIDE_PROLOGUE(a.plan.units0())
+  const int P0 = a.plan.units0(), T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  R* x = slab + S::oL;
+  R* y = slab + S::oO;
+  R* du = y + NX;
+  R* st = slab + S::oSt;
+  R* Gam = slab + S::oT2;
+  R* gam = slab + S::oT3;
+  R* dd = gam + NU;
+  if (a.plan.L >= 1) w_ld<NX>(a.pcar[1], j, a.plan.n[1], B, b, x);
+  else if (a.x_in) w_ld<NX>(a.x_in, 0, 1, B, b, x);
+  else w_fill<NX>(x, R(0));
+  double s2 = 0.0, sd = 0.0, mx = 0.0;  // accumulated by lane 0
+  const int ln = lane_id();
+  for (int t = t0; t < t1; ++t) {
+    w_st<NX>(a.dX, t, T + 1, B, b, x);
+    w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
+    w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
+    w_ld<NU * NX>(a.Gam, t, T, B, b, Gam);
+    w_ld<NU>(a.gam, t, T, B, b, gam);
+    if (a.d) w_ld<NU>(a.d, t, T, B, b, dd);
+    else w_fill<NU>(dd, R(0));
+    w_mv<NU, NX, false, 0>(Gam, x, du);
+    for (int i = ln; i < NU; i += 32) du[i] += gam[i];
+    __syncwarp();
+    if (ln == 0) {
+#pragma unroll
+      for (int i = 0; i < NU; ++i) {
+        s2 += double(du[i]) * double(du[i]);
+        sd += double(du[i]) * double(dd[i]);
+        mx = nanmax(mx, double(fabs(du[i])));
+      }
+    }
+    w_st<NU>(a.dU, t, T, B, b, du);
+    // x <- (Fx + Fu Gamma) x + Fu gamma  (F = 0 at global stage 0)
+    const bool head = t + a.t_base == 0;
+    for (int i = ln; i < NX; i += 32) {
+      R fgx = R(0);
+#pragma unroll
+      for (int k = 0; k < NU; ++k) {
+        R gx = R(0);
+#pragma unroll
+        for (int q = 0; q < NX; ++q) gx = (q == 0) ? Gam[k * NX] * x[0] : fma(Gam[k * NX + q], x[q], gx);
+        fgx = (k == 0) ? st[S::sFu + i * NU] * gx : fma(st[S::sFu + i * NU + k], gx, fgx);
+      }
+      R fx = R(0);
+#pragma unroll
+      for (int q = 0; q < NX; ++q) fx = (q == 0) ? st[S::sFx + i * NX] * x[0] : fma(st[S::sFx + i * NX + q], x[q], fx);
+      R e = R(0);
+#pragma unroll
+      for (int k = 0; k < NU; ++k) e = (k == 0) ? st[S::sFu + i * NU] * gam[0] : fma(st[S::sFu + i * NU + k], gam[k], e);
+      y[i] = (head ? R(0) : fx + fgx) + e;
+    }
+    __syncwarp();
+    w_copy<NX>(y, x);
+  }
+  if (j == P0 - 1) w_st<NX>(a.dX, T, T + 1, B, b, x);
+  if (a.red && ln == 0) {
+    a.red[((size_t)0 * P0 + j) * B + b] = s2;
+    a.red[((size_t)1 * P0 + j) * B + b] = sd;
+    a.red[((size_t)2 * P0 + j) * B + b] = mx;
+  }
+}
+
+// ------------------------------------------------------------ time blocks
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_value_block(LqrArgs<R> a, R* out) {
+  PTC_WIDE_PROLOGUE(1)
+  const int L = a.plan.L > 0 ? a.plan.L : 1, nL = a.plan.n[L];
+  R* acc = slab + S::oL;
+  R* e = slab + S::oRt;
+  R* o = slab + S::oO;
+  w_ld<S::VC>(a.vagg[L], nL - 1, nL, a.B, b, acc);
+  bool okc = true;
+  for (int i = nL - 2; i >= 0; --i) {
+    w_ld<S::VC>(a.vagg[L], i, nL, a.B, b, e);
+    okc &= w_vcombine<R, NX, NU>(e, acc, o, slab);
+    w_copy<S::VC>(o, acc);
+  }
+  w_st<S::VC>(out, 0, 1, a.B, b, acc);
+  if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_value_carry(LqrArgs<R> a, const R* blocks, int rank,
+                                                      int world) {
+  PTC_WIDE_PROLOGUE(1)
+  constexpr int CC = NX * NX + NX;
+  R* c = slab + S::oL;
+  R* e = slab + S::oRt;
+  R* o = slab + S::oO;
+  w_fill<CC>(c, R(0));
+  bool okc = true;
+  for (int r = world - 1; r > rank; --r) {
+    w_ld<S::VC>(blocks + (size_t)r * S::VC * a.B, 0, 1, a.B, b, e);
+    okc &= w_vstep<R, NX, NU>(e, c, o, slab);
+    w_copy<CC>(o, c);
+  }
+  w_st<CC>(a.vcin_buf, 0, 1, a.B, b, c);
+  if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_prop_block(LqrArgs<R> a, R* out) {
+  PTC_WIDE_PROLOGUE(1)
+  constexpr int CC = NX * NX + NX;
+  const int L = a.plan.L > 0 ? a.plan.L : 1, nL = a.plan.n[L];
+  R* acc = slab + S::oL;
+  R* m = slab + S::oRt;
+  R* o = slab + S::oO;
+  w_ld<CC>(a.pagg[L], 0, nL, a.B, b, acc);
+  for (int i = 1; i < nL; ++i) {
+    w_ld<CC>(a.pagg[L], i, nL, a.B, b, m);
+    w_aff_compose<R, NX>(m, acc, o);
+    w_copy<CC>(o, acc);
+  }
+  w_st<CC>(out, 0, 1, a.B, b, acc);
+}
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(128) kw_prop_carry(LqrArgs<R> a, const R* blocks, int rank) {
+  PTC_WIDE_PROLOGUE(1)
+  constexpr int CC = NX * NX + NX;
+  R* x = slab + S::oL;
+  R* m = slab + S::oRt;
+  R* y = slab + S::oO;
+  w_fill<NX>(x, R(0));
+  for (int r = 0; r < rank; ++r) {
+    w_ld<CC>(blocks + (size_t)r * CC * a.B, 0, 1, a.B, b, m);
+    w_mv<NX, NX, false, 0>(m, x, y);
+    for (int k = lane_id(); k < NX; k += 32) x[k] = y[k] + m[NX * NX + k];
+    __syncwarp();
+  }
+  w_st<NX>(a.xin_buf, 0, 1, a.B, b, x);
+}
+
+#undef PTC_WIDE_PROLOGUE
+
+// ------------------------------------------------------------ launchers
+
+template <typename R, int NX, int NU>
+struct Wide {
+  static constexpr int kSmem = kWarpsPerBlock * WSlab<R, NX, NU>::bytes;
+  static dim3 grid(long long units) {
+    return dim3((unsigned)((units + kWarpsPerBlock - 1) / kWarpsPerBlock));
+  }
+  template <class K>
+  static void allow(K kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  }
+  static void setup() {
+    static bool done = false;
+    if (done) return;
+    allow(kw_value_up0<R, NX, NU>);
+    allow(kw_value_up<R, NX, NU>);
+    allow(kw_value_top<R, NX, NU>);
+    allow(kw_value_down<R, NX, NU>);
+    allow(kw_value_down0<R, NX, NU, true>);
+    allow(kw_value_down0<R, NX, NU, false>);
+    allow(kw_prop_up<R, NX, NU>);
+    allow(kw_prop_up0<R, NX, NU>);
+    allow(kw_prop_top<R, NX, NU>);
+    allow(kw_prop_down<R, NX, NU>);
+    allow(kw_prop_down0<R, NX, NU>);
+    allow(kw_value_block<R, NX, NU>);
+    allow(kw_value_carry<R, NX, NU>);
+    allow(kw_prop_block<R, NX, NU>);
+    allow(kw_prop_carry<R, NX, NU>);
+    done = true;
+  }
+};
+
+template <typename R, int NX, int NU>
+void launch_prop_tree_wide(const LqrArgs<R>& a, cudaStream_t s) {
+  using W = Wide<R, NX, NU>;
+  const Plan& pl = a.plan;
+  const long long B = a.B;
+  for (int l = 1; l < pl.L; ++l) kw_prop_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+  kw_prop_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
+  for (int l = pl.L - 1; l >= 1; --l)
+    kw_prop_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+}
+
+template <typename R, int NX, int NU>
+void launch_lqr_wide(const LqrArgs<R>& a, cudaStream_t s) {
+  using W = Wide<R, NX, NU>;
+  W::setup();
+  const Plan& pl = a.plan;
+  const long long B = a.B, P0 = pl.units0();
+  if (pl.L >= 1) {
+    kw_value_up0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) kw_value_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+    kw_value_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
+    for (int l = pl.L - 1; l >= 1; --l)
+      kw_value_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+    kw_value_down0<R, NX, NU, true><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    launch_prop_tree_wide<R, NX, NU>(a, s);
+  } else {
+    kw_value_down0<R, NX, NU, false><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+  }
+  kw_prop_down0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+}
+
+template <typename R, int NX, int NU>
+void launch_prop_wide(const LqrArgs<R>& a, cudaStream_t s) {
+  using W = Wide<R, NX, NU>;
+  W::setup();
+  const Plan& pl = a.plan;
+  const long long B = a.B, P0 = pl.units0();
+  if (pl.L >= 1) {
+    kw_prop_up0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    launch_prop_tree_wide<R, NX, NU>(a, s);
+  }
+  kw_prop_down0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+}
+
+template <typename R, int NX, int NU>
+void launch_lqr_block_wide(const LqrArgs<R>& a0, int phase, const void* blocks, void* out,
+                           int rank, int world, cudaStream_t s) {
+  using W = Wide<R, NX, NU>;
+  W::setup();
+  LqrArgs<R> a = a0;
+  const Plan& pl = a.plan;
+  const long long B = a.B, P0 = pl.units0();
+  if (phase == 0) {
+    kw_value_up0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) kw_value_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+    kw_value_block<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<R*>(out));
+  } else if (phase == 1) {
+    kw_value_carry<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<const R*>(blocks), rank, world);
+    a.vcarry_in = a.vcin_buf;
+    if (pl.L >= 1) {
+      kw_value_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
+      for (int l = pl.L - 1; l >= 1; --l)
+        kw_value_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+    }
+    kw_value_down0<R, NX, NU, true><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    for (int l = 1; l < pl.L; ++l) kw_prop_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+    kw_prop_block<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<R*>(out));
+  } else {
+    kw_prop_carry<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<const R*>(blocks), rank);
+    a.x_in = a.xin_buf;
+    if (pl.L >= 1) {
+      kw_prop_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
+      for (int l = pl.L - 1; l >= 1; --l)
+        kw_prop_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+    }
+    kw_prop_down0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+  }
+}
+
+}  // namespace ptc

@@ -145,9 +145,10 @@ def test_cuda_time_blocks_match_oracle(world, nx, nu, T):
         for name, got, want in zip(("S", "s", "Gamma", "gamma", "dx", "du"), _assemble(ops), ref):
             assert got.shape == want.shape, name
             assert rel_gap(got, want) < 1e-9, (world, plan, name)
-        # block-boundary consistency: rank r's last dx row is rank r+1's first
+        # block-boundary consistency: rank r's swept last dx row and rank
+        # r+1's carried first row agree to rounding (different association)
         for a, b in zip(ops, ops[1:]):
-            assert torch.equal(a.dx[:, -1], b.dx[:, 0])
+            assert torch.allclose(a.dx[:, -1], b.dx[:, 0], rtol=1e-12, atol=1e-12)
 
 
 @pytest.mark.gpu
