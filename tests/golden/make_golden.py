@@ -395,6 +395,29 @@ def case_admm_cartpole_cfg2():
     save("admm_cartpole_cfg2", **out)
 
 
+def case_admm_cartpole_cfg2_nudge():
+    """Reproducibility of config 2's Newton iteration counts in the reference
+    itself: the first three ADMM outer steps from the config-2 start and from
+    the start moved by one ulp either way (~1.5 min)."""
+    T = 500
+    dyn = CartPoleDynamics(T, CartPoleParams(cart_mass=1.0, pole_mass=0.1,
+                                             pole_length=0.5, dt=0.02))
+    Q = np.diag([1.0, 10.0, 0.1, 0.1])
+    cost = QuadraticCost(Q, np.diag([0.01]), 10 * Q, x_goal=np.array([0.0, math.pi, 0.0, 0.0]))
+    box = BoxConstraint(4, 1, control_lower=-10.0, control_upper=10.0,
+                        state_lower=[-1.5, -np.inf, -np.inf, -np.inf],
+                        state_upper=[1.5, np.inf, np.inf, np.inf])
+    rng = np.random.default_rng(0)
+    u0 = 0.1 * rng.standard_normal((T, 1))
+    x0 = np.zeros(4)
+    rows = []
+    for xp, up in [(x0, u0)] + ulp_nudges(x0, u0):
+        _, rep = admm_solve(ControlProblem(dyn, cost, box), rollout(dyn, xp, up),
+                            AdmmOptions(rho=1.0, max_outer=3))
+        rows.append([r.iterations for r in rep.newton_reports])
+    save("admm_cartpole_cfg2_nudge", iters=np.array(rows))
+
+
 FAST = [case_lqr_small, case_lqr_config1, case_passes_models, case_newton_lq,
         case_barrier_pendulum_cfg0, case_barrier_pendulum_conv, case_barrier_tvlinear, case_admm_small]
 
@@ -403,7 +426,7 @@ if __name__ == "__main__":
     ap.add_argument("--slow", action="store_true")
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
-    cases = FAST + ([case_admm_cartpole_cfg2] if args.slow else [])
+    cases = FAST + ([case_admm_cartpole_cfg2, case_admm_cartpole_cfg2_nudge] if args.slow else [])
     for fn in cases:
         if args.only and args.only not in fn.__name__:
             continue

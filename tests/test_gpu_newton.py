@@ -238,5 +238,12 @@ def test_admm_cartpole_config2_full_size():
           f"u gap {rel_gap(traj.controls, g['sol_us']):.3e}")
     assert rep.outer_iterations == len(ref_iters)
     assert rep.converged == bool(g["sol_converged"])
-    # the first outer steps (before LM-path chaos can act) match exactly
-    assert first_diff is None or first_diff >= 5
+    # Iteration counts must match wherever the REFERENCE reproduces its own
+    # counts under one-ulp input nudges (fixture admm_cartpole_cfg2_nudge:
+    # the reference gives 100, {35, 37, 34}, 17 for the first three outer
+    # steps -- outer step 0 ends in 100 non-converged LM iterations, so
+    # step 1's count is rounding noise in the reference itself).
+    nudge = golden("admm_cartpole_cfg2_nudge")["iters"]
+    for k in range(nudge.shape[1]):
+        if np.all(nudge[:, k] == nudge[0, k]):
+            assert got[k] == ref_iters[k] == nudge[0, k], k
