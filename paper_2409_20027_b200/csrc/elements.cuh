@@ -365,6 +365,142 @@ PTC_D bool gains(const Stage<R, NX, NU>& s, const VCarry<R, NX>& next, R (&Gam)[
   return ok;
 }
 
+// One stage element (earlier, from its expansion) combined with a general
+// aggregate r (later): vcombine(velem_from_stage(st), r) without forming
+// the stage's dual element or the NX x NX system I + C_l Y_r.  The stage's
+// C_l = Fu Rr^-1 Fu^T has rank NU, so by Woodbury
+//   (I + C_l Y_r)^-1 = I - Fu Q^-1 Fu^T Y_r,  Q = Rr + Fu^T Y_r Fu  (NU x NU),
+//   (I + C_l Y_r)^-1 C_l = Fu Q^-1 Fu^T,
+// and with v = eta_r - Y_r b_l, q = Q^-1 Fu^T v, W = Q^-1 Fu^T Y_r A_l:
+//   Y   = sym(A_l^T (Y_r A_l - Y_r Fu W) + Y_l),  eta = A_l^T (v - Y_r Fu q) + eta_l,
+//   A   = A_r (A_l - Fu W),   C = sym(A_r Fu Q^-1 (A_r Fu)^T + C_r),
+//   b   = A_r (b_l + Fu q) + b_r.
+// det(I + C_l Y_r) = det(Q) / det(Rr): a singular combine is a singular Q
+// (FLAG_COND); Rr failing its Cholesky raises FLAG_DEF_R as velem does.
+template <typename R, int NX, int NU>
+PTC_D int vcombine_stage(const Stage<R, NX, NU>& st, const VElem<R, NX>& r, VElem<R, NX>& o) {
+  int fl = 0;
+  R L[NU][NU];
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) L[i][j] = st.Rr[i][j];
+  if (!cholesky<NU>(L)) fl |= FLAG_DEF_R;
+  R RiMt[NU][NX], Rid[NU];
+#pragma unroll
+  for (int i = 0; i < NU; ++i) {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) RiMt[i][j] = st.M[j][i];
+    Rid[i] = st.d[i];
+  }
+  chol_solve<NU, NX>(L, RiMt);
+  chol_solve_vec<NU>(L, Rid);
+  R Al[NX][NX], tmp[NX][NX];
+  mm<NX, NU, NX>(st.Fu, RiMt, tmp);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Al[i][j] = st.Fx[i][j] - tmp[i][j];
+  R Yl[NX][NX];
+  mm<NX, NU, NX>(st.M, RiMt, tmp);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Yl[i][j] = st.P[i][j] - tmp[i][j];
+  symmetrize<NX>(Yl);
+  R etal[NX], bl[NX];
+  mv<NX, NU>(st.M, Rid, etal);
+  mv<NX, NU>(st.Fu, Rid, bl);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) bl[i] = -bl[i];
+  // Q = sym(Rr + Fu^T Y_r Fu), LU-factored (Q of a partial suffix may be
+  // indefinite; only a singular one is an error)
+  R YF[NX][NU];
+  mm<NX, NX, NU>(r.Y, st.Fu, YF);
+  R Q[NU][NU];
+  mtm<NU, NX, NU>(st.Fu, YF, Q);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) Q[i][j] += st.Rr[i][j];
+  symmetrize<NU>(Q);
+  int piv[NU];
+  if (!lu_factor<NU>(Q, piv)) fl |= FLAG_COND;
+  // W = Q^-1 Fu^T Y_r A_l  (Fu^T Y_r = YF^T, Y_r symmetric)
+  R W[NU][NX];
+  mtm<NU, NX, NX>(YF, Al, W);
+  lu_solve<NU, NX>(Q, piv, W);
+  // v, q = Q^-1 Fu^T v
+  R v[NX], Yb[NX];
+  mv<NX, NX>(r.Y, bl, Yb);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) v[i] = r.eta[i] - Yb[i];
+  R q[NU][1];
+  {
+    R Ftv[NU];
+    mtv<NU, NX>(st.Fu, v, Ftv);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) q[i][0] = Ftv[i];
+  }
+  lu_solve<NU, 1>(Q, piv, q);
+  // Y = sym(A_l^T (Y_r A_l - YF W) + Y_l)
+  R Z1[NX][NX];
+  mm<NX, NX, NX>(r.Y, Al, Z1);
+  mm<NX, NU, NX>(YF, W, tmp);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Z1[i][j] -= tmp[i][j];
+  mtm<NX, NX, NX>(Al, Z1, o.Y);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) o.Y[i][j] += Yl[i][j];
+  symmetrize<NX>(o.Y);
+  // eta = A_l^T (v - YF q) + eta_l ;  x = b_l + Fu q
+  R z[NX], x[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    R yq = R(0), fq = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      yq = fma(YF[i][k], q[k][0], yq);
+      fq = fma(st.Fu[i][k], q[k][0], fq);
+    }
+    z[i] = v[i] - yq;
+    x[i] = bl[i] + fq;
+  }
+  mtv<NX, NX>(Al, z, o.eta);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) o.eta[i] += etal[i];
+  // A = A_r (A_l - Fu W)
+  mm<NX, NU, NX>(st.Fu, W, tmp);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Al[i][j] -= tmp[i][j];
+  mm<NX, NX, NX>(r.A, Al, o.A);
+  // C = sym(AF Q^-1 AF^T + C_r),  AF = A_r Fu
+  R AF[NX][NU], Y2[NU][NX];
+  mm<NX, NX, NU>(r.A, st.Fu, AF);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) Y2[i][j] = AF[j][i];
+  lu_solve<NU, NX>(Q, piv, Y2);
+  mm<NX, NU, NX>(AF, Y2, o.C);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) o.C[i][j] += r.C[i][j];
+  symmetrize<NX>(o.C);
+  // b = A_r x + b_r
+  mv<NX, NX>(r.A, x, o.b);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) o.b[i] += r.b[i];
+  return fl;
+}
+
 // One stage element folded into a terminal-containing suffix, fused with the
 // gains of that stage: the composition  gains(st, c)  +  vstep(velem(st), c)
 // of the reference's value pass (passes.py:192-228 element, 264-288 combine,

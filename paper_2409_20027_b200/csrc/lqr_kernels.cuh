@@ -89,15 +89,15 @@ __global__ void __launch_bounds__(128) k_value_up0(LqrArgs<R> a) {
     okr &= velem_from_stage(st, acc, L);
     start = t1 - 2;
   }
+  int fl = 0;
   for (int t = start; t >= t0; --t) {
     ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t, T, B, b, alpha, st);
-    VElem<R, NX> e, o;
-    okr &= velem_from_stage(st, e, L);
-    okc &= vcombine(e, acc, o);
+    VElem<R, NX> o;
+    fl |= vcombine_stage(st, acc, o);
     acc = o;
   }
   st_velem(a.vagg[1], j, a.plan.n[1], B, b, acc);
-  int fl = (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND);
+  fl |= (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND);
   if (fl) atomicOr(a.flags + b, fl);
 }
 

@@ -22,23 +22,64 @@ PTC_D int warp_unit() { return blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
 
 // ------------------------------------------------------------ primitives
 
+// Register blocking of a warp product: each lane owns a BI x BJ block of the
+// output, so one k-step costs BI + BJ shared loads for BI*BJ FMAs.  The plan
+// minimises per-lane work ceil(blocks / 32) * (BI*BJ + 2 (BI + BJ)) over
+// divisors BI | M, BJ | N up to 6.
+struct MMPlan {
+  int bi, bj;
+};
+
+constexpr MMPlan mm_plan(int M, int N) {
+  MMPlan best{1, 1};
+  int best_cost = 1 << 30;
+  for (int bi = 1; bi <= 6; ++bi) {
+    if (M % bi) continue;
+    for (int bj = 1; bj <= 6; ++bj) {
+      if (N % bj) continue;
+      const int blocks = (M / bi) * (N / bj);
+      const int cost = ((blocks + 31) / 32) * (bi * bj + 2 * (bi + bj));
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = MMPlan{bi, bj};
+      }
+    }
+  }
+  return best;
+}
+
 // C (MxN) = op(A) op(B); A stored row-major as (TA ? KxM : MxK), B as
 // (TB ? NxK : KxN).  MODE 0: C = AB, 1: C += AB, -1: C -= AB.  C must not
 // alias A or B.
 template <int M, int K, int N, bool TA, bool TB, int MODE, typename R>
 PTC_D void w_mm(const R* A, const R* B, R* C) {
-  for (int e = lane_id(); e < M * N; e += 32) {
-    const int i = e / N, j = e - (e / N) * N;
-    R s = R(0);
+  constexpr MMPlan pl = mm_plan(M, N);
+  constexpr int BI = pl.bi, BJ = pl.bj, NBJ = N / BJ, NB = (M / BI) * NBJ;
+  for (int blk = lane_id(); blk < NB; blk += 32) {
+    const int i0 = (blk / NBJ) * BI, j0 = (blk - (blk / NBJ) * NBJ) * BJ;
+    R acc[BI][BJ];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const R av = TA ? A[k * M + i] : A[i * K + k];
-      const R bv = TB ? B[j * K + k] : B[k * N + j];
-      s = (k == 0) ? av * bv : fma(av, bv, s);
+      R av[BI], bv[BJ];
+#pragma unroll
+      for (int ii = 0; ii < BI; ++ii) av[ii] = TA ? A[k * M + i0 + ii] : A[(i0 + ii) * K + k];
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj) bv[jj] = TB ? B[(j0 + jj) * K + k] : B[k * N + j0 + jj];
+#pragma unroll
+      for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj)
+          acc[ii][jj] = (k == 0) ? av[ii] * bv[jj] : fma(av[ii], bv[jj], acc[ii][jj]);
     }
-    if (MODE == 0) C[e] = s;
-    else if (MODE > 0) C[e] += s;
-    else C[e] -= s;
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj) {
+        R& c = C[(i0 + ii) * N + j0 + jj];
+        if (MODE == 0) c = acc[ii][jj];
+        else if (MODE > 0) c += acc[ii][jj];
+        else c -= acc[ii][jj];
+      }
   }
   __syncwarp();
 }
@@ -179,31 +220,45 @@ PTC_D bool w_chol_regs(const R* Q, R (&L)[N][N]) {
 
 template <typename R, int NX, int NU>
 struct WSlab {
-  static constexpr int VC = 3 * NX * NX + 2 * NX;
-  static constexpr int SC = NX * NX + NU * NU + NX * NU + NU + NX * NX + NX * NU;
-  // offsets (in elements of R)
-  static constexpr int oL = 0, oRt = VC, oO = 2 * VC, oSt = 3 * VC;
-  static constexpr int oG = oSt + SC, oX = oG + NX * NX, oZ = oX + NX * (2 * NX + 1);
-  static constexpr int oT1 = oZ + NX * (NX + 1), oT2 = oT1 + NX * NX, oT3 = oT2 + NX * NX;
-  static constexpr int nR = oT3 + NX * NX;
-  static constexpr int bytes = nR * (int)sizeof(R) + 16 * (int)sizeof(int);
+  static constexpr int VC = 3 * NX * NX + 2 * NX;   // value element
+  static constexpr int CC = NX * NX + NX;           // carry / affine map
+  static constexpr int SC = NX * NX + NU * NU + NX * NU + NU + NX * NX + NX * NU;  // stage
   // stage sub-offsets
   static constexpr int sP = 0, sR = NX * NX, sM = sR + NU * NU, sd = sM + NX * NU,
                        sFx = sd + NU, sFu = sFx + NX * NX;
   // value element sub-offsets (global component order)
   static constexpr int eA = 0, eY = NX * NX, eC = 2 * NX * NX, eEta = 3 * NX * NX,
                        eB = 3 * NX * NX + NX;
+  // scratch needs of the element algebra
+  static constexpr int SCR_COMB = NX * NX + NX * (2 * NX + 1) + NX * (NX + 1) + NX * NX;
+  static constexpr int SCR_STEP = NX * NX + NX * (NX + 1);
+  static constexpr int SCR_RIC = 2 * NU * NX + NU * NU + NX * NX;
+  static constexpr int BASE = 5 * NU * NX + 2 * NU + 4 * NX + NU * NU;
+  static constexpr int SCR_STAGE = BASE + 2 * NX * NX;
+  static constexpr int SCR_VELEM = NU * (2 * NX + 1);
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  // per-kernel slab sizes (elements of R per warp; 16 pivot ints follow)
+  static constexpr int kUp0 = 2 * VC + SC + mx(SCR_STAGE, mx(SCR_VELEM, NX * NX));
+  static constexpr int kUp = 3 * VC + SCR_COMB;
+  static constexpr int kStep = 2 * CC + VC + SCR_STEP;
+  static constexpr int kDown0 = 5 * CC + SC + NU * NX + NU + SCR_RIC;
+  static constexpr int kProp = 3 * CC;
+  static constexpr int kPropUp0 = 3 * CC + NX * NX + NX * NU + NU * NX + NU;
+  static constexpr int kPropDown0 = 2 * NX + NU + NX * NX + NX * NU + NU * NX + 2 * NU;
+  static constexpr int bytes_of(int elems) { return elems * (int)sizeof(R) + 16 * (int)sizeof(int); }
 };
 
-template <typename R, int NX, int NU>
-PTC_D R* warp_slab() {
+// this warp's slab of `elems` elements (+16 pivot ints) in dynamic shared memory
+template <typename R>
+PTC_D R* warp_slab(int elems) {
   extern __shared__ __align__(16) unsigned char w_smem[];
-  return reinterpret_cast<R*>(w_smem + (threadIdx.x >> 5) * WSlab<R, NX, NU>::bytes);
+  const int stride = elems * (int)sizeof(R) + 16 * (int)sizeof(int);
+  return reinterpret_cast<R*>(w_smem + (threadIdx.x >> 5) * stride);
 }
 
-template <typename R, int NX, int NU>
-PTC_D int* warp_piv(R* slab) {
-  return reinterpret_cast<int*>(slab + WSlab<R, NX, NU>::nR);
+template <typename R>
+PTC_D int* warp_piv(R* slab, int elems) {
+  return reinterpret_cast<int*>(slab + elems);
 }
 
 // global <-> slab (component c of item t at f[(c * rows + t) * B + b])
@@ -229,6 +284,66 @@ PTC_D void w_ld_stage(const LqrArgs<R>& a, int t, int b, R alpha, R* st) {
   w_ld<NU>(a.d, t, T, B, b, st + S::sd);
   w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
   w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
+  for (int i = lane_id(); i < NU; i += 32) st[S::sR + i * NU + i] += alpha;
+  __syncwarp();
+}
+
+// Register prefetch of one stage's fields: lane l holds components
+// l, l+32, ... of the concatenation of up to 6 fields (each a SoA field of
+// NC_f components over `rows` items).  load(t) issues the global loads for
+// item t, store(dst) writes them to the slab in concatenated order -- so the
+// loads of stage t-1 are in flight while stage t is being combined.
+template <typename R, int N0, int N1 = 0, int N2 = 0, int N3 = 0, int N4 = 0, int N5 = 0>
+struct WPrefetch {
+  static constexpr int TOTAL = N0 + N1 + N2 + N3 + N4 + N5;
+  static constexpr int PER = (TOTAL + 31) / 32;
+  const R* p[PER];
+  R v[PER];
+  size_t step;
+  PTC_D void init(const R* f0, const R* f1, const R* f2, const R* f3, const R* f4, const R* f5,
+                  int rows, int B, int b) {
+    step = (size_t)B;
+    const int ln = lane_id();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      int c = ln + 32 * k;
+      const R* base = nullptr;
+      int comp = 0;
+      if (c < N0) { base = f0; comp = c; }
+      else if ((c -= N0) < N1) { base = f1; comp = c; }
+      else if ((c -= N1) < N2) { base = f2; comp = c; }
+      else if ((c -= N2) < N3) { base = f3; comp = c; }
+      else if ((c -= N3) < N4) { base = f4; comp = c; }
+      else if ((c -= N4) < N5) { base = f5; comp = c; }
+      p[k] = base ? base + (size_t)comp * rows * B + b : nullptr;
+    }
+  }
+  PTC_D void load(int t) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) v[k] = p[k] ? __ldg(p[k] + (size_t)t * step) : R(0);
+  }
+  PTC_D void store(R* dst) const {
+    const int ln = lane_id();
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (ln + 32 * k < TOTAL) dst[ln + 32 * k] = v[k];
+    __syncwarp();
+  }
+};
+
+template <typename R, int NX, int NU>
+using StagePrefetch = WPrefetch<R, NX * NX, NU * NU, NX * NU, NU, NX * NX, NX * NU>;
+
+template <typename R, int NX, int NU>
+PTC_D void w_stage_prefetch_init(StagePrefetch<R, NX, NU>& pf, const LqrArgs<R>& a, int b) {
+  pf.init(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, a.T, a.B, b);
+}
+
+// prefetched stage -> slab, with Rr = R + alpha I
+template <typename R, int NX, int NU>
+PTC_D void w_stage_store(const StagePrefetch<R, NX, NU>& pf, R alpha, R* st) {
+  using S = WSlab<R, NX, NU>;
+  pf.store(st);
   for (int i = lane_id(); i < NU; i += 32) st[S::sR + i * NU + i] += alpha;
   __syncwarp();
 }
@@ -298,13 +413,12 @@ PTC_D void w_velem_terminal(const R* PT, R* e) {
 
 // general combine o = l (x) r (vcombine); slab scratch G, X, Z, T1
 template <typename R, int NX, int NU>
-PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* slab) {
+PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* scr, int* piv) {
   using S = WSlab<R, NX, NU>;
-  R* G = slab + S::oG;
-  R* X = slab + S::oX;
-  R* Z = slab + S::oZ;
-  R* T1 = slab + S::oT1;
-  int* piv = warp_piv<R, NX, NU>(slab);
+  R* G = scr;
+  R* X = G + NX * NX;
+  R* Z = X + NX * (2 * NX + 1);
+  R* T1 = Z + NX * (NX + 1);
   constexpr int WX = 2 * NX + 1, WZ = NX + 1;
   // G = I + C_l Y_r ; G^T is what the Z solve needs, so factor G^T directly
   // Z = G^-T [Y_r A_l | eta_r - Y_r b_l]   X = G^-1 [A_l | C_l | b_l + C_l eta_r]
@@ -396,14 +510,130 @@ PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* slab) {
   return ok;
 }
 
+// stage (x) aggregate in Woodbury form (vcombine_stage of elements.cuh):
+// st is a loaded stage, r the aggregate, o the result (o != r).  Scratch:
+// the contiguous G | X | Z region and T1, T2.
+template <typename R, int NX, int NU>
+PTC_D int w_vcombine_stage(const R* st, const R* r, R* o, R* scr, int* piv) {
+  using S = WSlab<R, NX, NU>;
+  R* base = scr;
+  R* RiMt = base;                 // NU x NX
+  R* Rid = RiMt + NU * NX;        // NU
+  R* YF = Rid + NU;               // NX x NU
+  R* W = YF + NX * NU;            // NU x NX
+  R* v = W + NU * NX;             // NX
+  R* x = v + NX;                  // NX
+  R* z = x + NX;                  // NX
+  R* bl = z + NX;                 // NX
+  R* AF = bl + NX;                // NX x NU
+  R* Y2 = AF + NX * NU;           // NU x NX
+  R* q = Y2 + NU * NX;            // NU
+  R* Al = scr + S::BASE;          // NX x NX
+  R* Z1 = Al + NX * NX;           // NX x NX
+  const R* Fu = st + S::sFu;
+  const int ln = lane_id();
+  int fl = 0;
+  R L[NU][NU];
+  if (!w_chol_regs<NU>(st + S::sR, L)) fl |= FLAG_DEF_R;
+  if (ln <= NX) {  // columns of Rr^-1 [M^T | d]
+    R c[NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) c[i] = ln < NX ? st[S::sM + ln * NU + i] : st[S::sd + i];
+    chol_solve_vec<NU>(L, c);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      if (ln < NX) RiMt[i * NX + ln] = c[i];
+      else Rid[i] = c[i];
+    }
+  }
+  __syncwarp();
+  // A_l = Fx - Fu RiMt ;  Y_l = sym(P - M RiMt) (into o.Y) ;  YF = Y_r Fu
+  w_copy<NX * NX>(st + S::sFx, Al);
+  w_mm<NX, NU, NX, false, false, -1>(Fu, RiMt, Al);
+  w_copy<NX * NX>(st + S::sP, o + S::eY);
+  w_mm<NX, NU, NX, false, false, -1>(st + S::sM, RiMt, o + S::eY);
+  w_sym<NX>(o + S::eY);
+  w_mm<NX, NX, NU, false, false, 0>(r + S::eY, Fu, YF);
+  for (int i = ln; i < NX; i += 32) {  // eta_l (into o.eta), b_l
+    R me = R(0), fb = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      me = fma(st[S::sM + i * NU + k], Rid[k], me);
+      fb = fma(Fu[i * NU + k], Rid[k], fb);
+    }
+    o[S::eEta + i] = me;
+    bl[i] = -fb;
+  }
+  __syncwarp();
+  // Y_r A_l, and v = eta_r - Y_r b_l
+  w_mm<NX, NX, NX, false, false, 0>(r + S::eY, Al, Z1);
+  for (int i = ln; i < NX; i += 32) {
+    R yb = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) yb = fma(r[S::eY + i * NX + k], bl[k], yb);
+    v[i] = r[S::eEta + i] - yb;
+  }
+  __syncwarp();
+  // Q = sym(Rr + Fu^T YF) (NU x NU), warp LU in shared memory
+  R* Q = q + NU;                  // NU x NU
+  for (int e = ln; e < NU * NU; e += 32) {
+    const int i = e / NU, j = e - (e / NU) * NU;
+    R s1 = R(0), s2 = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) {
+      s1 = fma(Fu[k * NU + i], YF[k * NU + j], s1);
+      s2 = fma(Fu[k * NU + j], YF[k * NU + i], s2);
+    }
+    Q[e] = R(0.5) * ((s1 + st[S::sR + i * NU + j]) + (s2 + st[S::sR + j * NU + i]));
+  }
+  // W = YF^T A_l (NU x NX), q = Fu^T v, AF = A_r Fu; then Y2 = AF^T
+  w_mm<NU, NX, NX, true, false, 0>(YF, Al, W);
+  w_mv<NU, NX, true, 0>(Fu, v, q);
+  w_mm<NX, NX, NU, false, false, 0>(r + S::eA, Fu, AF);
+  for (int e = ln; e < NU * NX; e += 32) {
+    const int i = e / NX, j = e - (e / NX) * NX;
+    Y2[e] = AF[j * NU + i];
+  }
+  __syncwarp();
+  if (!w_lu<NU>(Q, piv)) fl |= FLAG_COND;
+  w_lu_solve<NU, NX>(Q, piv, W);
+  w_lu_solve<NU, 1>(Q, piv, q);
+  w_lu_solve<NU, NX>(Q, piv, Y2);
+  // Z1 = Y_r A_l - YF W ;  o.Y += A_l^T Z1 ; z = v - YF q ; x = b_l + Fu q
+  w_mm<NX, NU, NX, false, false, -1>(YF, W, Z1);
+  for (int i = ln; i < NX; i += 32) {
+    R yq = R(0), fq = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      yq = fma(YF[i * NU + k], q[k], yq);
+      fq = fma(Fu[i * NU + k], q[k], fq);
+    }
+    z[i] = v[i] - yq;
+    x[i] = bl[i] + fq;
+  }
+  __syncwarp();
+  w_mm<NX, NX, NX, true, false, 1>(Al, Z1, o + S::eY);
+  w_mv<NX, NX, true, 1>(Al, z, o + S::eEta);
+  // A = A_r (A_l - Fu W)   (A_l no longer needed as such)
+  w_mm<NX, NU, NX, false, false, -1>(Fu, W, Al);
+  w_mm<NX, NX, NX, false, false, 0>(r + S::eA, Al, o + S::eA);
+  // C = sym(AF Y2 + C_r) ;  b = A_r x + b_r
+  w_copy<NX * NX>(r + S::eC, o + S::eC);
+  w_mm<NX, NU, NX, false, false, 1>(AF, Y2, o + S::eC);
+  w_copy<NX>(r + S::eB, o + S::eB);
+  w_mv<NX, NX, false, 1>(r + S::eA, x, o + S::eB);
+  w_sym<NX>(o + S::eY);
+  w_sym<NX>(o + S::eC);
+  return fl;
+}
+
 // carry step o = e (x) c for a carry (Y, eta) (vstep); c and o are carries
 // stored as [Y (NX*NX) | eta (NX)]
 template <typename R, int NX, int NU>
-PTC_D bool w_vstep(const R* e, const R* c, R* o, R* slab) {
+PTC_D bool w_vstep(const R* e, const R* c, R* o, R* scr, int* piv) {
   using S = WSlab<R, NX, NU>;
-  R* G = slab + S::oG;
-  R* Z = slab + S::oZ;
-  int* piv = warp_piv<R, NX, NU>(slab);
+  R* G = scr;
+  R* Z = scr + NX * NX;
   constexpr int WZ = NX + 1;
   // G = I + Y_c C_e ; Z = [Y_c A_e | eta_c - Y_c b_e] ; Z <- G^-1 Z
   w_mm<NX, NX, NX, false, false, 0>(c, e + S::eC, G);
@@ -446,12 +676,12 @@ PTC_D bool w_vstep(const R* e, const R* c, R* o, R* slab) {
 // Riccati-form level-0 step (riccati_step): stage st, carry c -> gains
 // (written to Gam (NU*NX) and gam (NU) in the slab) and carry o.
 template <typename R, int NX, int NU>
-PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* slab) {
+PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
   using S = WSlab<R, NX, NU>;
-  R* FtS = slab + S::oX;                 // NU x NX
+  R* FtS = scr;                          // NU x NX
   R* Qux = FtS + NU * NX;                // NU x NX
   R* Qm = Qux + NU * NX;                 // NU x NU
-  R* SF = slab + S::oT1;                 // NX x NX
+  R* SF = Qm + NU * NU;                  // NX x NX
   int fl = 0;
   {
     R L[NU][NU];
@@ -549,63 +779,71 @@ PTC_D void w_closed_loop(const R* Fx, const R* Fu, const R* Gam, const R* gam, b
   __syncwarp();
 }
 
-#define PTC_WIDE_PROLOGUE(count)                     \
+// Every kernel below carves its own compact per-warp slab (WSlab::k*), so
+// the light kernels (carries, propagation) run at high occupancy and only the
+// combine-heavy ones pay for large slabs.
+#define PTC_WIDE_PROLOGUE(count, ...)                \
   const int u = warp_unit();                         \
   if (u >= (count) * a.B) return;                    \
   const int b = u % a.B, j = u / a.B;                \
   (void)j;                                           \
   if (lqr_skip(a, b)) return;                        \
   using S = WSlab<R, NX, NU>;                        \
-  R* slab = warp_slab<R, NX, NU>();                  \
-  (void)slab;
+  constexpr int kElems = (__VA_ARGS__);              \
+  R* slab = warp_slab<R>(kElems);                    \
+  int* piv = warp_piv<R>(slab, kElems);              \
+  (void)piv;
 
 // ------------------------------------------------------------ value scan
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_value_up0(LqrArgs<R> a) {
-  PTC_WIDE_PROLOGUE(a.plan.units0())
+  PTC_WIDE_PROLOGUE(a.plan.units0(), WSlab<R, NX, NU>::kUp0)
   const int P0 = a.plan.units0(), T = a.T;
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   const R alpha = R(a.alpha[b]);
-  R* acc = slab + S::oL;
-  R* e = slab + S::oRt;
-  R* o = slab + S::oO;
-  R* st = slab + S::oSt;
-  bool okr = true, okc = true;
+  R* acc = slab;
+  R* o = acc + S::VC;
+  R* st = o + S::VC;
+  R* scr = st + S::SC;
+  int fl = 0;
   int start;
   if (j == P0 - 1 && !a.no_terminal) {
-    w_ld<NX * NX>(a.PT, 0, 1, a.B, b, slab + S::oT2);
-    w_velem_terminal<R, NX, NU>(slab + S::oT2, acc);
+    w_ld<NX * NX>(a.PT, 0, 1, a.B, b, scr);
+    w_velem_terminal<R, NX, NU>(scr, acc);
     start = t1 - 1;
   } else {
     w_ld_stage<R, NX, NU>(a, t1 - 1, b, alpha, st);
-    okr &= w_velem<R, NX, NU>(st, acc, slab + S::oX);
+    if (!w_velem<R, NX, NU>(st, acc, scr)) fl |= FLAG_DEF_R;
     start = t1 - 2;
   }
+  StagePrefetch<R, NX, NU> pf;
+  w_stage_prefetch_init<R, NX, NU>(pf, a, b);
+  if (start >= t0) pf.load(start);
   for (int t = start; t >= t0; --t) {
-    w_ld_stage<R, NX, NU>(a, t, b, alpha, st);
-    okr &= w_velem<R, NX, NU>(st, e, slab + S::oX);
-    okc &= w_vcombine<R, NX, NU>(e, acc, o, slab);
+    w_stage_store<R, NX, NU>(pf, alpha, st);
+    if (t > t0) pf.load(t - 1);
+    fl |= w_vcombine_stage<R, NX, NU>(st, acc, o, scr, piv);
     w_copy<S::VC>(o, acc);
   }
   w_st<S::VC>(a.vagg[1], j, a.plan.n[1], a.B, b, acc);
-  const int fl = (okr ? 0 : FLAG_DEF_R) | (okc ? 0 : FLAG_COND);
   if (fl && lane_id() == 0) atomicOr(a.flags + b, fl);
 }
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_value_up(LqrArgs<R> a, int l) {
-  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1], WSlab<R, NX, NU>::kUp)
   const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
   const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
-  R* acc = slab + S::oL;
-  R* e = slab + S::oRt;
-  R* o = slab + S::oO;
+  R* acc = slab;
+  R* e = acc + S::VC;
+  R* o = e + S::VC;
+  R* scr = o + S::VC;
   w_ld<S::VC>(a.vagg[l], last, nl, a.B, b, acc);
   bool okc = true;
   for (int i = last - 1; i >= first; --i) {
     w_ld<S::VC>(a.vagg[l], i, nl, a.B, b, e);
-    okc &= w_vcombine<R, NX, NU>(e, acc, o, slab);
+    okc &= w_vcombine<R, NX, NU>(e, acc, o, scr, piv);
     w_copy<S::VC>(o, acc);
   }
   w_st<S::VC>(a.vagg[l + 1], j, nn, a.B, b, acc);
@@ -614,63 +852,63 @@ __global__ void __launch_bounds__(128) kw_value_up(LqrArgs<R> a, int l) {
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_value_top(LqrArgs<R> a) {
-  PTC_WIDE_PROLOGUE(1)
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(1, WSlab<R, NX, NU>::kStep)
   const int L = a.plan.L, nL = a.plan.n[L];
-  R* c = slab + S::oL;
-  R* e = slab + S::oRt;
-  R* o = slab + S::oO;
-  if (a.vcarry_in) w_ld<CC>(a.vcarry_in, 0, 1, a.B, b, c);
-  else w_fill<CC>(c, R(0));
+  R* c = slab;
+  R* o = c + S::CC;
+  R* e = o + S::CC;
+  R* scr = e + S::VC;
+  if (a.vcarry_in) w_ld<S::CC>(a.vcarry_in, 0, 1, a.B, b, c);
+  else w_fill<S::CC>(c, R(0));
   bool okc = true;
   for (int i = nL - 1; i >= 0; --i) {
-    w_st<CC>(a.vcar[L], i, nL, a.B, b, c);
+    w_st<S::CC>(a.vcar[L], i, nL, a.B, b, c);
     w_ld<S::VC>(a.vagg[L], i, nL, a.B, b, e);
-    okc &= w_vstep<R, NX, NU>(e, c, o, slab);
-    w_copy<CC>(o, c);
+    okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
+    w_copy<S::CC>(o, c);
   }
   if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
 }
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_value_down(LqrArgs<R> a, int l) {
-  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1], WSlab<R, NX, NU>::kStep)
   const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
   const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
-  R* c = slab + S::oL;
-  R* e = slab + S::oRt;
-  R* o = slab + S::oO;
-  w_ld<CC>(a.vcar[l + 1], j, nn, a.B, b, c);
+  R* c = slab;
+  R* o = c + S::CC;
+  R* e = o + S::CC;
+  R* scr = e + S::VC;
+  w_ld<S::CC>(a.vcar[l + 1], j, nn, a.B, b, c);
   bool okc = true;
   for (int i = last; i >= first; --i) {
-    w_st<CC>(a.vcar[l], i, nl, a.B, b, c);
+    w_st<S::CC>(a.vcar[l], i, nl, a.B, b, c);
     w_ld<S::VC>(a.vagg[l], i, nl, a.B, b, e);
-    okc &= w_vstep<R, NX, NU>(e, c, o, slab);
-    w_copy<CC>(o, c);
+    okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
+    w_copy<S::CC>(o, c);
   }
   if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
 }
 
 template <typename R, int NX, int NU, bool kAgg>
 __global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
-  PTC_WIDE_PROLOGUE(a.plan.units0())
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(a.plan.units0(), WSlab<R, NX, NU>::kDown0)
   const int P0 = a.plan.units0(), T = a.T, B = a.B;
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   const R alpha = R(a.alpha[b]);
   const bool tree = a.plan.L >= 1;
-  R* c = slab + S::oL;               // carry [Y | eta]
-  R* o = c + CC;                     // next carry
-  R* pa = slab + S::oRt;             // propagation aggregate [F | e]
-  R* m = pa + CC;                    // stage closed-loop map
-  R* pt = slab + S::oO;              // composition scratch
-  R* st = slab + S::oSt;
-  R* Gam = slab + S::oT2;            // NU x NX
-  R* gam = slab + S::oT3;            // NU
-  if (tree) w_ld<CC>(a.vcar[1], j, a.plan.n[1], B, b, c);
-  else if (a.vcarry_in) w_ld<CC>(a.vcarry_in, 0, 1, B, b, c);
-  else w_fill<CC>(c, R(0));
+  R* c = slab;                       // carry [Y | eta]
+  R* o = c + S::CC;                  // next carry
+  R* pa = o + S::CC;                 // propagation aggregate [F | e]
+  R* m = pa + S::CC;                 // stage closed-loop map
+  R* pt = m + S::CC;                 // composition scratch
+  R* st = pt + S::CC;
+  R* Gam = st + S::SC;               // NU x NX
+  R* gam = Gam + NU * NX;            // NU
+  R* scr = gam + NU;
+  if (tree) w_ld<S::CC>(a.vcar[1], j, a.plan.n[1], B, b, c);
+  else if (a.vcarry_in) w_ld<S::CC>(a.vcarry_in, 0, 1, B, b, c);
+  else w_fill<S::CC>(c, R(0));
   if (j == P0 - 1 && a.no_terminal && a.S) {
     w_st<NX * NX>(a.S, T, T + 1, B, b, c);
     for (int i = lane_id(); i < NX; i += 32) o[i] = -c[NX * NX + i];
@@ -690,17 +928,21 @@ __global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
     w_fill<NX>(pa + NX * NX, R(0));
   }
   int fl = 0;
+  StagePrefetch<R, NX, NU> pf;
+  w_stage_prefetch_init<R, NX, NU>(pf, a, b);
+  if (t1 - 1 >= t0) pf.load(t1 - 1);
   for (int t = t1 - 1; t >= t0; --t) {
-    w_ld_stage<R, NX, NU>(a, t, b, alpha, st);
-    fl |= w_riccati<R, NX, NU>(st, c, o, Gam, gam, slab);
+    w_stage_store<R, NX, NU>(pf, alpha, st);
+    if (t > t0) pf.load(t - 1);
+    fl |= w_riccati<R, NX, NU>(st, c, o, Gam, gam, scr);
     w_st<NU * NX>(a.Gam, t, T, B, b, Gam);
     w_st<NU>(a.gam, t, T, B, b, gam);
     if constexpr (kAgg) {
       w_closed_loop<R, NX, NU>(st + S::sFx, st + S::sFu, Gam, gam, t + a.t_base == 0, m);
       w_aff_compose<R, NX>(pa, m, pt);
-      w_copy<CC>(pt, pa);
+      w_copy<S::CC>(pt, pa);
     }
-    w_copy<CC>(o, c);
+    w_copy<S::CC>(o, c);
     if (a.S) {
       w_st<NX * NX>(a.S, t, T + 1, B, b, c);
       for (int i = lane_id(); i < NX; i += 32) o[i] = -c[NX * NX + i];
@@ -708,7 +950,7 @@ __global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
       w_st<NX>(a.s, t, T + 1, B, b, o);
     }
   }
-  if constexpr (kAgg) w_st<CC>(a.pagg[1], j, a.plan.n[1], B, b, pa);
+  if constexpr (kAgg) w_st<S::CC>(a.pagg[1], j, a.plan.n[1], B, b, pa);
   if (fl && lane_id() == 0) atomicOr(a.flags + b, fl);
 }
 
@@ -716,61 +958,60 @@ __global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_prop_up(LqrArgs<R> a, int l) {
-  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1], WSlab<R, NX, NU>::kProp)
   const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
   const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
-  R* acc = slab + S::oL;
-  R* m = slab + S::oRt;
-  R* o = slab + S::oO;
-  w_ld<CC>(a.pagg[l], first, nl, a.B, b, acc);
+  R* acc = slab;
+  R* m = acc + S::CC;
+  R* o = m + S::CC;
+  w_ld<S::CC>(a.pagg[l], first, nl, a.B, b, acc);
   for (int i = first + 1; i <= last; ++i) {
-    w_ld<CC>(a.pagg[l], i, nl, a.B, b, m);
+    w_ld<S::CC>(a.pagg[l], i, nl, a.B, b, m);
     w_aff_compose<R, NX>(m, acc, o);
-    w_copy<CC>(o, acc);
+    w_copy<S::CC>(o, acc);
   }
-  w_st<CC>(a.pagg[l + 1], j, nn, a.B, b, acc);
+  w_st<S::CC>(a.pagg[l + 1], j, nn, a.B, b, acc);
 }
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_prop_up0(LqrArgs<R> a) {
-  PTC_WIDE_PROLOGUE(a.plan.units0())
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(a.plan.units0(), WSlab<R, NX, NU>::kPropUp0)
   const int T = a.T, B = a.B;
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
-  R* acc = slab + S::oL;
-  R* m = slab + S::oRt;
-  R* o = slab + S::oO;
-  R* st = slab + S::oSt;
-  R* Gam = slab + S::oT2;
-  R* gam = slab + S::oT3;
+  R* acc = slab;
+  R* m = acc + S::CC;
+  R* o = m + S::CC;
+  R* Fx = o + S::CC;
+  R* Fu = Fx + NX * NX;
+  R* Gam = Fu + NX * NU;
+  R* gam = Gam + NU * NX;
   w_identity<NX>(acc);
   w_fill<NX>(acc + NX * NX, R(0));
+  WPrefetch<R, NX * NX, NX * NU, NU * NX, NU> pf;
+  pf.init(a.Fx, a.Fu, a.Gam, a.gam, nullptr, nullptr, T, B, b);
+  if (t0 < t1) pf.load(t0);
   for (int t = t0; t < t1; ++t) {
-    w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
-    w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
-    w_ld<NU * NX>(a.Gam, t, T, B, b, Gam);
-    w_ld<NU>(a.gam, t, T, B, b, gam);
-    w_closed_loop<R, NX, NU>(st + S::sFx, st + S::sFu, Gam, gam, t + a.t_base == 0, m);
+    pf.store(Fx);
+    if (t + 1 < t1) pf.load(t + 1);
+    w_closed_loop<R, NX, NU>(Fx, Fu, Gam, gam, t + a.t_base == 0, m);
     w_aff_compose<R, NX>(m, acc, o);
-    w_copy<CC>(o, acc);
+    w_copy<S::CC>(o, acc);
   }
-  w_st<CC>(a.pagg[1], j, a.plan.n[1], B, b, acc);
+  w_st<S::CC>(a.pagg[1], j, a.plan.n[1], B, b, acc);
 }
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_prop_top(LqrArgs<R> a) {
-  PTC_WIDE_PROLOGUE(1)
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(1, WSlab<R, NX, NU>::kProp)
   const int L = a.plan.L, nL = a.plan.n[L];
-  R* x = slab + S::oL;
-  R* m = slab + S::oRt;
-  R* y = slab + S::oO;
+  R* x = slab;
+  R* m = x + S::CC;
+  R* y = m + S::CC;
   if (a.x_in) w_ld<NX>(a.x_in, 0, 1, a.B, b, x);
   else w_fill<NX>(x, R(0));
   for (int i = 0; i < nL; ++i) {
     w_st<NX>(a.pcar[L], i, nL, a.B, b, x);
-    w_ld<CC>(a.pagg[L], i, nL, a.B, b, m);
+    w_ld<S::CC>(a.pagg[L], i, nL, a.B, b, m);
     w_mv<NX, NX, false, 0>(m, x, y);
     for (int k = lane_id(); k < NX; k += 32) x[k] = y[k] + m[NX * NX + k];
     __syncwarp();
@@ -779,17 +1020,16 @@ __global__ void __launch_bounds__(128) kw_prop_top(LqrArgs<R> a) {
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_prop_down(LqrArgs<R> a, int l) {
-  PTC_WIDE_PROLOGUE(a.plan.n[l + 1])
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(a.plan.n[l + 1], WSlab<R, NX, NU>::kProp)
   const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
   const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
-  R* x = slab + S::oL;
-  R* m = slab + S::oRt;
-  R* y = slab + S::oO;
+  R* x = slab;
+  R* m = x + S::CC;
+  R* y = m + S::CC;
   w_ld<NX>(a.pcar[l + 1], j, nn, a.B, b, x);
   for (int i = first; i <= last; ++i) {
     w_st<NX>(a.pcar[l], i, nl, a.B, b, x);
-    w_ld<CC>(a.pagg[l], i, nl, a.B, b, m);
+    w_ld<S::CC>(a.pagg[l], i, nl, a.B, b, m);
     w_mv<NX, NX, false, 0>(m, x, y);
     for (int k = lane_id(); k < NX; k += 32) x[k] = y[k] + m[NX * NX + k];
     __syncwarp();
@@ -798,29 +1038,29 @@ __global__ void __launch_bounds__(128) kw_prop_down(LqrArgs<R> a, int l) {
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_prop_down0(LqrArgs<R> a) {
-  PTC_WIDE_PROLOGUE(a.plan.units0())
+  PTC_WIDE_PROLOGUE(a.plan.units0(), WSlab<R, NX, NU>::kPropDown0)
   const int P0 = a.plan.units0(), T = a.T, B = a.B;
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
-  R* x = slab + S::oL;
-  R* y = slab + S::oO;
+  R* x = slab;
+  R* y = x + NX;
   R* du = y + NX;
-  R* st = slab + S::oSt;
-  R* Gam = slab + S::oT2;
-  R* gam = slab + S::oT3;
+  R* Fx = du + NU;                   // prefetched [Fx | Fu | Gamma | gamma | d]
+  R* Fu = Fx + NX * NX;
+  R* Gam = Fu + NX * NU;
+  R* gam = Gam + NU * NX;
   R* dd = gam + NU;
   if (a.plan.L >= 1) w_ld<NX>(a.pcar[1], j, a.plan.n[1], B, b, x);
   else if (a.x_in) w_ld<NX>(a.x_in, 0, 1, B, b, x);
   else w_fill<NX>(x, R(0));
   double s2 = 0.0, sd = 0.0, mx = 0.0;  // accumulated by lane 0
   const int ln = lane_id();
+  WPrefetch<R, NX * NX, NX * NU, NU * NX, NU, NU> pf;
+  pf.init(a.Fx, a.Fu, a.Gam, a.gam, a.d, nullptr, T, B, b);
+  if (t0 < t1) pf.load(t0);
   for (int t = t0; t < t1; ++t) {
     w_st<NX>(a.dX, t, T + 1, B, b, x);
-    w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
-    w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
-    w_ld<NU * NX>(a.Gam, t, T, B, b, Gam);
-    w_ld<NU>(a.gam, t, T, B, b, gam);
-    if (a.d) w_ld<NU>(a.d, t, T, B, b, dd);
-    else w_fill<NU>(dd, R(0));
+    pf.store(Fx);
+    if (t + 1 < t1) pf.load(t + 1);
     w_mv<NU, NX, false, 0>(Gam, x, du);
     for (int i = ln; i < NU; i += 32) du[i] += gam[i];
     __syncwarp();
@@ -842,14 +1082,14 @@ __global__ void __launch_bounds__(128) kw_prop_down0(LqrArgs<R> a) {
         R gx = R(0);
 #pragma unroll
         for (int q = 0; q < NX; ++q) gx = (q == 0) ? Gam[k * NX] * x[0] : fma(Gam[k * NX + q], x[q], gx);
-        fgx = (k == 0) ? st[S::sFu + i * NU] * gx : fma(st[S::sFu + i * NU + k], gx, fgx);
+        fgx = (k == 0) ? Fu[i * NU] * gx : fma(Fu[i * NU + k], gx, fgx);
       }
       R fx = R(0);
 #pragma unroll
-      for (int q = 0; q < NX; ++q) fx = (q == 0) ? st[S::sFx + i * NX] * x[0] : fma(st[S::sFx + i * NX + q], x[q], fx);
+      for (int q = 0; q < NX; ++q) fx = (q == 0) ? Fx[i * NX] * x[0] : fma(Fx[i * NX + q], x[q], fx);
       R e = R(0);
 #pragma unroll
-      for (int k = 0; k < NU; ++k) e = (k == 0) ? st[S::sFu + i * NU] * gam[0] : fma(st[S::sFu + i * NU + k], gam[k], e);
+      for (int k = 0; k < NU; ++k) e = (k == 0) ? Fu[i * NU] * gam[0] : fma(Fu[i * NU + k], gam[k], e);
       y[i] = (head ? R(0) : fx + fgx) + e;
     }
     __syncwarp();
@@ -867,16 +1107,17 @@ __global__ void __launch_bounds__(128) kw_prop_down0(LqrArgs<R> a) {
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_value_block(LqrArgs<R> a, R* out) {
-  PTC_WIDE_PROLOGUE(1)
+  PTC_WIDE_PROLOGUE(1, WSlab<R, NX, NU>::kUp)
   const int L = a.plan.L > 0 ? a.plan.L : 1, nL = a.plan.n[L];
-  R* acc = slab + S::oL;
-  R* e = slab + S::oRt;
-  R* o = slab + S::oO;
+  R* acc = slab;
+  R* e = acc + S::VC;
+  R* o = e + S::VC;
+  R* scr = o + S::VC;
   w_ld<S::VC>(a.vagg[L], nL - 1, nL, a.B, b, acc);
   bool okc = true;
   for (int i = nL - 2; i >= 0; --i) {
     w_ld<S::VC>(a.vagg[L], i, nL, a.B, b, e);
-    okc &= w_vcombine<R, NX, NU>(e, acc, o, slab);
+    okc &= w_vcombine<R, NX, NU>(e, acc, o, scr, piv);
     w_copy<S::VC>(o, acc);
   }
   w_st<S::VC>(out, 0, 1, a.B, b, acc);
@@ -886,49 +1127,47 @@ __global__ void __launch_bounds__(128) kw_value_block(LqrArgs<R> a, R* out) {
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_value_carry(LqrArgs<R> a, const R* blocks, int rank,
                                                       int world) {
-  PTC_WIDE_PROLOGUE(1)
-  constexpr int CC = NX * NX + NX;
-  R* c = slab + S::oL;
-  R* e = slab + S::oRt;
-  R* o = slab + S::oO;
-  w_fill<CC>(c, R(0));
+  PTC_WIDE_PROLOGUE(1, WSlab<R, NX, NU>::kStep)
+  R* c = slab;
+  R* o = c + S::CC;
+  R* e = o + S::CC;
+  R* scr = e + S::VC;
+  w_fill<S::CC>(c, R(0));
   bool okc = true;
   for (int r = world - 1; r > rank; --r) {
     w_ld<S::VC>(blocks + (size_t)r * S::VC * a.B, 0, 1, a.B, b, e);
-    okc &= w_vstep<R, NX, NU>(e, c, o, slab);
-    w_copy<CC>(o, c);
+    okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
+    w_copy<S::CC>(o, c);
   }
-  w_st<CC>(a.vcin_buf, 0, 1, a.B, b, c);
+  w_st<S::CC>(a.vcin_buf, 0, 1, a.B, b, c);
   if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
 }
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_prop_block(LqrArgs<R> a, R* out) {
-  PTC_WIDE_PROLOGUE(1)
-  constexpr int CC = NX * NX + NX;
+  PTC_WIDE_PROLOGUE(1, WSlab<R, NX, NU>::kProp)
   const int L = a.plan.L > 0 ? a.plan.L : 1, nL = a.plan.n[L];
-  R* acc = slab + S::oL;
-  R* m = slab + S::oRt;
-  R* o = slab + S::oO;
-  w_ld<CC>(a.pagg[L], 0, nL, a.B, b, acc);
+  R* acc = slab;
+  R* m = acc + S::CC;
+  R* o = m + S::CC;
+  w_ld<S::CC>(a.pagg[L], 0, nL, a.B, b, acc);
   for (int i = 1; i < nL; ++i) {
-    w_ld<CC>(a.pagg[L], i, nL, a.B, b, m);
+    w_ld<S::CC>(a.pagg[L], i, nL, a.B, b, m);
     w_aff_compose<R, NX>(m, acc, o);
-    w_copy<CC>(o, acc);
+    w_copy<S::CC>(o, acc);
   }
-  w_st<CC>(out, 0, 1, a.B, b, acc);
+  w_st<S::CC>(out, 0, 1, a.B, b, acc);
 }
 
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_prop_carry(LqrArgs<R> a, const R* blocks, int rank) {
-  PTC_WIDE_PROLOGUE(1)
-  constexpr int CC = NX * NX + NX;
-  R* x = slab + S::oL;
-  R* m = slab + S::oRt;
-  R* y = slab + S::oO;
+  PTC_WIDE_PROLOGUE(1, WSlab<R, NX, NU>::kProp)
+  R* x = slab;
+  R* m = x + S::CC;
+  R* y = m + S::CC;
   w_fill<NX>(x, R(0));
   for (int r = 0; r < rank; ++r) {
-    w_ld<CC>(blocks + (size_t)r * CC * a.B, 0, 1, a.B, b, m);
+    w_ld<S::CC>(blocks + (size_t)r * S::CC * a.B, 0, 1, a.B, b, m);
     w_mv<NX, NX, false, 0>(m, x, y);
     for (int k = lane_id(); k < NX; k += 32) x[k] = y[k] + m[NX * NX + k];
     __syncwarp();
@@ -942,113 +1181,124 @@ __global__ void __launch_bounds__(128) kw_prop_carry(LqrArgs<R> a, const R* bloc
 
 template <typename R, int NX, int NU>
 struct Wide {
-  static constexpr int kSmem = kWarpsPerBlock * WSlab<R, NX, NU>::bytes;
+  using S = WSlab<R, NX, NU>;
+  static constexpr int smem(int elems) { return kWarpsPerBlock * S::bytes_of(elems); }
   static dim3 grid(long long units) {
     return dim3((unsigned)((units + kWarpsPerBlock - 1) / kWarpsPerBlock));
   }
   template <class K>
-  static void allow(K kernel) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  static void allow(K kernel, int elems) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem(elems));
   }
   static void setup() {
     static bool done = false;
     if (done) return;
-    allow(kw_value_up0<R, NX, NU>);
-    allow(kw_value_up<R, NX, NU>);
-    allow(kw_value_top<R, NX, NU>);
-    allow(kw_value_down<R, NX, NU>);
-    allow(kw_value_down0<R, NX, NU, true>);
-    allow(kw_value_down0<R, NX, NU, false>);
-    allow(kw_prop_up<R, NX, NU>);
-    allow(kw_prop_up0<R, NX, NU>);
-    allow(kw_prop_top<R, NX, NU>);
-    allow(kw_prop_down<R, NX, NU>);
-    allow(kw_prop_down0<R, NX, NU>);
-    allow(kw_value_block<R, NX, NU>);
-    allow(kw_value_carry<R, NX, NU>);
-    allow(kw_prop_block<R, NX, NU>);
-    allow(kw_prop_carry<R, NX, NU>);
+    allow(kw_value_up0<R, NX, NU>, S::kUp0);
+    allow(kw_value_up<R, NX, NU>, S::kUp);
+    allow(kw_value_top<R, NX, NU>, S::kStep);
+    allow(kw_value_down<R, NX, NU>, S::kStep);
+    allow(kw_value_down0<R, NX, NU, true>, S::kDown0);
+    allow(kw_value_down0<R, NX, NU, false>, S::kDown0);
+    allow(kw_prop_up<R, NX, NU>, S::kProp);
+    allow(kw_prop_up0<R, NX, NU>, S::kPropUp0);
+    allow(kw_prop_top<R, NX, NU>, S::kProp);
+    allow(kw_prop_down<R, NX, NU>, S::kProp);
+    allow(kw_prop_down0<R, NX, NU>, S::kPropDown0);
+    allow(kw_value_block<R, NX, NU>, S::kUp);
+    allow(kw_value_carry<R, NX, NU>, S::kStep);
+    allow(kw_prop_block<R, NX, NU>, S::kProp);
+    allow(kw_prop_carry<R, NX, NU>, S::kProp);
     done = true;
   }
 };
 
+#define PTC_WL(kernel, units, elems) kernel<<<W::grid(units), 128, W::smem(elems), s>>>
+
 template <typename R, int NX, int NU>
 void launch_prop_tree_wide(const LqrArgs<R>& a, cudaStream_t s) {
   using W = Wide<R, NX, NU>;
+  using S = WSlab<R, NX, NU>;
   const Plan& pl = a.plan;
   const long long B = a.B;
-  for (int l = 1; l < pl.L; ++l) kw_prop_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
-  kw_prop_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
-  for (int l = pl.L - 1; l >= 1; --l)
-    kw_prop_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+  for (int l = 1; l < pl.L; ++l) PTC_WL((kw_prop_up<R, NX, NU>), pl.n[l + 1] * B, S::kProp)(a, l);
+  PTC_WL((kw_prop_top<R, NX, NU>), B, S::kProp)(a);
+  for (int l = pl.L - 1; l >= 1; --l) PTC_WL((kw_prop_down<R, NX, NU>), pl.n[l + 1] * B, S::kProp)(a, l);
+}
+
+template <typename R, int NX, int NU>
+void launch_value_tree_wide(const LqrArgs<R>& a, cudaStream_t s) {
+  using W = Wide<R, NX, NU>;
+  using S = WSlab<R, NX, NU>;
+  const Plan& pl = a.plan;
+  const long long B = a.B;
+  PTC_WL((kw_value_top<R, NX, NU>), B, S::kStep)(a);
+  for (int l = pl.L - 1; l >= 1; --l) PTC_WL((kw_value_down<R, NX, NU>), pl.n[l + 1] * B, S::kStep)(a, l);
 }
 
 template <typename R, int NX, int NU>
 void launch_lqr_wide(const LqrArgs<R>& a, cudaStream_t s) {
   using W = Wide<R, NX, NU>;
+  using S = WSlab<R, NX, NU>;
   W::setup();
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (pl.L >= 1) {
-    kw_value_up0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
-    for (int l = 1; l < pl.L; ++l) kw_value_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
-    kw_value_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
-    for (int l = pl.L - 1; l >= 1; --l)
-      kw_value_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
-    kw_value_down0<R, NX, NU, true><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    PTC_WL((kw_value_up0<R, NX, NU>), P0 * B, S::kUp0)(a);
+    for (int l = 1; l < pl.L; ++l) PTC_WL((kw_value_up<R, NX, NU>), pl.n[l + 1] * B, S::kUp)(a, l);
+    launch_value_tree_wide<R, NX, NU>(a, s);
+    PTC_WL((kw_value_down0<R, NX, NU, true>), P0 * B, S::kDown0)(a);
     launch_prop_tree_wide<R, NX, NU>(a, s);
   } else {
-    kw_value_down0<R, NX, NU, false><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    PTC_WL((kw_value_down0<R, NX, NU, false>), P0 * B, S::kDown0)(a);
   }
-  kw_prop_down0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+  PTC_WL((kw_prop_down0<R, NX, NU>), P0 * B, S::kPropDown0)(a);
 }
 
 template <typename R, int NX, int NU>
 void launch_prop_wide(const LqrArgs<R>& a, cudaStream_t s) {
   using W = Wide<R, NX, NU>;
+  using S = WSlab<R, NX, NU>;
   W::setup();
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (pl.L >= 1) {
-    kw_prop_up0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    PTC_WL((kw_prop_up0<R, NX, NU>), P0 * B, S::kPropUp0)(a);
     launch_prop_tree_wide<R, NX, NU>(a, s);
   }
-  kw_prop_down0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+  PTC_WL((kw_prop_down0<R, NX, NU>), P0 * B, S::kPropDown0)(a);
 }
 
 template <typename R, int NX, int NU>
 void launch_lqr_block_wide(const LqrArgs<R>& a0, int phase, const void* blocks, void* out,
                            int rank, int world, cudaStream_t s) {
   using W = Wide<R, NX, NU>;
+  using S = WSlab<R, NX, NU>;
   W::setup();
   LqrArgs<R> a = a0;
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (phase == 0) {
-    kw_value_up0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
-    for (int l = 1; l < pl.L; ++l) kw_value_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
-    kw_value_block<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<R*>(out));
+    PTC_WL((kw_value_up0<R, NX, NU>), P0 * B, S::kUp0)(a);
+    for (int l = 1; l < pl.L; ++l) PTC_WL((kw_value_up<R, NX, NU>), pl.n[l + 1] * B, S::kUp)(a, l);
+    PTC_WL((kw_value_block<R, NX, NU>), B, S::kUp)(a, static_cast<R*>(out));
   } else if (phase == 1) {
-    kw_value_carry<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<const R*>(blocks), rank, world);
+    PTC_WL((kw_value_carry<R, NX, NU>), B, S::kStep)(a, static_cast<const R*>(blocks), rank, world);
     a.vcarry_in = a.vcin_buf;
-    if (pl.L >= 1) {
-      kw_value_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
-      for (int l = pl.L - 1; l >= 1; --l)
-        kw_value_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
-    }
-    kw_value_down0<R, NX, NU, true><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
-    for (int l = 1; l < pl.L; ++l) kw_prop_up<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
-    kw_prop_block<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<R*>(out));
+    if (pl.L >= 1) launch_value_tree_wide<R, NX, NU>(a, s);
+    PTC_WL((kw_value_down0<R, NX, NU, true>), P0 * B, S::kDown0)(a);
+    for (int l = 1; l < pl.L; ++l) PTC_WL((kw_prop_up<R, NX, NU>), pl.n[l + 1] * B, S::kProp)(a, l);
+    PTC_WL((kw_prop_block<R, NX, NU>), B, S::kProp)(a, static_cast<R*>(out));
   } else {
-    kw_prop_carry<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a, static_cast<const R*>(blocks), rank);
+    PTC_WL((kw_prop_carry<R, NX, NU>), B, S::kProp)(a, static_cast<const R*>(blocks), rank);
     a.x_in = a.xin_buf;
     if (pl.L >= 1) {
-      kw_prop_top<R, NX, NU><<<W::grid(B), 128, W::kSmem, s>>>(a);
-      for (int l = pl.L - 1; l >= 1; --l)
-        kw_prop_down<R, NX, NU><<<W::grid(pl.n[l + 1] * B), 128, W::kSmem, s>>>(a, l);
+      PTC_WL((kw_prop_top<R, NX, NU>), B, S::kProp)(a);
+      for (int l = pl.L - 1; l >= 1; --l) PTC_WL((kw_prop_down<R, NX, NU>), pl.n[l + 1] * B, S::kProp)(a, l);
     }
-    kw_prop_down0<R, NX, NU><<<W::grid(P0 * B), 128, W::kSmem, s>>>(a);
+    PTC_WL((kw_prop_down0<R, NX, NU>), P0 * B, S::kPropDown0)(a);
   }
 }
+
+#undef PTC_WL
 
 }  // namespace ptc
