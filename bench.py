@@ -455,6 +455,9 @@ def run_ours(args) -> None:
         sweep = lqr_latency_sweep(torch, LqrSolver)
     if rank == 0 and not args.no_newton_sweep:
         nsweep = newton_latency_sweep(torch, P)
+    mpc = None
+    if not args.no_mpc:
+        mpc = mpc_leg(torch, P, world, rank)
     longh = None
     if not args.no_long:
         del halves
@@ -483,7 +486,7 @@ def run_ours(args) -> None:
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk, "ill_posed_subproblems": ill_posed,
             "lqr_latency_sweep": sweep, "newton_latency_sweep": nsweep,
-            "long_horizon": longh,
+            "long_horizon": longh, "mpc_config3": mpc,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -561,6 +564,54 @@ def newton_latency_sweep(torch, P):
     return {"pendulum_ms_per_iteration": out}
 
 
+def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
+    """Config 3 end to end: the 65,536 problems (sharded by rank) solved by
+    the device-resident barrier method (mu 1e-1 -> 1e-6, zeta 0.2, Newton
+    max_iters 50 per round), then one receding-horizon MPC step: start from
+    x_10 of the solution, controls shifted by 10 (last repeated), re-rolled
+    and re-solved warm.  Reported: wall time of the cold and the warm solve
+    of the whole local batch (device-resident loop, host polls every 4
+    iterations), Newton iterations, and how many problems finished."""
+    from paper_2409_20027_b200 import BatchSolver
+    b_local = B_TOTAL // world
+    bp, bc = half_sizes(b_local)
+    probs = models_pkg(P)
+    out = {"problems": 0, "cold_ms": 0.0, "warm_ms": 0.0, "newton_iterations_warm": 0,
+           "finished_warm": 0, "infeasible_warm": 0}
+    opts = P.BarrierOptions(mu0=0.1, zeta=0.2, mu_tol=1e-6, newton=P.NewtonOptions(max_iters=50))
+    for system, n in (("pendulum", bp), ("cartpole", bc)):
+        rng = rng_for(rank, system)
+        x0 = initial_states(system, n, rng)
+        bound = 5.0 if system == "pendulum" else 10.0
+        u0 = np.clip(0.1 * bound * rng.standard_normal((n, T, 1)), -0.9 * bound, 0.9 * bound)
+        bs = BatchSolver(probs[system], n, "barrier", barrier=opts)
+        xs = bs.rollout(x0, torch.as_tensor(u0))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        res = bs.solve(xs, torch.as_tensor(u0).cuda())
+        ev[1].record()
+        x_next = res.states[:, shift].contiguous()
+        u_next = bs.shift_controls(res.controls, shift)
+        xs2 = bs.rollout(x_next, u_next)
+        torch.cuda.synchronize()
+        ev[2].record()
+        res2 = bs.solve(xs2, u_next)
+        ev[3].record()
+        torch.cuda.synchronize()
+        st = res2.status
+        out["problems"] += n
+        out["cold_ms"] += ev[0].elapsed_time(ev[1])
+        out["warm_ms"] += ev[2].elapsed_time(ev[3])
+        out["newton_iterations_warm"] += int(res2.inner_iterations.sum())
+        out["finished_warm"] += int((st == 1).sum())
+        out["infeasible_warm"] += int((st == -2).sum())
+        del bs, res, res2
+    out["mpc_steps_per_s_warm"] = out["problems"] / (out["warm_ms"] * 1e-3)
+    out["config"] = ("config 3 barrier MPC: pendulum (cfg-0 model/cost, |u|<=5) + cart-pole "
+                     "(cfg-2 model/cost, |x|<=1.5, |u|<=10), T=256, fp64, warm start shift %d" % shift)
+    return out
+
+
 def long_horizon_leg(torch, world: int, rank: int, steps: int = 5):
     """Config 4: one T = 2^20 LQR-scan solve, nx=12, nu=4, fp64, horizon split
     into `world` contiguous time blocks (one per rank) with an NCCL
@@ -632,6 +683,7 @@ def main() -> None:
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-newton-sweep", action="store_true")
     ap.add_argument("--no-long", action="store_true")
+    ap.add_argument("--no-mpc", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

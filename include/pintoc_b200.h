@@ -193,6 +193,9 @@ typedef struct ptc_problem_desc {
   int32_t round_cap;           /* per-problem outer rounds recorded */
   int32_t keep_round_controls; /* barrier: store each round's controls */
   int32_t chunk0, chunk;       /* scan plan, 0 = automatic */
+  int32_t rollout;             /* candidate rollout: 0 auto (log-depth Newton sweeps for
+                                  tree plans with horizon >= 2048), 1 sequential,
+                                  2 log-depth (tree plans) */
 } ptc_problem_desc;
 
 int64_t ptc_solver_workspace_bytes(const ptc_problem_desc* desc);

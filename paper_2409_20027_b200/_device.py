@@ -37,6 +37,7 @@ class SolveSettings:
     keep_round_controls: bool = False
     chunk0: int = 0
     chunk: int = 0
+    rollout: int = 0          # 0 auto, 1 sequential, 2 log-depth Newton sweeps
 
 
 def _dtype_code(torch, dtype) -> int:
@@ -105,6 +106,7 @@ class DeviceSolver:
         d.hist_cap, d.round_cap = s.hist_cap, max(1, s.round_cap)
         d.keep_round_controls = int(s.keep_round_controls)
         d.chunk0, d.chunk = s.chunk0, s.chunk
+        d.rollout = s.rollout
         self.desc = d
         nbytes = self.lib.ptc_solver_workspace_bytes(C.byref(d))
         if nbytes < 0:

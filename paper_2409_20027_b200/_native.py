@@ -50,6 +50,7 @@ class ProblemDesc(C.Structure):
         ("hist_cap", C.c_int32), ("round_cap", C.c_int32),
         ("keep_round_controls", C.c_int32),
         ("chunk0", C.c_int32), ("chunk", C.c_int32),
+        ("rollout", C.c_int32),
     ]
 
 

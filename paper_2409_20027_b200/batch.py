@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _native as N
 from ._device import DeviceSolver, SolveSettings
-from .newton import NewtonOptions, plan_chunks
+from .newton import NewtonOptions, plan_chunks, rollout_mode
 from .outer import AdmmOptions, BarrierOptions
 from .problem import ControlProblem
 
@@ -62,7 +62,7 @@ class BatchSolver:
             max_iters=newton.max_iters, mu0=barrier.mu0, zeta=barrier.zeta,
             mu_tol=barrier.mu_tol, rho=admm.rho, residual_tol=admm.residual_tol,
             max_outer=admm.max_outer, hist_cap=hist_cap, round_cap=max(1, rounds),
-            chunk0=c0, chunk=c1)
+            chunk0=c0, chunk=c1, rollout=rollout_mode(newton.executor))
         self.problem = problem
         self.solver = DeviceSolver(problem.dynamics, problem.cost, problem.constraints, batch,
                                    self.settings, dtype=dtype)

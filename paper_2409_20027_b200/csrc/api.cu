@@ -497,6 +497,13 @@ struct Solver final : ptc_solver {
     a.term = ib(); a.round = ib(); a.hist_len = ib(); a.bad_index = ib();
     a.n_running = c.template take<int>(1);
     int* bad_t = ib();
+    a.rstate = ib();
+    a.rres = c.template take<double>(P0 * B);
+    // candidate rollout: log-depth Newton sweeps for tree plans with long
+    // horizons (rollout 0 = auto), the sequential recurrence otherwise
+    const bool par = a.plan.L >= 1 && (d.rollout == 2 || (d.rollout == 0 && T >= 2048));
+    a.pr_iters = par ? 8 : 0;
+    a.xr = par ? c.template take<R>(a.xsz) : nullptr;
     a.alpha = db(); a.nu = db(); a.cur_cost = db(); a.cand_cost = db(); a.mu = db();
     a.opt.hist_cap = std::max(0, d.hist_cap);
     a.opt.round_cap = std::max(1, d.round_cap);

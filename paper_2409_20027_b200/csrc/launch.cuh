@@ -145,7 +145,27 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
   launch_costate<R, Dyn>(a, s);
   lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&la, s);
-  k_rollout<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
+  k_roll_gate<R><<<grid_for(B), kBlock, 0, s>>>(a);
+  if (a.pr_iters > 0 && a.plan.L >= 1) {
+    // log-depth Newton rollout, sequential fallback for what did not converge
+    const Plan& pl = a.plan;
+    const long long nT = (long long)(a.T + 1) * B;
+    k_pr_init<R, NX, NU><<<grid_for(nT), kBlock, 0, s>>>(a, la.dX, la.dU);
+    for (int k = 0; k <= a.pr_iters; ++k) {
+      k_pr_up0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, k);
+      k_pr_check<R><<<grid_for(B), kBlock, 0, s>>>(a, k);
+      if (k == a.pr_iters) break;
+      for (int l = 1; l < pl.L; ++l) k_pr_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+      k_pr_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, k);
+      for (int l = pl.L - 1; l >= 1; --l)
+        k_pr_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
+      k_pr_down0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, k);
+    }
+    k_pr_finish<R, NX><<<grid_for(nT), kBlock, 0, s>>>(a);
+    k_rollout<R, Dyn, true><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
+  } else {
+    k_rollout<R, Dyn, false><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
+  }
   k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
   k_control<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
   k_round_end<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);

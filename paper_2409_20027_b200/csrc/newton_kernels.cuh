@@ -56,6 +56,11 @@ struct NewtonArgs {
   double* cpart[2];        // (3, P0, B): sum l, sum c, first infeasible index
   double* apart;           // (2, P0, B): ADMM primal / dual residual maxima
   double* red;             // (3, P0, B) from the propagation sweep
+  // candidate rollout (see k_roll_gate / the parallel rollout below)
+  int* rstate;             // [B] bit 0 skip, bit 1 converged, bit 2 result in xr
+  double* rres;            // (P0, B) residual maxima of the rollout guess
+  R* xr;                   // second state buffer of the parallel rollout (xsz)
+  int pr_iters;            // Newton sweeps of the parallel rollout (0 = sequential)
 };
 
 template <typename R>
@@ -379,38 +384,318 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
 
 // --------------------------------------------------------------- rollout
 
-// candidate u + du rolled through the nonlinear dynamics (problem.py:449-473)
-// -- inherently sequential in time, parallel over the batch
-template <typename R, class Dyn>
-__global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
-  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+enum : int { RS_SKIP = 1, RS_CONV = 2, RS_IN_XR = 4 };
+
+// Which problems need the candidate rollout this iteration: k_control never
+// looks at the candidate of a problem that is not running, whose subproblem
+// failed (R/Q definiteness, singular combine) or whose step is below
+// inner_tol (newton.py:166-181), so those skip it.
+template <typename R>
+__global__ void k_roll_gate(NewtonArgs<R> a) {
   const int b = unit_id();
   if (b >= a.B) return;
-  if (!running(a, b)) return;
+  int st = 0;
+  if (!running(a, b) || (a.flags[b] & (FLAG_DEF_R | FLAG_DEF_Q | FLAG_COND))) {
+    st = RS_SKIP;
+  } else {
+    const int P0 = a.plan.units0();
+    double step = 0.0;
+    for (int j = 0; j < P0; ++j) step = nanmax(step, a.red[((size_t)2 * P0 + j) * a.B + b]);
+    if (step <= a.opt.inner_tol) st = RS_SKIP;
+  }
+  a.rstate[b] = st;
+}
+
+// candidate u + du rolled through the nonlinear dynamics (problem.py:449-473)
+// -- sequential in time, parallel over the batch; controls are prefetched
+// kRing steps ahead so the recurrence runs at the dynamics' latency, not
+// the memory's.  With kFromUc the candidate controls are already in place.
+template <typename R, class Dyn, bool kFromUc>
+__global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  constexpr int kRing = 8;
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (a.rstate[b] & (RS_SKIP | RS_CONV)) return;
   const int q = a.parity[b], c = 1 - q;
   const int T = a.T, B = a.B;
-  const ProblemParams& p = *a.pp;
+  // the model constants in registers: loop-invariant divisions hoist out of
+  // the recurrence (the parameters live in global memory, which the stores
+  // below could alias as far as the compiler knows)
+  ProblemParams p;
+  const ProblemParams& gp = *a.pp;
+  p.dyn_kind = gp.dyn_kind;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p.dyn[i] = gp.dyn[i];
+  p.lin_T = gp.lin_T;
+  p.lin_B = gp.lin_B;
+  p.lin_A = gp.lin_A;
+  p.lin_Bm = gp.lin_Bm;
+  p.lin_c = gp.lin_c;
+  R* Xc = a.X + c * a.xsz;
+  R* Uc = a.U + c * a.usz;
   R x[NX];
   ld_x(a, q, 0, b, x);
-  st_vec(a.X + c * a.xsz, 0, T + 1, B, b, x);
+  st_vec(Xc, 0, T + 1, B, b, x);
   bool finite = true;
-  for (int t = 0; t < T; ++t) {
-    R u[NU], du[NU];
-    ld_u(a, q, t, b, u);
-    ld_vec(dU, t, T, B, b, du);
+  R ring[kRing][NU];
+  auto fetch = [&](int t, R (&u)[NU]) {
+    if (t < T) {
+      if (kFromUc) {
+        ld_vec(Uc, t, T, B, b, u);
+      } else {
+        R du[NU];
+        ld_u(a, q, t, b, u);
+        ld_vec(dU, t, T, B, b, du);
 #pragma unroll
-    for (int i = 0; i < NU; ++i) u[i] += du[i];
-    st_vec(a.U + c * a.usz, t, T, B, b, u);
-    R xn[NX];
-    Dyn::step(p, t, b, x, u, xn);
-#pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      finite = finite && isfinite(xn[i]);
-      x[i] = xn[i];
+        for (int i = 0; i < NU; ++i) u[i] += du[i];
+      }
     }
-    st_vec(a.X + c * a.xsz, t + 1, T + 1, B, b, x);
+  };
+#pragma unroll
+  for (int k = 0; k < kRing; ++k) fetch(k, ring[k]);
+  for (int t0 = 0; t0 < T; t0 += kRing) {
+#pragma unroll
+    for (int k = 0; k < kRing; ++k) {
+      const int t = t0 + k;
+      if (t < T) {
+        R u[NU];
+#pragma unroll
+        for (int i = 0; i < NU; ++i) u[i] = ring[k][i];
+        fetch(t + kRing, ring[k]);
+        if (!kFromUc) st_vec(Uc, t, T, B, b, u);
+        R xn[NX];
+        Dyn::step(p, t, b, x, u, xn);
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+          finite = finite && isfinite(xn[i]);
+          x[i] = xn[i];
+        }
+        st_vec(Xc, t + 1, T + 1, B, b, x);
+      }
+    }
   }
   if (!finite) atomicOr(a.flags + b, FLAG_DIVERGED);
+}
+
+// ------------------------------------------------ parallel (log-depth) rollout
+//
+// For small batches with long horizons the rollout is solved as a nonlinear
+// system  x_{t+1} = f_t(x_t, u_t)  by Newton's method on the whole
+// trajectory: linearised at a guess x^k, the recurrence becomes the affine
+// scan  x_{t+1} = f(x^k_t) + Fx(x^k_t) (x_t - x^k_t),  solved with the same
+// blocked tree as the other scans.  The first guess x + dx is the LQR
+// propagation pass's prediction (itself the first Newton iterate from the
+// dynamically consistent current trajectory), so convergence is quadratic
+// from the start; a problem stops as soon as every step of its guess
+// satisfies the recurrence to a few ulps.  A problem that has not converged
+// after pr_iters sweeps (or meets a non-finite state) is rolled out by the
+// sequential kernel, so the result and the divergence report never depend
+// on the parallel path's convergence.
+
+template <typename R>
+PTC_D R* pr_buf(const NewtonArgs<R>& a, int b, int which) {
+  // which 0: the candidate buffer (1 - parity), 1: xr
+  return which == 0 ? a.X + (1 - a.parity[b]) * a.xsz : a.xr;
+}
+
+template <typename R, int NX, int NU>
+__global__ void k_pr_init(NewtonArgs<R> a, const R* dX, const R* dU) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)(a.T + 1) * a.B) return;
+  const int b = (int)(i % a.B), t = (int)(i / a.B);
+  if (a.rstate[b] & RS_SKIP) return;
+  const int q = a.parity[b];
+  R x[NX], d[NX];
+  ld_x(a, q, t, b, x);
+  ld_vec(dX, t, a.T + 1, a.B, b, d);
+#pragma unroll
+  for (int k = 0; k < NX; ++k) x[k] += d[k];
+  st_vec(pr_buf(a, b, 0), t, a.T + 1, a.B, b, x);
+  if (t < a.T) {
+    R u[NU], du[NU];
+    ld_u(a, q, t, b, u);
+    ld_vec(dU, t, a.T, a.B, b, du);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) u[k] += du[k];
+    st_vec(a.U + (1 - q) * a.usz, t, a.T, a.B, b, u);
+  }
+}
+
+// level-0: affine elements of the linearised recurrence folded over a chunk,
+// and the residual of the current guess
+template <typename R, class Dyn>
+__global__ void __launch_bounds__(128) k_pr_up0(NewtonArgs<R> a, int k) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int P0 = a.plan.units0();
+  const int u0 = unit_id();
+  if (u0 >= P0 * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (a.rstate[b] & (RS_SKIP | RS_CONV)) return;
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const ProblemParams& p = *a.pp;
+  const R* g = pr_buf(a, b, k & 1);
+  const R* Uc = a.U + (1 - a.parity[b]) * a.usz;
+  Aff<R, NX> acc;
+  aff_identity(acc);
+  double res = 0.0;
+  R lam0[NX];
+  set_zero(lam0);
+  for (int t = t0; t < t1; ++t) {
+    R x[NX], u[NU], xn[NX], fn[NX];
+    ld_vec(g, t, T + 1, B, b, x);
+    ld_vec(Uc, t, T, B, b, u);
+    ld_vec(g, t + 1, T + 1, B, b, xn);
+    Dyn::step(p, t, b, x, u, fn);
+    DynDerivs<R, NX, NU> D;
+    Dyn::template derivs<false>(p, t, b, x, u, lam0, D);
+    double mag = 1.0, gap = 0.0;
+    Aff<R, NX> m, o;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      gap = nanmax(gap, double(fabs(xn[i] - fn[i])));
+      mag = nanmax(mag, double(fabs(fn[i])));
+      R fxx = R(0);
+#pragma unroll
+      for (int c = 0; c < NX; ++c) {
+        m.F[i][c] = D.fx[i][c];
+        fxx = fma(D.fx[i][c], x[c], fxx);
+      }
+      m.e[i] = fn[i] - fxx;
+    }
+    res = nanmax(res, gap / mag);
+    if (!(gap == gap) || !(mag == mag)) res = INFINITY;
+    aff_compose(m, acc, o);
+    acc = o;
+  }
+  if (a.plan.L >= 1) st_aff(a.cagg[1], j, a.plan.n[1], B, b, acc);
+  a.rres[(size_t)j * B + b] = res;
+}
+
+template <typename R>
+__global__ void k_pr_check(NewtonArgs<R> a, int k) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  int st = a.rstate[b];
+  if (st & (RS_SKIP | RS_CONV)) return;
+  const int P0 = a.plan.units0();
+  double r = 0.0;
+  for (int j = 0; j < P0; ++j) r = nanmax(r, a.rres[(size_t)j * a.B + b]);
+  const double tol = 16.0 * (sizeof(R) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07);
+  if (r <= tol) a.rstate[b] = st | RS_CONV | ((k & 1) ? RS_IN_XR : 0);
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_pr_up(NewtonArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int u0 = unit_id();
+  if (u0 >= nn * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (a.rstate[b] & (RS_SKIP | RS_CONV)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  Aff<R, NX> acc;
+  ld_aff(a.cagg[l], first, nl, a.B, b, acc);
+  for (int i = first + 1; i <= last; ++i) {
+    Aff<R, NX> m, o;
+    ld_aff(a.cagg[l], i, nl, a.B, b, m);
+    aff_compose(m, acc, o);
+    acc = o;
+  }
+  st_aff(a.cagg[l + 1], j, nn, a.B, b, acc);
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_pr_top(NewtonArgs<R> a, int k) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (a.rstate[b] & (RS_SKIP | RS_CONV)) return;
+  const int L = a.plan.L, nL = a.plan.n[L];
+  R x[NX];
+  ld_vec(pr_buf(a, b, k & 1), 0, a.T + 1, a.B, b, x);  // x_0, identical in both buffers
+  for (int i = 0; i < nL; ++i) {
+    st_vec(a.ccar[L], i, nL, a.B, b, x);
+    Aff<R, NX> m;
+    ld_aff(a.cagg[L], i, nL, a.B, b, m);
+    R y[NX];
+    aff_apply(m, x, y);
+#pragma unroll
+    for (int c = 0; c < NX; ++c) x[c] = y[c];
+  }
+}
+
+template <typename R, int NX>
+__global__ void __launch_bounds__(128) k_pr_down(NewtonArgs<R> a, int l) {
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int u0 = unit_id();
+  if (u0 >= nn * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (a.rstate[b] & (RS_SKIP | RS_CONV)) return;
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  R x[NX];
+  ld_vec(a.ccar[l + 1], j, nn, a.B, b, x);
+  for (int i = first; i <= last; ++i) {
+    st_vec(a.ccar[l], i, nl, a.B, b, x);
+    Aff<R, NX> m;
+    ld_aff(a.cagg[l], i, nl, a.B, b, m);
+    R y[NX];
+    aff_apply(m, x, y);
+#pragma unroll
+    for (int c = 0; c < NX; ++c) x[c] = y[c];
+  }
+}
+
+// level-0 forward sweep: the next guess x^{k+1} from the chunk's carry
+template <typename R, class Dyn>
+__global__ void __launch_bounds__(128) k_pr_down0(NewtonArgs<R> a, int k) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int P0 = a.plan.units0();
+  const int u0 = unit_id();
+  if (u0 >= P0 * a.B) return;
+  const int b = u0 % a.B, j = u0 / a.B;
+  if (a.rstate[b] & (RS_SKIP | RS_CONV)) return;
+  const int T = a.T, B = a.B;
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const ProblemParams& p = *a.pp;
+  const R* g = pr_buf(a, b, k & 1);
+  R* n = pr_buf(a, b, (k + 1) & 1);
+  const R* Uc = a.U + (1 - a.parity[b]) * a.usz;
+  R x[NX];
+  if (j == 0) {
+    ld_vec(g, 0, T + 1, B, b, x);
+    st_vec(n, 0, T + 1, B, b, x);
+  } else {
+    ld_vec(a.ccar[1], j, a.plan.n[1], B, b, x);
+  }
+  R lam0[NX];
+  set_zero(lam0);
+  for (int t = t0; t < t1; ++t) {
+    R xg[NX], u[NU], fn[NX];
+    ld_vec(g, t, T + 1, B, b, xg);
+    ld_vec(Uc, t, T, B, b, u);
+    Dyn::step(p, t, b, xg, u, fn);
+    DynDerivs<R, NX, NU> D;
+    Dyn::template derivs<false>(p, t, b, xg, u, lam0, D);
+    R dxv[NX], y[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) dxv[i] = x[i] - xg[i];
+    mv<NX, NX>(D.fx, dxv, y);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) x[i] = fn[i] + y[i];
+    st_vec(n, t + 1, T + 1, B, b, x);
+  }
+}
+
+// a converged guess left in xr moves to the candidate buffer
+template <typename R, int NX>
+__global__ void k_pr_finish(NewtonArgs<R> a) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)(a.T + 1) * a.B) return;
+  const int b = (int)(i % a.B), t = (int)(i / a.B);
+  if ((a.rstate[b] & (RS_SKIP | RS_CONV | RS_IN_XR)) != (RS_CONV | RS_IN_XR)) return;
+  R x[NX];
+  ld_vec(a.xr, t, a.T + 1, a.B, b, x);
+  st_vec(a.X + (1 - a.parity[b]) * a.xsz, t, a.T + 1, a.B, b, x);
 }
 
 // ------------------------------------------------------- trust-region control

@@ -97,6 +97,13 @@ def predicted_reduction(dus, d, alpha: float) -> float:
     return 0.5 * float(alpha * np.sum(dus * dus) - np.sum(dus * d))
 
 
+def rollout_mode(executor: str) -> int:
+    """Candidate-rollout schedule of an executor: the parallel executor uses
+    the log-depth Newton rollout on tree plans, the sequential one the plain
+    recurrence, auto decides by horizon (see ptc_problem_desc.rollout)."""
+    return {SEQUENTIAL: 1, PARALLEL: 2}.get(executor, 0)
+
+
 def plan_chunks(executor: str, horizon: int) -> tuple[int, int]:
     if executor == SEQUENTIAL:
         return horizon, 0
@@ -162,7 +169,8 @@ def newton_solve(dyn: DynamicsModel, cost: CostModel, aug: AugmentedCost | None,
     c0, c1 = plan_chunks(opts.executor, dyn.horizon)
     settings = SolveSettings(method=N.METHOD_NEWTON, alpha0=opts.alpha0, nu0=opts.nu0,
                              inner_tol=opts.inner_tol, max_iters=opts.max_iters,
-                             hist_cap=opts.max_iters, round_cap=1, chunk0=c0, chunk=c1, **st)
+                             hist_cap=opts.max_iters, round_cap=1, chunk0=c0, chunk=c1,
+                             rollout=rollout_mode(opts.executor), **st)
     solver = DeviceSolver(dyn, cost, con, 1, settings, dtype=dtype)
     X, U = _traj_arrays(initial)
     z = v = None

@@ -16,7 +16,7 @@ from . import _native as N
 from ._device import DeviceSolver, SolveSettings
 from .exceptions import InfeasibleError
 from .newton import (NewtonOptions, NewtonReport, check_consistent_result, history_records,
-                     plan_chunks, raise_status)
+                     plan_chunks, raise_status, rollout_mode)
 from .problem import AugmentedCost, ConstraintModel, ControlProblem, Trajectory
 
 
@@ -192,7 +192,8 @@ def barrier_solve(problem: ControlProblem, initial: Trajectory,
     settings = SolveSettings(method=N.METHOD_BARRIER, alpha0=nw.alpha0, nu0=nw.nu0,
                              inner_tol=nw.inner_tol, max_iters=nw.max_iters, mu0=opts.mu0,
                              zeta=opts.zeta, mu_tol=opts.mu_tol, hist_cap=hist_cap,
-                             round_cap=n_rounds, keep_round_controls=True, chunk0=c0, chunk=c1)
+                             round_cap=n_rounds, keep_round_controls=True, chunk0=c0, chunk=c1,
+                             rollout=rollout_mode(nw.executor))
     solver = DeviceSolver(problem.dynamics, problem.cost, problem.constraints, 1, settings,
                           dtype=dtype)
     solver.load(initial.states[None], initial.controls[None])
@@ -223,7 +224,8 @@ def admm_solve(problem: ControlProblem, initial: Trajectory, opts: AdmmOptions |
     settings = SolveSettings(method=N.METHOD_ADMM, alpha0=nw.alpha0, nu0=nw.nu0,
                              inner_tol=nw.inner_tol, max_iters=nw.max_iters, rho=opts.rho,
                              residual_tol=opts.residual_tol, max_outer=opts.max_outer,
-                             hist_cap=hist_cap, round_cap=opts.max_outer, chunk0=c0, chunk=c1)
+                             hist_cap=hist_cap, round_cap=opts.max_outer, chunk0=c0, chunk=c1,
+                             rollout=rollout_mode(nw.executor))
     solver = DeviceSolver(problem.dynamics, problem.cost, problem.constraints, 1, settings,
                           dtype=dtype)
     solver.load(initial.states[None], initial.controls[None])
