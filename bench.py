@@ -527,41 +527,73 @@ def lqr_latency_sweep(torch, LqrSolver):
 
 
 def newton_latency_sweep(torch, P):
-    """Per-Newton-iteration latency vs horizon (pendulum, batch 1, fp64, zero
-    augmentation): costate scan + expansion, value + propagation scans,
-    nonlinear rollout, cost, trust-region control -- one ptc_solver_iterate.
-    Timed over the first iterations from a seeded random start (every
-    iteration does full work), reloaded between repetitions."""
+    """Per-Newton-iteration latency vs horizon, batch 1, fp64: one
+    ptc_solver_iterate = co-state scan + expansion, value + propagation
+    scans, candidate rollout, cost, trust-region control.  Two models:
+      tvlinear  config-1 style random time-varying system (nx=4, nu=2,
+                quadratic cost): the rollout is itself an affine scan, so the
+                whole iteration is log-depth;
+      pendulum  config-0 swing-up from random controls: the nonlinear
+                re-rollout the reference mandates (newton.py:188) is tried as
+                a log-depth Newton solve of the recurrence for T >= 1024 and
+                falls back to the sequential recurrence when that does not
+                converge to a few ulps (chaotic long swing-ups).
+    Timed over 4 iterations after the LM weight has settled (12 / 2
+    iterations), inputs reloaded between 3 repetitions; 'full' counts the
+    timed iterations that solved a definite subproblem (the rest are
+    LM rejections, which skip the rollout)."""
     from paper_2409_20027_b200 import _native as N
     from paper_2409_20027_b200._device import DeviceSolver, SolveSettings
-    out = {}
-    for logT in (8, 10, 12, 14, 16):
-        Tn = 1 << logT
-        dyn = P.PendulumDynamics(Tn, P.PendulumParams(damping=0.1, dt=0.05))
-        cost = P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0]))
-        s = DeviceSolver(dyn, cost, None, 1, SolveSettings(method=N.METHOD_NEWTON, max_iters=1000,
-                                                            inner_tol=1e-300))
-        rng = np.random.default_rng([3, logT])
-        us = torch.as_tensor(0.5 * rng.standard_normal((1, Tn, 1)))
-        X = torch.zeros(1, Tn + 1, 2, dtype=torch.float64)
-        X[0, 0, 0] = np.pi
-        s.load(X, us)
-        s.rollout()
-        X = s.field("states", Tn + 1, (2,)).contiguous()
-        iters, reps, per = 4, 3, []
-        for _ in range(reps):
+    res = {}
+    for model in ("tvlinear", "pendulum"):
+        out = {}
+        for logT in (8, 10, 12, 14, 16):
+            Tn = 1 << logT
+            rng = np.random.default_rng([3, logT])
+            if model == "pendulum":
+                dyn = P.PendulumDynamics(Tn, P.PendulumParams(damping=0.1, dt=0.05))
+                cost = P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]),
+                                       np.diag([100.0, 10.0]))
+                nx, nu, settle = 2, 1, 12
+                x0 = np.array([np.pi, 0.0])
+                us = 0.5 * rng.standard_normal((1, Tn, 1))
+            else:
+                nx, nu, settle = 4, 2, 2
+                A = np.eye(nx)[None] + 0.05 * rng.standard_normal((Tn, nx, nx))
+                A *= np.minimum(1.0, 1.0 / np.max(np.abs(np.linalg.eigvals(A)), axis=1))[:, None,
+                                                                                         None]
+                Bm = np.sqrt(0.1) * rng.standard_normal((Tn, nx, nu))
+                dyn = P.TimeVaryingLinearDynamics(A, Bm, 0.1 * rng.standard_normal((Tn, nx)))
+                cost = P.QuadraticCost(np.eye(nx), 0.1 * np.eye(nu), 10 * np.eye(nx))
+                x0 = rng.standard_normal(nx)
+                us = 0.1 * rng.standard_normal((1, Tn, nu))
+            s = DeviceSolver(dyn, cost, None, 1, SolveSettings(
+                method=N.METHOD_NEWTON, max_iters=1000, inner_tol=1e-300, hist_cap=32))
+            us = torch.as_tensor(us)
+            X = torch.zeros(1, Tn + 1, nx, dtype=torch.float64)
+            X[0, 0] = torch.as_tensor(x0)
             s.load(X, us)
-            s.iterate(1)  # first iteration also evaluates the start cost
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            s.iterate(iters)
-            b.record()
-            torch.cuda.synchronize()
-            per.append(a.elapsed_time(b) / iters)
-        out[str(Tn)] = round(statistics.median(per), 4)
-        del s
-    return {"pendulum_ms_per_iteration": out}
+            s.rollout()
+            X = s.field("states", Tn + 1, (nx,)).contiguous()
+            per, full, par = [], 0, 0
+            for _ in range(3):
+                s.load(X, us)
+                s.iterate(settle)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                s.iterate(4)
+                b.record()
+                torch.cuda.synchronize()
+                per.append(a.elapsed_time(b) / 4)
+                h = s.history()[:, :, 0].cpu().numpy()[settle:settle + 4]
+                full += int(np.isfinite(h[:, 3]).sum())
+                par += int(int(s.read("rollout_state")[0]) & 2 != 0)
+            out[str(Tn)] = {"ms": round(statistics.median(per), 4), "full": f"{full}/12",
+                            "log_depth_rollout_converged": f"{par}/3"}
+            del s
+        res[model] = out
+    return res
 
 
 def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):

@@ -194,7 +194,7 @@ typedef struct ptc_problem_desc {
   int32_t keep_round_controls; /* barrier: store each round's controls */
   int32_t chunk0, chunk;       /* scan plan, 0 = automatic */
   int32_t rollout;             /* candidate rollout: 0 auto (log-depth Newton sweeps for
-                                  tree plans with horizon >= 2048), 1 sequential,
+                                  tree plans with horizon >= 1024), 1 sequential,
                                   2 log-depth (tree plans) */
 } ptc_problem_desc;
 
@@ -235,7 +235,8 @@ int ptc_solver_total_cost(ptc_solver* s, void* stream);
  * (current trajectory), lam, P, R, M, d, Fx, Fu, PT, S, s, Gamma, gamma, dx,
  * du, z, v, status, iters, term, round, hist_len, hist, cur_cost, alpha, mu,
  * round_mu, round_cost, round_iters, round_term, round_rp, round_rd,
- * round_controls, bad_index, flags.  ptc_solver_buffer_info reports the
+ * round_controls, bad_index, flags, rollout_state (bit 0 skipped, bit 1 log-depth
+ * rollout converged, bit 2 converged in the scratch buffer).  ptc_solver_buffer_info reports the
  * element count and element size. */
 int ptc_solver_buffer_info(ptc_solver* s, const char* name, int64_t* numel, int32_t* elem_bytes);
 int ptc_solver_read(ptc_solver* s, const char* name, void* dst, int64_t bytes, int dst_on_device,

@@ -501,7 +501,7 @@ struct Solver final : ptc_solver {
     a.rres = c.template take<double>(P0 * B);
     // candidate rollout: log-depth Newton sweeps for tree plans with long
     // horizons (rollout 0 = auto), the sequential recurrence otherwise
-    const bool par = a.plan.L >= 1 && (d.rollout == 2 || (d.rollout == 0 && T >= 2048));
+    const bool par = a.plan.L >= 1 && (d.rollout == 2 || (d.rollout == 0 && T >= 1024));
     a.pr_iters = par ? 8 : 0;
     a.xr = par ? c.template take<R>(a.xsz) : nullptr;
     a.alpha = db(); a.nu = db(); a.cur_cost = db(); a.cand_cost = db(); a.mu = db();
@@ -614,6 +614,7 @@ struct Solver final : ptc_solver {
       reg("hist_len", a.hist_len, B, 4);
       reg("bad_index", a.bad_index, B, 4);
       reg("flags", a.flags, B, 4);
+      reg("rollout_state", a.rstate, B, 4);
       reg("parity", a.parity, B, 4);
       reg("hist", a.hist, (int64_t)a.opt.hist_cap * 5 * B, 8);
       reg("cur_cost", a.cur_cost, B, 8);

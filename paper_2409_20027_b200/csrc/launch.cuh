@@ -145,6 +145,10 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
   launch_costate<R, Dyn>(a, s);
   lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&la, s);
+  const bool fold = partial_rows((int)P0) < (int)P0;
+  constexpr int kOpsRed = RED_SUM | (RED_SUM << 2) | (RED_MAX << 4);     // sum du^2, sum du.d, max |du|
+  constexpr int kOpsCost = RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4);  // sum l, sum c, first infeasible
+  if (fold) k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.red, 3, kOpsRed, (int)P0, (int)B);
   k_roll_gate<R><<<grid_for(B), kBlock, 0, s>>>(a);
   if (a.pr_iters > 0 && a.plan.L >= 1) {
     // log-depth Newton rollout, sequential fallback for what did not converge
@@ -153,6 +157,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     k_pr_init<R, NX, NU><<<grid_for(nT), kBlock, 0, s>>>(a, la.dX, la.dU);
     for (int k = 0; k <= a.pr_iters; ++k) {
       k_pr_up0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, k);
+      if (fold) k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.rres, 1, RED_MAX, (int)P0, (int)B);
       k_pr_check<R><<<grid_for(B), kBlock, 0, s>>>(a, k);
       if (k == a.pr_iters) break;
       for (int l = 1; l < pl.L; ++l) k_pr_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
@@ -167,8 +172,14 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     k_rollout<R, Dyn, false><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
   }
   k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+  if (fold) {
+    k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[0], 3, kOpsCost, (int)P0, (int)B);
+    k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[1], 3, kOpsCost, (int)P0, (int)B);
+  }
   k_control<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
   k_round_end<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  if (fold && a.apart && a.opt.method == METHOD_ADMM)
+    k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.apart, 2, RED_MAX | (RED_MAX << 2), (int)P0, (int)B);
   k_outer<R><<<grid_for(B), kBlock, 0, s>>>(a);
 }
 
@@ -276,7 +287,12 @@ struct RegisterNewton {
   static void cost(const void* p, cudaStream_t s) {
     const NewtonArgs<R>& a = A(p);
     k_force_phase<R><<<grid_for(a.B), kBlock, 0, s>>>(a, PH_NEED_COST);
-    k_cost_partials<R, NX, NU><<<grid_for((long long)a.plan.units0() * a.B), kBlock, 0, s>>>(a, 0);
+    const int P0 = a.plan.units0();
+    k_cost_partials<R, NX, NU><<<grid_for((long long)P0 * a.B), kBlock, 0, s>>>(a, 0);
+    if (partial_rows(P0) < P0)
+      k_reduce_partials<<<(unsigned)a.B, 256, 0, s>>>(a.cpart[0], 3,
+                                                      RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4),
+                                                      P0, a.B);
     k_cost_finalize<R, NX><<<grid_for(a.B), kBlock, 0, s>>>(a);
   }
   RegisterNewton() {

@@ -87,6 +87,47 @@ PTC_D void ld_u(const NewtonArgs<R>& a, int q, int t, int b, R (&u)[NU]) {
 template <typename R>
 PTC_D bool running(const NewtonArgs<R>& a, int b) { return a.status[b] == ST_RUNNING; }
 
+// Per-problem partials (P0 rows per field) are folded by k_reduce_partials
+// into row 0 when there are many of them (long horizons, small batches);
+// consumers then read one row instead of looping over P0 in one thread.
+constexpr int kReduceMin = 64;
+PTC_HD int partial_rows(int P0) { return P0 > kReduceMin ? 1 : P0; }
+
+enum : int { RED_SUM = 0, RED_MAX = 1, RED_FIRST = 2 };
+
+// One block per problem: fold fields f of part[(f * P0 + j) * B + b] over j
+// into row 0.  ops: 2 bits per field (RED_SUM, RED_MAX = NaN-propagating
+// max, RED_FIRST = smallest non-negative value or -1, i.e. the first
+// infeasible index since rows follow the stage order).
+static __global__ void k_reduce_partials(double* part, int nf, int ops, int P0, int B) {
+  __shared__ double sh[256];
+  const int b = blockIdx.x;
+  for (int f = 0; f < nf; ++f) {
+    const int op = (ops >> (2 * f)) & 3;
+    double acc = op == RED_SUM ? 0.0 : (op == RED_MAX ? 0.0 : -1.0);
+    for (int j = threadIdx.x; j < P0; j += blockDim.x) {
+      const double v = part[((size_t)f * P0 + j) * B + b];
+      if (op == RED_SUM) acc += v;
+      else if (op == RED_MAX) acc = nanmax(acc, v);
+      else if (v >= 0.0 && (acc < 0.0 || v < acc)) acc = v;
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) {
+        const double o = sh[threadIdx.x + w];
+        double& m = sh[threadIdx.x];
+        if (op == RED_SUM) m += o;
+        else if (op == RED_MAX) m = nanmax(m, o);
+        else if (o >= 0.0 && (m < 0.0 || o < m)) m = o;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part[((size_t)f * P0) * B + b] = sh[0];
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------ initialisation
 
 template <typename R>
@@ -400,7 +441,7 @@ __global__ void k_roll_gate(NewtonArgs<R> a) {
   } else {
     const int P0 = a.plan.units0();
     double step = 0.0;
-    for (int j = 0; j < P0; ++j) step = nanmax(step, a.red[((size_t)2 * P0 + j) * a.B + b]);
+    for (int j = 0; j < partial_rows(P0); ++j) step = nanmax(step, a.red[((size_t)2 * P0 + j) * a.B + b]);
     if (step <= a.opt.inner_tol) st = RS_SKIP;
   }
   a.rstate[b] = st;
@@ -581,7 +622,7 @@ __global__ void k_pr_check(NewtonArgs<R> a, int k) {
   if (st & (RS_SKIP | RS_CONV)) return;
   const int P0 = a.plan.units0();
   double r = 0.0;
-  for (int j = 0; j < P0; ++j) r = nanmax(r, a.rres[(size_t)j * a.B + b]);
+  for (int j = 0; j < partial_rows(P0); ++j) r = nanmax(r, a.rres[(size_t)j * a.B + b]);
   const double tol = 16.0 * (sizeof(R) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07);
   if (r <= tol) a.rstate[b] = st | RS_CONV | ((k & 1) ? RS_IN_XR : 0);
 }
@@ -721,7 +762,7 @@ PTC_D double finalize_cost(const NewtonArgs<R>& a, int which, int q, int b, int&
   const double* cp = a.cpart[which];
   double sl = 0.0, sc = 0.0;
   bad = -1;
-  for (int j = 0; j < P0; ++j) {
+  for (int j = 0; j < partial_rows(P0); ++j) {
     sl += cp[((size_t)0 * P0 + j) * a.B + b];
     sc += cp[((size_t)1 * P0 + j) * a.B + b];
     int bj = int(cp[((size_t)2 * P0 + j) * a.B + b]);
@@ -775,7 +816,7 @@ __global__ void k_control(NewtonArgs<R> a) {
   } else {
     const int P0 = a.plan.units0();
     double s2 = 0.0, sd = 0.0, step = 0.0;
-    for (int j = 0; j < P0; ++j) {
+    for (int j = 0; j < partial_rows(P0); ++j) {
       s2 += a.red[((size_t)0 * P0 + j) * a.B + b];
       sd += a.red[((size_t)1 * P0 + j) * a.B + b];
       step = nanmax(step, a.red[((size_t)2 * P0 + j) * a.B + b]);
@@ -915,7 +956,7 @@ __global__ void k_outer(NewtonArgs<R> a) {
     } else if (m == METHOD_ADMM) {
       const int P0 = a.plan.units0();
       double rp = 0.0, rd = 0.0;
-      for (int j = 0; j < P0; ++j) {
+      for (int j = 0; j < partial_rows(P0); ++j) {
         rp = nanmax(rp, a.apart[((size_t)0 * P0 + j) * a.B + b]);
         rd = nanmax(rd, a.apart[((size_t)1 * P0 + j) * a.B + b]);
       }
