@@ -144,6 +144,10 @@ static cudaGraphExec_t lqr_graph_for(const LqrArgs<R>& a, const LqrOps& ops, cud
   static thread_local cudaStream_t cap = nullptr;
   const unsigned char* kb = reinterpret_cast<const unsigned char*>(&a);
   std::vector<unsigned char> key(kb, kb + sizeof(a));
+  // the kernel set (dtype, nx, nu) is not part of LqrArgs: key on it too
+  const uintptr_t fn = reinterpret_cast<uintptr_t>(ops.solve);
+  const unsigned char* fb = reinterpret_cast<const unsigned char*>(&fn);
+  key.insert(key.end(), fb, fb + sizeof(fn));
   key.push_back((unsigned char)sizeof(R));
   for (auto& g : cache)
     if (g.key == key) return g.exec;
