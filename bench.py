@@ -625,31 +625,45 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
                 "newton_iterations": int(res.inner_iterations.sum()),
                 "max_newton_iterations": int(res.inner_iterations.max())}
 
+    solvers, starts = {}, {}
     for system, n in (("pendulum", bp), ("cartpole", bc)):
         rng = rng_for(rank, system)
         x0 = initial_states(system, n, rng)
         bound = 5.0 if system == "pendulum" else 10.0
-        u0 = np.clip(0.1 * bound * rng.standard_normal((n, T, 1)), -0.9 * bound, 0.9 * bound)
+        u0 = torch.as_tensor(np.clip(0.1 * bound * rng.standard_normal((n, T, 1)),
+                                     -0.9 * bound, 0.9 * bound)).cuda()
         prob = P.ControlProblem(probs[system].dynamics, probs[system].cost, box[system])
         bs = BatchSolver(prob, n, "barrier", barrier=opts)
-        xs = bs.rollout(x0, torch.as_tensor(u0))
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        ev[0].record()
-        res = bs.solve(xs, torch.as_tensor(u0).cuda())
-        ev[1].record()
-        x_next = res.states[:, shift].contiguous()
+        solvers[system] = bs
+        starts[system] = (bs.rollout(x0, u0), u0)
+    names = list(solvers)
+    # the two halves advance concurrently (one stream each), as one MPC batch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    cold = BatchSolver.solve_concurrently([(solvers[k],) + starts[k] for k in names])
+    ev[1].record()
+    torch.cuda.synchronize()
+    warm_in = {}
+    for k, res in zip(names, cold):
+        bs = solvers[k]
         u_next = bs.shift_controls(res.controls, shift)
-        xs2 = bs.rollout(x_next, u_next)
-        torch.cuda.synchronize()
-        ev[2].record()
-        res2 = bs.solve(xs2, u_next)
-        ev[3].record()
-        torch.cuda.synchronize()
-        out[system] = {"problems": n, "cold": outcome(res, ev[0].elapsed_time(ev[1])),
-                       "warm": outcome(res2, ev[2].elapsed_time(ev[3]))}
-        out["problems"] += n
-        out["warm_ms"] += ev[2].elapsed_time(ev[3])
-        del bs, res, res2
+        warm_in[k] = (bs.rollout(res.states[:, shift].contiguous(), u_next), u_next)
+    torch.cuda.synchronize()
+    ev[2].record()
+    warm = BatchSolver.solve_concurrently([(solvers[k],) + warm_in[k] for k in names])
+    ev[3].record()
+    torch.cuda.synchronize()
+    cold_ms, warm_ms = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
+    for k, rc, rw in zip(names, cold, warm):
+        out[k] = {"problems": solvers[k].batch, "cold": outcome(rc, cold_ms),
+                  "warm": outcome(rw, warm_ms)}
+        out["problems"] += solvers[k].batch
+    out["cold_ms"] = cold_ms
+    out["warm_ms"] = warm_ms
+    out["newton_iterations_per_s_warm"] = sum(out[k]["warm"]["newton_iterations"]
+                                              for k in names) / (warm_ms * 1e-3)
+    del solvers, cold, warm
     out["mpc_steps_per_s_warm"] = out["problems"] / (out["warm_ms"] * 1e-3)
     out["config"] = ("config 3 barrier MPC: pendulum (cfg-0 model/cost) + cart-pole (cfg-2 "
                      "model/cost), control boxes, T=256, fp64, warm start shift %d" % shift)

@@ -90,11 +90,50 @@ class BatchSolver:
                 raise ValueError(f"{int((bad >= 0).sum())} initial trajectories are not "
                                  "dynamically consistent")
         launches = s.run()
+        return self._result(launches)
+
+    def _result(self, launches: int) -> BatchResult:
+        s = self.solver
         return BatchResult(
             states=s.states().contiguous(), controls=s.controls().contiguous(),
             status=s.read("status"), rounds=s.read("round"),
             round_iters=s.rounds("round_iters"), round_term=s.rounds("round_term"),
             cost=s.read("cur_cost"), launches=launches)
+
+    @staticmethod
+    def solve_concurrently(jobs, group: int = 4) -> list:
+        """Advance several batches (e.g. the two models of config 3) at once,
+        one CUDA stream each: ``jobs`` = [(BatchSolver, states, controls)].
+        Every solver keeps its own device-resident loop; the host polls each
+        stream every ``group`` iterations, so one batch's stragglers never
+        serialise the other's iterations."""
+        import torch
+        streams = [torch.cuda.Stream() for _ in jobs]
+        for (bs, X, U), st in zip(jobs, streams):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                bs.solver.load(X, U)
+        launched = [0] * len(jobs)
+        caps = [(bs.settings.max_iters + 2) * max(1, bs.settings.round_cap) + 16
+                for bs, _, _ in jobs]
+        active = set(range(len(jobs)))
+        n = 1
+        while active:
+            for i in sorted(active):
+                with torch.cuda.stream(streams[i]):
+                    jobs[i][0].solver.iterate(n)
+                launched[i] += n
+            for i in sorted(active):
+                with torch.cuda.stream(streams[i]):
+                    if jobs[i][0].solver.running() == 0 or launched[i] >= caps[i]:
+                        active.discard(i)
+            n = group
+        out = []
+        for (bs, _, _), st, k in zip(jobs, streams, launched):
+            with torch.cuda.stream(st):
+                out.append(bs._result(k))
+            torch.cuda.current_stream().wait_stream(st)
+        return out
 
     @staticmethod
     def shift_controls(controls, shift: int):

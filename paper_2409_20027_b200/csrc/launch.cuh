@@ -143,8 +143,21 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   const long long B = a.B, P0 = a.plan.units0();
   cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
   k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
-  launch_costate<R, Dyn>(a, s);
-  lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&la, s);
+  bool fused = false;
+  if constexpr (NX < 8) {
+    if (a.plan.L == 0) {
+      // single-sweep schedule: the LQR sweeps re-derive the expansion in
+      // registers from x, u and the co-states (no stored expansion)
+      k_costate_down0<R, Dyn, false><<<grid_for(B), kBlock, 0, s>>>(a);
+      k_value_fused<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la);
+      k_prop_fused<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la);
+      fused = true;
+    }
+  }
+  if (!fused) {
+    launch_costate<R, Dyn>(a, s);
+    lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&la, s);
+  }
   const bool fold = partial_rows((int)P0) < (int)P0;
   constexpr int kOpsRed = RED_SUM | (RED_SUM << 2) | (RED_MAX << 4);     // sum du^2, sum du.d, max |du|
   constexpr int kOpsCost = RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4);  // sum l, sum c, first infeasible
@@ -168,10 +181,14 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     }
     k_pr_finish<R, NX><<<grid_for(nT), kBlock, 0, s>>>(a);
     k_rollout<R, Dyn, true><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
+    k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+  } else if (P0 == 1) {
+    // one unit per problem: the rollout also accumulates the candidate cost
+    k_rollout<R, Dyn, false, true><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
   } else {
     k_rollout<R, Dyn, false><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
+    k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
   }
-  k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
   if (fold) {
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[0], 3, kOpsCost, (int)P0, (int)B);
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[1], 3, kOpsCost, (int)P0, (int)B);

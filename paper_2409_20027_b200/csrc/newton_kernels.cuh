@@ -340,10 +340,70 @@ __global__ void __launch_bounds__(128) k_costate_down(NewtonArgs<R> a, int l) {
   }
 }
 
+// Second-order data of stage t of the augmented Lagrangian at (x_t, u_t)
+// with the next co-state lambda_{t+1} (passes.py:155-185): P, R, M, d, Fx,
+// Fu, plus lambda_t = lx + cx + fx^T lambda_{t+1}.  Shared by the co-state
+// sweep (which stores it) and the fused value sweep (which consumes it in
+// registers), so both paths produce identical bits.
+template <typename R, class Dyn>
+PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const AugArgs<R>& g,
+                           int t, int b, const R (&x)[Dyn::NX], const R (&u)[Dyn::NU],
+                           const R (&ln)[Dyn::NX], Stage<R, Dyn::NX, Dyn::NU>& st,
+                           R (&lt)[Dyn::NX]) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  DynDerivs<R, NX, NU> D;
+  Dyn::template derivs<true>(p, t, b, x, u, ln, D);
+  R cx[NX], cu[NU], cxx[NX], cuu[NU];
+  aug_derivs<R, NX, NU>(p, g, t, a.T, a.B, b, x, u, cx, cu, cxx, cuu);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int k = 0; k < NX; ++k)
+      st.P[i][k] = (R(p.Q[i * NX + k]) + (i == k ? cxx[i] : R(0))) + D.Hxx[i][k];
+  symmetrize<NX>(st.P);
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int k = 0; k < NU; ++k)
+      st.Rr[i][k] = (R(p.Rc[i * NU + k]) + (i == k ? cuu[i] : R(0))) + D.Huu[i][k];
+  symmetrize<NU>(st.Rr);
+  R ftl[NU];
+  mtv<NU, NX>(D.fu, ln, ftl);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) {
+    R ru = R(0);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) ru += u[k] * R(p.Rc[i * NU + k]);
+    st.d[i] = (ru + cu[i]) + ftl[i];
+  }
+  R fxl[NX];
+  mtv<NX, NX>(D.fx, ln, fxl);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    R lx = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+    lt[i] = (lx + cx[i]) + fxl[i];
+  }
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      st.M[i][k] = D.Hxu[i][k];
+      st.Fu[i][k] = D.fu[i][k];
+    }
+#pragma unroll
+    for (int k = 0; k < NX; ++k) st.Fx[i][k] = D.fx[i][k];
+  }
+}
+
 // level-0 down-sweep fused with the Hamiltonian expansion (passes.py:155-185):
 // with lambda_{t+1} in registers, evaluate every model derivative at
 // (x_t, u_t) once and emit P, R, M, d, Fx, Fu and lambda_t.
-template <typename R, class Dyn>
+// kExp: store the expansion (pass-level API, tree plans); without it only
+// the co-states are stored and the fused value sweep re-derives the stage
+// data in registers (the 2nx^2 + nu^2 + 2nx nu + nu words never touch HBM).
+template <typename R, class Dyn, bool kExp = true>
 __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
   constexpr int NX = Dyn::NX, NU = Dyn::NU;
   const int P0 = a.plan.units0();
@@ -376,51 +436,117 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
     R x[NX], u[NU];
     ld_x(a, q, t, b, x);
     ld_u(a, q, t, b, u);
-    DynDerivs<R, NX, NU> D;
-    Dyn::template derivs<true>(p, t, b, x, u, ln, D);
-    R cx[NX], cu[NU], cxx[NX], cuu[NU];
-    aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
-    R Pm[NX][NX], Rm[NU][NU], dv[NU], lt[NX];
-#pragma unroll
-    for (int i = 0; i < NX; ++i)
-#pragma unroll
-      for (int k = 0; k < NX; ++k)
-        Pm[i][k] = (R(p.Q[i * NX + k]) + (i == k ? cxx[i] : R(0))) + D.Hxx[i][k];
-    symmetrize<NX>(Pm);
-#pragma unroll
-    for (int i = 0; i < NU; ++i)
-#pragma unroll
-      for (int k = 0; k < NU; ++k)
-        Rm[i][k] = (R(p.Rc[i * NU + k]) + (i == k ? cuu[i] : R(0))) + D.Huu[i][k];
-    symmetrize<NU>(Rm);
-    R ftl[NU];
-    mtv<NU, NX>(D.fu, ln, ftl);
-#pragma unroll
-    for (int i = 0; i < NU; ++i) {
-      R ru = R(0);
-#pragma unroll
-      for (int k = 0; k < NU; ++k) ru += u[k] * R(p.Rc[i * NU + k]);
-      dv[i] = (ru + cu[i]) + ftl[i];
+    Stage<R, NX, NU> st;
+    R lt[NX];
+    stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
+    if constexpr (kExp) {
+      st_mat(a.P, t, T, B, b, st.P);
+      st_mat(a.Rm, t, T, B, b, st.Rr);
+      st_mat(a.M, t, T, B, b, st.M);
+      st_vec(a.d, t, T, B, b, st.d);
+      st_mat(a.Fx, t, T, B, b, st.Fx);
+      st_mat(a.Fu, t, T, B, b, st.Fu);
     }
-    R fxl[NX];
-    mtv<NX, NX>(D.fx, ln, fxl);
-#pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      R lx = R(0);
-#pragma unroll
-      for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
-      lt[i] = (lx + cx[i]) + fxl[i];
-    }
-    st_mat(a.P, t, T, B, b, Pm);
-    st_mat(a.Rm, t, T, B, b, Rm);
-    st_mat(a.M, t, T, B, b, D.Hxu);
-    st_vec(a.d, t, T, B, b, dv);
-    st_mat(a.Fx, t, T, B, b, D.fx);
-    st_mat(a.Fu, t, T, B, b, D.fu);
     st_vec(a.lam, t, T + 1, B, b, lt);
 #pragma unroll
     for (int i = 0; i < NX; ++i) ln[i] = lt[i];
   }
+}
+
+// ----------------------------------------------- fused single-sweep LQR
+// For single-sweep plans (one level-0 unit per problem: the large-batch
+// schedule) the Newton iteration's value and propagation sweeps re-derive
+// every stage's expansion from (x_t, u_t, lambda_{t+1}) in registers
+// instead of reading the stored one: same functions, same bits, ~1/4 of
+// the HBM traffic of the unfused iteration.
+
+template <typename R, class Dyn>
+__global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R> la) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (!running(a, b)) return;
+  const int q = a.parity[b];
+  const int T = a.T, B = a.B;
+  const ProblemParams& p = *a.pp;
+  const AugArgs<R> g = aug_of(a);
+  const R alpha = R(a.alpha[b]);
+  VCarry<R, NX> c;
+  ld_mat(a.PT, 0, 1, B, b, c.Y);
+  set_zero(c.eta);
+  int fl = 0;
+  R ln[NX];
+  ld_vec(a.lam, T, T + 1, B, b, ln);
+  for (int t = T - 1; t >= 0; --t) {
+    R x[NX], u[NU];
+    ld_x(a, q, t, b, x);
+    ld_u(a, q, t, b, u);
+    Stage<R, NX, NU> st;
+    R lt[NX];
+    stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) st.Rr[i][i] += alpha;
+    R Gam[NU][NX], gam[NU];
+    VCarry<R, NX> o;
+    fl |= riccati_step(st, c, Gam, gam, o);
+    st_mat(la.Gam, t, T, B, b, Gam);
+    st_vec(la.gam, t, T, B, b, gam);
+    st_vec(a.d, t, T, B, b, st.d);
+    c = o;
+    ld_vec(a.lam, t, T + 1, B, b, ln);  // lambda_t, stored by the co-state sweep
+  }
+  if (fl) atomicOr(a.flags + b, fl);
+}
+
+template <typename R, class Dyn>
+__global__ void __launch_bounds__(128) k_prop_fused(NewtonArgs<R> a, LqrArgs<R> la) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (!running(a, b)) return;
+  const int q = a.parity[b];
+  const int T = a.T, B = a.B;
+  const ProblemParams& p = *a.pp;
+  R x[NX];
+  set_zero(x);
+  double s2 = 0.0, sd = 0.0, mx = 0.0;
+  R lam0[NX];
+  set_zero(lam0);
+  for (int t = 0; t < T; ++t) {
+    st_vec(la.dX, t, T + 1, B, b, x);
+    R xs[NX], us[NU], Gam[NU][NX], gam[NU], dd[NU];
+    ld_x(a, q, t, b, xs);
+    ld_u(a, q, t, b, us);
+    ld_mat(la.Gam, t, T, B, b, Gam);
+    ld_vec(la.gam, t, T, B, b, gam);
+    ld_vec(a.d, t, T, B, b, dd);
+    DynDerivs<R, NX, NU> D;
+    Dyn::template derivs<false>(p, t, b, xs, us, lam0, D);
+    R du[NU];
+    mv<NU, NX>(Gam, x, du);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      du[i] += gam[i];
+      s2 += double(du[i]) * double(du[i]);
+      sd += double(du[i]) * double(dd[i]);
+      mx = nanmax(mx, double(fabs(du[i])));
+    }
+    st_vec(la.dU, t, T, B, b, du);
+    R F[NX][NX], e[NX], y[NX];
+    mm<NX, NU, NX>(D.fu, Gam, F);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NX; ++k) F[i][k] = (t == 0) ? R(0) : F[i][k] + D.fx[i][k];
+    mv<NX, NU>(D.fu, gam, e);
+    mv<NX, NX>(F, x, y);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
+  }
+  st_vec(la.dX, T, T + 1, B, b, x);
+  la.red[(size_t)0 * B + b] = s2;
+  la.red[(size_t)1 * B + b] = sd;
+  la.red[(size_t)2 * B + b] = mx;
 }
 
 // --------------------------------------------------------------- rollout
@@ -451,7 +577,10 @@ __global__ void k_roll_gate(NewtonArgs<R> a) {
 // -- sequential in time, parallel over the batch; controls are prefetched
 // kRing steps ahead so the recurrence runs at the dynamics' latency, not
 // the memory's.  With kFromUc the candidate controls are already in place.
-template <typename R, class Dyn, bool kFromUc>
+// kCost: also accumulate the candidate's stage and augmentation costs (the
+// partials k_cost_partials(a, 1) would produce, single-unit plans only), so
+// the candidate trajectory is not read back a second time.
+template <typename R, class Dyn, bool kFromUc, bool kCost = false>
 __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
   constexpr int NX = Dyn::NX, NU = Dyn::NU;
   constexpr int kRing = 8;
@@ -479,6 +608,9 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
   ld_x(a, q, 0, b, x);
   st_vec(Xc, 0, T + 1, B, b, x);
   bool finite = true;
+  double sl = 0.0, sc = 0.0;
+  int bad = -1;
+  const AugArgs<R> g = aug_of(a);
   R ring[kRing][NU];
   auto fetch = [&](int t, R (&u)[NU]) {
     if (t < T) {
@@ -505,6 +637,12 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
         for (int i = 0; i < NU; ++i) u[i] = ring[k][i];
         fetch(t + kRing, ring[k]);
         if (!kFromUc) st_vec(Uc, t, T, B, b, u);
+        if constexpr (kCost) {
+          sl += double(stage_cost<R, NX, NU>(gp, x, u));
+          int br;
+          sc += double(aug_value<R, NX, NU>(gp, g, t, T, B, b, x, u, br));
+          if (br >= 0 && bad < 0) bad = t * gp.W + br;
+        }
         R xn[NX];
         Dyn::step(p, t, b, x, u, xn);
 #pragma unroll
@@ -517,6 +655,12 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
     }
   }
   if (!finite) atomicOr(a.flags + b, FLAG_DIVERGED);
+  if constexpr (kCost) {
+    double* cp = a.cpart[1];  // P0 == 1
+    cp[(size_t)0 * B + b] = sl;
+    cp[(size_t)1 * B + b] = sc;
+    cp[(size_t)2 * B + b] = double(bad);
+  }
 }
 
 // ------------------------------------------------ parallel (log-depth) rollout

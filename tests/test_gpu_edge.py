@@ -200,3 +200,50 @@ def test_single_stage_newton_matches_oracle():
     ref = O.newton_solve(odyn, ocost, ("zero",), init.states, init.controls)
     assert rep.iterations == ref.iterations
     assert rel_gap(traj.controls, ref.us) < 1e-9
+
+
+def test_batch_solver_concurrent_matches_single_and_oracle():
+    """Two batches advanced concurrently on two streams give the same result
+    as solving them one after the other; a problem of the batch matches the
+    CPU oracle's barrier solve (iteration counts and controls)."""
+    import torch
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200 import BatchSolver
+    T, n = 24, 5
+    rng = np.random.default_rng(31)
+    pend = P.ControlProblem(P.PendulumDynamics(T, P.PendulumParams(damping=0.1, dt=0.05)),
+                            P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]),
+                                            np.diag([100.0, 10.0])),
+                            P.BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0))
+    Q = np.diag([1.0, 10.0, 0.1, 0.1])
+    cart = P.ControlProblem(P.CartPoleDynamics(T, P.CartPoleParams(cart_mass=1.0, pole_mass=0.1,
+                                                                   pole_length=0.5, dt=0.02)),
+                            P.QuadraticCost(Q, np.diag([0.01]), 10 * Q,
+                                            x_goal=np.array([0.0, np.pi, 0.0, 0.0])),
+                            P.BoxConstraint(4, 1, control_lower=-10.0, control_upper=10.0))
+    opts = P.BarrierOptions(mu0=0.1, zeta=0.2, mu_tol=1e-3, newton=P.NewtonOptions(max_iters=40))
+    jobs, singles = [], []
+    for prob, nx, bound in ((pend, 2, 5.0), (cart, 4, 10.0)):
+        x0 = rng.uniform(-0.3, 0.3, (n, nx))   # near the goal: a converging, well-posed solve
+        u0 = torch.as_tensor(np.clip(0.1 * bound * rng.standard_normal((n, T, 1)),
+                                     -0.9 * bound, 0.9 * bound))
+        bs = BatchSolver(prob, n, "barrier", barrier=opts)
+        xs = bs.rollout(x0, u0)
+        singles.append(bs.solve(xs, u0))
+        bs2 = BatchSolver(prob, n, "barrier", barrier=opts)
+        jobs.append((bs2, xs, u0))
+    conc = BatchSolver.solve_concurrently(jobs)
+    for a, b in zip(singles, conc):
+        assert torch.equal(a.status, b.status)
+        assert torch.equal(a.round_iters, b.round_iters)
+        assert torch.equal(a.controls, b.controls)
+    # problem 0 of the pendulum batch against the oracle barrier solve
+    x_init = jobs[0][1][0].cpu().numpy()
+    u_init = jobs[0][2][0].numpy()
+    ref = O.barrier_solve(O.Pendulum(damping=0.1, dt=0.05),
+                          O.Quadratic(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0])),
+                          O.Box(2, 1, control_lower=-5.0, control_upper=5.0), x_init, u_init,
+                          mu0=0.1, zeta=0.2, mu_tol=1e-3, max_iters=40)
+    got = conc[0].round_iters[:, 0].cpu().numpy()[:len(ref.newton)]
+    assert list(got) == [r.iterations for r in ref.newton]
+    assert rel_gap(conc[0].controls[0].cpu().numpy(), ref.us) < 1e-9
