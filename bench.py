@@ -670,7 +670,8 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
     return out
 
 
-def long_horizon_leg(torch, world: int, rank: int, steps: int = 5):
+def long_horizon_leg(torch, world: int, rank: int, steps: int = 5, chunk0: int = 0,
+                     chunk: int = 0):
     """Config 4: one T = 2^20 LQR-scan solve, nx=12, nu=4, fp64, horizon split
     into `world` contiguous time blocks (one per rank) with an NCCL
     all-gather of the block aggregates per scan.  Random time-varying
@@ -705,7 +706,8 @@ def long_horizon_leg(torch, world: int, rank: int, steps: int = 5):
     PT = (10.0 * torch.diag(qd)).reshape(nx * nx, 1, 1).contiguous()
     alpha = torch.zeros(1, dtype=f64, device=dev)
     del F, A, Bm, c
-    ops = CudaBlockOps(rank, world, t0, Pm, Rm, Mm, dm, Fx, Fu, PT, alpha, nx, nu)
+    ops = CudaBlockOps(rank, world, t0, Pm, Rm, Mm, dm, Fx, Fu, PT, alpha, nx, nu,
+                       chunk0=chunk0, chunk=chunk)
     drv = TimeShardedLqr(ops, nccl_gather() if world > 1 else (lambda t: t.unsqueeze(0)))
     for _ in range(2):
         drv.solve()

@@ -64,10 +64,18 @@ struct Carver {
 };
 
 template <typename R>
-static void carve_lqr_tree(Carver& c, LqrArgs<R>& a, int nx) {
+static void carve_lqr_tree(Carver& c, LqrArgs<R>& a, int nx, int nu) {
   const Plan& pl = a.plan;
   const size_t B = a.B;
   a.red = c.template take<double>(3 * (size_t)pl.units0() * B);
+  // single long wide problem: stage-major copies of the expansion and of the
+  // gains (wide.cuh "staged" mode) make every per-stage access contiguous
+  a.xst = a.gst = nullptr;
+  if (B == 1 && nx >= 8 && a.T >= 1024) {
+    const size_t sc = (size_t)nx * nx + nu * nu + nx * nu + nu + nx * nx + nx * nu;
+    a.xst = c.template take<R>((size_t)a.T * sc);
+    a.gst = c.template take<R>((size_t)a.T * (nu * nx + nu));
+  }
   for (int l = 0; l <= kMaxLevels; ++l) a.vagg[l] = a.vcar[l] = a.pagg[l] = a.pcar[l] = nullptr;
   a.vcin_buf = a.xin_buf = nullptr;
   if (a.block_mode) {
@@ -118,13 +126,13 @@ int64_t ptc_lqr_workspace_bytes(int dtype, int batch, int horizon, int nx, int n
     a.B = batch;
     a.T = horizon;
     a.plan = auto_plan(batch, horizon, chunk0, chunk);
-    carve_lqr_tree(c, a, nx);
+    carve_lqr_tree(c, a, nx, nu);
   } else {
     LqrArgs<float> a{};
     a.B = batch;
     a.T = horizon;
     a.plan = auto_plan(batch, horizon, chunk0, chunk);
-    carve_lqr_tree(c, a, nx);
+    carve_lqr_tree(c, a, nx, nu);
   }
   return (int64_t)c.off + 256;
 }
@@ -208,7 +216,7 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
   a.dU = (R*)du;
   a.flags = flags;
   Carver c{(char*)ws};
-  carve_lqr_tree(c, a, nx);
+  carve_lqr_tree(c, a, nx, nu);
   if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
   if ((S == nullptr) != (s == nullptr)) return fail(PTC_ERR_ARG, "S and s must both be given or both NULL");
   if (a.plan.L >= 1 && !getenv("PTC_NO_GRAPH")) {
@@ -245,7 +253,7 @@ static int propagate_t(int batch, int horizon, int nx, int nu, const void* Fx, c
   a.dX = (R*)dx;
   a.dU = (R*)du;
   Carver c{(char*)ws};
-  carve_lqr_tree(c, a, nx);
+  carve_lqr_tree(c, a, nx, nu);
   if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
   it->second.propagate(&a, st);
   PTC_CUDA(cudaGetLastError());
@@ -286,14 +294,14 @@ int64_t ptc_lqr_block_workspace_bytes(int dtype, int batch, int horizon, int nx,
     a.T = horizon;
     a.block_mode = 1;
     a.plan = auto_plan(batch, horizon, chunk0, chunk);
-    carve_lqr_tree(c, a, nx);
+    carve_lqr_tree(c, a, nx, nu);
   } else {
     LqrArgs<float> a{};
     a.B = batch;
     a.T = horizon;
     a.block_mode = 1;
     a.plan = auto_plan(batch, horizon, chunk0, chunk);
-    carve_lqr_tree(c, a, nx);
+    carve_lqr_tree(c, a, nx, nu);
   }
   return (int64_t)c.off + 256;
 }
@@ -343,7 +351,7 @@ int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, in
     a.dU = (Rt*)du;
     a.flags = flags;
     Carver c{(char*)workspace};
-    carve_lqr_tree(c, a, nx);
+    carve_lqr_tree(c, a, nx, nu);
     if ((int64_t)c.off > workspace_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
     it->second.block(&a, phase, blocks_in, block_out, rank, world, st);
     PTC_CUDA(cudaGetLastError());
@@ -548,7 +556,7 @@ struct Solver final : ptc_solver {
     l.gam = c.template take<R>(nu * T * B);
     l.dX = c.template take<R>(nx * (T + 1) * B);
     l.dU = c.template take<R>(nu * T * B);
-    carve_lqr_tree(c, l, (int)nx);
+    carve_lqr_tree(c, l, (int)nx, (int)nu);
     a.red = l.red;
     if (self) {
       self->hp = pp;

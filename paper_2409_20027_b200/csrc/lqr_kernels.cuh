@@ -47,6 +47,12 @@ struct LqrArgs {
   const R* vcarry_in;
   const R* x_in;
   R* vcin_buf;             // workspace for vcarry_in   (nx*nx + nx, 1, B)
+  // stage-major staging (wide kernels, batch 1, see wide.cuh): expansion
+  // [t][P R M d Fx Fu] and gains [t][Gamma gamma]; `staged` = the launcher
+  // has filled xst for this solve
+  R* xst;
+  R* gst;
+  int staged;
   R* xin_buf;              // workspace for x_in        (nx, 1, B)
   // tree scratch, index l = 1..L, item rows n[l]
   R* vagg[kMaxLevels + 1];

@@ -48,11 +48,80 @@ constexpr MMPlan mm_plan(int M, int N) {
   return best;
 }
 
+// FP64 tensor-core product on 8x8x4 DMMA tiles (mma.sync m8n8k4 .f64):
+// the warp's operands are gathered from the slab straight into fragments
+// (zero padding to multiples of 8 / 4), accumulated in registers, and
+// scattered back -- for nx = 12 a 12x12x12 product is 12 DMMA instructions
+// and 24 shared loads per lane instead of ~72 DFMA + ~60 loads.  FP64 MMA
+// peak equals the FP64 vector peak on B200; the win is issue and
+// shared-memory traffic, which bound these latency-limited kernels.
+// Fragment layouts (PTX ISA, mma.m8n8k4 .f64): a: A[l/4][l%4], b: B[l%4][l/4],
+// c/d: C[l/4][2 (l%4) + {0, 1}].
+PTC_D void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int M, int K, int N, bool TA, bool TB, int MODE>
+PTC_D void w_mm_dmma(const double* A, const double* B, double* C) {
+  constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8, KB = (K + 3) / 4;
+  const int ln = lane_id();
+  const int fr = ln >> 2, fc = ln & 3;
+  double acc[MB][NB][2];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+#pragma unroll
+  for (int kb = 0; kb < KB; ++kb) {
+    const int k = kb * 4 + fc;
+    double af[MB], bf[NB];
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+      const int i = mb * 8 + fr;
+      af[mb] = (i < M && k < K) ? (TA ? A[k * M + i] : A[i * K + k]) : 0.0;
+    }
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int j = nb * 8 + fr;
+      bf[nb] = (j < N && k < K) ? (TB ? B[j * K + k] : B[k * N + j]) : 0.0;
+    }
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma_8x8x4(acc[mb][nb], af[mb], bf[nb]);
+  }
+  __syncwarp();  // every lane has read its operands before C is written
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
+        if (i < M && j < N) {
+          double& c = C[i * N + j];
+          if (MODE == 0) c = acc[mb][nb][e];
+          else if (MODE > 0) c += acc[mb][nb][e];
+          else c -= acc[mb][nb][e];
+        }
+      }
+  __syncwarp();
+}
+
 // C (MxN) = op(A) op(B); A stored row-major as (TA ? KxM : MxK), B as
 // (TB ? NxK : KxN).  MODE 0: C = AB, 1: C += AB, -1: C -= AB.  C must not
-// alias A or B.
+// alias A or B.  FP64 products with at least 48 outputs go to the tensor
+// cores (w_mm_dmma); the rest are register-blocked lane products.
 template <int M, int K, int N, bool TA, bool TB, int MODE, typename R>
 PTC_D void w_mm(const R* A, const R* B, R* C) {
+  if constexpr (sizeof(R) == 8 && M * N >= 48 && M >= 4 && N >= 4) {
+    w_mm_dmma<M, K, N, TA, TB, MODE>(reinterpret_cast<const double*>(A),
+                                     reinterpret_cast<const double*>(B),
+                                     reinterpret_cast<double*>(C));
+    return;
+  }
   constexpr MMPlan pl = mm_plan(M, N);
   constexpr int BI = pl.bi, BJ = pl.bj, NBJ = N / BJ, NB = (M / BI) * NBJ;
   for (int blk = lane_id(); blk < NB; blk += 32) {
@@ -346,6 +415,84 @@ PTC_D void w_stage_store(const StagePrefetch<R, NX, NU>& pf, R alpha, R* st) {
   pf.store(st);
   for (int i = lane_id(); i < NU; i += 32) st[S::sR + i * NU + i] += alpha;
   __syncwarp();
+}
+
+// Contiguous-row prefetch (staged mode): row t of a stage-major array is N
+// consecutive words, so the warp's loads are fully coalesced.
+template <typename R, int N>
+struct WPrefetchRow {
+  static constexpr int PER = (N + 31) / 32;
+  const R* base;
+  size_t stride;
+  R v[PER];
+  PTC_D void init(const R* b, size_t st) {
+    base = b;
+    stride = st;
+  }
+  PTC_D void load(int t) {
+    const R* p = base + (size_t)t * stride;
+    const int ln = lane_id();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) v[k] = (ln + 32 * k < N) ? p[ln + 32 * k] : R(0);
+  }
+  PTC_D void store(R* dst) const {
+    const int ln = lane_id();
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (ln + 32 * k < N) dst[ln + 32 * k] = v[k];
+    __syncwarp();
+  }
+};
+
+// component c of the stage tuple [P R M d Fx Fu] at stage t (batch 1)
+template <typename R, int NX, int NU>
+PTC_D R stage_comp(const LqrArgs<R>& a, int c, int t) {
+  using S = WSlab<R, NX, NU>;
+  const size_t T = a.T;
+  if (c < S::sR) return a.P[c * T + t];
+  if (c < S::sM) return a.Rm[(c - S::sR) * T + t];
+  if (c < S::sd) return a.M[(c - S::sM) * T + t];
+  if (c < S::sFx) return a.d[(c - S::sd) * T + t];
+  if (c < S::sFu) return a.Fx[(c - S::sFx) * T + t];
+  return a.Fu[(c - S::sFu) * T + t];
+}
+
+// expansion (component-major, batch 1) -> xst (stage-major): 32 x 32 tiles
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(256) kw_stage_in(LqrArgs<R> a) {
+  constexpr int SC = WSlab<R, NX, NU>::SC;
+  __shared__ R tile[32][33];
+  const int c0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, t = t0 + threadIdx.x;
+    tile[i][threadIdx.x] = (c < SC && t < a.T) ? stage_comp<R, NX, NU>(a, c, t) : R(0);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int t = t0 + i, c = c0 + threadIdx.x;
+    if (c < SC && t < a.T) a.xst[(size_t)t * SC + c] = tile[threadIdx.x][i];
+  }
+}
+
+// gst (stage-major [Gamma | gamma]) -> Gamma, gamma (component-major, batch 1)
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(256) kw_gains_out(LqrArgs<R> a) {
+  constexpr int GC = NU * NX + NU;
+  __shared__ R tile[32][33];
+  const int c0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int t = t0 + i, c = c0 + threadIdx.x;
+    tile[threadIdx.x][i] = (c < GC && t < a.T) ? a.gst[(size_t)t * GC + c] : R(0);
+  }
+  __syncthreads();
+  const size_t T = a.T;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, t = t0 + threadIdx.x;
+    if (c < GC && t < a.T) {
+      if (c < NU * NX) a.Gam[c * T + t] = tile[i][threadIdx.x];
+      else a.gam[(c - NU * NX) * T + t] = tile[i][threadIdx.x];
+    }
+  }
 }
 
 // --------------------------------------------------------- element algebra
@@ -727,16 +874,10 @@ PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
   }
   __syncwarp();
   // S' = sym(P + Fx^T SF + Qux^T Gam), eta' = Fx^T eta - Qux^T gam
-  for (int q = ln; q < NX * NX; q += 32) {
-    const int i = q / NX, j = q - (q / NX) * NX;
-    R s = R(0);
-#pragma unroll
-    for (int k = 0; k < NX; ++k) s = (k == 0) ? st[S::sFx + i] * SF[j] : fma(st[S::sFx + k * NX + i], SF[k * NX + j], s);
-    R g = R(0);
-#pragma unroll
-    for (int k = 0; k < NU; ++k) g = (k == 0) ? Qux[i] * Gam[j] : fma(Qux[k * NX + i], Gam[k * NX + j], g);
-    o[q] = s + (st[S::sP + q] + g);
-  }
+  w_mm<NX, NX, NX, true, false, 0>(st + S::sFx, SF, o);
+  w_mm<NX, NU, NX, true, false, 1>(Qux, Gam, o);
+  for (int q = ln; q < NX * NX; q += 32) o[q] += st[S::sP + q];
+  __syncwarp();
   for (int i = ln; i < NX; i += 32) {
     R s = R(0);
 #pragma unroll
@@ -817,14 +958,28 @@ __global__ void __launch_bounds__(128) kw_value_up0(LqrArgs<R> a) {
     if (!w_velem<R, NX, NU>(st, acc, scr)) fl |= FLAG_DEF_R;
     start = t1 - 2;
   }
-  StagePrefetch<R, NX, NU> pf;
-  w_stage_prefetch_init<R, NX, NU>(pf, a, b);
-  if (start >= t0) pf.load(start);
-  for (int t = start; t >= t0; --t) {
-    w_stage_store<R, NX, NU>(pf, alpha, st);
-    if (t > t0) pf.load(t - 1);
-    fl |= w_vcombine_stage<R, NX, NU>(st, acc, o, scr, piv);
-    w_copy<S::VC>(o, acc);
+  if (a.staged) {
+    WPrefetchRow<R, S::SC> pf;
+    pf.init(a.xst, S::SC);
+    if (start >= t0) pf.load(start);
+    for (int t = start; t >= t0; --t) {
+      pf.store(st);
+      for (int i = lane_id(); i < NU; i += 32) st[S::sR + i * NU + i] += alpha;
+      __syncwarp();
+      if (t > t0) pf.load(t - 1);
+      fl |= w_vcombine_stage<R, NX, NU>(st, acc, o, scr, piv);
+      w_copy<S::VC>(o, acc);
+    }
+  } else {
+    StagePrefetch<R, NX, NU> pf;
+    w_stage_prefetch_init<R, NX, NU>(pf, a, b);
+    if (start >= t0) pf.load(start);
+    for (int t = start; t >= t0; --t) {
+      w_stage_store<R, NX, NU>(pf, alpha, st);
+      if (t > t0) pf.load(t - 1);
+      fl |= w_vcombine_stage<R, NX, NU>(st, acc, o, scr, piv);
+      w_copy<S::VC>(o, acc);
+    }
   }
   w_st<S::VC>(a.vagg[1], j, a.plan.n[1], a.B, b, acc);
   if (fl && lane_id() == 0) atomicOr(a.flags + b, fl);
@@ -928,15 +1083,33 @@ __global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
     w_fill<NX>(pa + NX * NX, R(0));
   }
   int fl = 0;
+  constexpr int GC = NU * NX + NU;
   StagePrefetch<R, NX, NU> pf;
-  w_stage_prefetch_init<R, NX, NU>(pf, a, b);
-  if (t1 - 1 >= t0) pf.load(t1 - 1);
+  WPrefetchRow<R, S::SC> pfr;
+  if (a.staged) {
+    pfr.init(a.xst, S::SC);
+    if (t1 - 1 >= t0) pfr.load(t1 - 1);
+  } else {
+    w_stage_prefetch_init<R, NX, NU>(pf, a, b);
+    if (t1 - 1 >= t0) pf.load(t1 - 1);
+  }
   for (int t = t1 - 1; t >= t0; --t) {
-    w_stage_store<R, NX, NU>(pf, alpha, st);
-    if (t > t0) pf.load(t - 1);
+    if (a.staged) {
+      pfr.store(st);
+      for (int i = lane_id(); i < NU; i += 32) st[S::sR + i * NU + i] += alpha;
+      __syncwarp();
+      if (t > t0) pfr.load(t - 1);
+    } else {
+      w_stage_store<R, NX, NU>(pf, alpha, st);
+      if (t > t0) pf.load(t - 1);
+    }
     fl |= w_riccati<R, NX, NU>(st, c, o, Gam, gam, scr);
-    w_st<NU * NX>(a.Gam, t, T, B, b, Gam);
-    w_st<NU>(a.gam, t, T, B, b, gam);
+    if (a.staged) {  // [Gamma | gamma] contiguous in the slab and in gst
+      for (int i = lane_id(); i < GC; i += 32) a.gst[(size_t)t * GC + i] = Gam[i];
+    } else {
+      w_st<NU * NX>(a.Gam, t, T, B, b, Gam);
+      w_st<NU>(a.gam, t, T, B, b, gam);
+    }
     if constexpr (kAgg) {
       w_closed_loop<R, NX, NU>(st + S::sFx, st + S::sFu, Gam, gam, t + a.t_base == 0, m);
       w_aff_compose<R, NX>(pa, m, pt);
@@ -1055,12 +1228,37 @@ __global__ void __launch_bounds__(128) kw_prop_down0(LqrArgs<R> a) {
   double s2 = 0.0, sd = 0.0, mx = 0.0;  // accumulated by lane 0
   const int ln = lane_id();
   WPrefetch<R, NX * NX, NX * NU, NU * NX, NU, NU> pf;
-  pf.init(a.Fx, a.Fu, a.Gam, a.gam, a.d, nullptr, T, B, b);
-  if (t0 < t1) pf.load(t0);
+  WPrefetchRow<R, NX * NX + NX * NU> pfa;   // staged: [Fx | Fu] of xst
+  WPrefetchRow<R, NU * NX + NU> pfb;        //         [Gamma | gamma] of gst
+  WPrefetchRow<R, NU> pfc;                  //         d of xst
+  if (a.staged) {
+    pfa.init(a.xst + S::sFx, S::SC);
+    pfb.init(a.gst, NU * NX + NU);
+    pfc.init(a.xst + S::sd, S::SC);
+    if (t0 < t1) {
+      pfa.load(t0);
+      pfb.load(t0);
+      pfc.load(t0);
+    }
+  } else {
+    pf.init(a.Fx, a.Fu, a.Gam, a.gam, a.d, nullptr, T, B, b);
+    if (t0 < t1) pf.load(t0);
+  }
   for (int t = t0; t < t1; ++t) {
     w_st<NX>(a.dX, t, T + 1, B, b, x);
-    pf.store(Fx);
-    if (t + 1 < t1) pf.load(t + 1);
+    if (a.staged) {
+      pfa.store(Fx);
+      pfb.store(Gam);
+      pfc.store(dd);
+      if (t + 1 < t1) {
+        pfa.load(t + 1);
+        pfb.load(t + 1);
+        pfc.load(t + 1);
+      }
+    } else {
+      pf.store(Fx);
+      if (t + 1 < t1) pf.load(t + 1);
+    }
     w_mv<NU, NX, false, 0>(Gam, x, du);
     for (int i = ln; i < NU; i += 32) du[i] += gam[i];
     __syncwarp();
@@ -1236,10 +1434,25 @@ void launch_value_tree_wide(const LqrArgs<R>& a, cudaStream_t s) {
 }
 
 template <typename R, int NX, int NU>
-void launch_lqr_wide(const LqrArgs<R>& a, cudaStream_t s) {
+void launch_stage_in(const LqrArgs<R>& a, cudaStream_t s) {
+  constexpr int SC = WSlab<R, NX, NU>::SC;
+  kw_stage_in<R, NX, NU><<<dim3((SC + 31) / 32, (a.T + 31) / 32), dim3(32, 8), 0, s>>>(a);
+}
+
+template <typename R, int NX, int NU>
+void launch_gains_out(const LqrArgs<R>& a, cudaStream_t s) {
+  constexpr int GC = NU * NX + NU;
+  kw_gains_out<R, NX, NU><<<dim3((GC + 31) / 32, (a.T + 31) / 32), dim3(32, 8), 0, s>>>(a);
+}
+
+template <typename R, int NX, int NU>
+void launch_lqr_wide(const LqrArgs<R>& a0, cudaStream_t s) {
   using W = Wide<R, NX, NU>;
   using S = WSlab<R, NX, NU>;
   W::setup();
+  LqrArgs<R> a = a0;
+  a.staged = (a.xst != nullptr && a.B == 1) ? 1 : 0;
+  if (a.staged) launch_stage_in<R, NX, NU>(a, s);
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (pl.L >= 1) {
@@ -1252,6 +1465,7 @@ void launch_lqr_wide(const LqrArgs<R>& a, cudaStream_t s) {
     PTC_WL((kw_value_down0<R, NX, NU, false>), P0 * B, S::kDown0)(a);
   }
   PTC_WL((kw_prop_down0<R, NX, NU>), P0 * B, S::kPropDown0)(a);
+  if (a.staged) launch_gains_out<R, NX, NU>(a, s);
 }
 
 template <typename R, int NX, int NU>
@@ -1275,9 +1489,11 @@ void launch_lqr_block_wide(const LqrArgs<R>& a0, int phase, const void* blocks, 
   using S = WSlab<R, NX, NU>;
   W::setup();
   LqrArgs<R> a = a0;
+  a.staged = (a.xst != nullptr && a.B == 1) ? 1 : 0;
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (phase == 0) {
+    if (a.staged) launch_stage_in<R, NX, NU>(a, s);
     PTC_WL((kw_value_up0<R, NX, NU>), P0 * B, S::kUp0)(a);
     for (int l = 1; l < pl.L; ++l) PTC_WL((kw_value_up<R, NX, NU>), pl.n[l + 1] * B, S::kUp)(a, l);
     PTC_WL((kw_value_block<R, NX, NU>), B, S::kUp)(a, static_cast<R*>(out));
@@ -1296,6 +1512,7 @@ void launch_lqr_block_wide(const LqrArgs<R>& a0, int phase, const void* blocks, 
       for (int l = pl.L - 1; l >= 1; --l) PTC_WL((kw_prop_down<R, NX, NU>), pl.n[l + 1] * B, S::kProp)(a, l);
     }
     PTC_WL((kw_prop_down0<R, NX, NU>), P0 * B, S::kPropDown0)(a);
+    if (a.staged) launch_gains_out<R, NX, NU>(a, s);
   }
 }
 

@@ -247,3 +247,38 @@ def test_batch_solver_concurrent_matches_single_and_oracle():
     got = conc[0].round_iters[:, 0].cpu().numpy()[:len(ref.newton)]
     assert list(got) == [r.iterations for r in ref.newton]
     assert rel_gap(conc[0].controls[0].cpu().numpy(), ref.us) < 1e-9
+
+
+@pytest.mark.parametrize("nx,nu,T", [(8, 4, 1500), (12, 4, 2048), (12, 6, 1100)])
+def test_wide_staged_long_horizon_matches_oracle(nx, nu, T):
+    """Batch-1 wide problems with T >= 1024 run the stage-major staged path
+    (transposed expansion, stage-major gains); also through two emulated
+    time blocks of >= 1024 stages."""
+    import torch
+    from paper_2409_20027_b200.sharded import CudaBlockOps, block_bounds, emulate_ranks
+    e = O.random_lqr_expansion(np.random.default_rng([nx, nu, T]), T, nx, nu, alpha=0.2)
+    ref = O.lqr_solve(e)
+    for plan in ((0, 0), (8, 8), (T, 0)):
+        out = _solve(e, plan)
+        assert out[6] == 0
+        for k in range(6):
+            assert rel_gap(out[k], ref[k]) < 1e-9, (plan, k)
+    soa = lambda a, c: torch.as_tensor(np.asarray(a, float)).reshape(a.shape[0], c).t() \
+        .contiguous().unsqueeze(-1).cuda()
+    full = dict(P=soa(e.P, nx * nx), R=soa(e.R, nu * nu), M=soa(e.M, nx * nu), d=soa(e.d, nu),
+                Fx=soa(e.Fx, nx * nx), Fu=soa(e.Fu, nx * nu))
+    PT = soa(e.PT[None], nx * nx)
+    alpha = torch.full((1,), 0.2, dtype=torch.float64, device="cuda")
+    world = 2 if T >= 2048 else 1
+    ops = []
+    for r in range(world):
+        t0, m = block_bounds(T, world, r)
+        loc = {k: v[:, t0:t0 + m].contiguous() for k, v in full.items()}
+        ops.append(CudaBlockOps(r, world, t0, loc["P"], loc["R"], loc["M"], loc["d"], loc["Fx"],
+                                loc["Fu"], PT, alpha, nx, nu))
+    emulate_ranks(ops)
+    torch.cuda.synchronize()
+    host = lambda t: t[..., 0].t().cpu().numpy()
+    G = np.concatenate([host(o.Gamma) for o in ops]).reshape(T, nu, nx)
+    du = np.concatenate([host(o.du) for o in ops])
+    assert rel_gap(G, ref[2]) < 1e-9 and rel_gap(du, ref[5]) < 1e-9
