@@ -41,12 +41,15 @@ static int fail(int code, const std::string& msg) {
 // per problem sweeps its horizon (no tree, work optimal).  Small batches
 // split the horizon into chunks of K0 stages so that ~32K threads are busy,
 // with an 8-ary tree above them (log-depth in the horizon).
-static Plan auto_plan(int B, int T, int K0, int K) {
+static Plan auto_plan(int B, int T, int K0, int K, int nx = 0) {
   if (K <= 0) K = 8;
   if (K0 <= 0) {
     const long long work = (long long)B * T;
+    // thread-per-unit kernels want ~32K units; the warp-per-unit kernels of
+    // nx >= 8 (wide.cuh) ~8K warps, i.e. longer level-0 chunks
+    const long long units = nx >= 8 ? 8192 : 32768;
     if (B >= 8192) K0 = T;
-    else K0 = (int)std::max<long long>(4, (work + 32767) / 32768);
+    else K0 = (int)std::max<long long>(4, (work + units - 1) / units);
   }
   return make_plan(T, K0, K);
 }
@@ -125,13 +128,13 @@ int64_t ptc_lqr_workspace_bytes(int dtype, int batch, int horizon, int nx, int n
     LqrArgs<double> a{};
     a.B = batch;
     a.T = horizon;
-    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
     carve_lqr_tree(c, a, nx, nu);
   } else {
     LqrArgs<float> a{};
     a.B = batch;
     a.T = horizon;
-    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
     carve_lqr_tree(c, a, nx, nu);
   }
   return (int64_t)c.off + 256;
@@ -198,7 +201,7 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
   std::memset(&a, 0, sizeof(a));  // padding too: the graph cache keys on the bytes
   a.B = batch;
   a.T = horizon;
-  a.plan = auto_plan(batch, horizon, chunk0, chunk);
+  a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
   a.P = (const R*)P;
   a.Rm = (const R*)Rm;
   a.M = (const R*)M;
@@ -244,7 +247,7 @@ static int propagate_t(int batch, int horizon, int nx, int nu, const void* Fx, c
   LqrArgs<R> a{};
   a.B = batch;
   a.T = horizon;
-  a.plan = auto_plan(batch, horizon, chunk0, chunk);
+  a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
   a.Fx = (const R*)Fx;
   a.Fu = (const R*)Fu;
   a.d = (const R*)d;
@@ -293,14 +296,14 @@ int64_t ptc_lqr_block_workspace_bytes(int dtype, int batch, int horizon, int nx,
     a.B = batch;
     a.T = horizon;
     a.block_mode = 1;
-    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
     carve_lqr_tree(c, a, nx, nu);
   } else {
     LqrArgs<float> a{};
     a.B = batch;
     a.T = horizon;
     a.block_mode = 1;
-    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
     carve_lqr_tree(c, a, nx, nu);
   }
   return (int64_t)c.off + 256;
@@ -331,7 +334,7 @@ int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, in
     LqrArgs<Rt> a{};
     a.B = batch;
     a.T = horizon;
-    a.plan = auto_plan(batch, horizon, chunk0, chunk);
+    a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
     a.block_mode = 1;
     a.t_base = t_base;
     a.no_terminal = is_last ? 0 : 1;
@@ -489,7 +492,7 @@ struct Solver final : ptc_solver {
     LqrArgs<R> l{};
     a.B = l.B = (int)B;
     a.T = l.T = (int)T;
-    a.plan = l.plan = auto_plan((int)B, (int)T, d.chunk0, d.chunk);
+    a.plan = l.plan = auto_plan((int)B, (int)T, d.chunk0, d.chunk, (int)nx);
     const size_t P0 = a.plan.units0();
     ProblemParams* dpp = c.template take<ProblemParams>(1);
     R *linA = nullptr, *linB = nullptr, *linc = nullptr;
