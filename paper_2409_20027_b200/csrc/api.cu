@@ -222,6 +222,7 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
   carve_lqr_tree(c, a, nx, nu);
   if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
   if ((S == nullptr) != (s == nullptr)) return fail(PTC_ERR_ARG, "S and s must both be given or both NULL");
+  a.red = nullptr;  // trust-region partial sums are a Newton-loop product only
   if (a.plan.L >= 1 && !getenv("PTC_NO_GRAPH")) {
     // a tree plan is 4L+4 short launches: replay them as one CUDA graph,
     // cached per argument set (same buffers -> same graph)

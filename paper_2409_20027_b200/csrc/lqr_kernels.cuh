@@ -362,7 +362,7 @@ PTC_D void ld_prop_stage(const LqrArgs<R>& a, int t, int b, PropStage<R, NX, NU>
   ld_vec(a.gam, t, a.T, a.B, b, p.gam);
   ld_mat(a.Fx, t, a.T, a.B, b, p.Fx);
   ld_mat(a.Fu, t, a.T, a.B, b, p.Fu);
-  if (a.d) ld_vec(a.d, t, a.T, a.B, b, p.dd);
+  if (a.d && a.red) ld_vec(a.d, t, a.T, a.B, b, p.dd);  // d only feeds the partial sums
   else set_zero(p.dd);
 }
 

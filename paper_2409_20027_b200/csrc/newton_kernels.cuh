@@ -436,10 +436,26 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
     R x[NX], u[NU];
     ld_x(a, q, t, b, x);
     ld_u(a, q, t, b, u);
-    Stage<R, NX, NU> st;
     R lt[NX];
-    stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
-    if constexpr (kExp) {
+    if constexpr (!kExp) {
+      // co-states only: first derivatives suffice (bitwise the same lambda
+      // as stage_expansion computes)
+      DynDerivs<R, NX, NU> D;
+      Dyn::template derivs<false>(p, t, b, x, u, ln, D);
+      R cx[NX], cu[NU], cxx[NX], cuu[NU];
+      aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
+      R fxl[NX];
+      mtv<NX, NX>(D.fx, ln, fxl);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) {
+        R lx = R(0);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+        lt[i] = (lx + cx[i]) + fxl[i];
+      }
+    } else {
+      Stage<R, NX, NU> st;
+      stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
       st_mat(a.P, t, T, B, b, st.P);
       st_mat(a.Rm, t, T, B, b, st.Rr);
       st_mat(a.M, t, T, B, b, st.M);

@@ -968,7 +968,9 @@ __global__ void __launch_bounds__(128) kw_value_up0(LqrArgs<R> a) {
       __syncwarp();
       if (t > t0) pf.load(t - 1);
       fl |= w_vcombine_stage<R, NX, NU>(st, acc, o, scr, piv);
-      w_copy<S::VC>(o, acc);
+      R* tmp = acc;  // ping-pong instead of copying the aggregate back
+      acc = o;
+      o = tmp;
     }
   } else {
     StagePrefetch<R, NX, NU> pf;
@@ -978,7 +980,9 @@ __global__ void __launch_bounds__(128) kw_value_up0(LqrArgs<R> a) {
       w_stage_store<R, NX, NU>(pf, alpha, st);
       if (t > t0) pf.load(t - 1);
       fl |= w_vcombine_stage<R, NX, NU>(st, acc, o, scr, piv);
-      w_copy<S::VC>(o, acc);
+      R* tmp = acc;
+      acc = o;
+      o = tmp;
     }
   }
   w_st<S::VC>(a.vagg[1], j, a.plan.n[1], a.B, b, acc);
@@ -1113,9 +1117,15 @@ __global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
     if constexpr (kAgg) {
       w_closed_loop<R, NX, NU>(st + S::sFx, st + S::sFu, Gam, gam, t + a.t_base == 0, m);
       w_aff_compose<R, NX>(pa, m, pt);
-      w_copy<S::CC>(pt, pa);
+      R* tp = pa;  // ping-pong
+      pa = pt;
+      pt = tp;
     }
-    w_copy<S::CC>(o, c);
+    {
+      R* tc = c;
+      c = o;
+      o = tc;
+    }
     if (a.S) {
       w_st<NX * NX>(a.S, t, T + 1, B, b, c);
       for (int i = lane_id(); i < NX; i += 32) o[i] = -c[NX * NX + i];
