@@ -148,6 +148,16 @@ __global__ void k_init_state(NewtonArgs<R> a) {
   a.cur_cost[b] = 0.0;
   a.cand_cost[b] = 0.0;
   a.mu[b] = a.opt.mu0;
+  // outer-round records of rounds that never run read as zero
+  for (int r = 0; r < a.opt.round_cap; ++r) {
+    const size_t o = (size_t)r * a.B + b;
+    a.round_iters[o] = 0;
+    a.round_term[o] = TERM_NONE;
+    a.round_mu[o] = 0.0;
+    a.round_cost[o] = 0.0;
+    a.round_rp[o] = 0.0;
+    a.round_rd[o] = 0.0;
+  }
   if (a.opt.method == METHOD_BARRIER && !(a.opt.mu0 > a.opt.mu_tol)) a.status[b] = ST_DONE;
 }
 
