@@ -1,0 +1,103 @@
+"""The experiment harness on the device solver, judged by the reference's
+own acceptance criteria (reference pkg/tests/test_acceptance.py, SPEC.md
+acceptance 5-7) and harness tests (test_bench.py):
+
+* run_benchmark: one row per (horizon, rep), converged and re-validated
+  (criterion 5: pendulum barrier swing-up, |tau| <= 5);
+* seeded determinism of iteration counts;
+* run_mpc: 4 s at 100 Hz, N = 60, both systems stabilise within the
+  reference's tolerances with the control bound respected at every step
+  (criterion 7);
+* run_mpc_batch: B closed loops in lockstep equal B single loops.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_benchmark_rows_converge_and_respect_bounds(tmp_path):
+    import paper_2409_20027_b200 as P
+    cfg = P.RunConfig(system="pendulum", solver="barrier", horizons=(20, 40), repetitions=2,
+                      out=str(tmp_path / "bench.csv"))
+    recs = P.run_benchmark(cfg)
+    assert len(recs) == 4
+    assert all(r.converged for r in recs), recs
+    back = P.read_benchmark_csv(tmp_path / "bench.csv")
+    assert back == recs
+    paths = P.emit_plotdata(recs, tmp_path / "plot")
+    assert paths[0].exists()
+
+
+def test_benchmark_deterministic_iteration_counts():
+    import paper_2409_20027_b200 as P
+    cfg = P.RunConfig(system="pendulum", solver="barrier", horizons=(20,), repetitions=1, seed=3)
+    a, b = P.run_benchmark(cfg), P.run_benchmark(cfg)
+    assert [(r.outer_iters, r.inner_iters) for r in a] == [(r.outer_iters, r.inner_iters)
+                                                            for r in b]
+
+
+@pytest.mark.parametrize("system,bound,tol_pos", [("pendulum", 5.0, None),
+                                                  ("cartpole", 60.0, 0.1)])
+def test_mpc_closed_loop_stabilises(system, bound, tol_pos):
+    """Reference acceptance criterion 7 (SPEC.md: 4 s at 100 Hz, N = 60;
+    final angle within 0.05 rad and rate within 0.05 rad/s of upright, cart
+    within 0.1 m of the target, controls within the box at every step)."""
+    import paper_2409_20027_b200 as P
+    log = P.run_mpc(P.RunConfig(system=system, solver="barrier"))
+    assert log.steps == 400
+    assert np.all(np.abs(log.controls) <= bound + 1e-9)
+    final = log.states[-1]
+    if system == "pendulum":
+        assert abs(final[0]) < 0.05 and abs(final[1]) < 0.05, final
+    else:
+        assert abs(final[1] - math.pi) < 0.05 and abs(final[3]) < 0.05, final
+        assert abs(final[0] - 0.0) < tol_pos, final
+
+
+def test_mpc_batch_equals_single_loops():
+    import paper_2409_20027_b200 as P
+    cfg = P.RunConfig(system="pendulum", solver="barrier", sim_time=0.3)
+    starts = np.array([[math.pi, 0.0], [math.pi - 0.2, 0.1], [2.5, -0.3]])
+    logs = P.run_mpc_batch(cfg, starts)
+    for b, x0 in enumerate(starts):
+        single = P.run_mpc_batch(cfg, x0[None])[0]
+        assert np.allclose(single.controls, logs[b].controls, rtol=0, atol=1e-12)
+        assert np.allclose(single.states, logs[b].states, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("horizon", [20, 100, 500])
+def test_criterion_5_pendulum_barrier_swingup(horizon):
+    """Reference acceptance criterion 5: the barrier solve of the pendulum
+    swing-up converges (every round's Newton solve) with |tau| <= 5."""
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200.harness import draw_initial_controls
+    cfg = P.RunConfig(system="pendulum", solver="barrier", seed=0, horizons=(horizon,),
+                      total_time=2.0)
+    problem = cfg.build_problem(horizon, cfg.step_size(horizon))
+    controls = draw_initial_controls(problem, cfg, horizon, 0)
+    init = P.rollout(problem.dynamics, P.swingup_start("pendulum"), controls)
+    traj, report = P.barrier_solve(problem, init, cfg.barrier_options())
+    assert report.converged, [r.newton.termination for r in report.rounds]
+    assert np.abs(traj.controls).max() <= 5.0
+
+
+@pytest.mark.parametrize("system,rho", [("pendulum", 1.0), ("cartpole", 0.5)])
+def test_criterion_6_admm_termination(system, rho):
+    """Reference acceptance criterion 6: ADMM reaches both residuals <= 1e-2
+    and the returned controls violate the box by at most 1e-2."""
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200.harness import draw_initial_controls
+    n = 40
+    cfg = P.RunConfig(system=system, solver="admm", seed=0, horizons=(n,), total_time=2.0,
+                      rho=rho)
+    problem = cfg.build_problem(n, cfg.step_size(n))
+    controls = draw_initial_controls(problem, cfg, n, 0)
+    init = P.rollout(problem.dynamics, P.swingup_start(system), controls)
+    traj, report = P.admm_solve(problem, init, cfg.admm_options())
+    assert report.converged
+    assert report.state.primal_residual <= 1e-2 and report.state.dual_residual <= 1e-2
+    assert problem.constraints.max_violation(traj) <= 1e-2
