@@ -418,6 +418,37 @@ def case_admm_cartpole_cfg2_nudge():
     save("admm_cartpole_cfg2_nudge", iters=np.array(rows))
 
 
+def case_criterion5_pendulum():
+    """Reference acceptance criterion 5 setup (harness draw, N = 20/100/500):
+    the reference's per-round iteration counts and terminations (N = 500
+    does not converge in its first round), their stability under one-ulp
+    control nudges, and the final controls."""
+    from pintoc.bench import RunConfig, draw_initial_controls
+    from pintoc import swingup_start
+    out = {}
+    for n in (20, 100, 500):
+        cfg = RunConfig(system="pendulum", solver="barrier", seed=0, horizons=(n,),
+                        total_time=2.0)
+        problem = cfg.build_problem(n, cfg.step_size(n))
+        u0 = draw_initial_controls(problem, cfg, n, 0)
+        x0 = swingup_start("pendulum")
+
+        def solve(xp, up):
+            traj, rep = barrier_solve(problem, rollout(problem.dynamics, xp, up),
+                                      cfg.barrier_options())
+            return traj, [r.newton.iterations for r in rep.rounds]
+
+        traj, rep = barrier_solve(problem, rollout(problem.dynamics, x0, u0),
+                                  cfg.barrier_options())
+        counts = [r.newton.iterations for r in rep.rounds]
+        out[f"n{n}_u0"] = u0
+        out[f"n{n}_iters"] = np.array(counts)
+        out[f"n{n}_terms"] = np.array([r.newton.termination for r in rep.rounds])
+        out[f"n{n}_us"] = traj.controls
+        out.update({f"n{n}_{k}": v for k, v in noise_floor(solve, x0, u0, traj, counts).items()})
+    save("criterion5_pendulum", **out)
+
+
 FAST = [case_lqr_small, case_lqr_config1, case_passes_models, case_newton_lq,
         case_barrier_pendulum_cfg0, case_barrier_pendulum_conv, case_barrier_tvlinear, case_admm_small]
 
@@ -426,7 +457,8 @@ if __name__ == "__main__":
     ap.add_argument("--slow", action="store_true")
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
-    cases = FAST + ([case_admm_cartpole_cfg2, case_admm_cartpole_cfg2_nudge] if args.slow else [])
+    cases = FAST + ([case_admm_cartpole_cfg2, case_admm_cartpole_cfg2_nudge,
+                     case_criterion5_pendulum] if args.slow else [])
     for fn in cases:
         if args.only and args.only not in fn.__name__:
             continue
