@@ -15,7 +15,7 @@
 
 namespace ptc {
 
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 2;
 
 PTC_D int lane_id() { return threadIdx.x & 31; }
 PTC_D int warp_unit() { return blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); }
@@ -1420,7 +1420,7 @@ struct Wide {
   }
 };
 
-#define PTC_WL(kernel, units, elems) kernel<<<W::grid(units), 128, W::smem(elems), s>>>
+#define PTC_WL(kernel, units, elems) kernel<<<W::grid(units), 32 * kWarpsPerBlock, W::smem(elems), s>>>
 
 template <typename R, int NX, int NU>
 void launch_prop_tree_wide(const LqrArgs<R>& a, cudaStream_t s) {
