@@ -473,6 +473,45 @@ def run_ours(args) -> None:
                                   "achieved_gbs": alg_bytes(halves["pendulum"][3], 2, 1)
                                   / (half_ms["pendulum"] * 1e-3) / 1e9}}
 
+    # the same workload in fp32 (configs 1 and 3 name both precisions): the
+    # expansions rounded to float, solved by the fp32 kernel sets
+    fp32 = None
+    if not args.no_fp32:
+        h32 = {}
+        for k, (solver, inputs, alpha, n, nx, nu) in halves.items():
+            h32[k] = (LqrSolver(n, T, nx, nu, dtype=torch.float32),
+                      [t.float() for t in inputs], alpha)
+        side32 = [torch.cuda.Stream() for _ in h32]
+
+        def step32():
+            for st in side32:
+                st.wait_stream(stream)
+            for (sol, ins, al), st in zip(h32.values(), side32):
+                with torch.cuda.stream(st):
+                    sol.solve(*ins, al, stream=st)
+            for st in side32:
+                stream.wait_stream(st)
+
+        for _ in range(max(3, args.warmup)):
+            step32()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a32, b32 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a32.record(stream)
+        for _ in range(args.steps):
+            step32()
+        b32.record(stream)
+        torch.cuda.synchronize()
+        ms32 = torch.tensor([a32.elapsed_time(b32) / args.steps], dtype=torch.float64,
+                            device="cuda")
+        if world > 1:
+            dist.all_reduce(ms32, op=dist.ReduceOp.MAX)
+        flagged = sum(int((v[0].flags != 0).sum()) for v in h32.values())
+        fp32 = {"value": B_TOTAL / (float(ms32) * 1e-3), "unit": UNIT, "ms_per_step": float(ms32),
+                "dtype": "f32", "subproblems_flagged": flagged}
+        del h32
+
     # horizon sweep of the single-problem LQR-scan latency (config 1, nx=4)
     sweep = nsweep = None
     if rank == 0 and not args.no_sweep:
@@ -510,7 +549,7 @@ def run_ours(args) -> None:
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk, "ill_posed_subproblems": ill_posed,
             "lqr_latency_sweep": sweep, "newton_latency_sweep": nsweep,
-            "long_horizon": longh, "mpc_config3": mpc,
+            "long_horizon": longh, "mpc_config3": mpc, "fp32": fp32,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -768,6 +807,7 @@ def main() -> None:
     ap.add_argument("--no-newton-sweep", action="store_true")
     ap.add_argument("--no-long", action="store_true")
     ap.add_argument("--no-mpc", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -77,3 +77,54 @@ def test_solver_path_refuses_without_cuda():
     dyn = P.LinearDynamics(np.eye(2), np.ones((2, 1)), horizon=4)
     with pytest.raises(P.NativeUnavailable):
         P.rollout(dyn, np.zeros(2), np.zeros((4, 1)))
+
+
+def test_argument_errors_are_reported_without_touching_the_device():
+    """Invalid arguments come back as PTC_ERR_ARG / PTC_ERR_UNSUPPORTED with a
+    message, before any device work (so this runs on a GPU-less host)."""
+    from paper_2409_20027_b200 import _native
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    lib = _native.load_library()
+    F64 = _native.PTC_F64
+    null = [None] * 15          # P..PT, alpha, S..du, flags
+    # bad dims
+    rc = lib.ptc_lqr_solve(F64, 0, 10, 4, 2, *null, None, 0, 0, 0, None)
+    assert rc == -1 and b"bad dims" in lib.ptc_last_error()
+    # unsupported kernel set
+    rc = lib.ptc_lqr_solve(F64, 1, 10, 5, 5, *null, None, 0, 0, 0, None)
+    assert rc == -2 and b"not instantiated" in lib.ptc_last_error()
+    # unknown dtype
+    rc = lib.ptc_lqr_solve(7, 1, 10, 4, 2, *null, None, 0, 0, 0, None)
+    assert rc == -1
+    # time-block phases
+    vc, pc = ctypes.c_int(), ctypes.c_int()
+    assert lib.ptc_lqr_block_comps(12, ctypes.byref(vc), ctypes.byref(pc)) == 0
+    assert (vc.value, pc.value) == (3 * 144 + 24, 144 + 12)
+    args = [None] * 16 + [None, None, 0, 0, 0, None]
+    assert lib.ptc_lqr_block_solve(3, F64, 1, 10, 4, 2, 0, 1, 0, 1, *args) == -1   # phase
+    assert lib.ptc_lqr_block_solve(0, F64, 1, 10, 4, 2, 0, 1, 2, 2, *args) == -1   # rank
+    assert lib.ptc_lqr_block_solve(1, F64, 1, 10, 4, 2, 0, 0, 0, 2, *args) == -1   # blocks_in
+    assert lib.ptc_lqr_block_solve(0, F64, 1, 10, 4, 2, 0, 1, 0, 1, *args) == -1   # PT on last
+    assert lib.ptc_lqr_block_workspace_bytes(F64, 1, 1 << 12, 12, 4, 0, 0) > \
+        lib.ptc_lqr_workspace_bytes(F64, 1, 1 << 12, 12, 4, 0, 0)   # + stage-major staging
+
+
+def test_solver_descriptor_validation_without_gpu():
+    """ptc_solver_workspace_bytes sizes the solver from the descriptor alone
+    and rejects dimension / model combinations that are not compiled in."""
+    import numpy as np
+    from paper_2409_20027_b200 import _native
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    lib = _native.load_library()
+    d = _native.ProblemDesc()
+    d.dtype, d.batch, d.horizon, d.nx, d.nu = _native.PTC_F64, 4, 64, 2, 1
+    d.model = _native.DYN_PENDULUM
+    Q = np.eye(2)
+    R = np.eye(1)
+    d.Q, d.R, d.Qf = Q.ctypes.data, R.ctypes.data, Q.ctypes.data
+    d.max_iters, d.hist_cap, d.round_cap = 10, 10, 1
+    small = lib.ptc_solver_workspace_bytes(ctypes.byref(d))
+    d.batch = 400
+    assert lib.ptc_solver_workspace_bytes(ctypes.byref(d)) > small > 0
