@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
 // propagation pass's prediction (itself the first Newton iterate from the
 // dynamically consistent current trajectory), so convergence is quadratic
 // from the start; a problem stops as soon as every step of its guess
-// satisfies the recurrence to a few ulps.  A problem that has not converged
+// satisfies the recurrence to 1e-13 relative (fp64; fp32 1e-5).  A problem that has not converged
 // after pr_iters sweeps (or meets a non-finite state) is rolled out by the
 // sequential kernel, so the result and the divergence report never depend
 // on the parallel path's convergence.
@@ -793,7 +793,10 @@ __global__ void k_pr_check(NewtonArgs<R> a, int k) {
   const int P0 = a.plan.units0();
   double r = 0.0;
   for (int j = 0; j < partial_rows(P0); ++j) r = nanmax(r, a.rres[(size_t)j * a.B + b]);
-  const double tol = 16.0 * (sizeof(R) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07);
+  // per-step consistency |x_{t+1} - f(x_t, u_t)| / max(1, |f|): the scan's
+  // own rounding (tree carries compose many steps) sits at a few hundred
+  // ulp for long horizons, so fp64 accepts 1e-13 (fp32 1e-5)
+  const double tol = sizeof(R) == 8 ? 1e-13 : 1e-5;
   if (r <= tol) a.rstate[b] = st | RS_CONV | ((k & 1) ? RS_IN_XR : 0);
 }
 
