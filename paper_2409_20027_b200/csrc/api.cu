@@ -48,7 +48,10 @@ static Plan auto_plan(int B, int T, int K0, int K, int nx = 0) {
     // thread-per-unit kernels want ~32K units; the warp-per-unit kernels of
     // nx >= 8 (wide.cuh) ~8K warps, i.e. longer level-0 chunks
     const long long units = nx >= 8 ? 8192 : 32768;
-    if (B >= 8192) K0 = T;
+    // one sweep per problem (work-optimal) once the batch alone keeps the
+    // GPU busy: measured crossover between 8K (tree 15% faster) and 16K
+    // (sweep 25% faster) problems per launch (nx = 2 / 4, T = 256)
+    if (B >= 16384) K0 = T;
     else K0 = (int)std::max<long long>(4, (work + units - 1) / units);
   }
   return make_plan(T, K0, K);
