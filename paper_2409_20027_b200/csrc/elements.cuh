@@ -2,10 +2,12 @@
 //
 //  * value elements (A, Y, C, eta, b): dual form of a conditional value
 //    function (reference passes.py:38-46, element init 244-261, combine
-//    264-288).  `vcombine` is the general operator used on tree interior
-//    nodes; `vstep` is the same operator specialised to a right operand with
-//    A = C = b = 0 -- every suffix that contains the terminal element has
-//    that shape, so all down-sweep work is this cheap Riccati-like step.
+//    264-288).  `vcombine` is the general operator (tree interior nodes);
+//    `vcombine_stage` the same with a single-stage left operand in Woodbury
+//    form (level-0 up-sweep); `vstep` the operator specialised to a right
+//    operand with A = C = b = 0 (every suffix containing the terminal has
+//    that shape: tree down-sweep); `riccati_step` = vstep of a single stage
+//    fused with that stage's gains (level-0 down-sweep).
 //  * affine maps (F, e): x -> F x + e.  Propagation (passes.py:330-361) and
 //    linear rollout compose them forwards; the co-state suffix
 //    (passes.py:113-148) composes them backwards with F = fx^T.
@@ -328,43 +330,6 @@ PTC_D bool vstep(const VElem<R, NX>& e, const VCarry<R, NX>& c, VCarry<R, NX>& o
   return ok;
 }
 
-// Feedback gains at stage t from the cost-to-go (S, s = -eta) of stage t+1
-// (reference passes.py:316-323):
-//   Q = sym(Rr + Fu^T S Fu),  Gamma = -Q^-1 (M^T + Fu^T S Fx),
-//   gamma = -Q^-1 (d + Fu^T s)
-template <typename R, int NX, int NU>
-PTC_D bool gains(const Stage<R, NX, NU>& s, const VCarry<R, NX>& next, R (&Gam)[NU][NX],
-                 R (&gam)[NU]) {
-  R FtS[NU][NX];
-  mtm<NU, NX, NX>(s.Fu, next.Y, FtS);
-  R Q[NU][NU];
-  mm<NU, NX, NU>(FtS, s.Fu, Q);
-#pragma unroll
-  for (int i = 0; i < NU; ++i)
-#pragma unroll
-    for (int j = 0; j < NU; ++j) Q[i][j] += s.Rr[i][j];
-  symmetrize<NU>(Q);
-  bool ok = cholesky<NU>(Q);
-  mm<NU, NX, NX>(FtS, s.Fx, Gam);
-#pragma unroll
-  for (int i = 0; i < NU; ++i)
-#pragma unroll
-    for (int j = 0; j < NX; ++j) Gam[i][j] += s.M[j][i];
-  R Fe[NU];
-  mtv<NU, NX>(s.Fu, next.eta, Fe);  // Fu^T eta = -Fu^T s
-#pragma unroll
-  for (int i = 0; i < NU; ++i) gam[i] = s.d[i] - Fe[i];
-  chol_solve<NU, NX>(Q, Gam);
-  chol_solve_vec<NU>(Q, gam);
-#pragma unroll
-  for (int i = 0; i < NU; ++i) {
-#pragma unroll
-    for (int j = 0; j < NX; ++j) Gam[i][j] = -Gam[i][j];
-    gam[i] = -gam[i];
-  }
-  return ok;
-}
-
 // One stage element (earlier, from its expansion) combined with a general
 // aggregate r (later): vcombine(velem_from_stage(st), r) without forming
 // the stage's dual element or the NX x NX system I + C_l Y_r.  The stage's
@@ -502,9 +467,10 @@ PTC_D int vcombine_stage(const Stage<R, NX, NU>& st, const VElem<R, NX>& r, VEle
 }
 
 // One stage element folded into a terminal-containing suffix, fused with the
-// gains of that stage: the composition  gains(st, c)  +  vstep(velem(st), c)
-// of the reference's value pass (passes.py:192-228 element, 264-288 combine,
-// 316-323 gains) written without forming the dual element.  With
+// gains of that stage: the reference's gains of stage t from the cost-to-go
+// of stage t+1 (passes.py:316-323) together with vstep(velem(st), c)
+// (element 192-228, combine 264-288), written without forming the dual
+// element.  With
 //   Q = sym(Rr + Fu^T S Fu),  Qux = M^T + Fu^T S Fx,  qu = d + Fu^T s
 // the push-through identity  (I + S C)^-1 S = S - S Fu Q^-1 Fu^T S  (C =
 // Fu Rr^-1 Fu^T) turns the combine into

@@ -3,14 +3,14 @@
 //
 // Scan structure:
 //   up-sweep   level 0: each thread folds K0 consecutive stages into one
-//              aggregate (elements built from the expansion on the fly, so
-//              the dual elements never touch HBM);
+//              aggregate (each stage combined in Woodbury form,
+//              vcombine_stage, so the dual elements never touch HBM);
 //              level l: each thread folds K aggregates of level l.
 //   top        one thread per problem walks the <= K top items.
 //   down-sweep level l: carries flow back down; at level 0 the carry is the
 //              cost-to-go (S_{t+1}, s_{t+1}) and the thread sweeps its chunk
-//              with the cheap specialised combine, emitting the gains and
-//              (fused) the level-1 aggregates of the propagation scan.
+//              with the Riccati-form step (riccati_step), emitting the gains
+//              and (fused) the level-1 aggregates of the propagation scan.
 // With K0 >= T (large batches) the tree vanishes and every problem is one
 // sequential sweep per pass -- the work-optimal schedule when the batch
 // alone fills the GPU.
