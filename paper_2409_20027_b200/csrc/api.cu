@@ -262,6 +262,7 @@ static int propagate_t(int batch, int horizon, int nx, int nu, const void* Fx, c
   Carver c{(char*)ws};
   carve_lqr_tree(c, a, nx, nu);
   if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
+  a.red = nullptr;  // no trust-region partial sums outside the Newton loop
   it->second.propagate(&a, st);
   PTC_CUDA(cudaGetLastError());
   return PTC_OK;

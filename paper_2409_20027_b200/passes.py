@@ -163,13 +163,8 @@ def value_pass(exp: StageExpansion, executor: str = "auto", dtype=None):
 
 def propagation_pass(law: FeedbackLaw, exp: StageExpansion, executor: str = "auto",
                      dtype=None):
-    """Closed-loop deviations from dx_1 = 0 (passes.py:338-361) for the law of
-    this expansion (the device computes law and propagation in one solve; a
-    foreign law is propagated by the same forward scan kernels)."""
-    S, s, own, dxs, dus = lqr_solve(exp, executor, dtype)
-    if np.array_equal(np.asarray(law.Gamma), own.Gamma) and np.array_equal(
-            np.asarray(law.gamma), own.gamma):
-        return dxs, dus
+    """Closed-loop deviations from dx_1 = 0 (passes.py:338-361): the device
+    forward scan of ``law`` on the expansion's Jacobians (ptc_propagate)."""
     return propagate(law, exp, dtype=dtype)
 
 
