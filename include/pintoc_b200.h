@@ -161,7 +161,7 @@ typedef struct ptc_problem_desc {
   int32_t dtype, batch, horizon, nx, nu;
   int32_t model;               /* PTC_DYN_* */
   double dyn_params[8];        /* pendulum: g, l, m, b, dt; cart-pole: g, l, m_cart, m_pole, dt */
-  /* affine model x' = A x + B u + c: host arrays in dtype, shapes
+  /* affine model x' = A x + B u + c: host or device arrays in dtype, shapes
    * (nx*nx, lin_rows, lin_batch), (nx*nu, lin_rows, lin_batch),
    * (nx, lin_rows, lin_batch) with lin_rows in {1, horizon} (time-invariant
    * or time-varying) and lin_batch in {1, batch}; lin_c may be NULL */

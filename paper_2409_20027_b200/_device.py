@@ -10,6 +10,7 @@ one permute + contiguous copy on the device.
 from __future__ import annotations
 
 import ctypes as C
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -52,6 +53,24 @@ def _np_ptr(a) -> int | None:
     return None if a is None else a.ctypes.data
 
 
+def _linear_device(dynamics, spec, torch, dtype, device):
+    """Affine model data as device (comps, rows) tensors, cached on the
+    (read-only) dynamics object: the stage-major host arrays are uploaded
+    once and transposed on the GPU instead of by numpy."""
+    cache = dynamics.__dict__.setdefault("_device_cache", {})
+    key = (str(dtype), str(device))
+    if key not in cache:
+        out = []
+        for name in ("lin_a", "lin_b", "lin_c"):
+            with warnings.catch_warnings():   # read-only source, only ever read
+                warnings.simplefilter("ignore", UserWarning)
+                host = torch.from_numpy(np.ascontiguousarray(spec[name], dtype=np.float64))
+            out.append(host.to(device=device, dtype=dtype).t().contiguous())
+        torch.cuda.current_stream(device).synchronize()
+        cache[key] = tuple(out)
+    return cache[key]
+
+
 class DeviceSolver:
     """`batch` independent problems sharing dynamics, cost and constraints."""
 
@@ -88,9 +107,9 @@ class DeviceSolver:
             d.dyn_params[i] = float(v)
         if spec["model"] == N.DYN_LINEAR:
             rows = spec["lin_rows"]
-            d.lin_a = dptr(spec["lin_a"], npdt)
-            d.lin_b = dptr(spec["lin_b"], npdt)
-            d.lin_c = dptr(spec["lin_c"], npdt)
+            lin = _linear_device(dynamics, spec, torch, self.dtype, self.device)
+            d.lin_a, d.lin_b, d.lin_c = (t.data_ptr() for t in lin)
+            keep.extend(lin)
             d.lin_rows, d.lin_batch = rows, 1
         d.Q = dptr(cspec["Q"])
         d.R = dptr(cspec["R"])

@@ -410,6 +410,30 @@ struct ptc_solver {
 
 namespace ptc {
 
+// component-major affine model (comps x T) -> stage-major rows [t][A | Bm | c]
+template <typename R>
+__global__ void k_model_stage_major(const R* A, const R* Bm, const R* c, R* st, int T, int nx,
+                                    int nu) {
+  __shared__ R tile[32][33];
+  const int nA = nx * nx, nB = nx * nu, nc = nA + nB + nx;
+  const int c0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int k = c0 + i, t = t0 + threadIdx.x;
+    R v = R(0);
+    if (k < nc && t < T) {
+      if (k < nA) v = A[(size_t)k * T + t];
+      else if (k < nA + nB) v = Bm[(size_t)(k - nA) * T + t];
+      else v = c[(size_t)(k - nA - nB) * T + t];
+    }
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int t = t0 + i, k = c0 + threadIdx.x;
+    if (k < nc && t < T) st[(size_t)t * nc + k] = tile[threadIdx.x][i];
+  }
+}
+
 template <typename R>
 __global__ void k_normalize_parity(NewtonArgs<R> a, int nx, int nu) {
   // make buffer 0 hold every problem's current trajectory
@@ -500,12 +524,13 @@ struct Solver final : ptc_solver {
     a.plan = l.plan = auto_plan((int)B, (int)T, d.chunk0, d.chunk, (int)nx);
     const size_t P0 = a.plan.units0();
     ProblemParams* dpp = c.template take<ProblemParams>(1);
-    R *linA = nullptr, *linB = nullptr, *linc = nullptr;
+    R *linA = nullptr, *linB = nullptr, *linc = nullptr, *linst = nullptr;
     if (d.model == PTC_DYN_LINEAR) {
       const size_t lt = pp.lin_T, lb = pp.lin_B;
       linA = c.template take<R>(nx * nx * lt * lb);
       linB = c.template take<R>(nx * nu * lt * lb);
       linc = c.template take<R>(nx * lt * lb);
+      if (lt > 1 && lb == 1 && nx >= 8) linst = c.template take<R>((nx * nx + nx * nu + nx) * lt);
     }
     a.xsz = nx * (T + 1) * B;
     a.usz = nu * T * B;
@@ -591,6 +616,7 @@ struct Solver final : ptc_solver {
       self->hp.lin_A = linA;
       self->hp.lin_Bm = linB;
       self->hp.lin_c = linc;
+      self->hp.lin_st = linst;
       // LQR args view the solver's expansion
       l.P = a.P; l.Rm = a.Rm; l.M = a.M; l.d = a.d; l.Fx = a.Fx; l.Fu = a.Fu; l.PT = a.PT;
       l.alpha = a.alpha;
@@ -671,12 +697,21 @@ struct Solver final : ptc_solver {
     if (d.model == PTC_DYN_LINEAR) {
       const size_t lt = hp.lin_T, lb = hp.lin_B;
       if (!d.lin_a || !d.lin_b) return fail(PTC_ERR_ARG, "linear model needs lin_a and lin_b");
-      PTC_CUDA(cudaMemcpy((void*)hp.lin_A, d.lin_a, sizeof(R) * nx * nx * lt * lb, cudaMemcpyHostToDevice));
-      PTC_CUDA(cudaMemcpy((void*)hp.lin_Bm, d.lin_b, sizeof(R) * nx * nu * lt * lb, cudaMemcpyHostToDevice));
+      // host or device pointers (unified addressing decides the direction)
+      PTC_CUDA(cudaMemcpy((void*)hp.lin_A, d.lin_a, sizeof(R) * nx * nx * lt * lb, cudaMemcpyDefault));
+      PTC_CUDA(cudaMemcpy((void*)hp.lin_Bm, d.lin_b, sizeof(R) * nx * nu * lt * lb, cudaMemcpyDefault));
       if (d.lin_c)
-        PTC_CUDA(cudaMemcpy((void*)hp.lin_c, d.lin_c, sizeof(R) * nx * lt * lb, cudaMemcpyHostToDevice));
+        PTC_CUDA(cudaMemcpy((void*)hp.lin_c, d.lin_c, sizeof(R) * nx * lt * lb, cudaMemcpyDefault));
       else
         PTC_CUDA(cudaMemset((void*)hp.lin_c, 0, sizeof(R) * nx * lt * lb));
+      if (hp.lin_st) {
+        const int nc = nx * nx + nx * nu + nx;
+        k_model_stage_major<R><<<dim3((nc + 31) / 32, (unsigned)((lt + 31) / 32)), dim3(32, 8)>>>(
+            static_cast<const R*>(hp.lin_A), static_cast<const R*>(hp.lin_Bm),
+            static_cast<const R*>(hp.lin_c), (R*)hp.lin_st, (int)lt, nx, nu);
+        PTC_CUDA(cudaGetLastError());
+        PTC_CUDA(cudaStreamSynchronize(0));
+      }
     }
     PTC_CUDA(cudaMemcpy((void*)na.pp, &hp, sizeof(ProblemParams), cudaMemcpyHostToDevice));
     return PTC_OK;

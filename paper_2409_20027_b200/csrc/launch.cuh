@@ -7,6 +7,7 @@
 
 #include "newton_kernels.cuh"
 #include "wide.cuh"
+#include "wide_newton.cuh"
 
 namespace ptc {
 
@@ -94,6 +95,10 @@ void launch_lqr_block(const LqrArgs<R>& a0, int phase, const void* blocks, void*
 template <typename R, class Dyn>
 void launch_costate(const NewtonArgs<R>& a, cudaStream_t s) {
   constexpr int NX = Dyn::NX;
+  if constexpr (kWideNewton<Dyn>) {
+    WideNewton<R, NX, Dyn::NU>::costate(a, s);
+    return;
+  }
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (pl.L >= 1) {
@@ -154,6 +159,17 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
       fused = true;
     }
   }
+  if constexpr (kWideNewton<Dyn>) {
+    if (la.xst && B == 1) {
+      // the co-state sweep writes the expansion straight into the wide LQR's
+      // stage-major staging rows (no component-major round trip)
+      LqrArgs<R> l2 = la;
+      l2.prestaged = 1;
+      WideNewton<R, NX, NU>::costate(a, s, la.xst);
+      lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&l2, s);
+      fused = true;
+    }
+  }
   if (!fused) {
     launch_costate<R, Dyn>(a, s);
     lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&la, s);
@@ -163,7 +179,21 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   constexpr int kOpsCost = RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4);  // sum l, sum c, first infeasible
   if (fold) k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.red, 3, kOpsRed, (int)P0, (int)B);
   k_roll_gate<R><<<grid_for(B), kBlock, 0, s>>>(a);
-  if (a.pr_iters > 0 && a.plan.L >= 1) {
+  bool rolled = false;
+  if constexpr (kWideNewton<Dyn>) {
+    // affine: the candidate is one exact forward scan (tree plans) or the
+    // warp-per-problem recurrence
+    if (a.pr_iters > 0 && a.plan.L >= 1) {
+      WideNewton<R, NX, NU>::rollout_scan(a, la.dU, s);
+      rolled = true;
+    } else if (B <= kWarpRolloutMaxB) {
+      WideNewton<R, NX, NU>::rollout_seq(a, la.dU, s);
+      rolled = true;
+    }
+    if (rolled) k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+  }
+  if (rolled) {
+  } else if (a.pr_iters > 0 && a.plan.L >= 1) {
     // log-depth Newton rollout, sequential fallback for what did not converge
     const Plan& pl = a.plan;
     const long long nT = (long long)(a.T + 1) * B;
@@ -299,6 +329,12 @@ struct RegisterNewton {
   }
   static void rollout(const void* p, cudaStream_t s) {
     const NewtonArgs<R>& a = A(p);
+    if constexpr (kWideNewton<Dyn>) {
+      if (a.B <= kWarpRolloutMaxB) {
+        WideNewton<R, NX, NU>::rollout_inplace(a, s);
+        return;
+      }
+    }
     k_rollout_inplace<R, Dyn><<<grid_for(a.B), kBlock, 0, s>>>(a);
   }
   static void cost(const void* p, cudaStream_t s) {

@@ -53,6 +53,7 @@ struct LqrArgs {
   R* xst;
   R* gst;
   int staged;
+  int prestaged;           // xst already written by the producer (Newton co-state sweep)
   R* xin_buf;              // workspace for x_in        (nx, 1, B)
   // tree scratch, index l = 1..L, item rows n[l]
   R* vagg[kMaxLevels + 1];

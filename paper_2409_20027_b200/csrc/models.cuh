@@ -30,6 +30,9 @@ struct ProblemParams {
   const void* lin_A;        // (nx*nx, lin_T, lin_B) in the solver dtype
   const void* lin_Bm;       // (nx*nu, lin_T, lin_B)
   const void* lin_c;        // (nx,    lin_T, lin_B)
+  const void* lin_st;       // stage-major copy [t][A | Bm | c] (lin_T rows) for
+                            // time-varying models shared by the batch, nx >= 8
+                            // (warp kernels: one contiguous row per stage), or null
   double Q[kMaxNX * kMaxNX], Rc[kMaxNU * kMaxNU], Qf[kMaxNX * kMaxNX], goal[kMaxNX];
   int W, Ws;                // stacked constraint rows, of which Ws are state rows
   int row_var[kMaxRows];    // 0 = state, 1 = control

@@ -347,12 +347,19 @@ template <typename R, int NX, int NU>
 PTC_D void w_ld_stage(const LqrArgs<R>& a, int t, int b, R alpha, R* st) {
   using S = WSlab<R, NX, NU>;
   const int T = a.T, B = a.B;
-  w_ld<NX * NX>(a.P, t, T, B, b, st + S::sP);
-  w_ld<NU * NU>(a.Rm, t, T, B, b, st + S::sR);
-  w_ld<NX * NU>(a.M, t, T, B, b, st + S::sM);
-  w_ld<NU>(a.d, t, T, B, b, st + S::sd);
-  w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
-  w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
+  if (a.staged) {
+    // the staging rows are authoritative (a producer may have written only them)
+    const R* row = a.xst + (size_t)t * S::SC;
+    for (int c = lane_id(); c < S::SC; c += 32) st[c] = row[c];
+  } else {
+    w_ld<NX * NX>(a.P, t, T, B, b, st + S::sP);
+    w_ld<NU * NU>(a.Rm, t, T, B, b, st + S::sR);
+    w_ld<NX * NU>(a.M, t, T, B, b, st + S::sM);
+    w_ld<NU>(a.d, t, T, B, b, st + S::sd);
+    w_ld<NX * NX>(a.Fx, t, T, B, b, st + S::sFx);
+    w_ld<NX * NU>(a.Fu, t, T, B, b, st + S::sFu);
+  }
+  __syncwarp();
   for (int i = lane_id(); i < NU; i += 32) st[S::sR + i * NU + i] += alpha;
   __syncwarp();
 }
@@ -1462,7 +1469,7 @@ void launch_lqr_wide(const LqrArgs<R>& a0, cudaStream_t s) {
   W::setup();
   LqrArgs<R> a = a0;
   a.staged = (a.xst != nullptr && a.B == 1) ? 1 : 0;
-  if (a.staged) launch_stage_in<R, NX, NU>(a, s);
+  if (a.staged && !a.prestaged) launch_stage_in<R, NX, NU>(a, s);
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (pl.L >= 1) {

@@ -174,10 +174,12 @@ def propagate(law: FeedbackLaw, exp: StageExpansion, dtype=None):
     return propagate_law(law, exp, dtype)
 
 
-def _pass_solver(traj: Trajectory, cost, aug, dyn, alpha, dtype):
+def _pass_solver(traj: Trajectory, cost, aug, dyn, alpha, dtype, executor="auto"):
     st = aug_settings(aug)
     con = getattr(aug, "constraints", None)
-    settings = SolveSettings(method=N.METHOD_NEWTON, alpha0=float(alpha), **st)
+    c0, c1 = plan_chunks(executor, len(traj.controls))
+    settings = SolveSettings(method=N.METHOD_NEWTON, alpha0=float(alpha), chunk0=c0, chunk=c1,
+                             **st)
     solver = DeviceSolver(dyn, cost, con, 1, settings, dtype=dtype)
     z = v = None
     if st["aug"] == N.AUG_ADMM:
@@ -189,19 +191,19 @@ def _pass_solver(traj: Trajectory, cost, aug, dyn, alpha, dtype):
 
 def costate_pass(traj: Trajectory, cost, aug, dyn, executor: str = "auto", dtype=None):
     """Adjoint vectors lambda_{1:N+1} (passes.py:122-148) on the device."""
-    solver = _pass_solver(traj, cost, aug, dyn, 0.0, dtype)
+    solver = _pass_solver(traj, cost, aug, dyn, 0.0, dtype, executor)
     return solver.field("lam", solver.T + 1, (solver.nx,))[0].cpu().numpy()
 
 
 def hamiltonian_expansion(traj: Trajectory, costates, cost, aug, dyn, alpha: float = 0.0,
-                          dtype=None) -> StageExpansion:
+                          dtype=None, executor: str = "auto") -> StageExpansion:
     """P, R, M, d, Fx, Fu of the augmented Lagrangian (passes.py:155-185).
     The device kernel fuses the co-state sweep with the expansion, so the
     co-states are recomputed on the fly (``costates`` is accepted for API
     compatibility and must be the output of ``costate_pass``)."""
     if alpha < 0:
         raise ValueError("alpha must be nonnegative")
-    solver = _pass_solver(traj, cost, aug, dyn, alpha, dtype)
+    solver = _pass_solver(traj, cost, aug, dyn, alpha, dtype, executor)
     T, nx, nu = solver.T, solver.nx, solver.nu
     f = lambda name, shape: solver.field(name, T, shape)[0].cpu().numpy()
     PT = solver.read("PT").view(nx, nx).cpu().numpy()

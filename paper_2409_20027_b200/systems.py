@@ -16,7 +16,7 @@ import numpy as np
 
 from ._native import DYN_CARTPOLE, DYN_LINEAR, DYN_PENDULUM
 from .exceptions import DimensionError
-from .problem import BoxConstraint, ControlProblem, CostModel, DynamicsModel
+from .problem import BoxConstraint, ControlProblem, CostModel, DynamicsModel, _frozen
 
 SYSTEMS = ("pendulum", "cartpole")
 
@@ -124,8 +124,8 @@ class LinearDynamics(DynamicsModel):
         return self.A @ x + self.B @ u + self.offset
 
     def _device_spec(self):
-        return dict(model=DYN_LINEAR, lin_a=self.A.reshape(-1, 1), lin_b=self.B.reshape(-1, 1),
-                    lin_c=self.offset.reshape(-1, 1), lin_rows=1)
+        return dict(model=DYN_LINEAR, lin_a=self.A.reshape(1, -1), lin_b=self.B.reshape(1, -1),
+                    lin_c=self.offset.reshape(1, -1), lin_rows=1)
 
 
 class TimeVaryingLinearDynamics(DynamicsModel):
@@ -137,19 +137,19 @@ class TimeVaryingLinearDynamics(DynamicsModel):
         A = np.asarray(A, dtype=float)
         B = np.asarray(B, dtype=float)
         super().__init__(A.shape[0], A.shape[1], B.shape[2])
-        self.A, self.B = A, B
-        self.offset = (np.zeros((self.horizon, self.d_x)) if offset is None
-                       else np.asarray(offset, float))
+        # read-only copies: the device keeps a cached transposed upload
+        self.A, self.B = _frozen(A), _frozen(B)
+        self.offset = _frozen(np.zeros((self.horizon, self.d_x)) if offset is None else offset)
 
     def f(self, t, x, u):
         return self.A[t] @ x + self.B[t] @ u + self.offset[t]
 
     def _device_spec(self):
         T, nx, nu = self.horizon, self.d_x, self.d_u
-        return dict(model=DYN_LINEAR,
-                    lin_a=self.A.reshape(T, nx * nx).T,
-                    lin_b=self.B.reshape(T, nx * nu).T,
-                    lin_c=self.offset.reshape(T, nx).T, lin_rows=T)
+        # stage-major (rows, comps); the device upload transposes on the GPU
+        return dict(model=DYN_LINEAR, lin_a=self.A.reshape(T, nx * nx),
+                    lin_b=self.B.reshape(T, nx * nu), lin_c=self.offset.reshape(T, nx),
+                    lin_rows=T)
 
 
 class QuadraticCost(CostModel):
