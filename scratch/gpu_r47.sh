@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/r47_tests.log 2>&1; echo tests rc=$?
+tail -3 gpurun_out/r47_tests.log
+timeout 900 python bench.py > gpurun_out/r47_bench.json 2> gpurun_out/r47_bench.err; echo bench rc=$?
+tail -c 3000 gpurun_out/r47_bench.json
