@@ -141,3 +141,47 @@ def test_wide_admm_matches_oracle(executor):
     assert rep.converged == ref.converged
     assert [r.iterations for r in rep.newton_reports] == [r.iterations for r in ref.newton]
     assert rel_gap(traj.controls, ref.us) < 1e-8
+
+
+@pytest.mark.parametrize("executor,T", [("sequential", 200), ("parallel", 1100)])
+def test_wide_batch_matches_single_solves(executor, T):
+    """Several wide problems per launch sequence (warp units over problems,
+    batch-strided model / trajectory gathers) reproduce the batch-1 solves."""
+    import torch
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200 import BatchSolver
+    nx, nu, n = 12, 4, 3
+    A, B, c, _, u0, rng = _system(nx, nu, T, 5)
+    dyn, cost, box, odyn, ocost, obox = _models(P, nx, nu, A, B, c)
+    problem = P.ControlProblem(dyn, cost, box)
+    opts = P.BarrierOptions(newton=P.NewtonOptions(executor=executor))
+    x0 = rng.standard_normal((n, nx))
+    U = torch.as_tensor(np.repeat(u0[None], n, 0))
+    bs = BatchSolver(problem, n, "barrier", barrier=opts)
+    X = bs.rollout(x0, U)
+    res = bs.solve(X, U)
+    for k in range(n):
+        init = P.rollout(dyn, x0[k], u0)
+        assert rel_gap(X[k].cpu().numpy(), init.states) < 1e-12
+        traj, rep = P.barrier_solve(problem, init, opts)
+        got = res.round_iters[:len(rep.rounds), k].cpu().numpy()
+        assert list(got) == [r.newton.iterations for r in rep.rounds]
+        assert rel_gap(res.controls[k].cpu().numpy(), traj.controls) < 1e-10
+
+
+@pytest.mark.parametrize("executor", ["sequential", "parallel"])
+def test_wide_newton_fp32(executor):
+    """fp32 instantiation of the wide Newton kernels: converges to the fp64
+    solution within single-precision accuracy (tolerance 1e-4 relative)."""
+    import torch
+    import paper_2409_20027_b200 as P
+    nx, nu, T = 12, 4, 1100
+    A, B, c, x0, u0, _ = _system(nx, nu, T, 6)
+    dyn, cost, box, odyn, ocost, obox = _models(P, nx, nu, A, B, c)
+    init = P.rollout(dyn, x0, u0)
+    opts = P.NewtonOptions(executor=executor, inner_tol=1e-5)
+    t64, r64 = P.newton_solve(dyn, cost, None, init, opts)
+    t32, r32 = P.newton_solve(dyn, cost, None, init, opts, dtype=torch.float32)
+    assert r32.converged
+    assert rel_gap(t32.controls, t64.controls) < 1e-4
+    assert abs(r32.final_cost - r64.final_cost) <= 1e-4 * abs(r64.final_cost)
