@@ -515,7 +515,8 @@ def run_ours(args) -> None:
     # horizon sweep of the single-problem LQR-scan latency (config 1, nx=4)
     sweep = nsweep = None
     if rank == 0 and not args.no_sweep:
-        sweep = lqr_latency_sweep(torch, LqrSolver)
+        sweep = {"fp64": lqr_latency_sweep(torch, LqrSolver),
+                 "fp32": lqr_latency_sweep(torch, LqrSolver, torch.float32)}
     if rank == 0 and not args.no_newton_sweep:
         nsweep = newton_latency_sweep(torch, P)
     mpc = None
@@ -560,24 +561,40 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def lqr_latency_sweep(torch, LqrSolver):
+def config1_inputs(rng, T: int, nx: int, nu: int) -> dict:
+    """Config 1 (BASELINE.json): time-varying random LQR subproblem, stage
+    arrays (T, ...).  A_k = I + 0.05 N(0, 1) with spectral radius clipped to
+    <= 1.05, B_k ~ N(0, 0.1), Q_k = M M^T + 0.1 I, R_k = 0.1 I, c_k ~ N(0, 0.01)
+    entering d_k = B_k^T c_k, M_k = 0, P_T = M M^T + 0.1 I."""
+    A = np.eye(nx)[None] + 0.05 * rng.standard_normal((T, nx, nx))
+    rad = np.max(np.abs(np.linalg.eigvals(A)), axis=1)
+    A = A * np.where(rad > 1.05, 1.05 / rad, 1.0)[:, None, None]
+    B = np.sqrt(0.1) * rng.standard_normal((T, nx, nu))
+    Mq = rng.standard_normal((T, nx, nx))
+    c = 0.1 * rng.standard_normal((T, nx))
+    Mt = rng.standard_normal((nx, nx))
+    return dict(P=Mq @ np.swapaxes(Mq, 1, 2) + 0.1 * np.eye(nx),
+                R=np.broadcast_to(0.1 * np.eye(nu), (T, nu, nu)), M=np.zeros((T, nx, nu)),
+                d=np.einsum("tij,ti->tj", B, c), Fx=A, Fu=B, PT=(Mt @ Mt.T + 0.1 * np.eye(nx))[None])
+
+
+def lqr_latency_sweep(torch, LqrSolver, dtype=None):
     """Single-problem LQR-scan solve latency vs horizon (config 1: random
-    time-varying systems, batch 1, fp64) -- the log-T claim."""
-    from oracle.pintoc_oracle import random_lqr_expansion  # input generator only
+    time-varying systems, batch 1, fp64 and fp32) -- the log-T claim."""
+    dtype = dtype or torch.float64
     out = {}
     for nx in (2, 4, 8, 12):
         nu = nx // 2
         row = {}
         for logT in (8, 10, 12, 14, 16):
             Tn = 1 << logT
-            rng = np.random.default_rng([1, nx, logT])
-            e = random_lqr_expansion(rng, Tn, nx, nu)
+            e = config1_inputs(np.random.default_rng([1, nx, logT]), Tn, nx, nu)
             dev = torch.device("cuda")
-            soa = lambda a, c: torch.as_tensor(a.reshape(a.shape[0], c).T.copy()).unsqueeze(-1).to(dev)
-            ins = [soa(e.P, nx * nx), soa(e.R, nu * nu), soa(e.M, nx * nu), soa(e.d, nu),
-                   soa(e.Fx, nx * nx), soa(e.Fu, nx * nu), soa(e.PT[None], nx * nx)]
+            soa = lambda a: torch.as_tensor(a.reshape(a.shape[0], -1).T.copy(),
+                                            dtype=dtype).unsqueeze(-1).to(dev)
+            ins = [soa(e[k]) for k in ("P", "R", "M", "d", "Fx", "Fu", "PT")]
             alpha = torch.zeros(1, dtype=torch.float64, device=dev)
-            s = LqrSolver(1, Tn, nx, nu)
+            s = LqrSolver(1, Tn, nx, nu, dtype=dtype)
             for _ in range(3):
                 s.solve(*ins, alpha)
             torch.cuda.synchronize()
