@@ -527,6 +527,9 @@ def run_ours(args) -> None:
         del halves
         torch.cuda.empty_cache()
         longh = long_horizon_leg(torch, world, rank)
+    solves = None
+    if rank == 0 and world == 1 and not args.no_solves:
+        solves = single_solve_leg(torch, P, cpu=not args.no_cpu_baseline)
     c4solve = None
     if rank == 0 and world == 1 and not args.no_c4solve:
         torch.cuda.empty_cache()
@@ -554,7 +557,7 @@ def run_ours(args) -> None:
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk, "ill_posed_subproblems": ill_posed,
             "lqr_latency_sweep": sweep, "newton_latency_sweep": nsweep,
-            "long_horizon": longh, "config4_solve": c4solve, "mpc_config3": mpc, "fp32": fp32,
+            "long_horizon": longh, "config4_solve": c4solve, "single_solves": solves, "mpc_config3": mpc, "fp32": fp32,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -816,6 +819,79 @@ def long_horizon_leg(torch, world: int, rank: int, steps: int = 5, chunk0: int =
             "algorithmic_bytes": in_bytes + out_bytes}
 
 
+def single_solve_leg(torch, P, cpu: bool = True):
+    """Configs 0 and 2 end to end, one problem each, fp64, through the public
+    API (`barrier_solve` / `admm_solve`, host arrays in and out), against the
+    reference algorithm on the host (the oracle port; it is the only CPU
+    implementation there is).
+      config 0: pendulum swing-up, T = 100, x0 = (pi, 0), |u| <= 5, barrier
+                mu 0.1 -> 1e-6 (zeta 0.2), seeded initial controls.
+      config 2: cart-pole, T = 500, |x| <= 1.5, |u| <= 10, ADMM rho = 1,
+                <= 200 outer iterations, seeded initial controls.
+    The CPU arm runs config 0 whole; for config 2 (> 15 min on one core) it
+    times the first 3 ADMM outer iterations and reports the per-Newton-
+    iteration time, projected over the device run's iteration count (the
+    counts follow the reference's own semantics)."""
+    probs = models_pkg(P)
+    out = {}
+    rng = np.random.default_rng(20027)
+    # config 0
+    T0 = 100
+    pend = probs["pendulum"]
+    pend = P.ControlProblem(P.PendulumDynamics(T0, P.PendulumParams(damping=0.1, dt=0.05)),
+                            pend.cost, pend.constraints)
+    u0 = np.clip(0.5 * rng.standard_normal((T0, 1)), -4.5, 4.5)
+    init0 = P.rollout(pend.dynamics, np.array([np.pi, 0.0]), u0)
+    o0 = P.BarrierOptions(mu0=0.1, zeta=0.2, mu_tol=1e-6)
+    P.barrier_solve(pend, init0, o0)
+    t = time.perf_counter()
+    _, rep0 = P.barrier_solve(pend, init0, o0)
+    g0 = time.perf_counter() - t
+    it0 = sum(r.newton.iterations for r in rep0.rounds)
+    out["config0"] = {"gpu_s": round(g0, 4), "newton_iterations": it0,
+                      "rounds": len(rep0.rounds)}
+    # config 2
+    T2 = 500
+    cart = probs["cartpole"]
+    cart = P.ControlProblem(P.CartPoleDynamics(T2, P.CartPoleParams(cart_mass=1.0, pole_mass=0.1,
+                                                                    pole_length=0.5, dt=0.02)),
+                            cart.cost, cart.constraints)
+    u2 = np.clip(1.0 * rng.standard_normal((T2, 1)), -9.0, 9.0)
+    init2 = P.rollout(cart.dynamics, np.zeros(4), u2)
+    o2 = P.AdmmOptions(rho=1.0, max_outer=200)
+    P.admm_solve(cart, init2, o2)
+    t = time.perf_counter()
+    _, rep2 = P.admm_solve(cart, init2, o2)
+    g2 = time.perf_counter() - t
+    it2 = rep2.inner_iterations
+    out["config2"] = {"gpu_s": round(g2, 4), "newton_iterations": it2,
+                      "outer_iterations": rep2.outer_iterations, "converged": rep2.converged}
+    if cpu:
+        from oracle import pintoc_oracle as O   # the CPU arm
+        dyn, cost = models_oracle(O)["pendulum"]
+        box = O.Box(2, 1, control_lower=-5.0, control_upper=5.0)
+        t = time.perf_counter()
+        r = O.barrier_solve(dyn, cost, box, init0.states, init0.controls, mu0=0.1, zeta=0.2,
+                            mu_tol=1e-6)
+        c0 = time.perf_counter() - t
+        out["config0"].update(cpu_s=round(c0, 3),
+                              cpu_newton_iterations=sum(n.iterations for n in r.newton),
+                              speedup=round(c0 / g0, 1))
+        dyn, cost = models_oracle(O)["cartpole"]
+        box = O.Box(4, 1, control_lower=-10.0, control_upper=10.0,
+                    state_lower=[-1.5, -np.inf, -np.inf, -np.inf],
+                    state_upper=[1.5, np.inf, np.inf, np.inf])
+        t = time.perf_counter()
+        r = O.admm_solve(dyn, cost, box, init2.states, init2.controls, rho=1.0, max_outer=3)
+        c2 = time.perf_counter() - t
+        per = c2 / max(1, sum(n.iterations for n in r.newton))
+        out["config2"].update(cpu_ms_per_newton_iteration=round(1e3 * per, 2),
+                              cpu_projected_s=round(per * it2, 1),
+                              projected_speedup=round(per * it2 / g2, 1),
+                              cpu_sample="first 3 ADMM outer iterations, oracle port, 1 core")
+    return out
+
+
 def config4_solve_leg(torch, P, logT: int = 20, damp: float = 0.9999):
     """Config 4 as a full constrained solve on one GPU: the barrier method
     (mu 0.1 -> 1e-4, zeta 0.2) on the T = 2^20, nx=12, nu=4 time-varying
@@ -898,6 +974,7 @@ def main() -> None:
     ap.add_argument("--no-mpc", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--no-c4solve", action="store_true")
+    ap.add_argument("--no-solves", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
