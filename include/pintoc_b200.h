@@ -196,6 +196,13 @@ typedef struct ptc_problem_desc {
   int32_t rollout;             /* candidate rollout: 0 auto (log-depth Newton sweeps for
                                   tree plans with horizon >= 1024), 1 sequential,
                                   2 log-depth (tree plans) */
+  /* time-block mode (config 4, horizon split across ranks): this solver
+   * holds stages [t_base, t_base + horizon) of a longer horizon; the model
+   * data, trajectories and z/v are the block's (states: horizon+1 rows, row 0
+   * = the block's first state).  block_last: the block ends the horizon
+   * (terminal cost and gradient live here).  Iterations then run through
+   * ptc_solver_block_phase.  Affine models with nx >= 8, tree plans. */
+  int32_t block_mode, t_base, block_last;
 } ptc_problem_desc;
 
 int64_t ptc_solver_workspace_bytes(const ptc_problem_desc* desc);
@@ -230,6 +237,33 @@ int ptc_solver_expand(ptc_solver* s, void* stream);
 int ptc_solver_lqr(ptc_solver* s, const double* alpha_host, void* stream);
 int ptc_solver_rollout(ptc_solver* s, void* stream);
 int ptc_solver_total_cost(ptc_solver* s, void* stream);
+
+/* One phase of a time-sharded Newton iteration (block_mode solvers); the
+ * caller runs the collective named after each phase between phases, every
+ * rank the same sequence (sharded.TimeShardedNewton).  R = solver dtype,
+ * CC = nx*nx + nx, VC = 3*nx*nx + 2*nx, all buffers device, (comps, 1, batch):
+ *   phase 0  cost partials, co-state up-sweep    out: CC  (R)   -> all-gather
+ *   phase 1  in: gathered co-state aggregates (world, CC); carry, co-state
+ *            down-sweep + expansion, value up-sweep  out: VC (R) -> all-gather
+ *   phase 2  in: gathered value aggregates; value carry + down-sweep + gains,
+ *            propagation up-sweep                out: CC  (R)   -> all-gather
+ *   phase 3  in: gathered propagation aggregates; propagation down-sweep
+ *            out: 6 (double): [sum du^2, sum du.d | max |du|, 3 LQR flag bits]
+ *            -> all-reduce SUM rows 0-1, MAX rows 2-5
+ *   phase 4  in: reduced phase-3 vector; rollout up-sweep of u + du
+ *            out: CC (R) -> all-gather
+ *   phase 5  in: gathered rollout aggregates; x0 = aux (nx, 1, batch): the
+ *            horizon's initial state; rollout down-sweep, cost partials
+ *            out: 7 (double): [cur l, cur c, cand l, cand c | diverged |
+ *            cur first infeasible, cand first infeasible (global stage*W +
+ *            row, 1e300 = none)] -> all-reduce SUM 0-3, MAX 4, MIN 5-6
+ *   phase 6  in: reduced phase-5 vector; trust-region control, round end
+ *            out: 2 (double): ADMM residual maxima -> all-reduce MAX
+ *   phase 7  in: reduced phase-6 vector; outer-loop control
+ *   phase 8  (rollout of buffer 0, problem.py:449) up-sweep  out: CC -> all-gather
+ *   phase 9  in: gathered phase-8 aggregates, aux = x0; down-sweep */
+int ptc_solver_block_phase(ptc_solver* s, int phase, const void* in, void* out, const void* aux,
+                           int rank, int world, void* stream);
 
 /* Copy a named buffer out (dst host or device).  Names: states, controls
  * (current trajectory), lam, P, R, M, d, Fx, Fu, PT, S, s, Gamma, gamma, dx,

@@ -39,6 +39,9 @@ class SolveSettings:
     chunk0: int = 0
     chunk: int = 0
     rollout: int = 0          # 0 auto, 1 sequential, 2 log-depth Newton sweeps
+    block_mode: int = 0       # time-block mode (sharded.TimeShardedNewton)
+    t_base: int = 0
+    block_last: int = 0
 
 
 def _dtype_code(torch, dtype) -> int:
@@ -126,6 +129,7 @@ class DeviceSolver:
         d.keep_round_controls = int(s.keep_round_controls)
         d.chunk0, d.chunk = s.chunk0, s.chunk
         d.rollout = s.rollout
+        d.block_mode, d.t_base, d.block_last = s.block_mode, s.t_base, s.block_last
         self.desc = d
         nbytes = self.lib.ptc_solver_workspace_bytes(C.byref(d))
         if nbytes < 0:
@@ -195,6 +199,13 @@ class DeviceSolver:
 
     def iterate(self, n: int = 1):
         N.check(self.lib.ptc_solver_iterate(self.handle, int(n), self.stream))
+
+    def block_phase(self, phase: int, inp=None, out=None, aux=None, rank: int = 0,
+                    world: int = 1):
+        """One phase of a time-sharded iteration (include/pintoc_b200.h)."""
+        ptr = lambda t: None if t is None else t.data_ptr()
+        N.check(self.lib.ptc_solver_block_phase(self.handle, int(phase), ptr(inp), ptr(out),
+                                                ptr(aux), int(rank), int(world), self.stream))
 
     def running(self) -> int:
         out = C.c_int32(0)

@@ -51,6 +51,7 @@ class ProblemDesc(C.Structure):
         ("keep_round_controls", C.c_int32),
         ("chunk0", C.c_int32), ("chunk", C.c_int32),
         ("rollout", C.c_int32),
+        ("block_mode", C.c_int32), ("t_base", C.c_int32), ("block_last", C.c_int32),
     ]
 
 
@@ -79,6 +80,8 @@ _SIGS = {
     "ptc_solver_load": (C.c_int, [C.c_void_p] * 5 + [C.c_int, C.c_void_p]),
     "ptc_solver_check_consistency": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "ptc_solver_iterate": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "ptc_solver_block_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "ptc_solver_running": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_void_p]),
     "ptc_solver_expand": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ptc_solver_lqr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -406,6 +406,8 @@ struct ptc_solver {
   virtual int total_cost(cudaStream_t s) = 0;
   virtual int info(const char* name, int64_t* numel, int32_t* es) = 0;
   virtual int read(const char* name, void* dst, int64_t bytes, int on_dev, cudaStream_t s) = 0;
+  virtual int block_phase(int phase, const void* in, void* out, const void* aux, int rank,
+                          int world, cudaStream_t s) = 0;
 };
 
 namespace ptc {
@@ -589,6 +591,18 @@ struct Solver final : ptc_solver {
     l.gam = c.template take<R>(nu * T * B);
     l.dX = c.template take<R>(nx * (T + 1) * B);
     l.dU = c.template take<R>(nu * T * B);
+    a.blk = d.block_mode ? 1 : 0;
+    a.blk_last = d.block_last ? 1 : 0;
+    a.t_base = d.block_mode ? d.t_base : 0;
+    a.lam_in = a.x_in = nullptr;
+    a.x0g = nullptr;
+    if (d.block_mode) {
+      l.block_mode = 1;
+      l.t_base = d.t_base;
+      l.no_terminal = d.block_last ? 0 : 1;
+      a.lam_in = c.template take<R>(nx * B);
+      a.x_in = c.template take<R>(nx * B);
+    }
     carve_lqr_tree(c, l, (int)nx, (int)nu);
     a.red = l.red;
     if (self) {
@@ -691,6 +705,11 @@ struct Solver final : ptc_solver {
       return fail(PTC_ERR_UNSUPPORTED, "LQR kernels not instantiated for nx=" +
                                            std::to_string(d.nx) + " nu=" + std::to_string(d.nu));
     ops = &it->second;
+    if (d.block_mode && !ops->block)
+      return fail(PTC_ERR_UNSUPPORTED, "time-block mode is implemented for affine models with "
+                                       "nx >= 8 (the config-4 systems)");
+    if (d.block_mode && auto_plan(d.batch, d.horizon, d.chunk0, d.chunk, d.nx).L < 1)
+      return fail(PTC_ERR_ARG, "time-block mode needs a tree plan (chunk0 < horizon)");
     Carver c{(char*)ws};
     size_t need = layout(d, c, this);
     if ((int64_t)need > bytes) return fail(PTC_ERR_WORKSPACE, "solver workspace too small");
@@ -775,11 +794,31 @@ struct Solver final : ptc_solver {
   }
 
   int iterate(int n, cudaStream_t s) override {
+    if (na.blk) return fail(PTC_ERR_ARG, "block_mode solvers iterate through ptc_solver_block_phase");
     if (n > 0 && !iter_exec && !graph_off && !getenv("PTC_NO_GRAPH")) build_iteration_graph();
     for (int i = 0; i < n; ++i) {
       if (iter_exec) PTC_CUDA(cudaGraphLaunch(iter_exec, s));
       else ops->iterate(&na, &la, s);
     }
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
+
+  int block_phase(int phase, const void* in, void* out, const void* aux, int rank, int world,
+                  cudaStream_t s) override {
+    if (!na.blk) return fail(PTC_ERR_ARG, "ptc_solver_block_phase needs a block_mode solver");
+    if (phase < 0 || phase > 9) return fail(PTC_ERR_ARG, "block phase must be 0..9");
+    if (world < 1 || rank < 0 || rank >= world) return fail(PTC_ERR_ARG, "bad rank / world");
+    if (na.blk_last != (rank == world - 1))
+      return fail(PTC_ERR_ARG, "block_last must be set exactly on rank world-1");
+    const bool needs_in = phase == 1 || phase == 2 || phase == 3 || phase == 4 || phase == 5 ||
+                          phase == 6 || phase == 7 || phase == 9;
+    const bool needs_out = phase <= 6 || phase == 8;
+    if (needs_in && !in) return fail(PTC_ERR_ARG, "this block phase needs its input buffer");
+    if (needs_out && !out) return fail(PTC_ERR_ARG, "this block phase needs its output buffer");
+    if ((phase == 5 || phase == 9) && !aux) return fail(PTC_ERR_ARG, "phases 5 and 9 need x0 (aux)");
+    na.x0g = static_cast<const R*>(aux);
+    ops->block(&na, &la, phase, in, out, rank, world, s);
     PTC_CUDA(cudaGetLastError());
     return PTC_OK;
   }
@@ -810,6 +849,7 @@ struct Solver final : ptc_solver {
   }
 
   int rollout(cudaStream_t s) override {
+    if (na.blk) return fail(PTC_ERR_ARG, "block_mode solvers roll out through block phases 8 / 9");
     PTC_CUDA(cudaMemsetAsync(na.bad_index, 0xff, sizeof(int) * na.B, s));
     ops->rollout(&na, s);
     PTC_CUDA(cudaGetLastError());
@@ -858,6 +898,8 @@ static int validate(const ptc_problem_desc* d) {
   if (d->batch < 1 || d->horizon < 1 || d->nx < 1 || d->nu < 1) return fail(PTC_ERR_ARG, "bad dims");
   if (d->nx > kMaxNX || d->nu > kMaxNU) return fail(PTC_ERR_ARG, "nx <= 12 and nu <= 6 required");
   if (d->method < 0 || d->method > 2) return fail(PTC_ERR_ARG, "bad method");
+  if (d->block_mode != 0 && d->block_mode != 1) return fail(PTC_ERR_ARG, "block_mode must be 0 or 1");
+  if (d->block_mode && d->t_base < 0) return fail(PTC_ERR_ARG, "t_base must be >= 0");
   if (d->model == PTC_DYN_LINEAR) {
     if (d->lin_rows != 1 && d->lin_rows != d->horizon) return fail(PTC_ERR_ARG, "lin_rows must be 1 or horizon");
     if (d->lin_batch != 1 && d->lin_batch != d->batch) return fail(PTC_ERR_ARG, "lin_batch must be 1 or batch");
@@ -911,6 +953,11 @@ int ptc_solver_check_consistency(ptc_solver* s, int32_t* bad, void* stream) {
 int ptc_solver_iterate(ptc_solver* s, int n, void* stream) {
   PTC_S(s);
   return s->iterate(n, (cudaStream_t)stream);
+}
+int ptc_solver_block_phase(ptc_solver* s, int phase, const void* in, void* out, const void* aux,
+                           int rank, int world, void* stream) {
+  PTC_S(s);
+  return s->block_phase(phase, in, out, aux, rank, world, (cudaStream_t)stream);
 }
 int ptc_solver_running(ptc_solver* s, int32_t* n, void* stream) {
   PTC_S(s);

@@ -131,6 +131,9 @@ struct NewtonOps {
   void (*expand)(const void* na, cudaStream_t s);
   void (*rollout)(const void* na, cudaStream_t s);
   void (*cost)(const void* na, cudaStream_t s);
+  // time-block phase (null: the model has no block mode)
+  void (*block)(const void* na, const void* la, int phase, const void* in, void* out, int rank,
+                int world, cudaStream_t s);
 };
 
 using LqrKey = std::tuple<int, int, int>;            // dtype, nx, nu
@@ -348,9 +351,17 @@ struct RegisterNewton {
                                                       P0, a.B);
     k_cost_finalize<R, NX><<<grid_for(a.B), kBlock, 0, s>>>(a);
   }
+  static void block(const void* p, const void* la, int phase, const void* in, void* out,
+                    int rank, int world, cudaStream_t s) {
+    if constexpr (kWideNewton<Dyn>)
+      WideNewton<R, NX, NU>::block_phase(A(p), *static_cast<const LqrArgs<R>*>(la),
+                                         lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).block,
+                                         phase, in, out, rank, world, s);
+  }
   RegisterNewton() {
     newton_registry()[NewtonKey(dtype_code<R>(), DYN, NX, NU)] =
-        NewtonOps{&lqr, &init, &check, &iterate, &expand, &rollout, &cost};
+        NewtonOps{&lqr, &init, &check, &iterate, &expand, &rollout, &cost,
+                  kWideNewton<Dyn> ? &block : nullptr};
   }
 };
 

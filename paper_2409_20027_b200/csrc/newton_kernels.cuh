@@ -61,6 +61,12 @@ struct NewtonArgs {
   double* rres;            // (P0, B) residual maxima of the rollout guess
   R* xr;                   // second state buffer of the parallel rollout (xsz)
   int pr_iters;            // Newton sweeps of the parallel rollout (0 = sequential)
+  // time-block mode (ptc_solver_block_phase): stages [t_base, t_base + T) of
+  // a longer horizon; blk_last = the block ends it (terminal cost / gradient)
+  int blk, blk_last, t_base;
+  R* lam_in;               // (nx, 1, B) co-state entering at the block end
+  R* x_in;                 // (nx, 1, B) state at the block start (rollout carry)
+  const R* x0g;            // (nx, 1, B) the horizon's initial state (phase argument)
 };
 
 template <typename R>
@@ -941,6 +947,7 @@ PTC_D double finalize_cost(const NewtonArgs<R>& a, int which, int q, int b, int&
     int bj = int(cp[((size_t)2 * P0 + j) * a.B + b]);
     if (bad < 0 && bj >= 0) bad = bj;
   }
+  if (a.blk) return sl + sc;   // block mode: the terminal cost is in the reduced partials
   R xT[NX];
   ld_x(a, q, a.T, b, xT);
   double term = double(terminal_cost(*a.pp, xT));

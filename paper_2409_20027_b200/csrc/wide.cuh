@@ -1510,7 +1510,7 @@ void launch_lqr_block_wide(const LqrArgs<R>& a0, int phase, const void* blocks, 
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (phase == 0) {
-    if (a.staged) launch_stage_in<R, NX, NU>(a, s);
+    if (a.staged && !a.prestaged) launch_stage_in<R, NX, NU>(a, s);
     PTC_WL((kw_value_up0<R, NX, NU>), P0 * B, S::kUp0)(a);
     for (int l = 1; l < pl.L; ++l) PTC_WL((kw_value_up<R, NX, NU>), pl.n[l + 1] * B, S::kUp)(a, l);
     PTC_WL((kw_value_block<R, NX, NU>), B, S::kUp)(a, static_cast<R*>(out));

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(64) kwn_costate_up0(NewtonArgs<R> a) {
       m[NX * NX + i] = lx + aug[i];
     }
     __syncwarp();
-    if (t == T - 1) {
+    if (t == T - 1 && (!a.blk || a.blk_last)) {
       w_ld<NX>(a.X + q * a.xsz, T, T + 1, B, b, v0);
       for (int i = ln; i < NX; i += 32) {
         R s = R(0);
@@ -310,8 +310,16 @@ __global__ void __launch_bounds__(64) kwn_tree_top(NewtonArgs<R> a, int gate, in
   R* x = slab;
   R* m = x + N::CC;
   R* y = m + N::CC;
-  if (kRev) w_fill<NX>(x, R(0));
-  else w_ld<NX>(a.X + (xbuf < 0 ? a.parity[b] : xbuf) * a.xsz, 0, a.T + 1, a.B, b, x);  // x_0
+  if (kRev) {
+    // co-state entering at the horizon end: 0 (the last chunk absorbed the
+    // terminal gradient), or the later blocks' carry in block mode
+    if (a.blk && !a.blk_last) w_ld<NX>(a.lam_in, 0, 1, a.B, b, x);
+    else w_fill<NX>(x, R(0));
+  } else if (a.blk) {
+    w_ld<NX>(a.x_in, 0, 1, a.B, b, x);   // state at the block start
+  } else {
+    w_ld<NX>(a.X + (xbuf < 0 ? a.parity[b] : xbuf) * a.xsz, 0, a.T + 1, a.B, b, x);  // x_0
+  }
   for (int s = 0; s < nL; ++s) {
     const int i = kRev ? nL - 1 - s : s;
     w_st<NX>(a.ccar[L], i, nL, a.B, b, x);
@@ -360,7 +368,10 @@ __global__ void __launch_bounds__(64) kwn_costate_down0(NewtonArgs<R> a, R* xst)
   R* aug = lt + NX;
   const int ln = lane_id();
   const R* X = a.X + q * a.xsz;
-  if (j == P0 - 1) {
+  if (j == P0 - 1 && a.blk && !a.blk_last) {
+    w_ld<NX>(a.lam_in, 0, 1, B, b, lnx);   // carry from the later blocks
+    w_st<NX>(a.lam, T, T + 1, B, b, lnx);
+  } else if (j == P0 - 1) {
     w_ld<NX>(X, T, T + 1, B, b, lt);
     for (int i = ln; i < NX; i += 32) {
       R s = R(0);
@@ -520,7 +531,10 @@ __global__ void __launch_bounds__(64) kwn_roll_down0(NewtonArgs<R> a, const R* d
   R* uu = Bm + NX * NU;
   R* du = uu + NU;
   const int ln = lane_id();
-  if (j == 0) {
+  if (j == 0 && a.blk) {
+    w_ld<NX>(a.x_in, 0, 1, B, b, x);
+    w_st<NX>(Xc, 0, T + 1, B, b, x);
+  } else if (j == 0) {
     w_ld<NX>(a.X + q * a.xsz, 0, T + 1, B, b, x);
     if (kMode == 1) w_st<NX>(Xc, 0, T + 1, B, b, x);
   } else {
@@ -531,6 +545,7 @@ __global__ void __launch_bounds__(64) kwn_roll_down0(NewtonArgs<R> a, const R* d
           gf_traj(a.U + q * a.usz, T, B, b), gf_traj(dU, T, B, b));
   if (t0 < t1) pf.load(t0);
   bool finite = true;
+  int first_bad = -1;
   for (int t = t0; t < t1; ++t) {
     pf.store(F);
     if (t + 1 < t1) pf.load(t + 1);
@@ -547,6 +562,7 @@ __global__ void __launch_bounds__(64) kwn_roll_down0(NewtonArgs<R> a, const R* d
 #pragma unroll
       for (int k = 1; k < NU; ++k) bu = fma(Bm[i * NU + k], uu[k], bu);
       const R xn = (ax + bu) + c[i];
+      if (finite && !isfinite(xn)) first_bad = t + 1;
       finite = finite && isfinite(xn);
       y[i] = xn;
       Xc[((size_t)i * (T + 1) + t + 1) * B + b] = xn;
@@ -555,7 +571,17 @@ __global__ void __launch_bounds__(64) kwn_roll_down0(NewtonArgs<R> a, const R* d
     if (ln < NX) x[ln] = y[ln];
     __syncwarp();
   }
-  if (__any_sync(0xffffffffu, !finite) && ln == 0) atomicOr(a.rstate + b, RS_FALLBACK);
+  if (!a.blk) {
+    if (__any_sync(0xffffffffu, !finite) && ln == 0) atomicOr(a.rstate + b, RS_FALLBACK);
+  } else if (kMode == 1) {
+    // block mode has no sequential fallback (the recurrence crosses ranks):
+    // a non-finite candidate is a rejected step, as the reference's
+    // DivergenceError inside newton_solve
+    if (__any_sync(0xffffffffu, !finite) && ln == 0) atomicOr(a.flags + b, FLAG_DIVERGED);
+  } else if (!finite) {
+    // rollout API: first non-finite global state index (min over chunks)
+    atomicMin(reinterpret_cast<unsigned*>(a.bad_index + b), unsigned(a.t_base + first_bad));
+  }
 }
 
 // ------------------------------------------------------------ sequential
@@ -655,7 +681,167 @@ __global__ void __launch_bounds__(32) kwn_rollout_seq(NewtonArgs<R> a, const R* 
   if (kMode == 1 && __any_sync(0xffffffffu, !finite) && ln == 0) atomicOr(a.flags + b, FLAG_DIVERGED);
 }
 
+// ------------------------------------------------------------ time blocks
+
+// the block's whole map: fold the top tree level (kRev: reverse order) into
+// one affine aggregate, out (CC, 1, B)
+template <typename R, int NX, int NU, bool kRev>
+__global__ void __launch_bounds__(64) kwn_tree_block(NewtonArgs<R> a, R* out, int gate) {
+  PTC_NW_PROLOGUE(1, gate, NSlab<R, NX, NU>::kTree)
+  const int L = a.plan.L, nL = a.plan.n[L];
+  R* acc = slab;
+  R* m = acc + N::CC;
+  R* o = m + N::CC;
+  w_ld<N::CC>(a.cagg[L], kRev ? nL - 1 : 0, nL, a.B, b, acc);
+  for (int s = 1; s < nL; ++s) {
+    w_ld<N::CC>(a.cagg[L], kRev ? nL - 1 - s : s, nL, a.B, b, m);
+    w_aff_compose<R, NX>(m, acc, o);
+    R* sw = acc;
+    acc = o;
+    o = sw;
+  }
+  w_st<N::CC>(out, 0, 1, a.B, b, acc);
+}
+
+// carry entering this rank's block from the gathered block maps
+// g (world, CC, 1, B): kRev: co-state at the block end = maps of ranks
+// world-1 .. rank+1 applied to 0 (the last block's map is constant);
+// forward: state at the block start = maps of ranks 0 .. rank-1 applied to x0
+template <typename R, int NX, int NU, bool kRev>
+__global__ void __launch_bounds__(64) kwn_blk_carry(NewtonArgs<R> a, const R* g, int rank,
+                                                    int world, int gate) {
+  PTC_NW_PROLOGUE(1, gate, NSlab<R, NX, NU>::kTree)
+  if (kRev && a.blk_last) return;
+  R* x = slab;
+  R* m = x + N::CC;
+  R* y = m + N::CC;
+  const size_t stride = (size_t)N::CC * a.B;
+  if (kRev) {
+    w_fill<NX>(x, R(0));
+    for (int k = world - 1; k > rank; --k) {
+      w_ld<N::CC>(g + k * stride, 0, 1, a.B, b, m);
+      w_aff_apply_inplace<R, NX>(m, x, y);
+    }
+    w_st<NX>(a.lam_in, 0, 1, a.B, b, x);
+  } else {
+    w_ld<NX>(a.x0g, 0, 1, a.B, b, x);
+    for (int k = 0; k < rank; ++k) {
+      w_ld<N::CC>(g + k * stride, 0, 1, a.B, b, m);
+      w_aff_apply_inplace<R, NX>(m, x, y);
+    }
+    w_st<NX>(a.x_in, 0, 1, a.B, b, x);
+  }
+}
+
 #undef PTC_NW_PROLOGUE
+
+// Reduction vectors exchanged between ranks (ptc_solver_block_phase): each
+// folds the per-chunk partial rows into one value per problem (export) and
+// writes the all-reduced value back as row 0 with identity rows after it
+// (import), so k_control / k_outer read the horizon-wide numbers.
+template <typename R>
+__global__ void k_blk_export_red(NewtonArgs<R> a, double* out) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int P0 = a.plan.units0(), B = a.B;
+  double s2 = 0.0, sd = 0.0, mx = 0.0;
+  for (int j = 0; j < partial_rows(P0); ++j) {
+    s2 += a.red[((size_t)0 * P0 + j) * B + b];
+    sd += a.red[((size_t)1 * P0 + j) * B + b];
+    mx = nanmax(mx, a.red[((size_t)2 * P0 + j) * B + b]);
+  }
+  const int fl = a.flags[b];
+  out[0 * B + b] = s2;
+  out[1 * B + b] = sd;
+  out[2 * B + b] = mx;
+  out[3 * B + b] = (fl & FLAG_DEF_R) ? 1.0 : 0.0;
+  out[4 * B + b] = (fl & FLAG_DEF_Q) ? 1.0 : 0.0;
+  out[5 * B + b] = (fl & FLAG_COND) ? 1.0 : 0.0;
+}
+
+template <typename R>
+__global__ void k_blk_import_red(NewtonArgs<R> a, const double* in) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int P0 = a.plan.units0(), B = a.B;
+  for (int f = 0; f < 3; ++f)
+    for (int j = 0; j < partial_rows(P0); ++j)
+      a.red[((size_t)f * P0 + j) * B + b] = j == 0 ? in[f * B + b] : 0.0;
+  int fl = a.flags[b];
+  if (in[3 * B + b] > 0.0) fl |= FLAG_DEF_R;
+  if (in[4 * B + b] > 0.0) fl |= FLAG_DEF_Q;
+  if (in[5 * B + b] > 0.0) fl |= FLAG_COND;
+  a.flags[b] = fl;
+}
+
+template <typename R, int NX>
+__global__ void k_blk_export_cost(NewtonArgs<R> a, double* out) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int P0 = a.plan.units0(), B = a.B, W = a.pp->W;
+  for (int w = 0; w < 2; ++w) {
+    const double* cp = a.cpart[w];
+    double sl = 0.0, sc = 0.0;
+    int bad = -1;
+    for (int j = 0; j < partial_rows(P0); ++j) {
+      sl += cp[((size_t)0 * P0 + j) * B + b];
+      sc += cp[((size_t)1 * P0 + j) * B + b];
+      const int bj = int(cp[((size_t)2 * P0 + j) * B + b]);
+      if (bad < 0 && bj >= 0) bad = bj;
+    }
+    if (a.blk_last) {
+      R xT[NX];
+      ld_x(a, w == 0 ? a.parity[b] : 1 - a.parity[b], a.T, b, xT);
+      sl += double(terminal_cost(*a.pp, xT));
+    }
+    out[(2 * w + 0) * B + b] = sl;
+    out[(2 * w + 1) * B + b] = sc;
+    out[(5 + w) * B + b] = bad >= 0 ? double(bad) + double(a.t_base) * W : 1e300;
+  }
+  out[4 * B + b] = (a.flags[b] & FLAG_DIVERGED) ? 1.0 : 0.0;
+}
+
+template <typename R>
+__global__ void k_blk_import_cost(NewtonArgs<R> a, const double* in) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int P0 = a.plan.units0(), B = a.B;
+  for (int w = 0; w < 2; ++w) {
+    double* cp = a.cpart[w];
+    const double bad = in[(5 + w) * B + b];
+    for (int j = 0; j < partial_rows(P0); ++j) {
+      cp[((size_t)0 * P0 + j) * B + b] = j == 0 ? in[(2 * w + 0) * B + b] : 0.0;
+      cp[((size_t)1 * P0 + j) * B + b] = j == 0 ? in[(2 * w + 1) * B + b] : 0.0;
+      cp[((size_t)2 * P0 + j) * B + b] = (j == 0 && bad < 1e299) ? bad : -1.0;
+    }
+  }
+  if (in[4 * B + b] > 0.0) a.flags[b] |= FLAG_DIVERGED;
+}
+
+template <typename R>
+__global__ void k_blk_export_apart(NewtonArgs<R> a, double* out) {
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int P0 = a.plan.units0(), B = a.B;
+  double rp = 0.0, rd = 0.0;
+  if (a.apart)
+    for (int j = 0; j < partial_rows(P0); ++j) {
+      rp = nanmax(rp, a.apart[((size_t)0 * P0 + j) * B + b]);
+      rd = nanmax(rd, a.apart[((size_t)1 * P0 + j) * B + b]);
+    }
+  out[0 * B + b] = rp;
+  out[1 * B + b] = rd;
+}
+
+template <typename R>
+__global__ void k_blk_import_apart(NewtonArgs<R> a, const double* in) {
+  const int b = unit_id();
+  if (b >= a.B || !a.apart) return;
+  const int P0 = a.plan.units0(), B = a.B;
+  for (int f = 0; f < 2; ++f)
+    for (int j = 0; j < partial_rows(P0); ++j)
+      a.apart[((size_t)f * P0 + j) * B + b] = j == 0 ? in[f * B + b] : 0.0;
+}
 
 // ------------------------------------------------------------ launchers
 
@@ -705,6 +891,104 @@ struct WideNewton {
 
   static void rollout_seq(const NewtonArgs<R>& a, const R* dU, cudaStream_t s) {
     kwn_rollout_seq<R, NX, NU, 1><<<(unsigned)a.B, 32, kSeqSmem, s>>>(a, dU, 0);
+  }
+
+  // One phase of a time-sharded iteration (include/pintoc_b200.h
+  // ptc_solver_block_phase); the caller exchanges `out` between ranks.
+  template <class LqrBlock>
+  static void block_phase(const NewtonArgs<R>& a, const LqrArgs<R>& la, LqrBlock lqr_block,
+                          int phase, const void* in, void* out, int rank, int world,
+                          cudaStream_t s) {
+    const Plan& pl = a.plan;
+    const long long B = a.B, P0 = pl.units0();
+    const int tb = W::smem(N::kTree);
+    const dim3 g1 = W::grid(B);
+    const unsigned gB = (unsigned)((B + 127) / 128);
+    const bool fold = partial_rows((int)P0) < (int)P0;
+    constexpr int kOpsRed = RED_SUM | (RED_SUM << 2) | (RED_MAX << 4);
+    constexpr int kOpsCost = RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4);
+    LqrArgs<R> l2 = la;
+    l2.prestaged = (la.xst && B == 1) ? 1 : 0;
+    R* o = static_cast<R*>(out);
+    const R* gin = static_cast<const R*>(in);
+    const double* din = static_cast<const double*>(in);
+    double* dout = static_cast<double*>(out);
+    auto up_levels = [&](auto kRevTag, int gate) {
+      constexpr bool kRev = decltype(kRevTag)::value;
+      for (int l = 1; l < pl.L; ++l)
+        kwn_tree_up<R, NX, NU, kRev><<<W::grid(pl.n[l + 1] * B), 32 * kWarpsPerBlock, tb, s>>>(a, l, gate);
+      kwn_tree_block<R, NX, NU, kRev><<<g1, 32 * kWarpsPerBlock, tb, s>>>(a, o, gate);
+    };
+    auto down_levels = [&](auto kRevTag, int gate) {
+      constexpr bool kRev = decltype(kRevTag)::value;
+      kwn_blk_carry<R, NX, NU, kRev><<<g1, 32 * kWarpsPerBlock, tb, s>>>(a, gin, rank, world, gate);
+      kwn_tree_top<R, NX, NU, kRev><<<g1, 32 * kWarpsPerBlock, tb, s>>>(a, gate, -1);
+      for (int l = pl.L - 1; l >= 1; --l)
+        kwn_tree_down<R, NX, NU, kRev><<<W::grid(pl.n[l + 1] * B), 32 * kWarpsPerBlock, tb, s>>>(a, l, gate);
+    };
+    using Rev = std::true_type;
+    using Fwd = std::false_type;
+    switch (phase) {
+      case 0:
+        cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
+        k_cost_partials<R, NX, NU><<<(unsigned)((P0 * B + 127) / 128), 128, 0, s>>>(a, 0);
+        kwn_costate_up0<R, NX, NU><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kCoUp0), s>>>(a);
+        up_levels(Rev{}, 1);
+        break;
+      case 1:
+        down_levels(Rev{}, 1);
+        kwn_costate_down0<R, NX, NU><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kCoDown0), s>>>(
+            a, l2.prestaged ? la.xst : nullptr);
+        lqr_block(&l2, 0, nullptr, out, rank, world, s);
+        break;
+      case 2:
+        lqr_block(&l2, 1, in, out, rank, world, s);
+        break;
+      case 3:
+        lqr_block(&l2, 2, in, nullptr, rank, world, s);
+        if (fold) k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.red, 3, kOpsRed, (int)P0, (int)B);
+        k_blk_export_red<R><<<gB, 128, 0, s>>>(a, dout);
+        break;
+      case 4:
+        k_blk_import_red<R><<<gB, 128, 0, s>>>(a, din);
+        k_roll_gate<R><<<gB, 128, 0, s>>>(a);
+        kwn_roll_up0<R, NX, NU, 1><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kRollUp0), s>>>(a, la.dU);
+        up_levels(Fwd{}, 2);
+        break;
+      case 5:
+        down_levels(Fwd{}, 2);
+        kwn_roll_down0<R, NX, NU, 1><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kRollDown0), s>>>(a, la.dU);
+        k_cost_partials<R, NX, NU><<<(unsigned)((P0 * B + 127) / 128), 128, 0, s>>>(a, 1);
+        if (fold) {
+          k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[0], 3, kOpsCost, (int)P0, (int)B);
+          k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[1], 3, kOpsCost, (int)P0, (int)B);
+        }
+        k_blk_export_cost<R, NX><<<gB, 128, 0, s>>>(a, dout);
+        break;
+      case 6:
+        k_blk_import_cost<R><<<gB, 128, 0, s>>>(a, din);
+        k_control<R, NX><<<gB, 128, 0, s>>>(a);
+        k_round_end<R, NX, NU><<<(unsigned)((P0 * B + 127) / 128), 128, 0, s>>>(a);
+        if (fold && a.apart && a.opt.method == METHOD_ADMM)
+          k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.apart, 2, RED_MAX | (RED_MAX << 2), (int)P0, (int)B);
+        k_blk_export_apart<R><<<gB, 128, 0, s>>>(a, dout);
+        break;
+      case 7:
+        k_blk_import_apart<R><<<gB, 128, 0, s>>>(a, din);
+        k_outer<R><<<gB, 128, 0, s>>>(a);
+        break;
+      case 8:
+        cudaMemsetAsync(a.bad_index, 0xff, sizeof(int) * B, s);
+        kwn_roll_up0<R, NX, NU, 0><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kRollUp0), s>>>(a, nullptr);
+        up_levels(Fwd{}, 0);
+        break;
+      case 9:
+        down_levels(Fwd{}, 0);
+        kwn_roll_down0<R, NX, NU, 0><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kRollDown0), s>>>(a, nullptr);
+        break;
+      default:
+        break;
+    }
   }
 
   // problem.py `rollout`: the affine scan on tree plans with the log-depth

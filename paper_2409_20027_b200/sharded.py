@@ -167,3 +167,175 @@ class CudaBlockOps:
 
     def propagate(self, gathered):
         self._run(2, gathered.contiguous(), None)
+
+
+# ------------------------------------------------- time-sharded Newton solve
+
+# reduction layout of the exchanged vectors (include/pintoc_b200.h,
+# ptc_solver_block_phase): (first row, end row, op) per phase
+_RED_SPECS = {
+    3: ((0, 2, "sum"), (2, 6, "max")),
+    5: ((0, 4, "sum"), (4, 5, "max"), (5, 7, "min")),
+    6: ((0, 2, "max"),),
+}
+
+
+def split_dynamics(dyn, world: int, rank: int):
+    """(t_base, block dynamics) of rank's contiguous time block of a
+    TimeVaryingLinearDynamics (config 4's time-varying affine model)."""
+    from .systems import TimeVaryingLinearDynamics
+    if not isinstance(dyn, TimeVaryingLinearDynamics):
+        raise TypeError("time-sharded solves take a TimeVaryingLinearDynamics model")
+    t0, m = block_bounds(dyn.horizon, world, rank)
+    return t0, TimeVaryingLinearDynamics(dyn.A[t0:t0 + m], dyn.B[t0:t0 + m],
+                                         dyn.offset[t0:t0 + m])
+
+
+class BlockNewton:
+    """One rank's time block of a Newton / barrier / ADMM solve: a
+    block-mode device solver (stages [t_base, t_base + T) of the horizon)
+    plus the buffers it exchanges with the other ranks."""
+
+    def __init__(self, block_dynamics, cost, constraints, batch: int, settings, rank: int,
+                 world: int, t_base: int, dtype=None):
+        from dataclasses import replace
+        from ._device import DeviceSolver
+        torch = N.require_cuda()
+        self.torch = torch
+        self.rank, self.world, self.t_base = int(rank), int(world), int(t_base)
+        st = replace(settings, block_mode=1, t_base=int(t_base),
+                     block_last=int(rank == world - 1), keep_round_controls=False)
+        self.solver = s = DeviceSolver(block_dynamics, cost, constraints, batch, st, dtype=dtype)
+        nx, B = s.nx, s.B
+        cc, vc = nx * nx + nx, 3 * nx * nx + 2 * nx
+        mk = lambda c, dt: torch.empty(c, 1, B, dtype=dt, device=s.device)
+        self.outs = {0: mk(cc, s.dtype), 1: mk(vc, s.dtype), 2: mk(cc, s.dtype),
+                     3: mk(6, torch.float64), 4: mk(cc, s.dtype), 5: mk(7, torch.float64),
+                     6: mk(2, torch.float64), 8: mk(cc, s.dtype)}
+        self.x0 = None
+
+    def phase(self, p: int, inp=None):
+        out = self.outs.get(p)
+        aux = self.x0 if p in (5, 9) else None
+        self.solver.block_phase(p, None if inp is None else inp.contiguous(), out, aux,
+                                self.rank, self.world)
+        return out
+
+
+class _Emulated:
+    """All ranks' blocks in one process on one device, run phase by phase in
+    rank order; gathers become stacks and all-reduces elementwise folds
+    (no kernel ever waits on another rank's)."""
+
+    def gather(self, outs):
+        import torch
+        g = torch.stack(outs)
+        return [g] * len(outs)
+
+    def reduce(self, outs, spec):
+        import torch
+        r = outs[0].clone()
+        for a, b, op in spec:
+            st = torch.stack([o[a:b] for o in outs])
+            r[a:b] = {"sum": st.sum(0), "max": st.amax(0), "min": st.amin(0)}[op]
+        return [r] * len(outs)
+
+
+class _Distributed:
+    """One block per process; NCCL (or gloo) collectives on the current
+    stream between the phases."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self._gather = nccl_gather(group)
+
+    def gather(self, outs):
+        return [self._gather(outs[0])]
+
+    def reduce(self, outs, spec):
+        import torch.distributed as dist
+        ops = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}
+        t = outs[0]
+        for a, b, op in spec:
+            part = t[a:b].contiguous()
+            dist.all_reduce(part, op=ops[op], group=self.group)
+            t[a:b] = part
+        return [t]
+
+
+class TimeShardedNewton:
+    """Newton / barrier / ADMM solve of one long horizon split into time
+    blocks (config 4): every scan of the iteration -- co-state, value,
+    propagation, candidate rollout -- folds each block into one aggregate,
+    the aggregates are all-gathered and each rank finishes its block from
+    the carry; the trust-region and outer-loop scalars (cost, step norm,
+    predicted reduction, ADMM residuals, subproblem flags) are all-reduced
+    before the per-problem control runs, so every rank takes the same
+    accept / reject and outer decisions (newton.py:157-208, outer.py).
+
+    ``blocks`` are the BlockNewton objects this process drives: all ranks'
+    (``emulate=True``, one device) or its own one (a torch.distributed group
+    with one process per GPU)."""
+
+    def __init__(self, blocks, emulate: bool = False, group=None):
+        self.blocks = list(blocks)
+        self.comm = _Emulated() if emulate else _Distributed(group)
+
+    def _round(self, p, outs):
+        if p in _RED_SPECS:
+            return self.comm.reduce(outs, _RED_SPECS[p])
+        return self.comm.gather(outs)
+
+    def set_initial_state(self, x0):
+        """x0 (B, nx): the horizon's initial states (every rank passes the same)."""
+        torch = self.blocks[0].torch
+        for bl in self.blocks:
+            s = bl.solver
+            bl.x0 = torch.as_tensor(x0, dtype=s.dtype).reshape(s.B, s.nx).t().contiguous() \
+                .unsqueeze(1).to(s.device)
+
+    def rollout(self, controls):
+        """problem.py:449 over the split horizon: ``controls`` = per-block
+        (B, T_block, nu) arrays; returns per-block (B, T_block + 1, nx)
+        device states (row 0 = the block's first state)."""
+        torch = self.blocks[0].torch
+        for bl, U in zip(self.blocks, controls):
+            s = bl.solver
+            X = torch.zeros(s.B, s.T + 1, s.nx, dtype=s.dtype)
+            s.load(X, U)
+        outs = [bl.phase(8) for bl in self.blocks]
+        ins = self.comm.gather(outs)
+        for bl, g in zip(self.blocks, ins):
+            bl.phase(9, g)
+        return [bl.solver.field("states", bl.solver.T + 1, (bl.solver.nx,)).contiguous()
+                for bl in self.blocks]
+
+    def iteration(self):
+        outs = [bl.phase(0) for bl in self.blocks]
+        for p in (1, 2, 3, 4, 5, 6):
+            ins = self._round(p - 1, outs)
+            outs = [bl.phase(p, g) for bl, g in zip(self.blocks, ins)]
+        ins = self._round(6, outs)
+        for bl, g in zip(self.blocks, ins):
+            bl.phase(7, g)
+
+    def solve(self, states, controls, z=None, v=None, group_iters: int = 4):
+        """Load per-block trajectories (B, T_block + 1, nx) / (B, T_block, nu)
+        and iterate until every problem is done.  Returns the number of
+        device iterations launched."""
+        for k, bl in enumerate(self.blocks):
+            bl.solver.load(states[k], controls[k], None if z is None else z[k],
+                           None if v is None else v[k])
+        s0 = self.blocks[0].solver
+        st = s0.settings
+        rounds = max(1, st.max_outer if st.method == N.METHOD_ADMM else 64)
+        cap = (st.max_iters + 2) * rounds + 16
+        launched, n = 0, 1
+        while launched < cap:
+            for _ in range(n):
+                self.iteration()
+            launched += n
+            if s0.running() == 0:
+                break
+            n = group_iters
+        return launched
