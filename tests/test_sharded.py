@@ -176,3 +176,73 @@ def test_cuda_time_blocks_through_nccl_gather_world1():
             assert rel_gap(got, want) < 1e-9, name
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------- time-sharded Newton driver plumbing
+
+class _FakeBlock:
+    """Stands in for sharded.BlockNewton: deterministic per-(phase, rank)
+    outputs of the real shapes, records what each phase received."""
+
+    def __init__(self, rank, world, nx=3, B=2):
+        self.rank, self.world, self.B = rank, world, B
+        cc, vc = nx * nx + nx, 3 * nx * nx + 2 * nx
+        self.rows = {0: cc, 1: vc, 2: cc, 3: 6, 4: cc, 5: 7, 6: 2, 8: cc}
+        self.got = {}
+
+    def phase(self, p, inp=None):
+        self.got[p] = None if inp is None else inp.clone()
+        if p not in self.rows:
+            return None
+        g = torch.Generator().manual_seed(1000 * p + self.rank)
+        return torch.randn(self.rows[p], 1, self.B, generator=g, dtype=torch.float64)
+
+
+def _expected_inputs(world):
+    from paper_2409_20027_b200.sharded import _RED_SPECS
+    fakes = [_FakeBlock(r, world) for r in range(world)]
+    outs = {p: [f.phase(p) for f in fakes] for p in (0, 1, 2, 3, 4, 5, 6)}
+    exp = {}
+    for p in (1, 2, 3, 5):
+        exp[p] = torch.stack(outs[p - 1])
+    for p, src in ((4, 3), (6, 5), (7, 6)):
+        r = outs[src][0].clone()
+        for a, b, op in _RED_SPECS[src]:
+            st = torch.stack([o[a:b] for o in outs[src]])
+            r[a:b] = {"sum": st.sum(0), "max": st.amax(0), "min": st.amin(0)}[op]
+        exp[p] = r
+    return exp
+
+
+def _newton_plumbing_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_20027_b200.sharded import TimeShardedNewton
+        fb = _FakeBlock(rank, world)
+        TimeShardedNewton([fb]).iteration()
+        torch.save(fb.got, os.path.join(out, f"g{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_time_sharded_newton_driver_collectives_gloo(world, tmp_path):
+    """The driver's exchange plan over a real process group (gloo, CPU):
+    after phases 0, 1, 2 and 4 every rank receives the rank-major stack of
+    all ranks' block maps; after 3, 5 and 6 the trust-region vectors reduced
+    with the per-row SUM / MAX / MIN of include/pintoc_b200.h -- identical to
+    the single-process emulation the GPU parity tests use."""
+    from paper_2409_20027_b200.sharded import TimeShardedNewton
+    mp.spawn(_newton_plumbing_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+             join=True)
+    exp = _expected_inputs(world)
+    fakes = [_FakeBlock(r, world) for r in range(world)]
+    TimeShardedNewton(fakes, emulate=True).iteration()
+    for r in range(world):
+        got = torch.load(os.path.join(tmp_path, f"g{r}.pt"))
+        assert got[0] is None
+        for p in range(1, 8):
+            # gloo's ring sum associates differently: equal to the last ulp
+            assert torch.allclose(got[p], exp[p], rtol=1e-14, atol=0), (r, p)
+            assert torch.equal(fakes[r].got[p], exp[p]), (r, p)
