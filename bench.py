@@ -530,10 +530,13 @@ def run_ours(args) -> None:
     solves = None
     if rank == 0 and world == 1 and not args.no_solves:
         solves = single_solve_leg(torch, P, cpu=not args.no_cpu_baseline)
-    c4solve = None
+    c4solve = c4shard = None
     if rank == 0 and world == 1 and not args.no_c4solve:
         torch.cuda.empty_cache()
         c4solve = config4_solve_leg(torch, P)
+    if not args.no_c4solve:
+        torch.cuda.empty_cache()
+        c4shard = config4_sharded_solve_leg(torch, P, world, rank)
 
     if rank == 0:
         cpu = None
@@ -557,7 +560,7 @@ def run_ours(args) -> None:
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk, "ill_posed_subproblems": ill_posed,
             "lqr_latency_sweep": sweep, "newton_latency_sweep": nsweep,
-            "long_horizon": longh, "config4_solve": c4solve, "single_solves": solves, "mpc_config3": mpc, "fp32": fp32,
+            "long_horizon": longh, "config4_solve": c4solve, "config4_sharded_solve": c4shard, "single_solves": solves, "mpc_config3": mpc, "fp32": fp32,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -890,6 +893,71 @@ def single_solve_leg(torch, P, cpu: bool = True):
                               projected_speedup=round(per * it2 / g2, 1),
                               cpu_sample="first 3 ADMM outer iterations, oracle port, 1 core")
     return out
+
+
+def config4_sharded_solve_leg(torch, P, world: int, rank: int, logT: int = 20,
+                              damp: float = 0.9999):
+    """The config-4 barrier solve of config4_solve_leg with the horizon split
+    into `world` contiguous time blocks, one per rank (sharded.
+    TimeShardedNewton: every scan of the Newton iteration exchanges one
+    block map per rank by NCCL all-gather, the trust-region scalars by
+    all-reduce).  Every rank draws the same seeded system on its device and
+    keeps its block.  Timed on the device (CUDA events around the solve, max
+    over ranks); at N = 1 it is the same block path with one block."""
+    import torch.distributed as dist
+    from paper_2409_20027_b200 import _native as N
+    from paper_2409_20027_b200._device import SolveSettings
+    from paper_2409_20027_b200.sharded import BlockNewton, TimeShardedNewton, block_bounds
+    T, nx, nu = 1 << logT, 12, 4
+    dev = torch.device("cuda")
+    f64 = torch.float64
+    g = torch.Generator(device=dev).manual_seed(20028)
+    band = torch.zeros(nx, nx, dtype=f64, device=dev)
+    for i in range(4):
+        for j in (i, i + 1):
+            if j < 4:
+                band[3 * i:3 * i + 3, 3 * j:3 * j + 3] = 1.0
+    t0, m = block_bounds(T, world, rank)
+    F = torch.randn(T, nx, nx, generator=g, device=dev, dtype=f64) * (0.2 ** 0.5) * band
+    A = (damp * (torch.eye(nx, dtype=f64, device=dev) + 0.01 * F[t0:t0 + m])).cpu().numpy()
+    del F
+    Bm = torch.randn(T, nx, nu, generator=g, device=dev, dtype=f64) * (0.1 ** 0.5)
+    Bm = Bm[t0:t0 + m].cpu().numpy()
+    qd = torch.empty(nx, dtype=f64, device=dev).uniform_(0.1, 10.0, generator=g).cpu().numpy()
+    x0 = torch.randn(nx, generator=g, device=dev, dtype=f64).cpu().numpy()
+    dyn = P.TimeVaryingLinearDynamics(A, Bm)
+    del A, Bm
+    cost = P.QuadraticCost(np.diag(qd), 0.1 * np.eye(nu), 10 * np.diag(qd))
+    box = P.BoxConstraint(nx, nu, control_lower=-2.0, control_upper=2.0)
+    opts = P.BarrierOptions(mu0=0.1, zeta=0.2, mu_tol=1e-4, newton=P.NewtonOptions(max_iters=50))
+    st = SolveSettings(method=N.METHOD_BARRIER, max_iters=50, mu0=opts.mu0, zeta=opts.zeta,
+                       mu_tol=opts.mu_tol, round_cap=opts.rounds())
+    blk = BlockNewton(dyn, cost, box, 1, st, rank, world, t0)
+    drv = TimeShardedNewton([blk], emulate=(world == 1))
+    drv.set_initial_state(x0[None])
+    U = [np.zeros((1, m, nu))]
+    X = drv.rollout(U)
+    drv.solve(X, U)                       # warm (kernel load, allocator)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    launched = drv.solve(X, U)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=f64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    s = blk.solver
+    n_rounds = int(s.read("round")[0])
+    iters = [int(v) for v in s.rounds("round_iters")[:n_rounds, 0].cpu().numpy()]
+    return {"config": f"config 4 full barrier solve, T=2^20 in {world} time blocks (one per "
+                      f"GPU), nx=12, nu=4, fp64, A scaled by {damp}",
+            "device_ms": round(float(ms), 3), "newton_iterations": iters,
+            "device_ms_per_newton_iteration": round(float(ms) / max(1, sum(iters)), 3),
+            "iterations_launched": launched, "status": int(s.read("status")[0]),
+            "final_cost": float(s.read("cur_cost")[0])}
 
 
 def config4_solve_leg(torch, P, logT: int = 20, damp: float = 0.9999):
