@@ -115,3 +115,31 @@ def test_block_mode_rejects_unsupported_models():
     cost = P.QuadraticCost(np.eye(2), np.eye(1), np.eye(2))
     with pytest.raises(NativeError):
         DeviceSolver(dyn, cost, None, 1, _settings("newton", block_mode=1, block_last=1))
+
+
+def test_time_sharded_batch_and_unequal_blocks():
+    """Two problems per block and blocks of unequal length (T = 1201 over 3
+    ranks): each problem's rounds and controls equal its whole-horizon solve."""
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200.sharded import TimeShardedNewton
+    nx, nu, T, world, n = 12, 4, 1201, 3, 2
+    A, B, c, _, u0, rng = _system(nx, nu, T, 9)
+    dyn, cost, box, *_ = _models(P, nx, nu, A, B, c)
+    problem = P.ControlProblem(dyn, cost, box)
+    opts = P.BarrierOptions(newton=P.NewtonOptions(executor="parallel"))
+    x0 = rng.standard_normal((n, nx))
+    st = _settings("barrier", opts.rounds(), mu0=opts.mu0, zeta=opts.zeta, mu_tol=opts.mu_tol)
+    blocks = _blocks(P, dyn, cost, box, st, world, batch=n)
+    assert len({m for _, m, _ in blocks}) == 2
+    drv = TimeShardedNewton([b for _, _, b in blocks], emulate=True)
+    drv.set_initial_state(x0)
+    U = [np.repeat(u0[t0:t0 + m][None], n, 0) for t0, m, _ in blocks]
+    drv.solve(drv.rollout(U), U)
+    s0 = blocks[0][2].solver
+    for k in range(n):
+        traj, rep = P.barrier_solve(problem, P.rollout(dyn, x0[k], u0), opts)
+        nr = int(s0.read("round")[k])
+        iters = s0.rounds("round_iters")[:nr, k].cpu().numpy()
+        assert list(iters) == [r.newton.iterations for r in rep.rounds]
+        Uk = np.concatenate([b.solver.controls()[k].cpu().numpy() for _, _, b in blocks])
+        assert rel_gap(Uk, traj.controls) < 1e-9
