@@ -143,3 +143,38 @@ def test_time_sharded_batch_and_unequal_blocks():
         assert list(iters) == [r.newton.iterations for r in rep.rounds]
         Uk = np.concatenate([b.solver.controls()[k].cpu().numpy() for _, _, b in blocks])
         assert rel_gap(Uk, traj.controls) < 1e-9
+
+
+def test_time_sharded_barrier_through_nccl_world1():
+    """The torch.distributed path of the driver (NCCL all-gather and SUM /
+    MAX / MIN all-reduces on the solver's stream) at world 1 equals the
+    emulated path bit for bit."""
+    import os
+    import socket
+    import torch.distributed as dist
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200.sharded import TimeShardedNewton
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        nx, nu, T = 12, 4, 1100
+        A, B, c, x0, u0, _ = _system(nx, nu, T, 10)
+        dyn, cost, box, *_ = _models(P, nx, nu, A, B, c)
+        opts = P.BarrierOptions(newton=P.NewtonOptions(executor="parallel"))
+        st = _settings("barrier", opts.rounds(), mu0=opts.mu0, zeta=opts.zeta, mu_tol=opts.mu_tol)
+        res = []
+        for emulate in (True, False):
+            (_, _, blk), = _blocks(P, dyn, cost, box, st, 1)
+            drv = TimeShardedNewton([blk], emulate=emulate)
+            drv.set_initial_state(x0[None])
+            U = [u0[None]]
+            drv.solve(drv.rollout(U), U)
+            res.append((blk.solver.controls()[0].cpu().numpy(),
+                        blk.solver.rounds("round_iters")[:, 0].cpu().numpy()))
+        assert np.array_equal(res[0][0], res[1][0])
+        assert np.array_equal(res[0][1], res[1][1])
+    finally:
+        dist.destroy_process_group()
