@@ -101,6 +101,21 @@ int ptc_lqr_solve(int dtype, int batch, int horizon, int nx, int nu,
                   void* S, void* s, void* Gamma, void* gamma, void* dx, void* du,
                   int* flags, void* workspace, int64_t workspace_bytes,
                   int chunk0, int chunk, void* stream);
+/* value_pass + propagation_pass with HOST buffers (the numpy arrays of the
+ * reference's StageExpansion, passes.py:291-361): same layouts and outputs
+ * (Gamma, gamma, dx, du; flags may be NULL), host->device copies, solve and
+ * device->host copies enqueued on `stream` (pinned host memory makes them
+ * asynchronous, so calls on several streams overlap PCIe with compute).
+ * Only what the kernels read is copied: for nx < 8 the upper triangles of
+ * the symmetric P and R.  Workspace: ptc_lqr_host_workspace_bytes (device). */
+int64_t ptc_lqr_host_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
+                                     int chunk0, int chunk);
+int ptc_lqr_solve_host(int dtype, int batch, int horizon, int nx, int nu,
+                       const void* P, const void* R, const void* M, const void* d,
+                       const void* Fx, const void* Fu, const void* PT, const double* alpha,
+                       void* Gamma, void* gamma, void* dx, void* du, int* flags,
+                       void* workspace, int64_t workspace_bytes, int chunk0, int chunk,
+                       void* stream);
 /* propagation_pass alone (passes.py:338-361) for a given feedback law:
  * Fx, Fu, Gamma (nu*nx), gamma (nu) in; dx, du out; d (nu) may be NULL.
  * Same workspace as ptc_lqr_solve. */

@@ -79,6 +79,10 @@ _SIGS = {
     "ptc_solver_destroy": (C.c_int, [C.c_void_p]),
     "ptc_solver_load": (C.c_int, [C.c_void_p] * 5 + [C.c_int, C.c_void_p]),
     "ptc_solver_check_consistency": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+        "ptc_lqr_host_workspace_bytes": (C.c_int64, [C.c_int] * 7),
+    "ptc_lqr_solve_host": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7 + [C.c_void_p]
+                           + [C.c_void_p] * 4 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
+                                                  C.c_int, C.c_void_p]),
     "ptc_solver_iterate": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "ptc_solver_block_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_int, C.c_int, C.c_void_p]),

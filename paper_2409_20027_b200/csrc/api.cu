@@ -370,6 +370,119 @@ int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, in
   return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
 }
 
+}  // extern "C"
+
+// device staging of the host-buffer entry: inputs, alpha, flags, outputs
+template <typename R>
+static size_t host_staging(Carver& c, int batch, int horizon, int nx, int nu, R** in, double** al,
+                           int** fl, R** out) {
+  const size_t TB = (size_t)horizon * batch, B = batch;
+  const size_t ci[7] = {(size_t)nx * nx * TB, (size_t)nu * nu * TB, (size_t)nx * nu * TB,
+                        (size_t)nu * TB, (size_t)nx * nx * TB, (size_t)nx * nu * TB,
+                        (size_t)nx * nx * B};
+  for (int k = 0; k < 7; ++k) in[k] = c.template take<R>(ci[k]);
+  *al = c.template take<double>(B);
+  *fl = c.template take<int>(B);
+  const size_t co[4] = {(size_t)nu * nx * TB, (size_t)nu * TB, (size_t)nx * (horizon + 1) * B,
+                        (size_t)nu * TB};
+  for (int k = 0; k < 4; ++k) out[k] = c.template take<R>(co[k]);
+  return c.off;
+}
+
+template <typename R>
+static int lqr_solve_host_t(int batch, int horizon, int nx, int nu, const void* const* hin,
+                            const double* alpha, void* const* hout, int* flags, void* ws,
+                            int64_t ws_bytes, int chunk0, int chunk, cudaStream_t st) {
+  Carver c{(char*)ws};
+  R* in[7];
+  R* out[4];
+  double* al;
+  int* fl;
+  host_staging<R>(c, batch, horizon, nx, nu, in, &al, &fl, out);
+  c.off = (c.off + 255) & ~(size_t)255;
+  const int64_t rest = ws_bytes - (int64_t)c.off;
+  if (rest <= 0) return fail(PTC_ERR_WORKSPACE, "LQR host workspace too small");
+  const size_t TB = (size_t)horizon * batch, es = sizeof(R);
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  };
+  // only what the kernels read crosses PCIe: the thread-per-unit kernels
+  // (nx < 8) read the upper triangles of the symmetric P and R
+  // (elements.cuh ld_stage); the warp kernels read whole stage rows
+  auto sym_copy = [&](R* dst, const void* src, int n) -> cudaError_t {
+    if (nx >= 8) return h2d(dst, src, (size_t)n * n * TB * es);
+    for (int i = 0; i < n; ++i) {
+      // components i*n + i .. i*n + n-1 of one row are contiguous slabs
+      const size_t c0 = (size_t)i * n + i;
+      cudaError_t e = h2d(dst + c0 * TB, static_cast<const R*>(src) + c0 * TB,
+                          (size_t)(n - i) * TB * es);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  PTC_CUDA(sym_copy(in[0], hin[0], nx));
+  PTC_CUDA(sym_copy(in[1], hin[1], nu));
+  PTC_CUDA(h2d(in[2], hin[2], (size_t)nx * nu * TB * es));
+  PTC_CUDA(h2d(in[3], hin[3], (size_t)nu * TB * es));
+  PTC_CUDA(h2d(in[4], hin[4], (size_t)nx * nx * TB * es));
+  PTC_CUDA(h2d(in[5], hin[5], (size_t)nx * nu * TB * es));
+  PTC_CUDA(h2d(in[6], hin[6], (size_t)nx * nx * batch * es));
+  PTC_CUDA(h2d(al, alpha, (size_t)batch * sizeof(double)));
+  PTC_CUDA(cudaMemsetAsync(fl, 0, sizeof(int) * batch, st));
+  int rc = lqr_solve_t<R>(batch, horizon, nx, nu, in[0], in[1], in[2], in[3], in[4], in[5], in[6],
+                          al, nullptr, nullptr, out[0], out[1], out[2], out[3], fl,
+                          (char*)ws + c.off, rest, chunk0, chunk, st);
+  if (rc != PTC_OK) return rc;
+  const size_t ob[4] = {(size_t)nu * nx * TB * es, (size_t)nu * TB * es,
+                        (size_t)nx * (horizon + 1) * batch * es, (size_t)nu * TB * es};
+  for (int k = 0; k < 4; ++k)
+    PTC_CUDA(cudaMemcpyAsync(hout[k], out[k], ob[k], cudaMemcpyDeviceToHost, st));
+  if (flags) PTC_CUDA(cudaMemcpyAsync(flags, fl, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+  return PTC_OK;
+}
+
+extern "C" {
+
+int64_t ptc_lqr_host_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
+                                     int chunk0, int chunk) {
+  const int64_t lw = ptc_lqr_workspace_bytes(dtype, batch, horizon, nx, nu, chunk0, chunk);
+  if (lw < 0) return lw;
+  Carver c{nullptr};
+  double* al;
+  int* fl;
+  if (dtype == PTC_F64) {
+    double *in[7], *out[4];
+    host_staging<double>(c, batch, horizon, nx, nu, in, &al, &fl, out);
+  } else {
+    float *in[7], *out[4];
+    host_staging<float>(c, batch, horizon, nx, nu, in, &al, &fl, out);
+  }
+  return (int64_t)((c.off + 255) & ~(size_t)255) + lw;
+}
+
+int ptc_lqr_solve_host(int dtype, int batch, int horizon, int nx, int nu, const void* P,
+                       const void* R, const void* M, const void* d, const void* Fx,
+                       const void* Fu, const void* PT, const double* alpha, void* Gamma,
+                       void* gamma, void* dx, void* du, int* flags, void* workspace,
+                       int64_t workspace_bytes, int chunk0, int chunk, void* stream) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  const void* hin[7] = {P, R, M, d, Fx, Fu, PT};
+  for (const void* p : hin)
+    if (!p) return fail(PTC_ERR_ARG, "every input buffer is required");
+  void* hout[4] = {Gamma, gamma, dx, du};
+  for (void* p : hout)
+    if (!p) return fail(PTC_ERR_ARG, "every output buffer is required");
+  if (!alpha) return fail(PTC_ERR_ARG, "alpha is required");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == PTC_F64)
+    return lqr_solve_host_t<double>(batch, horizon, nx, nu, hin, alpha, hout, flags, workspace,
+                                    workspace_bytes, chunk0, chunk, st);
+  if (dtype == PTC_F32)
+    return lqr_solve_host_t<float>(batch, horizon, nx, nu, hin, alpha, hout, flags, workspace,
+                                   workspace_bytes, chunk0, chunk, st);
+  return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
+}
+
 int ptc_lqr_solve(int dtype, int batch, int horizon, int nx, int nu, const void* P, const void* R,
                   const void* M, const void* d, const void* Fx, const void* Fu, const void* PT,
                   const double* alpha, void* S, void* s, void* Gamma, void* gamma, void* dx,

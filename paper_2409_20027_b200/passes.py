@@ -122,6 +122,47 @@ class LqrSolver:
             self.chunk0, self.chunk, N.stream_ptr(stream)))
 
 
+class HostLqrSolver:
+    """The same batched LQR-scan solve on HOST tensors (``ptc_lqr_solve_host``):
+    inputs and outputs are CPU tensors in the LqrSolver layouts (pin them
+    for asynchronous copies); the host->device copies (only the parts the
+    kernels read), the solve and the device->host copies are enqueued on
+    ``stream``, so calls on several streams overlap PCIe with compute."""
+
+    def __init__(self, batch, horizon, nx, nu, dtype=None, chunk0=0, chunk=0, device=None):
+        torch = N.require_cuda()
+        self.torch = torch
+        self.lib = N.load_library()
+        self.B, self.T, self.nx, self.nu = int(batch), int(horizon), int(nx), int(nu)
+        self.dtype = dtype or torch.float64
+        self.code = N.PTC_F64 if self.dtype == torch.float64 else N.PTC_F32
+        if not self.lib.ptc_supported(self.code, -1, self.nx, self.nu):
+            raise N.NativeError(f"LQR kernels not compiled for nx={nx} nu={nu}")
+        self.chunk0, self.chunk = int(chunk0), int(chunk)
+        nbytes = self.lib.ptc_lqr_host_workspace_bytes(self.code, self.B, self.T, self.nx,
+                                                       self.nu, self.chunk0, self.chunk)
+        N.check(0 if nbytes >= 0 else int(nbytes))
+        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8,
+                                     device=torch.device(device or "cuda"))
+
+    def outputs(self, pin=True):
+        """Host output tensors Gamma, gamma, dx, du (pinned by default)."""
+        torch = self.torch
+        B, T, nx, nu = self.B, self.T, self.nx, self.nu
+        mk = lambda *s: torch.empty(*s, dtype=self.dtype, pin_memory=pin)
+        return mk(nu * nx, T, B), mk(nu, T, B), mk(nx, T + 1, B), mk(nu, T, B)
+
+    def solve(self, P, R, M, d, Fx, Fu, PT, alpha, out, flags=None, stream=None):
+        ins = (P, R, M, d, Fx, Fu, PT)
+        if any(t.is_cuda for t in ins + tuple(out)) or alpha.is_cuda:
+            raise ValueError("HostLqrSolver takes host tensors (use LqrSolver for device ones)")
+        ptr = lambda t: None if t is None else t.data_ptr()
+        N.check(self.lib.ptc_lqr_solve_host(
+            self.code, self.B, self.T, self.nx, self.nu, *[ptr(t) for t in ins], ptr(alpha),
+            *[ptr(t) for t in out], ptr(flags), ptr(self.workspace), self.workspace.numel(),
+            self.chunk0, self.chunk, N.stream_ptr(stream)))
+
+
 def _soa(torch, a, dtype, device, comps):
     """(T, *comp) numpy -> (prod comp, T, 1) device."""
     t = torch.as_tensor(np.asarray(a, float), dtype=dtype).reshape(a.shape[0], comps)

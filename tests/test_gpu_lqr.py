@@ -153,3 +153,40 @@ def test_value_pass_pure_regularisation_is_zero():
                                  np.ones((n, 2, 1)), np.zeros((2, 2)), alpha=4.0)
     S, s, law = P.value_pass(exp)
     assert np.allclose(S, 0.0) and np.allclose(law.Gamma, 0.0) and np.allclose(law.gamma, 0.0)
+
+
+@pytest.mark.parametrize("nx,nu,T,B", [(2, 1, 256, 64), (4, 1, 256, 300), (4, 2, 1024, 3),
+                                       (12, 4, 1500, 1)])
+def test_lqr_host_buffers_equal_device_solve(nx, nu, T, B):
+    """ptc_lqr_solve_host (host tensors in and out, copies on the solver's
+    stream) gives bit-identical gains and deviations to the device entry on
+    the same inputs; for nx < 8 the strictly-lower triangles of the host P
+    and R are NaN, proving only the upper triangles the kernels read cross
+    PCIe."""
+    import torch
+    from paper_2409_20027_b200 import passes
+    rng = np.random.default_rng([nx, nu, T, B])
+    exps = [O.random_lqr_expansion(rng, T, nx, nu, alpha=0.2) for _ in range(B)]
+    stack = lambda f, c: torch.as_tensor(np.stack([f(e).reshape(-1, c) for e in exps], -1)
+                                         ).permute(1, 0, 2).contiguous()
+    h = [stack(lambda e: e.P, nx * nx), stack(lambda e: e.R, nu * nu),
+         stack(lambda e: e.M, nx * nu), stack(lambda e: e.d, nu), stack(lambda e: e.Fx, nx * nx),
+         stack(lambda e: e.Fu, nx * nu), stack(lambda e: e.PT[None], nx * nx)]
+    alpha = torch.full((B,), 0.2, dtype=torch.float64)
+    dev = passes.LqrSolver(B, T, nx, nu)
+    dev.solve(*[t.cuda() for t in h], alpha.cuda())
+    if nx < 8:
+        for t, n in ((h[0], nx), (h[1], nu)):
+            for i in range(n):
+                for j in range(i):
+                    t[i * n + j] = float("nan")
+    hs = passes.HostLqrSolver(B, T, nx, nu)
+    out = hs.outputs()
+    flags = torch.zeros(B, dtype=torch.int32).pin_memory()
+    h = [t.pin_memory() for t in h]
+    s = torch.cuda.Stream()
+    hs.solve(*h, alpha.pin_memory(), out, flags=flags, stream=s)
+    s.synchronize()
+    assert int(flags.max()) == 0
+    for got, want in zip(out, (dev.Gamma, dev.gamma, dev.dx, dev.du)):
+        assert torch.equal(got, want.cpu())
