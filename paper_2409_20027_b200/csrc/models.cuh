@@ -337,6 +337,42 @@ PTC_D R stage_cost(const ProblemParams& p, const R (&x)[NX], const R (&u)[NU]) {
   return R(0.5) * (qx + ru);
 }
 
+// The stage-cost constants in registers (kernels that evaluate the cost at
+// every stage of a sweep load them once; same arithmetic as stage_cost).
+template <typename R, int NX, int NU>
+struct CostRegs {
+  R goal[NX], Q[NX][NX], Rc[NU][NU];
+  PTC_D void load(const ProblemParams& p) {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      goal[i] = R(p.goal[i]);
+#pragma unroll
+      for (int j = 0; j < NX; ++j) Q[i][j] = R(p.Q[i * NX + j]);
+    }
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+#pragma unroll
+      for (int j = 0; j < NU; ++j) Rc[i][j] = R(p.Rc[i * NU + j]);
+  }
+};
+
+template <typename R, int NX, int NU>
+PTC_D R stage_cost(const CostRegs<R, NX, NU>& p, const R (&x)[NX], const R (&u)[NU]) {
+  R e[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e[i] = x[i] - p.goal[i];
+  R qx = R(0), ru = R(0);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) qx += e[i] * p.Q[i][j] * e[j];
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) ru += u[i] * p.Rc[i][j] * u[j];
+  return R(0.5) * (qx + ru);
+}
+
 template <typename R, int NX>
 PTC_D R terminal_cost(const ProblemParams& p, const R (&x)[NX]) {
   R e[NX];

@@ -224,11 +224,13 @@ __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int whic
   const AugArgs<R> g = aug_of(a);
   double sl = 0.0, sc = 0.0;
   int bad = -1;
+  CostRegs<R, NX, NU> cr;
+  cr.load(p);
   for (int t = t0; t < t1; ++t) {
     R x[NX], u[NU];
     ld_x(a, q, t, b, x);
     ld_u(a, q, t, b, u);
-    sl += double(stage_cost<R, NX, NU>(p, x, u));
+    sl += double(stage_cost<R, NX, NU>(cr, x, u));
     int br;
     sc += double(aug_value<R, NX, NU>(p, g, t, T, B, b, x, u, br));
     if (br >= 0 && bad < 0) bad = t * p.W + br;
@@ -643,6 +645,8 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
   double sl = 0.0, sc = 0.0;
   int bad = -1;
   const AugArgs<R> g = aug_of(a);
+  CostRegs<R, NX, NU> cr;
+  if constexpr (kCost) cr.load(gp);
   R ring[kRing][NU];
   auto fetch = [&](int t, R (&u)[NU]) {
     if (t < T) {
@@ -670,7 +674,7 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
         fetch(t + kRing, ring[k]);
         if (!kFromUc) st_vec(Uc, t, T, B, b, u);
         if constexpr (kCost) {
-          sl += double(stage_cost<R, NX, NU>(gp, x, u));
+          sl += double(stage_cost<R, NX, NU>(cr, x, u));
           int br;
           sc += double(aug_value<R, NX, NU>(gp, g, t, T, B, b, x, u, br));
           if (br >= 0 && bad < 0) bad = t * gp.W + br;
