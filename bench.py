@@ -619,6 +619,8 @@ def newton_latency_sweep(torch, P):
       tvlinear  config-1 style random time-varying system (nx=4, nu=2,
                 quadratic cost): the rollout is itself an affine scan, so the
                 whole iteration is log-depth;
+      tvlinear12  the same at nx=12, nu=4 (config-4 sizes: the warp-per-unit
+                co-state / LQR / affine-rollout kernels);
       pendulum  config-0 swing-up from random controls: the nonlinear
                 re-rollout the reference mandates (newton.py:188) is tried as
                 a log-depth Newton solve of the recurrence for T >= 1024 and
@@ -631,7 +633,7 @@ def newton_latency_sweep(torch, P):
     from paper_2409_20027_b200 import _native as N
     from paper_2409_20027_b200._device import DeviceSolver, SolveSettings
     res = {}
-    for model in ("tvlinear", "pendulum"):
+    for model in ("tvlinear", "tvlinear12", "pendulum"):
         out = {}
         for logT in (8, 10, 12, 14, 16):
             Tn = 1 << logT
@@ -644,7 +646,7 @@ def newton_latency_sweep(torch, P):
                 x0 = np.array([np.pi, 0.0])
                 us = 0.5 * rng.standard_normal((1, Tn, 1))
             else:
-                nx, nu, settle = 4, 2, 2
+                nx, nu, settle = (4, 2, 2) if model == "tvlinear" else (12, 4, 2)
                 A = np.eye(nx)[None] + 0.05 * rng.standard_normal((Tn, nx, nx))
                 A *= np.minimum(1.0, 1.0 / np.max(np.abs(np.linalg.eigvals(A)), axis=1))[:, None,
                                                                                          None]
@@ -675,8 +677,12 @@ def newton_latency_sweep(torch, P):
                 h = s.history()[:, :, 0].cpu().numpy()[settle:settle + 4]
                 full += int(np.isfinite(h[:, 3]).sum())
                 par += int(int(s.read("rollout_state")[0]) & 2 != 0)
-            out[str(Tn)] = {"ms": round(statistics.median(per), 4), "full": f"{full}/12",
-                            "log_depth_rollout_converged": f"{par}/3"}
+            row = {"ms": round(statistics.median(per), 4), "full": f"{full}/12"}
+            if model == "tvlinear12":   # affine nx >= 8: exact affine-scan rollout on tree plans
+                row["rollout"] = "affine scan" if Tn >= 1024 else "sequential (warp)"
+            else:
+                row["log_depth_rollout_converged"] = f"{par}/3"
+            out[str(Tn)] = row
             del s
         res[model] = out
     return res
