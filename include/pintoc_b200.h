@@ -116,6 +116,24 @@ int ptc_lqr_solve_host(int dtype, int batch, int horizon, int nx, int nu,
                        void* Gamma, void* gamma, void* dx, void* du, int* flags,
                        void* workspace, int64_t workspace_bytes, int chunk0, int chunk,
                        void* stream);
+/* Element-level operations of the three scans, batched over items; item i
+ * of a field with C components at f[c * n + i] (device pointers).
+ *   ptc_value_elements   value_element_init (passes.py:192-228) of stages
+ *     0..horizon-1 and the boundary element (stage horizon): out
+ *     (3nx^2 + 2nx, horizon + 1) in the order A, Y, C, eta, b; flags[t]
+ *     bit 1 when R_t + alpha I is not positive definite.  alpha: 1 double.
+ *   ptc_value_combine    value_combine (passes.py:264-288), left = earlier
+ *     stages: n pairs; flags[i] bit 4 when I + C_left Y_right is singular.
+ *   ptc_affine_combine   kind 0: rollout_combine (passes.py:330-335),
+ *     [F | e] maps, out = b after a; kind 1: costate_combine
+ *     (passes.py:113-119), [df | dl | dc], a = the earlier segment. */
+int ptc_value_elements(int dtype, int horizon, int nx, int nu, const void* P, const void* R,
+                       const void* M, const void* d, const void* Fx, const void* Fu,
+                       const void* PT, const double* alpha, void* out, int* flags, void* stream);
+int ptc_value_combine(int dtype, int n, int nx, const void* left, const void* right, void* out,
+                      int* flags, void* stream);
+int ptc_affine_combine(int dtype, int n, int nx, int kind, const void* a, const void* b,
+                       void* out, void* stream);
 /* propagation_pass alone (passes.py:338-361) for a given feedback law:
  * Fx, Fu, Gamma (nu*nx), gamma (nu) in; dx, du out; d (nu) may be NULL.
  * Same workspace as ptc_lqr_solve. */

@@ -443,6 +443,54 @@ static int lqr_solve_host_t(int batch, int horizon, int nx, int nu, const void* 
 
 extern "C" {
 
+// element-level entry points: any registered kernel set of this dtype / nx
+static const LqrOps* ops_for_nx(int dtype, int nx) {
+  const int code = dtype == PTC_F64 ? 1 : 0;
+  for (auto& kv : lqr_registry())
+    if (std::get<0>(kv.first) == code && std::get<1>(kv.first) == nx) return &kv.second;
+  return nullptr;
+}
+
+int ptc_value_elements(int dtype, int horizon, int nx, int nu, const void* P, const void* R,
+                       const void* M, const void* d, const void* Fx, const void* Fu,
+                       const void* PT, const double* alpha, void* out, int* flags, void* stream) {
+  if (horizon < 0 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  if (dtype != PTC_F32 && dtype != PTC_F64) return fail(PTC_ERR_ARG, "bad dtype");
+  if (!PT || !alpha || !out || !flags || (horizon > 0 && (!P || !R || !M || !d || !Fx || !Fu)))
+    return fail(PTC_ERR_ARG, "missing buffer");
+  auto it = lqr_registry().find(LqrKey(dtype == PTC_F64 ? 1 : 0, nx, nu));
+  if (it == lqr_registry().end())
+    return fail(PTC_ERR_UNSUPPORTED, "kernels not instantiated for nx=" + std::to_string(nx) +
+                                         " nu=" + std::to_string(nu));
+  const void* st[7] = {P, R, M, d, Fx, Fu, PT};
+  it->second.velem_init(horizon, st, alpha, out, flags, (cudaStream_t)stream);
+  PTC_CUDA(cudaGetLastError());
+  return PTC_OK;
+}
+
+int ptc_value_combine(int dtype, int n, int nx, const void* left, const void* right, void* out,
+                      int* flags, void* stream) {
+  if (n < 1 || nx < 1) return fail(PTC_ERR_ARG, "bad dims");
+  if (!left || !right || !out || !flags) return fail(PTC_ERR_ARG, "missing buffer");
+  const LqrOps* ops = ops_for_nx(dtype, nx);
+  if (!ops) return fail(PTC_ERR_UNSUPPORTED, "kernels not instantiated for nx=" + std::to_string(nx));
+  ops->vcombine(n, left, right, out, flags, (cudaStream_t)stream);
+  PTC_CUDA(cudaGetLastError());
+  return PTC_OK;
+}
+
+int ptc_affine_combine(int dtype, int n, int nx, int kind, const void* a, const void* b, void* out,
+                       void* stream) {
+  if (n < 1 || nx < 1) return fail(PTC_ERR_ARG, "bad dims");
+  if (kind != 0 && kind != 1) return fail(PTC_ERR_ARG, "kind must be 0 (rollout) or 1 (costate)");
+  if (!a || !b || !out) return fail(PTC_ERR_ARG, "missing buffer");
+  const LqrOps* ops = ops_for_nx(dtype, nx);
+  if (!ops) return fail(PTC_ERR_UNSUPPORTED, "kernels not instantiated for nx=" + std::to_string(nx));
+  ops->affine(n, kind, a, b, out, (cudaStream_t)stream);
+  PTC_CUDA(cudaGetLastError());
+  return PTC_OK;
+}
+
 int64_t ptc_lqr_host_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
                                      int chunk0, int chunk) {
   const int64_t lw = ptc_lqr_workspace_bytes(dtype, batch, horizon, nx, nu, chunk0, chunk);

@@ -121,7 +121,84 @@ struct LqrOps {
   void (*propagate)(const void* args, cudaStream_t s);
   void (*block)(const void* args, int phase, const void* blocks, void* out, int rank, int world,
                 cudaStream_t s);
+  // element-level operations (reference passes.py value_element_init,
+  // value_combine, costate_combine, rollout_combine), batched over items
+  void (*velem_init)(int n, const void* const* stage, const double* alpha, void* out, int* flags,
+                     cudaStream_t s);
+  void (*vcombine)(int n, const void* l, const void* r, void* o, int* flags, cudaStream_t s);
+  void (*affine)(int n, int kind, const void* a, const void* b, void* o, cudaStream_t s);
 };
+
+// ------------------------------------------------------- element operations
+
+// dual value elements of stages 0..n-1 (velem_from_stage) and the boundary
+// element at n (velem_terminal); out (VC, n + 1, 1), flags[t] |= DEF_R when
+// R_t + alpha I fails its Cholesky
+template <typename R, int NX, int NU>
+__global__ void k_velem_init(int n, const R* P, const R* Rm, const R* M, const R* d, const R* Fx,
+                             const R* Fu, const R* PT, const double* alpha, R* out, int* flags) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > n) return;
+  VElem<R, NX> e;
+  if (t == n) {
+    R PTm[NX][NX];
+    ld_mat(PT, 0, 1, 1, 0, PTm);
+    velem_terminal(PTm, e);
+  } else {
+    Stage<R, NX, NU> st;
+    ld_stage(P, Rm, M, d, Fx, Fu, t, n, 1, 0, R(alpha[0]), st);
+    R L[NU][NU];
+    if (!velem_from_stage(st, e, L)) flags[t] |= FLAG_DEF_R;
+  }
+  st_velem(out, t, n + 1, 1, 0, e);
+}
+
+// o_i = l_i (earlier) (x) r_i (later); flags[i] |= COND when I + C_l Y_r is singular
+template <typename R, int NX>
+__global__ void k_vcombine_n(int n, const R* l, const R* r, R* o, int* flags) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  VElem<R, NX> a, b, c;
+  ld_velem(l, i, n, 1, 0, a);
+  ld_velem(r, i, n, 1, 0, b);
+  if (!vcombine(a, b, c)) flags[i] |= FLAG_COND;
+  st_velem(o, i, n, 1, 0, c);
+}
+
+// kind 0 (rollout_combine): [F | e] maps, o = b after a;
+// kind 1 (costate_combine): [df | dl | dc], a the earlier segment:
+//   df = b.df a.df,  dl = a.dl + a.df^T b.dl,  dc = a.dc + a.df^T b.dc
+template <typename R, int NX>
+__global__ void k_affine_n(int n, int kind, const R* a, const R* b, R* o) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (kind == 0) {
+    Aff<R, NX> fa, fb, fo;
+    ld_aff(a, i, n, 1, 0, fa);
+    ld_aff(b, i, n, 1, 0, fb);
+    aff_compose(fb, fa, fo);
+    st_aff(o, i, n, 1, 0, fo);
+    return;
+  }
+  R Fa[NX][NX], Fb[NX][NX], Fo[NX][NX], la[NX], lb[NX], ca[NX], cb[NX], tl[NX], tc[NX];
+  ld_mat(a, i, n, 1, 0, Fa);
+  ld_mat(b, i, n, 1, 0, Fb);
+  ld_vec(a, i, n, 1, 0, la, NX * NX);
+  ld_vec(b, i, n, 1, 0, lb, NX * NX);
+  ld_vec(a, i, n, 1, 0, ca, NX * NX + NX);
+  ld_vec(b, i, n, 1, 0, cb, NX * NX + NX);
+  mm<NX, NX, NX>(Fb, Fa, Fo);
+  mtv<NX, NX>(Fa, lb, tl);
+  mtv<NX, NX>(Fa, cb, tc);
+#pragma unroll
+  for (int k = 0; k < NX; ++k) {
+    tl[k] += la[k];
+    tc[k] += ca[k];
+  }
+  st_mat(o, i, n, 1, 0, Fo);
+  st_vec(o, i, n, 1, 0, tl, NX * NX);
+  st_vec(o, i, n, 1, 0, tc, NX * NX + NX);
+}
 
 struct NewtonOps {
   void (*lqr)(const void* la, cudaStream_t s);
@@ -300,8 +377,27 @@ struct RegisterLqr {
       launch_lqr_block<R, NX, NU>(*static_cast<const LqrArgs<R>*>(a), phase, blocks, out, rank,
                                   world, s);
   }
+  static void velem_init(int n, const void* const* st, const double* alpha, void* out, int* flags,
+                         cudaStream_t s) {
+    k_velem_init<R, NX, NU><<<grid_for(n + 1), kBlock, 0, s>>>(
+        n, static_cast<const R*>(st[0]), static_cast<const R*>(st[1]),
+        static_cast<const R*>(st[2]), static_cast<const R*>(st[3]), static_cast<const R*>(st[4]),
+        static_cast<const R*>(st[5]), static_cast<const R*>(st[6]), alpha, static_cast<R*>(out),
+        flags);
+  }
+  static void vcombine(int n, const void* l, const void* r, void* o, int* flags, cudaStream_t s) {
+    k_vcombine_n<R, NX><<<grid_for(n), kBlock, 0, s>>>(n, static_cast<const R*>(l),
+                                                         static_cast<const R*>(r),
+                                                         static_cast<R*>(o), flags);
+  }
+  static void affine(int n, int kind, const void* a, const void* b, void* o, cudaStream_t s) {
+    k_affine_n<R, NX><<<grid_for(n), kBlock, 0, s>>>(n, kind, static_cast<const R*>(a),
+                                                       static_cast<const R*>(b),
+                                                       static_cast<R*>(o));
+  }
   RegisterLqr() {
-    lqr_registry()[LqrKey(dtype_code<R>(), NX, NU)] = LqrOps{&solve, &propagate, &block};
+    lqr_registry()[LqrKey(dtype_code<R>(), NX, NU)] =
+        LqrOps{&solve, &propagate, &block, &velem_init, &vcombine, &affine};
   }
 };
 

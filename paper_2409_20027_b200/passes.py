@@ -22,6 +22,28 @@ from .newton import aug_settings, plan_chunks
 from .problem import Trajectory
 
 
+class CostateElement(NamedTuple):
+    """Adjoint segment (dl/dx, dc/dx, df/dx)  (passes.py:30-35)."""
+    dl: np.ndarray  # (d_x,)
+    dc: np.ndarray  # (d_x,)
+    df: np.ndarray  # (d_x, d_x)
+
+
+class ValueElement(NamedTuple):
+    """Dual parameterisation (A, Y, C, eta, b)  (passes.py:38-45)."""
+    A: np.ndarray
+    Y: np.ndarray
+    C: np.ndarray
+    eta: np.ndarray
+    b: np.ndarray
+
+
+class RolloutElement(NamedTuple):
+    """Affine map dx -> F dx + e  (passes.py:48-52)."""
+    F: np.ndarray
+    e: np.ndarray
+
+
 class FeedbackLaw(NamedTuple):
     """du_t = Gamma_t dx_t + gamma_t  (passes.py:55-59)."""
     Gamma: np.ndarray  # (N, d_u, d_x)
@@ -251,3 +273,128 @@ def hamiltonian_expansion(traj: Trajectory, costates, cost, aug, dyn, alpha: flo
     return StageExpansion.build(f("P", (nx, nx)), f("R", (nu, nu)), f("M", (nx, nu)),
                                 f("d", (nu,)), f("Fx", (nx, nx)), f("Fu", (nx, nu)), PT,
                                 alpha)
+
+
+# ------------------------------------------------------------------ elements
+#
+# The element-level functions of the reference (one combine at a time) run
+# the same device functions the scans use (elements.cuh: velem_from_stage,
+# vcombine, aff_compose), batched over items: pass elements whose arrays
+# carry a leading item axis to combine many pairs in one launch.
+
+def _items(torch, dtype, dev, fields, dims):
+    """Fields with shape (*lead, *dims[k]) -> one device (sum comps, n) tensor."""
+    lead = np.asarray(fields[0]).shape[:len(np.asarray(fields[0]).shape) - len(dims[0])]
+    n = int(np.prod(lead)) if lead else 1
+    parts = [torch.as_tensor(np.asarray(f, dtype=float)).reshape(n, -1) for f in fields]
+    return torch.cat(parts, 1).t().contiguous().to(device=dev, dtype=dtype), lead, n
+
+
+def _split(t, lead, dims):
+    out, c0 = [], 0
+    host = t.t().double().cpu().numpy()
+    for dm in dims:
+        c = int(np.prod(dm)) if dm else 1
+        out.append(host[:, c0:c0 + c].reshape(tuple(lead) + tuple(dm)))
+        c0 += c
+    return out
+
+
+def _ctx(dtype):
+    torch = N.require_cuda()
+    return torch, N.load_library(), dtype or torch.float64, torch.device("cuda")
+
+
+def _code(torch, dtype):
+    return N.PTC_F64 if dtype == torch.float64 else N.PTC_F32
+
+
+def costate_boundary(cost, x_final, dtype=None) -> np.ndarray:
+    """Terminal adjoint: the terminal cost's gradient Qf (x - goal) (passes.py:106-110)."""
+    torch, _, dtype, dev = _ctx(dtype)
+    spec = cost._device_spec()
+    Qf = torch.as_tensor(np.asarray(spec["Qf"], float), dtype=dtype, device=dev)
+    e = torch.as_tensor(np.asarray(x_final, float) - np.asarray(spec["goal"], float),
+                        dtype=dtype, device=dev)
+    return (Qf @ e).double().cpu().numpy()
+
+
+def value_element_init(exp: StageExpansion, t: int, dtype=None) -> ValueElement:
+    """Dual-form value element of stage t (t == N: the boundary element)
+    (passes.py:192-228).  Raises DefinitenessError if R_t + alpha I is not
+    positive definite."""
+    torch, lib, dtype, dev = _ctx(dtype)
+    n, nx, nu = exp.horizon, exp.d_x, exp.d_u
+    if not 0 <= t <= n:
+        raise IndexError(f"stage {t} outside 0..{n}")
+    soa = lambda a, c: _soa(torch, np.asarray(a)[None] if np.ndim(a) == 2 else a, dtype, dev, c)
+    PT = soa(exp.P_terminal, nx * nx)
+    alpha = torch.full((1,), float(exp.alpha), dtype=torch.float64, device=dev)
+    vc = 3 * nx * nx + 2 * nx
+    if t == n:
+        out = torch.empty(vc, 1, dtype=dtype, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        N.check(lib.ptc_value_elements(_code(torch, dtype), 0, nx, nu, None, None, None, None,
+                                       None, None, PT.data_ptr(), alpha.data_ptr(),
+                                       out.data_ptr(), flags.data_ptr(), N.stream_ptr()))
+        col = out[:, :1]
+    else:
+        sl = lambda a, c: soa(np.asarray(a)[t:t + 1], c)
+        ins = [sl(exp.P, nx * nx), sl(exp.R, nu * nu), sl(exp.M, nx * nu), sl(exp.d, nu),
+               sl(exp.Fx, nx * nx), sl(exp.Fu, nx * nu)]
+        out = torch.empty(vc, 2, dtype=dtype, device=dev)
+        flags = torch.zeros(2, dtype=torch.int32, device=dev)
+        N.check(lib.ptc_value_elements(_code(torch, dtype), 1, nx, nu,
+                                       *[x.data_ptr() for x in ins], PT.data_ptr(),
+                                       alpha.data_ptr(), out.data_ptr(), flags.data_ptr(),
+                                       N.stream_ptr()))
+        if int(flags[0]) & FLAG_DEF_R:
+            raise DefinitenessError(t, "R + alpha*I")
+        col = out[:, :1]
+    return ValueElement(*_split(col, (), [(nx, nx), (nx, nx), (nx, nx), (nx,), (nx,)]))
+
+
+def value_combine(left: ValueElement, right: ValueElement, dtype=None) -> ValueElement:
+    """Merge adjacent conditional value functions, ``left`` covering the
+    earlier stages (passes.py:264-288).  Raises ConditioningError if
+    I + C_left Y_right is singular."""
+    torch, lib, dtype, dev = _ctx(dtype)
+    nx = np.asarray(left.A).shape[-1]
+    dims = [(nx, nx), (nx, nx), (nx, nx), (nx,), (nx,)]
+    L, lead, n = _items(torch, dtype, dev, list(left), dims)
+    Rt, _, _ = _items(torch, dtype, dev, list(right), dims)
+    out = torch.empty_like(L)
+    flags = torch.zeros(n, dtype=torch.int32, device=dev)
+    N.check(lib.ptc_value_combine(_code(torch, dtype), n, nx, L.data_ptr(), Rt.data_ptr(),
+                                  out.data_ptr(), flags.data_ptr(), N.stream_ptr()))
+    if bool((flags & FLAG_COND).any()):
+        raise ConditioningError("singular I + C*Y while combining value elements")
+    return ValueElement(*_split(out, lead, dims))
+
+
+def costate_combine(left: CostateElement, right: CostateElement, dtype=None) -> CostateElement:
+    """Compose two adjoint segments, ``left`` covering the earlier stages
+    (passes.py:113-119)."""
+    torch, lib, dtype, dev = _ctx(dtype)
+    nx = np.asarray(left.dl).shape[-1]
+    dims = [(nx, nx), (nx,), (nx,)]
+    A, lead, n = _items(torch, dtype, dev, [left.df, left.dl, left.dc], dims)
+    B, _, _ = _items(torch, dtype, dev, [right.df, right.dl, right.dc], dims)
+    out = torch.empty_like(A)
+    N.check(lib.ptc_affine_combine(_code(torch, dtype), n, nx, 1, A.data_ptr(), B.data_ptr(),
+                                   out.data_ptr(), N.stream_ptr()))
+    df, dl, dc = _split(out, lead, dims)
+    return CostateElement(dl, dc, df)
+
+
+def rollout_combine(first: RolloutElement, second: RolloutElement, dtype=None) -> RolloutElement:
+    """Compose affine maps, applying ``first`` then ``second`` (passes.py:330-335)."""
+    torch, lib, dtype, dev = _ctx(dtype)
+    nx = np.asarray(first.e).shape[-1]
+    dims = [(nx, nx), (nx,)]
+    A, lead, n = _items(torch, dtype, dev, list(first), dims)
+    B, _, _ = _items(torch, dtype, dev, list(second), dims)
+    out = torch.empty_like(A)
+    N.check(lib.ptc_affine_combine(_code(torch, dtype), n, nx, 0, A.data_ptr(), B.data_ptr(),
+                                   out.data_ptr(), N.stream_ptr()))
+    return RolloutElement(*_split(out, lead, dims))
