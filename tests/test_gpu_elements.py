@@ -144,3 +144,29 @@ def test_costate_boundary_is_terminal_gradient():
     cost = P.QuadraticCost(np.eye(3), np.eye(1), Qf, x_goal=goal)
     x = rng.standard_normal(3)
     assert rel_gap(P.costate_boundary(cost, x), Qf @ (x - goal)) < 1e-12
+
+
+def test_device_scan_over_element_tuples():
+    """scan() (scan.py:133-166) with the path's combines: a REVERSE scan of
+    the value elements is the value function (S_t = Y, s_t = -eta), a
+    FORWARD scan of rollout maps equals the sequential composition; other
+    combines have no device form."""
+    import paper_2409_20027_b200 as P
+    e, exp = _exp(9, T=11)
+    elems = [P.value_element_init(exp, t) for t in range(exp.horizon + 1)]
+    out = P.scan(elems, P.value_combine, P.ScanDirection.REVERSE, executor="parallel")
+    S, s = O.value_pass(e)[:2]
+    for t in range(exp.horizon):
+        assert rel_gap(out[t].Y, S[t]) < 1e-10 and rel_gap(-out[t].eta, s[t]) < 1e-10
+    rng = np.random.default_rng(10)
+    maps = [P.RolloutElement(np.eye(3) + 0.1 * rng.standard_normal((3, 3)),
+                             rng.standard_normal(3)) for _ in range(13)]
+    out = P.scan(maps, P.rollout_combine)
+    F, c = maps[0].F, maps[0].e
+    for t in range(1, 13):
+        F, c = maps[t].F @ F, maps[t].F @ c + maps[t].e
+        assert rel_gap(out[t].F, F) < 1e-10 and rel_gap(out[t].e, c) < 1e-10
+    with pytest.raises(TypeError):
+        P.scan(maps, lambda a, b: a)
+    with pytest.raises(P.EmptySequenceError):
+        P.scan([], P.rollout_combine)
