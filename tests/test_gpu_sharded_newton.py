@@ -178,3 +178,30 @@ def test_time_sharded_barrier_through_nccl_world1():
         assert np.array_equal(res[0][1], res[1][1])
     finally:
         dist.destroy_process_group()
+
+
+def test_time_sharded_fp32_solve_close_to_fp64():
+    """fp32 block-mode solvers (2 emulated ranks): converged controls within
+    single-precision accuracy of the fp64 whole-horizon solve (1e-3)."""
+    import torch
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200 import _native as N
+    from paper_2409_20027_b200.sharded import BlockNewton, TimeShardedNewton, split_dynamics
+    nx, nu, T, world = 12, 4, 1000, 2
+    A, B, c, x0, u0, _ = _system(nx, nu, T, 11)
+    dyn, cost, *_ = _models(P, nx, nu, A, B, c)
+    init = P.rollout(dyn, x0, u0)
+    traj, _ = P.newton_solve(dyn, cost, None, init, P.NewtonOptions(executor="parallel"))
+    st = _settings("newton", aug=N.AUG_ZERO, inner_tol=1e-5)
+    blocks = []
+    for r in range(world):
+        t0, bd = split_dynamics(dyn, world, r)
+        blocks.append((t0, bd.horizon, BlockNewton(bd, cost, None, 1, st, r, world, t0,
+                                                   dtype=torch.float32)))
+    drv = TimeShardedNewton([b for _, _, b in blocks], emulate=True)
+    drv.set_initial_state(x0[None])
+    drv.solve([init.states[t0:t0 + m + 1][None] for t0, m, _ in blocks],
+              [u0[t0:t0 + m][None] for t0, m, _ in blocks])
+    assert int(blocks[0][2].solver.read("status")[0]) == 1   # done
+    U = np.concatenate([b.solver.controls()[0].double().cpu().numpy() for _, _, b in blocks])
+    assert rel_gap(U, traj.controls) < 1e-3
