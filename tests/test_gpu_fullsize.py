@@ -126,3 +126,41 @@ def test_config4_full_size_kkt_whole_and_time_blocks():
     scale = max(1.0, float(sol.du.abs().max()))
     assert float((du - sol.du).abs().max()) / scale < 1e-9
     assert float((dx - sol.dx).abs().max()) / max(1.0, float(sol.dx.abs().max())) < 1e-9
+
+
+def test_config4_full_size_barrier_solve_properties():
+    """Config 4 as a full barrier solve (T = 2^20, nx = 12, nu = 4, |u| <= 2;
+    A scaled by 0.9999 as in bench.py): every round converges, the returned
+    controls are strictly inside the box and the trajectory satisfies the
+    dynamics at every stage."""
+    import torch
+    import paper_2409_20027_b200 as P
+    T, nx, nu = 1 << 20, 12, 4
+    dev = torch.device("cuda")
+    f64 = torch.float64
+    g = torch.Generator(device=dev).manual_seed(5)
+    band = torch.zeros(nx, nx, dtype=f64, device=dev)
+    for i in range(4):
+        for j in (i, i + 1):
+            if j < 4:
+                band[3 * i:3 * i + 3, 3 * j:3 * j + 3] = 1.0
+    F = torch.randn(T, nx, nx, generator=g, device=dev, dtype=f64) * (0.2 ** 0.5) * band
+    A = (0.9999 * (torch.eye(nx, dtype=f64, device=dev) + 0.01 * F)).cpu().numpy()
+    del F
+    B = (torch.randn(T, nx, nu, generator=g, device=dev, dtype=f64) * (0.1 ** 0.5)).cpu().numpy()
+    qd = np.random.default_rng(5).uniform(0.1, 10.0, nx)
+    dyn = P.TimeVaryingLinearDynamics(A, B)
+    cost = P.QuadraticCost(np.diag(qd), 0.1 * np.eye(nu), 10 * np.diag(qd))
+    box = P.BoxConstraint(nx, nu, control_lower=-2.0, control_upper=2.0)
+    x0 = np.random.default_rng(6).standard_normal(nx)
+    init = P.rollout(dyn, x0, np.zeros((T, nu)))
+    traj, rep = P.barrier_solve(P.ControlProblem(dyn, cost, box), init,
+                                P.BarrierOptions(newton=P.NewtonOptions(max_iters=50)))
+    assert rep.converged and rep.outer_iterations == 5
+    assert np.abs(traj.controls).max() < 2.0
+    xs = torch.as_tensor(traj.states, device=dev)
+    us = torch.as_tensor(traj.controls, device=dev)
+    At, Bt = torch.as_tensor(A, device=dev), torch.as_tensor(B, device=dev)
+    pred = (At @ xs[:-1].unsqueeze(-1) + Bt @ us.unsqueeze(-1)).squeeze(-1)
+    assert float((pred - xs[1:]).abs().max()) / max(1.0, float(xs.abs().max())) < 1e-9
+    assert all(np.isfinite(r.cost) for r in rep.rounds)
