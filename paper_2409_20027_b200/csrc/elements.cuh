@@ -480,11 +480,13 @@ PTC_D int vcombine_stage(const Stage<R, NX, NU>& st, const VElem<R, NX>& r, VEle
 // det(I + C S) = det(Q) / det(Rr), a singular combine is a Q that fails its
 // Cholesky, so the two definiteness flags cover the conditioning case.
 // Returns FLAG_DEF_R / FLAG_DEF_Q bits.
-template <typename R, int NX, int NU>
+// kCheckR: also test R_t + alpha I (DefinitenessError).  Tree and block
+// schedules have already tested every stage in the level-0 up-sweep.
+template <typename R, int NX, int NU, bool kCheckR = true>
 PTC_D int riccati_step(const Stage<R, NX, NU>& st, const VCarry<R, NX>& c, R (&Gam)[NU][NX],
                        R (&gam)[NU], VCarry<R, NX>& o) {
   int fl = 0;
-  {
+  if constexpr (kCheckR) {
     R L[NU][NU];
 #pragma unroll
     for (int i = 0; i < NU; ++i)

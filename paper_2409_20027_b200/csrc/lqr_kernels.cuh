@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(128) k_value_down0(LqrArgs<R> a) {
     if (t > t0) ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t - 1, T, B, b, alpha, nst);
     R Gam[NU][NX], gam[NU];
     VCarry<R, NX> o;
-    fl |= riccati_step(st, c, Gam, gam, o);
+    fl |= riccati_step<R, NX, NU, !kAgg>(st, c, Gam, gam, o);
     st_mat(a.Gam, t, T, B, b, Gam);
     st_vec(a.gam, t, T, B, b, gam);
     if constexpr (emit_pagg) {

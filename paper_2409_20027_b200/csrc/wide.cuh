@@ -301,7 +301,7 @@ struct WSlab {
   // scratch needs of the element algebra
   static constexpr int SCR_COMB = NX * NX + NX * (2 * NX + 1) + NX * (NX + 1) + NX * NX;
   static constexpr int SCR_STEP = NX * NX + NX * (NX + 1);
-  static constexpr int SCR_RIC = 2 * NU * NX + NU * NU + NX * NX;
+  static constexpr int SCR_RIC = 2 * NU * NX + NU * NU + NX * NX + NU;
   static constexpr int BASE = 5 * NU * NX + 2 * NU + 4 * NX + NU * NU;
   static constexpr int SCR_STAGE = BASE + 2 * NX * NX;
   static constexpr int SCR_VELEM = NU * (2 * NX + 1);
@@ -829,15 +829,17 @@ PTC_D bool w_vstep(const R* e, const R* c, R* o, R* scr, int* piv) {
 
 // Riccati-form level-0 step (riccati_step): stage st, carry c -> gains
 // (written to Gam (NU*NX) and gam (NU) in the slab) and carry o.
-template <typename R, int NX, int NU>
+// kCheckR as riccati_step (elements.cuh)
+template <typename R, int NX, int NU, bool kCheckR = true>
 PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
   using S = WSlab<R, NX, NU>;
   R* FtS = scr;                          // NU x NX
   R* Qux = FtS + NU * NX;                // NU x NX
   R* Qm = Qux + NU * NX;                 // NU x NU
   R* SF = Qm + NU * NU;                  // NX x NX
+  R* fe = SF + NX * NX;                  // NU: Fu^T eta
   int fl = 0;
-  {
+  if constexpr (kCheckR) {
     R L[NU][NU];
     if (!w_chol_regs<NU>(st + S::sR, L)) fl |= FLAG_DEF_R;
   }
@@ -848,6 +850,12 @@ PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
   for (int q = lane_id(); q < NU * NX; q += 32) {
     const int i = q / NX, j = q - (q / NX) * NX;
     Qux[q] += st[S::sM + j * NU + i];
+  }
+  for (int i = lane_id(); i < NU; i += 32) {   // Fu^T eta, one lane per control
+    R f = R(0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) f = (k == 0) ? st[S::sFu + i] * c[NX * NX] : fma(st[S::sFu + k * NU + i], c[NX * NX + k], f);
+    fe[i] = f;
   }
   __syncwarp();
   R L[NU][NU];
@@ -863,14 +871,7 @@ PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
     R v[NU];
 #pragma unroll
     for (int i = 0; i < NU; ++i) {
-      if (ln < NX) {
-        v[i] = Qux[i * NX + ln];
-      } else {
-        R fe = R(0);
-#pragma unroll
-        for (int k = 0; k < NX; ++k) fe = (k == 0) ? st[S::sFu + i] * c[NX * NX] : fma(st[S::sFu + k * NU + i], c[NX * NX + k], fe);
-        v[i] = st[S::sd + i] - fe;
-      }
+      v[i] = ln < NX ? Qux[i * NX + ln] : st[S::sd + i] - fe[i];
     }
     chol_solve_vec<NU>(L, v);
 #pragma unroll
@@ -1114,7 +1115,7 @@ __global__ void __launch_bounds__(128) kw_value_down0(LqrArgs<R> a) {
       w_stage_store<R, NX, NU>(pf, alpha, st);
       if (t > t0) pf.load(t - 1);
     }
-    fl |= w_riccati<R, NX, NU>(st, c, o, Gam, gam, scr);
+    fl |= w_riccati<R, NX, NU, !kAgg>(st, c, o, Gam, gam, scr);
     if (a.staged) {  // [Gamma | gamma] contiguous in the slab and in gst
       for (int i = lane_id(); i < GC; i += 32) a.gst[(size_t)t * GC + i] = Gam[i];
     } else {
