@@ -135,6 +135,31 @@ PTC_D bool cholesky(R (&A)[N][N]) {
   return ok;
 }
 
+// The same factorisation with the reciprocal diagonal from one rsqrt
+// (<= 1 ulp, like 1/sqrt) instead of a square root and a division: the
+// warp-per-unit kernels' Cholesky factors sit on their latency-critical path.
+template <int N, typename R>
+PTC_D bool cholesky_rsqrt(R (&A)[N][N]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    R s = A[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) s = fma(-A[j][k], A[j][k], s);
+    ok = ok && (s > R(0));
+    const R inv = rsqrt(s);
+    A[j][j] = inv;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      R v = A[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v = fma(-A[i][k], A[j][k], v);
+      A[i][j] = v * inv;
+    }
+  }
+  return ok;
+}
+
 // Solve (L L^T) X = B in place, L from cholesky() (reciprocal diagonal).
 template <int N, int M, typename R>
 PTC_D void chol_solve(const R (&L)[N][N], R (&B)[N][M]) {

@@ -282,7 +282,7 @@ PTC_D bool w_chol_regs(const R* Q, R (&L)[N][N]) {
   for (int i = 0; i < N; ++i)
 #pragma unroll
     for (int j = 0; j < N; ++j) L[i][j] = Q[i * N + j];
-  return cholesky<N>(L);
+  return cholesky_rsqrt<N>(L);
 }
 
 // ------------------------------------------------------------ slab layout
@@ -865,7 +865,7 @@ PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
     for (int j = 0; j < NU; ++j)
       L[i][j] = R(0.5) * ((Qm[i * NU + j] + st[S::sR + i * NU + j]) +
                           (Qm[j * NU + i] + st[S::sR + j * NU + i]));
-  if (!cholesky<NU>(L)) fl |= FLAG_DEF_Q;
+  if (!cholesky_rsqrt<NU>(L)) fl |= FLAG_DEF_Q;
   const int ln = lane_id();
   if (ln <= NX) {  // lanes 0..NX-1: columns of Gamma, lane NX: gamma
     R v[NU];
