@@ -275,6 +275,77 @@ PTC_D void w_lu_solve(const R* LU, const int* piv, R* B) {
   __syncwarp();
 }
 
+// Small general matrices (nu <= 6): every lane factors its own register copy
+// with the arithmetic of w_lu (same pivot rule, reciprocal pivots), fully
+// unrolled so rows are swapped by static selects instead of local memory.
+template <int N, typename R>
+PTC_D bool lu_regs(R (&G)[N][N], int (&perm)[N]) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    R v = fabs(G[k][k]);
+    int p = k;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      const R vi = fabs(G[i][k]);
+      if (vi > v) {
+        v = vi;
+        p = i;
+      }
+    }
+    if (!(v == v)) p = k;
+    perm[k] = p;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i)
+      if (i == p)
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const R t = G[k][j];
+          G[k][j] = G[i][j];
+          G[i][j] = t;
+        }
+    const R pv = G[k][k];
+    ok = ok && (pv != R(0));
+    const R inv = R(1) / pv;
+    G[k][k] = inv;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) G[i][k] *= inv;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i)
+#pragma unroll
+      for (int j = k + 1; j < N; ++j) G[i][j] = fma(-G[i][k], G[k][j], G[i][j]);
+  }
+  return ok;
+}
+
+// one right-hand side through the factors of lu_regs (as w_lu_solve)
+template <int N, typename R>
+PTC_D void lu_solve_regs(const R (&LU)[N][N], const int (&perm)[N], R (&b)[N]) {
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int i = k + 1; i < N; ++i)
+      if (i == perm[k]) {
+        const R t = b[k];
+        b[k] = b[i];
+        b[i] = t;
+      }
+#pragma unroll
+  for (int i = 1; i < N; ++i) {
+    R v = b[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) v = fma(-LU[i][k], b[k], v);
+    b[i] = v;
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    R v = b[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) v = fma(-LU[i][k], b[k], v);
+    b[i] = v * LU[i][i];
+  }
+}
+
 // Small SPD matrices (nu <= 6): every lane factors its own register copy.
 template <int N, typename R>
 PTC_D bool w_chol_regs(const R* Q, R (&L)[N][N]) {
@@ -749,10 +820,29 @@ PTC_D int w_vcombine_stage(const R* st, const R* r, R* o, R* scr, int* piv) {
     Y2[e] = AF[j * NU + i];
   }
   __syncwarp();
-  if (!w_lu<NU>(Q, piv)) fl |= FLAG_COND;
-  w_lu_solve<NU, NX>(Q, piv, W);
-  w_lu_solve<NU, 1>(Q, piv, q);
-  w_lu_solve<NU, NX>(Q, piv, Y2);
+  {
+    // Q^-1 [W | Y2 | q]: each lane factors Q in registers and solves one of
+    // the 2 NX + 1 columns (no shuffles or warp barriers inside)
+    R G[NU][NU];
+    int perm[NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+#pragma unroll
+      for (int j = 0; j < NU; ++j) G[i][j] = Q[i * NU + j];
+    if (!lu_regs<NU>(G, perm)) fl |= FLAG_COND;
+    static_assert(2 * NX + 1 <= 32, "one lane per right-hand side");
+    if (ln < 2 * NX + 1) {
+      R* col = ln < NX ? W + ln : (ln < 2 * NX ? Y2 + (ln - NX) : q);
+      const int stride = ln < 2 * NX ? NX : 1;
+      R bv[NU];
+#pragma unroll
+      for (int i = 0; i < NU; ++i) bv[i] = col[i * stride];
+      lu_solve_regs<NU>(G, perm, bv);
+#pragma unroll
+      for (int i = 0; i < NU; ++i) col[i * stride] = bv[i];
+    }
+    __syncwarp();
+  }
   // Z1 = Y_r A_l - YF W ;  o.Y += A_l^T Z1 ; z = v - YF q ; x = b_l + Fu q
   w_mm<NX, NU, NX, false, false, -1>(YF, W, Z1);
   for (int i = ln; i < NX; i += 32) {
