@@ -64,7 +64,7 @@ PTC_D void dmma_8x8x4(double (&d)[2], double a, double b) {
 }
 
 template <int M, int K, int N, bool TA, bool TB, int MODE>
-PTC_D void w_mm_dmma(const double* A, const double* B, double* C) {
+PTC_D void w_mm_dmma(const double* A, const double* B, double* C, const double* D = nullptr) {
   constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8, KB = (K + 3) / 4;
   const int ln = lane_id();
   const int fr = ln >> 2, fc = ln & 3;
@@ -72,7 +72,13 @@ PTC_D void w_mm_dmma(const double* A, const double* B, double* C) {
 #pragma unroll
   for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        // MODE +-2: the accumulator starts from D (C = D +- AB)
+        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
+        acc[mb][nb][e] = ((MODE == 2 || MODE == -2) && i < M && j < N) ? D[i * N + j] : 0.0;
+      }
 #pragma unroll
   for (int kb = 0; kb < KB; ++kb) {
     const int k = kb * 4 + fc;
@@ -81,6 +87,7 @@ PTC_D void w_mm_dmma(const double* A, const double* B, double* C) {
     for (int mb = 0; mb < MB; ++mb) {
       const int i = mb * 8 + fr;
       af[mb] = (i < M && k < K) ? (TA ? A[k * M + i] : A[i * K + k]) : 0.0;
+      if (MODE == -2) af[mb] = -af[mb];
     }
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
@@ -102,7 +109,7 @@ PTC_D void w_mm_dmma(const double* A, const double* B, double* C) {
         const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
         if (i < M && j < N) {
           double& c = C[i * N + j];
-          if (MODE == 0) c = acc[mb][nb][e];
+          if (MODE == 0 || MODE == 2 || MODE == -2) c = acc[mb][nb][e];
           else if (MODE > 0) c += acc[mb][nb][e];
           else c -= acc[mb][nb][e];
         }
@@ -111,15 +118,17 @@ PTC_D void w_mm_dmma(const double* A, const double* B, double* C) {
 }
 
 // C (MxN) = op(A) op(B); A stored row-major as (TA ? KxM : MxK), B as
-// (TB ? NxK : KxN).  MODE 0: C = AB, 1: C += AB, -1: C -= AB.  C must not
-// alias A or B.  FP64 products with at least 48 outputs go to the tensor
-// cores (w_mm_dmma); the rest are register-blocked lane products.
+// (TB ? NxK : KxN).  MODE 0: C = AB, 1: C += AB, -1: C -= AB, 2: C = D + AB,
+// -2: C = D - AB (D MxN, may be C).  C must not alias A or B.  FP64 products
+// with at least 48 outputs go to the tensor cores (w_mm_dmma); the rest are
+// register-blocked lane products.
 template <int M, int K, int N, bool TA, bool TB, int MODE, typename R>
-PTC_D void w_mm(const R* A, const R* B, R* C) {
+PTC_D void w_mm(const R* A, const R* B, R* C, const R* D = nullptr) {
   if constexpr (sizeof(R) == 8 && M * N >= 48 && M >= 4 && N >= 4) {
     w_mm_dmma<M, K, N, TA, TB, MODE>(reinterpret_cast<const double*>(A),
                                      reinterpret_cast<const double*>(B),
-                                     reinterpret_cast<double*>(C));
+                                     reinterpret_cast<double*>(C),
+                                     reinterpret_cast<const double*>(D));
     return;
   }
   constexpr MMPlan pl = mm_plan(M, N);
@@ -127,25 +136,36 @@ PTC_D void w_mm(const R* A, const R* B, R* C) {
   for (int blk = lane_id(); blk < NB; blk += 32) {
     const int i0 = (blk / NBJ) * BI, j0 = (blk - (blk / NBJ) * NBJ) * BJ;
     R acc[BI][BJ];
+    constexpr bool kD = MODE == 2 || MODE == -2;
+    if constexpr (kD) {
+#pragma unroll
+      for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) acc[ii][jj] = D[(i0 + ii) * N + j0 + jj];
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       R av[BI], bv[BJ];
 #pragma unroll
-      for (int ii = 0; ii < BI; ++ii) av[ii] = TA ? A[k * M + i0 + ii] : A[(i0 + ii) * K + k];
+      for (int ii = 0; ii < BI; ++ii) {
+        av[ii] = TA ? A[k * M + i0 + ii] : A[(i0 + ii) * K + k];
+        if (MODE == -2) av[ii] = -av[ii];
+      }
 #pragma unroll
       for (int jj = 0; jj < BJ; ++jj) bv[jj] = TB ? B[(j0 + jj) * K + k] : B[k * N + j0 + jj];
 #pragma unroll
       for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
         for (int jj = 0; jj < BJ; ++jj)
-          acc[ii][jj] = (k == 0) ? av[ii] * bv[jj] : fma(av[ii], bv[jj], acc[ii][jj]);
+          acc[ii][jj] = (k == 0 && !kD) ? av[ii] * bv[jj] : fma(av[ii], bv[jj], acc[ii][jj]);
     }
+    // (D may be C: each output position is read and written by its own lane)
 #pragma unroll
     for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
       for (int jj = 0; jj < BJ; ++jj) {
         R& c = C[(i0 + ii) * N + j0 + jj];
-        if (MODE == 0) c = acc[ii][jj];
+        if (MODE == 0 || kD) c = acc[ii][jj];
         else if (MODE > 0) c += acc[ii][jj];
         else c -= acc[ii][jj];
       }
@@ -773,10 +793,8 @@ PTC_D int w_vcombine_stage(const R* st, const R* r, R* o, R* scr, int* piv) {
   }
   __syncwarp();
   // A_l = Fx - Fu RiMt ;  Y_l = sym(P - M RiMt) (into o.Y) ;  YF = Y_r Fu
-  w_copy<NX * NX>(st + S::sFx, Al);
-  w_mm<NX, NU, NX, false, false, -1>(Fu, RiMt, Al);
-  w_copy<NX * NX>(st + S::sP, o + S::eY);
-  w_mm<NX, NU, NX, false, false, -1>(st + S::sM, RiMt, o + S::eY);
+  w_mm<NX, NU, NX, false, false, -2>(Fu, RiMt, Al, st + S::sFx);
+  w_mm<NX, NU, NX, false, false, -2>(st + S::sM, RiMt, o + S::eY, st + S::sP);
   w_sym<NX>(o + S::eY);
   w_mm<NX, NX, NU, false, false, 0>(r + S::eY, Fu, YF);
   for (int i = ln; i < NX; i += 32) {  // eta_l (into o.eta), b_l
@@ -862,8 +880,7 @@ PTC_D int w_vcombine_stage(const R* st, const R* r, R* o, R* scr, int* piv) {
   w_mm<NX, NU, NX, false, false, -1>(Fu, W, Al);
   w_mm<NX, NX, NX, false, false, 0>(r + S::eA, Al, o + S::eA);
   // C = sym(AF Y2 + C_r) ;  b = A_r x + b_r
-  w_copy<NX * NX>(r + S::eC, o + S::eC);
-  w_mm<NX, NU, NX, false, false, 1>(AF, Y2, o + S::eC);
+  w_mm<NX, NU, NX, false, false, 2>(AF, Y2, o + S::eC, r + S::eC);
   w_copy<NX>(r + S::eB, o + S::eB);
   w_mv<NX, NX, false, 1>(r + S::eA, x, o + S::eB);
   w_sym<NX>(o + S::eY);
@@ -1002,13 +1019,8 @@ PTC_D void w_aff_compose(const R* outer, const R* inner, R* o) {
 // closed-loop map of stage t: F = Fx + Fu Gamma (0 at global stage 0), e = Fu gamma
 template <typename R, int NX, int NU>
 PTC_D void w_closed_loop(const R* Fx, const R* Fu, const R* Gam, const R* gam, bool head, R* m) {
-  for (int q = lane_id(); q < NX * NX; q += 32) {
-    const int i = q / NX, j = q - (q / NX) * NX;
-    R s = R(0);
-#pragma unroll
-    for (int k = 0; k < NU; ++k) s = (k == 0) ? Fu[i * NU] * Gam[j] : fma(Fu[i * NU + k], Gam[k * NX + j], s);
-    m[q] = head ? R(0) : s + Fx[q];
-  }
+  if (head) w_fill<NX * NX>(m, R(0));
+  else w_mm<NX, NU, NX, false, false, 2>(Fu, Gam, m, Fx);   // Fx + Fu Gamma
   for (int i = lane_id(); i < NX; i += 32) {
     R s = R(0);
 #pragma unroll
