@@ -989,10 +989,8 @@ PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
   }
   __syncwarp();
   // S' = sym(P + Fx^T SF + Qux^T Gam), eta' = Fx^T eta - Qux^T gam
-  w_mm<NX, NX, NX, true, false, 0>(st + S::sFx, SF, o);
+  w_mm<NX, NX, NX, true, false, 2>(st + S::sFx, SF, o, st + S::sP);
   w_mm<NX, NU, NX, true, false, 1>(Qux, Gam, o);
-  for (int q = ln; q < NX * NX; q += 32) o[q] += st[S::sP + q];
-  __syncwarp();
   for (int i = ln; i < NX; i += 32) {
     R s = R(0);
 #pragma unroll
