@@ -131,27 +131,71 @@ PTC_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) :
 
 // ------------------------------------------------------------ stage algebra
 
-// Augmentation derivatives (models.cuh aug_derivs), one lane per variable:
-// lane v < NX owns x_v, NX <= v < NX + NU owns u_{v-NX}; each folds the
-// stacked rows on its variable in row order.  out = [cx | cu | cxx | cuu].
+// The stacked constraint rows on one lane's variable (lane v < NX: x_v,
+// NX <= v < NX + NU: u_{v-NX}), collected once per kernel in row order:
+// box constraints put at most an upper and a lower row on a variable.
+template <typename R>
+struct LaneRows {
+  static constexpr int kMax = 4;
+  int n;             // rows on this variable; > kMax: use the general loop
+  int k[kMax];
+  R sgn[kMax], bnd[kMax];
+};
+
 template <typename R, int NX, int NU>
-PTC_D void w_aug_derivs(const ProblemParams& p, const AugArgs<R>& g, int t, int T, int B, int b,
-                        const R* x, const R* u, R* out) {
+PTC_D LaneRows<R> lane_rows(const ProblemParams& p) {
+  LaneRows<R> r;
+  r.n = 0;
+  const int v = lane_id();
+  const int var = v < NX ? 0 : 1, idx = v < NX ? v : v - NX;
+  for (int k = 0; k < p.W && v < NX + NU; ++k) {
+    if (p.row_var[k] != var || p.row_idx[k] != idx) continue;
+#pragma unroll
+    for (int q = 0; q < LaneRows<R>::kMax; ++q)
+      if (q == r.n) {
+        r.k[q] = k;
+        r.sgn[q] = R(p.row_sign[k]);
+        r.bnd[q] = R(p.row_bound[k]);
+      }
+    ++r.n;
+  }
+  return r;
+}
+
+// Augmentation derivatives (models.cuh aug_derivs), one lane per variable,
+// each folding the rows on its variable in row order (same arithmetic: the
+// row signs are +-1, so sgn / w == sgn * (1 / w) exactly).
+// out = [cx | cu | cxx | cuu].
+template <typename R, int NX, int NU>
+PTC_D void w_aug_derivs(const ProblemParams& p, const AugArgs<R>& g, const LaneRows<R>& lr, int t,
+                        int T, int B, int b, const R* x, const R* u, R* out) {
   const int v = lane_id();
   if (v < NX + NU) {
     const int var = v < NX ? 0 : 1, idx = v < NX ? v : v - NX;
     const R val = v < NX ? x[v] : u[v - NX];
     R gs = R(0), hs = R(0);
     if (g.kind == AUG_BARRIER) {
-      for (int k = 0; k < p.W; ++k) {
-        if (p.row_var[k] != var || p.row_idx[k] != idx) continue;
-        const R bnd = R(p.row_bound[k]);
-        const R w = p.row_sign[k] > 0 ? val - bnd : bnd - val;
-        const R inv = R(1) / w;
-        const R sgn = R(p.row_sign[k]);
-        const R sc = sgn / w;
-        gs += sgn * inv;
-        hs += sc * sc;
+      if (lr.n <= LaneRows<R>::kMax) {
+#pragma unroll
+        for (int q = 0; q < LaneRows<R>::kMax; ++q) {
+          if (q >= lr.n) break;
+          const R w = lr.sgn[q] > 0 ? val - lr.bnd[q] : lr.bnd[q] - val;
+          const R inv = R(1) / w;
+          const R sc = lr.sgn[q] * inv;
+          gs += lr.sgn[q] * inv;
+          hs += sc * sc;
+        }
+      } else {
+        for (int k = 0; k < p.W; ++k) {
+          if (p.row_var[k] != var || p.row_idx[k] != idx) continue;
+          const R bnd = R(p.row_bound[k]);
+          const R w = p.row_sign[k] > 0 ? val - bnd : bnd - val;
+          const R inv = R(1) / w;
+          const R sgn = R(p.row_sign[k]);
+          const R sc = sgn / w;
+          gs += sgn * inv;
+          hs += sc * sc;
+        }
       }
       const R mu = R(g.mu[b]);
       gs = -mu * gs;
@@ -220,6 +264,7 @@ __global__ void __launch_bounds__(64) kwn_costate_up0(NewtonArgs<R> a) {
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   const ProblemParams& p = *a.pp;
   const AugArgs<R> g = aug_of(a);
+  const LaneRows<R> lr = lane_rows<R, NX, NU>(p);
   R* acc = slab;
   R* m = acc + N::CC;
   R* o = m + N::CC;
@@ -239,7 +284,7 @@ __global__ void __launch_bounds__(64) kwn_costate_up0(NewtonArgs<R> a) {
   for (int t = t1 - 1; t >= t0; --t) {
     pf.store(F);
     if (t - 1 >= t0) pf.load(t - 1);
-    w_aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, uu, aug);
+    w_aug_derivs<R, NX, NU>(p, g, lr, t, T, B, b, x, uu, aug);
     for (int e = ln; e < NX * NX; e += 32) {
       const int i = e / NX, k = e - (e / NX) * NX;
       m[e] = F[k * NX + i];
@@ -359,6 +404,7 @@ __global__ void __launch_bounds__(64) kwn_costate_down0(NewtonArgs<R> a, R* xst)
   const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   const ProblemParams& p = *a.pp;
   const AugArgs<R> g = aug_of(a);
+  const LaneRows<R> lr = lane_rows<R, NX, NU>(p);
   R* F = slab;                 // [A | Bm | x | u]
   R* Bm = F + NX * NX;
   R* x = Bm + NX * NU;
@@ -398,7 +444,7 @@ __global__ void __launch_bounds__(64) kwn_costate_down0(NewtonArgs<R> a, R* xst)
   for (int t = t1 - 1; t >= t0; --t) {
     pf.store(F);
     if (t - 1 >= t0) pf.load(t - 1);
-    w_aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, uu, aug);
+    w_aug_derivs<R, NX, NU>(p, g, lr, t, T, B, b, x, uu, aug);
     if (ln < NX) {
       const int i = ln;
       R lx = R(0);
