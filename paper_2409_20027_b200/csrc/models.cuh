@@ -356,6 +356,37 @@ struct CostRegs {
   }
 };
 
+// Wide states: the constants in shared memory instead (one copy per block;
+// a register copy of Q would spill at nx = 12).
+template <typename R, int NX, int NU>
+struct CostSmem {
+  R goal[NX], Q[NX][NX], Rc[NU][NU];
+  // every thread of the block calls this (it synchronises the block)
+  PTC_D void load(const ProblemParams& p) {
+    for (int e = threadIdx.x; e < NX * NX; e += blockDim.x) Q[e / NX][e % NX] = R(p.Q[e]);
+    for (int e = threadIdx.x; e < NU * NU; e += blockDim.x) Rc[e / NU][e % NU] = R(p.Rc[e]);
+    for (int e = threadIdx.x; e < NX; e += blockDim.x) goal[e] = R(p.goal[e]);
+    __syncthreads();
+  }
+};
+
+template <typename R, int NX, int NU>
+PTC_D R stage_cost(const CostSmem<R, NX, NU>& p, const R (&x)[NX], const R (&u)[NU]) {
+  R e[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e[i] = x[i] - p.goal[i];
+  R qx = R(0), ru = R(0);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) qx += e[i] * p.Q[i][j] * e[j];
+#pragma unroll
+  for (int i = 0; i < NU; ++i)
+#pragma unroll
+    for (int j = 0; j < NU; ++j) ru += u[i] * p.Rc[i][j] * u[j];
+  return R(0.5) * (qx + ru);
+}
+
 template <typename R, int NX, int NU>
 PTC_D R stage_cost(const CostRegs<R, NX, NU>& p, const R (&x)[NX], const R (&u)[NU]) {
   R e[NX];

@@ -211,6 +211,10 @@ __global__ void k_admm_init(NewtonArgs<R> a) {
 // which = 0: current trajectory (only when PH_NEED_COST), 1: the candidate
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int which) {
+  // cost constants: registers for small states, the block's shared copy for
+  // wide ones (loaded before any thread leaves)
+  __shared__ CostSmem<R, NX, NU> cs_shared;
+  if constexpr (NX >= 8) cs_shared.load(*a.pp);
   const int P0 = a.plan.units0();
   const int u0 = unit_id();
   if (u0 >= P0 * a.B) return;
@@ -225,12 +229,13 @@ __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int whic
   double sl = 0.0, sc = 0.0;
   int bad = -1;
   CostRegs<R, NX, NU> cr;
-  cr.load(p);
+  if constexpr (NX < 8) cr.load(p);
   for (int t = t0; t < t1; ++t) {
     R x[NX], u[NU];
     ld_x(a, q, t, b, x);
     ld_u(a, q, t, b, u);
-    sl += double(stage_cost<R, NX, NU>(cr, x, u));
+    if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
+    else sl += double(stage_cost<R, NX, NU>(cs_shared, x, u));
     int br;
     sc += double(aug_value<R, NX, NU>(p, g, t, T, B, b, x, u, br));
     if (br >= 0 && bad < 0) bad = t * p.W + br;
@@ -646,7 +651,7 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
   int bad = -1;
   const AugArgs<R> g = aug_of(a);
   CostRegs<R, NX, NU> cr;
-  if constexpr (kCost) cr.load(gp);
+  if constexpr (kCost && NX < 8) cr.load(gp);
   R ring[kRing][NU];
   auto fetch = [&](int t, R (&u)[NU]) {
     if (t < T) {
@@ -674,7 +679,8 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
         fetch(t + kRing, ring[k]);
         if (!kFromUc) st_vec(Uc, t, T, B, b, u);
         if constexpr (kCost) {
-          sl += double(stage_cost<R, NX, NU>(cr, x, u));
+          if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
+          else sl += double(stage_cost<R, NX, NU>(gp, x, u));
           int br;
           sc += double(aug_value<R, NX, NU>(gp, g, t, T, B, b, x, u, br));
           if (br >= 0 && bad < 0) bad = t * gp.W + br;
