@@ -225,6 +225,15 @@ PTC_D void w_aug_derivs(const ProblemParams& p, const AugArgs<R>& g, const LaneR
   __syncwarp();
 }
 
+// the warp's copy of the stage-cost constants [Q | goal | Rc]
+template <typename R, int NX, int NU>
+PTC_D void w_cost_consts(const ProblemParams& p, R* ck) {
+  for (int e = lane_id(); e < NX * NX; e += 32) ck[e] = R(p.Q[e]);
+  for (int e = lane_id(); e < NX; e += 32) ck[NX * NX + e] = R(p.goal[e]);
+  for (int e = lane_id(); e < NU * NU; e += 32) ck[NX * NX + NX + e] = R(p.Rc[e]);
+  __syncwarp();
+}
+
 template <typename R>
 PTC_D bool nw_skip(const NewtonArgs<R>& a, int b, int gate) {
   if (gate == 1) return !running(a, b) || !(a.phase[b] & PH_NEED_EXP);
@@ -236,9 +245,10 @@ template <typename R, int NX, int NU>
 struct NSlab {
   static constexpr int CC = NX * NX + NX;
   static constexpr int AUG = 2 * NX + 2 * NU;
-  static constexpr int kCoUp0 = 3 * CC + (NX * NX + NX + NU) + AUG + 2 * NX;
+  static constexpr int CK = NX * NX + NX + NU * NU;   // Q, goal, Rc copies
+  static constexpr int kCoUp0 = 3 * CC + (NX * NX + NX + NU) + AUG + 2 * NX + CK;
   static constexpr int kTree = 3 * CC;
-  static constexpr int kCoDown0 = (NX * NX + NX * NU + NX + NU) + 2 * NX + AUG;
+  static constexpr int kCoDown0 = (NX * NX + NX * NU + NX + NU) + 2 * NX + AUG + CK;
   static constexpr int ROLL = CC + NX * NU + 2 * NU;   // [A | c | Bm | u | du]
   static constexpr int kRollUp0 = 2 * CC + ROLL;
   static constexpr int kRollDown0 = 2 * NX + ROLL;
@@ -274,7 +284,10 @@ __global__ void __launch_bounds__(64) kwn_costate_up0(NewtonArgs<R> a) {
   R* aug = uu + NU;
   R* v0 = aug + N::AUG;
   R* v1 = v0 + NX;
+  R* Qs = v1 + NX;             // [Q | goal | Rc]
+  const R* gs = Qs + NX * NX;
   const int ln = lane_id();
+  w_cost_consts<R, NX, NU>(p, Qs);
   w_identity<NX>(acc);
   w_fill<NX>(acc + NX * NX, R(0));
   WGather<R, NX * NX, NX, NU> pf;
@@ -292,7 +305,7 @@ __global__ void __launch_bounds__(64) kwn_costate_up0(NewtonArgs<R> a) {
     for (int i = ln; i < NX; i += 32) {
       R lx = R(0);
 #pragma unroll
-      for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+      for (int k = 0; k < NX; ++k) lx += (x[k] - gs[k]) * Qs[i * NX + k];
       m[NX * NX + i] = lx + aug[i];
     }
     __syncwarp();
@@ -412,8 +425,12 @@ __global__ void __launch_bounds__(64) kwn_costate_down0(NewtonArgs<R> a, R* xst)
   R* lnx = uu + NU;            // lambda_{t+1}
   R* lt = lnx + NX;            // lambda_t
   R* aug = lt + NX;
+  R* Qs = aug + N::AUG;        // [Q | goal | Rc]
+  const R* gs = Qs + NX * NX;
+  const R* Rcs = gs + NX;
   const int ln = lane_id();
   const R* X = a.X + q * a.xsz;
+  w_cost_consts<R, NX, NU>(p, Qs);
   if (j == P0 - 1 && a.blk && !a.blk_last) {
     w_ld<NX>(a.lam_in, 0, 1, B, b, lnx);   // carry from the later blocks
     w_st<NX>(a.lam, T, T + 1, B, b, lnx);
@@ -449,7 +466,7 @@ __global__ void __launch_bounds__(64) kwn_costate_down0(NewtonArgs<R> a, R* xst)
       const int i = ln;
       R lx = R(0);
 #pragma unroll
-      for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+      for (int k = 0; k < NX; ++k) lx += (x[k] - gs[k]) * Qs[i * NX + k];
       R fxl = F[i] * lnx[0];
 #pragma unroll
       for (int k = 1; k < NX; ++k) fxl = fma(F[k * NX + i], lnx[k], fxl);
@@ -461,7 +478,7 @@ __global__ void __launch_bounds__(64) kwn_costate_down0(NewtonArgs<R> a, R* xst)
       for (int k = 1; k < NX; ++k) ftl = fma(Bm[k * NU + i], lnx[k], ftl);
       R ru = R(0);
 #pragma unroll
-      for (int k = 0; k < NU; ++k) ru += uu[k] * R(p.Rc[i * NU + k]);
+      for (int k = 0; k < NU; ++k) ru += uu[k] * Rcs[i * NU + k];
       const R di = (ru + aug[NX + i]) + ftl;
       if (xst) xst[(size_t)t * WS::SC + WS::sd + i] = di;
       else a.d[((size_t)i * T + t) * B + b] = di;
@@ -472,15 +489,15 @@ __global__ void __launch_bounds__(64) kwn_costate_down0(NewtonArgs<R> a, R* xst)
     for (int e = ln; e < 2 * nP + nR + 2 * nM; e += 32) {
       if (e < nP) {
         const int i = e / NX, k = e - (e / NX) * NX;
-        const R pik = (R(p.Q[i * NX + k]) + (i == k ? cxx[i] : R(0))) + R(0);
-        const R pki = (R(p.Q[k * NX + i]) + (i == k ? cxx[i] : R(0))) + R(0);
+        const R pik = (Qs[i * NX + k] + (i == k ? cxx[i] : R(0))) + R(0);
+        const R pki = (Qs[k * NX + i] + (i == k ? cxx[i] : R(0))) + R(0);
         const R v = i == k ? pik : R(0.5) * (pik + pki);
         if (row) row[WS::sP + e] = v;
         else a.P[((size_t)e * T + t) * B + b] = v;
       } else if (e < nP + nR) {
         const int c = e - nP, i = c / NU, k = c - (c / NU) * NU;
-        const R rik = (R(p.Rc[i * NU + k]) + (i == k ? cuu[i] : R(0))) + R(0);
-        const R rki = (R(p.Rc[k * NU + i]) + (i == k ? cuu[i] : R(0))) + R(0);
+        const R rik = (Rcs[i * NU + k] + (i == k ? cuu[i] : R(0))) + R(0);
+        const R rki = (Rcs[k * NU + i] + (i == k ? cuu[i] : R(0))) + R(0);
         const R v = i == k ? rik : R(0.5) * (rik + rki);
         if (row) row[WS::sR + c] = v;
         else a.Rm[((size_t)c * T + t) * B + b] = v;
