@@ -190,15 +190,27 @@ PTC_D void w_mv(const R* A, const R* x, R* y) {
   __syncwarp();
 }
 
+// A = (A + A^T) / 2 in place: lanes walk the N (N - 1) / 2 strictly-upper
+// pairs (row-major), the pair's row from the quadratic offset formula
+// i (2N - 1 - i) / 2 <= p (float root, corrected by one step either way)
 template <int N, typename R>
 PTC_D void w_sym(R* A) {
-  for (int e = lane_id(); e < N * N; e += 32) {
-    const int i = e / N, j = e - (e / N) * N;
-    if (j > i) {
-      const R v = R(0.5) * (A[i * N + j] + A[j * N + i]);
-      A[i * N + j] = v;
-      A[j * N + i] = v;
+  constexpr int NP = N * (N - 1) / 2;
+  constexpr float kB = float(2 * N - 1);
+  for (int p = lane_id(); p < NP; p += 32) {
+    int i = int((kB - sqrtf(kB * kB - 8.0f * float(p))) * 0.5f);
+    int off = i * (2 * N - 1 - i) / 2;
+    if (off > p) {
+      --i;
+      off = i * (2 * N - 1 - i) / 2;
+    } else if (p >= off + (N - 1 - i)) {
+      off += N - 1 - i;
+      ++i;
     }
+    const int j = i + 1 + (p - off);
+    const R v = R(0.5) * (A[i * N + j] + A[j * N + i]);
+    A[i * N + j] = v;
+    A[j * N + i] = v;
   }
   __syncwarp();
 }
@@ -794,8 +806,9 @@ PTC_D int w_vcombine_stage(const R* st, const R* r, R* o, R* scr, int* piv) {
   __syncwarp();
   // A_l = Fx - Fu RiMt ;  Y_l = sym(P - M RiMt) (into o.Y) ;  YF = Y_r Fu
   w_mm<NX, NU, NX, false, false, -2>(Fu, RiMt, Al, st + S::sFx);
+  // (Y_l is only accumulated into o.Y, symmetrised once at the end:
+  // sym(sym(P - M RiMt) + A_l^T Z1) == sym(P - M RiMt + A_l^T Z1))
   w_mm<NX, NU, NX, false, false, -2>(st + S::sM, RiMt, o + S::eY, st + S::sP);
-  w_sym<NX>(o + S::eY);
   w_mm<NX, NX, NU, false, false, 0>(r + S::eY, Fu, YF);
   for (int i = ln; i < NX; i += 32) {  // eta_l (into o.eta), b_l
     R me = R(0), fb = R(0);
