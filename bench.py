@@ -770,7 +770,7 @@ def long_horizon_leg(torch, world: int, rank: int, steps: int = 5, chunk0: int =
     linearised-quadrotor-like data generated on the device (seeded per
     rank): A_k = I + dt F_k (dt = 0.01, F_k ~ N(0, 0.2) on a 3x3-block
     band), B_k ~ N(0, 0.1), Q = diag U(0.1, 10), R = 0.1 I, d = B_k^T c_k
-    with c_k ~ N(0, 0.01)."""
+    with c_k ~ N(0, 0.01); the expansion is handed over as stage rows."""
     import torch.distributed as dist
     from paper_2409_20027_b200.sharded import (CudaBlockOps, TimeShardedLqr, block_bounds,
                                                nccl_gather)
@@ -789,17 +789,18 @@ def long_horizon_leg(torch, world: int, rank: int, steps: int = 5, chunk0: int =
     Bm = torch.randn(Tl, nx, nu, generator=g, device=dev, dtype=f64) * (0.1 ** 0.5)
     qd = torch.empty(nx, dtype=f64, device=dev).uniform_(0.1, 10.0, generator=g)
     c = torch.randn(Tl, nx, generator=g, device=dev, dtype=f64) * 0.1
-    soa = lambda t, comps: t.reshape(Tl, comps).t().contiguous().unsqueeze(-1)
-    Pm = soa(torch.diag(qd).expand(Tl, nx, nx), nx * nx)
-    Rm = soa((0.1 * torch.eye(nu, dtype=f64, device=dev)).expand(Tl, nu, nu), nu * nu)
-    Mm = torch.zeros(nx * nu, Tl, 1, dtype=f64, device=dev)
-    dm = soa(torch.einsum("tij,ti->tj", Bm, c), nu)
-    Fx, Fu = soa(A, nx * nx), soa(Bm, nx * nu)
+    # one long problem: the expansion as stage rows [P | R | M | d | Fx | Fu]
+    # (the layout the warp kernels read; ptc_lqr_block_solve_rows)
+    rows = torch.cat([torch.diag(qd).expand(Tl, nx, nx).reshape(Tl, -1),
+                      (0.1 * torch.eye(nu, dtype=f64, device=dev)).expand(Tl, nu, nu).reshape(Tl, -1),
+                      torch.zeros(Tl, nx * nu, dtype=f64, device=dev),
+                      torch.einsum("tij,ti->tj", Bm, c), A.reshape(Tl, -1), Bm.reshape(Tl, -1)],
+                     dim=1).contiguous()
     PT = (10.0 * torch.diag(qd)).reshape(nx * nx, 1, 1).contiguous()
     alpha = torch.zeros(1, dtype=f64, device=dev)
     del F, A, Bm, c
-    ops = CudaBlockOps(rank, world, t0, Pm, Rm, Mm, dm, Fx, Fu, PT, alpha, nx, nu,
-                       chunk0=chunk0, chunk=chunk)
+    ops = CudaBlockOps.from_rows(rank, world, t0, rows, PT, alpha, nx, nu, chunk0=chunk0,
+                                 chunk=chunk)
     drv = TimeShardedLqr(ops, nccl_gather() if world > 1 else (lambda t: t.unsqueeze(0)))
     for _ in range(2):
         drv.solve()

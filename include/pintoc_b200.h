@@ -176,6 +176,17 @@ int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, in
                         void* block_out, void* S, void* s, void* Gamma, void* gamma, void* dx,
                         void* du, int* flags, void* workspace, int64_t workspace_bytes,
                         int chunk0, int chunk, void* stream);
+/* The same for one long problem (batch 1, nx >= 8, >= 1024 stages per
+ * block) whose expansion is given as stage rows: rows[t * SC + c] with the
+ * row [P (nx*nx) | R (nu*nu) | M (nx*nu) | d (nu) | Fx (nx*nx) | Fu (nx*nu)],
+ * SC their total -- the layout the warp-per-unit kernels read, so no
+ * transpose precedes the scans. */
+int ptc_lqr_block_solve_rows(int phase, int dtype, int horizon, int nx, int nu, int t_base,
+                             int is_last, int rank, int world, const void* rows, const void* PT,
+                             const double* alpha, const void* blocks_in, void* block_out,
+                             void* S, void* s, void* Gamma, void* gamma, void* dx, void* du,
+                             int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                             int chunk, void* stream);
 
 /* ------------------------------------------------------------------------
  * Batched device-resident solver

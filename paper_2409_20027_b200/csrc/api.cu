@@ -314,6 +314,15 @@ int64_t ptc_lqr_block_workspace_bytes(int dtype, int batch, int horizon, int nx,
   return (int64_t)c.off + 256;
 }
 
+static int lqr_block_solve_impl(int phase, int dtype, int batch, int horizon, int nx, int nu,
+                                int t_base, int is_last, int rank, int world, const void* P,
+                                const void* R, const void* M, const void* d, const void* Fx,
+                                const void* Fu, const void* rows, const void* PT,
+                                const double* alpha, const void* blocks_in, void* block_out,
+                                void* S, void* s, void* Gamma, void* gamma, void* dx, void* du,
+                                int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                                int chunk, void* stream);
+
 int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, int nu, int t_base,
                         int is_last, int rank, int world, const void* P, const void* R,
                         const void* M, const void* d, const void* Fx, const void* Fu,
@@ -321,6 +330,36 @@ int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, in
                         void* block_out, void* S, void* s, void* Gamma, void* gamma, void* dx,
                         void* du, int* flags, void* workspace, int64_t workspace_bytes,
                         int chunk0, int chunk, void* stream) {
+  if (!P || !R || !M || !d || !Fx || !Fu) return fail(PTC_ERR_ARG, "missing expansion buffer");
+  return lqr_block_solve_impl(phase, dtype, batch, horizon, nx, nu, t_base, is_last, rank, world,
+                              P, R, M, d, Fx, Fu, nullptr, PT, alpha, blocks_in, block_out, S, s,
+                              Gamma, gamma, dx, du, flags, workspace, workspace_bytes, chunk0,
+                              chunk, stream);
+}
+
+int ptc_lqr_block_solve_rows(int phase, int dtype, int horizon, int nx, int nu, int t_base,
+                             int is_last, int rank, int world, const void* rows, const void* PT,
+                             const double* alpha, const void* blocks_in, void* block_out,
+                             void* S, void* s, void* Gamma, void* gamma, void* dx, void* du,
+                             int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                             int chunk, void* stream) {
+  if (!rows) return fail(PTC_ERR_ARG, "rows is required");
+  if (nx < 8) return fail(PTC_ERR_UNSUPPORTED, "stage-row inputs are read by the nx >= 8 kernels");
+  if (horizon < 1024) return fail(PTC_ERR_ARG, "stage-row inputs need a block of >= 1024 stages");
+  return lqr_block_solve_impl(phase, dtype, 1, horizon, nx, nu, t_base, is_last, rank, world,
+                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, rows, PT,
+                              alpha, blocks_in, block_out, S, s, Gamma, gamma, dx, du, flags,
+                              workspace, workspace_bytes, chunk0, chunk, stream);
+}
+
+static int lqr_block_solve_impl(int phase, int dtype, int batch, int horizon, int nx, int nu,
+                                int t_base, int is_last, int rank, int world, const void* P,
+                                const void* R, const void* M, const void* d, const void* Fx,
+                                const void* Fu, const void* rows, const void* PT,
+                                const double* alpha, const void* blocks_in, void* block_out,
+                                void* S, void* s, void* Gamma, void* gamma, void* dx, void* du,
+                                int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                                int chunk, void* stream) {
   if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
   if (phase < 0 || phase > 2) return fail(PTC_ERR_ARG, "phase must be 0, 1 or 2");
   if (world < 1 || rank < 0 || rank >= world) return fail(PTC_ERR_ARG, "bad rank / world");
@@ -361,6 +400,10 @@ int ptc_lqr_block_solve(int phase, int dtype, int batch, int horizon, int nx, in
     Carver c{(char*)workspace};
     carve_lqr_tree(c, a, nx, nu);
     if ((int64_t)c.off > workspace_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
+    if (rows) {  // the caller's stage rows are the staging buffer: no transpose
+      a.xst = (Rt*)rows;
+      a.prestaged = 1;
+    }
     it->second.block(&a, phase, blocks_in, block_out, rank, world, st);
     PTC_CUDA(cudaGetLastError());
     return PTC_OK;

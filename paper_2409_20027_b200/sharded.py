@@ -115,18 +115,21 @@ class CudaBlockOps:
     """
 
     def __init__(self, rank, world, t_base, P, R, M, d, Fx, Fu, PT, alpha, nx, nu,
-                 with_value=False, chunk0=0, chunk=0):
+                 with_value=False, chunk0=0, chunk=0, rows=None):
         torch = N.require_cuda()
         self.torch = torch
         self.lib = N.load_library()
         self.rank, self.world, self.t_base = int(rank), int(world), int(t_base)
         self.nx, self.nu = int(nx), int(nu)
-        self.T, self.B = int(P.shape[1]), int(P.shape[2])
-        self.dtype = P.dtype
-        self.code = N.PTC_F64 if P.dtype == torch.float64 else N.PTC_F32
+        ref = rows if rows is not None else P
+        self.T, self.B = (int(rows.shape[0]), 1) if rows is not None else (int(P.shape[1]),
+                                                                            int(P.shape[2]))
+        self.dtype = ref.dtype
+        self.code = N.PTC_F64 if ref.dtype == torch.float64 else N.PTC_F32
+        self.rows = rows.contiguous() if rows is not None else None
         self.inputs = (P, R, M, d, Fx, Fu, PT if rank == world - 1 else None, alpha)
         self.chunk0, self.chunk = int(chunk0), int(chunk)
-        dev = P.device
+        dev = ref.device
         nbytes = self.lib.ptc_lqr_block_workspace_bytes(self.code, self.B, self.T, self.nx,
                                                         self.nu, self.chunk0, self.chunk)
         N.check(0 if nbytes >= 0 else int(nbytes))
@@ -144,9 +147,26 @@ class CudaBlockOps:
         self.s = mk(self.nx, T + 1, B) if with_value else None
         self.flags = torch.zeros(B, dtype=torch.int32, device=dev)
 
+    @classmethod
+    def from_rows(cls, rank, world, t_base, rows, PT, alpha, nx, nu, **kw):
+        """One long problem (batch 1, nx >= 8) whose block expansion is given
+        as stage rows (T, SC): [P | R | M | d | Fx | Fu] per stage, the layout
+        the wide kernels read (ptc_lqr_block_solve_rows: no transpose)."""
+        return cls(rank, world, t_base, None, None, None, None, None, None, PT, alpha, nx, nu,
+                   rows=rows, **kw)
+
     def _run(self, phase, blocks_in, block_out):
         ptr = lambda t: None if t is None else t.data_ptr()
         P, R, M, d, Fx, Fu, PT, alpha = self.inputs
+        if self.rows is not None:
+            N.check(self.lib.ptc_lqr_block_solve_rows(
+                phase, self.code, self.T, self.nx, self.nu, self.t_base,
+                int(self.rank == self.world - 1), self.rank, self.world, ptr(self.rows), ptr(PT),
+                ptr(alpha), ptr(blocks_in), ptr(block_out), ptr(self.S), ptr(self.s),
+                ptr(self.Gamma), ptr(self.gamma), ptr(self.dx), ptr(self.du), ptr(self.flags),
+                ptr(self.workspace), self.workspace.numel(), self.chunk0, self.chunk,
+                N.stream_ptr()))
+            return
         N.check(self.lib.ptc_lqr_block_solve(
             phase, self.code, self.B, self.T, self.nx, self.nu, self.t_base,
             int(self.rank == self.world - 1), self.rank, self.world,

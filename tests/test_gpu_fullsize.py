@@ -164,3 +164,38 @@ def test_config4_full_size_barrier_solve_properties():
     pred = (At @ xs[:-1].unsqueeze(-1) + Bt @ us.unsqueeze(-1)).squeeze(-1)
     assert float((pred - xs[1:]).abs().max()) / max(1.0, float(xs.abs().max())) < 1e-9
     assert all(np.isfinite(r.cost) for r in rep.rounds)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_block_solve_from_stage_rows_equals_component_layout(world):
+    """ptc_lqr_block_solve_rows (the expansion as stage rows, no transpose)
+    gives bit-identical gains and deviations to the component-major entry."""
+    import torch
+    from paper_2409_20027_b200.sharded import CudaBlockOps, block_bounds, emulate_ranks
+    T, nx, nu = 4096, 12, 4
+    e = O.random_lqr_expansion(np.random.default_rng(12), T, nx, nu, alpha=0.2)
+    dev = torch.device("cuda")
+    flat = lambda a: torch.as_tensor(np.ascontiguousarray(a)).reshape(T, -1).to(dev)
+    fields = [flat(e.P), flat(e.R), flat(e.M), flat(e.d), flat(e.Fx), flat(e.Fu)]
+    PT = torch.as_tensor(e.PT).reshape(nx * nx, 1, 1).to(dev)
+    alpha = torch.full((1,), 0.2, dtype=torch.float64, device=dev)
+    outs = []
+    for use_rows in (False, True):
+        ops = []
+        for r in range(world):
+            t0, m = block_bounds(T, world, r)
+            if use_rows:
+                rows = torch.cat([f[t0:t0 + m] for f in fields], 1).contiguous()
+                ops.append(CudaBlockOps.from_rows(r, world, t0, rows, PT, alpha, nx, nu))
+            else:
+                loc = [f[t0:t0 + m].t().contiguous().unsqueeze(-1) for f in fields]
+                ops.append(CudaBlockOps(r, world, t0, *loc, PT, alpha, nx, nu))
+        emulate_ranks(ops)
+        torch.cuda.synchronize()
+        outs.append([torch.cat([getattr(o, n) for o in ops], 1)
+                     for n in ("Gamma", "gamma", "du")])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    ref = O.lqr_solve(e)
+    du = outs[1][2][..., 0].t().cpu().numpy()
+    assert rel_gap(du, ref[5]) < 1e-9
