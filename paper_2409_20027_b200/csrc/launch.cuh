@@ -245,6 +245,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
       // stage-major staging rows (no component-major round trip)
       LqrArgs<R> l2 = la;
       l2.prestaged = 1;
+      l2.gains_in_gst = 1;
       WideNewton<R, NX, NU>::costate(a, s, la.xst);
       lqr_registry().at(LqrKey(dtype_code<R>(), NX, NU)).solve(&l2, s);
       fused = true;

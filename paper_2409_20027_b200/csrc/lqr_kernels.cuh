@@ -54,6 +54,7 @@ struct LqrArgs {
   R* gst;
   int staged;
   int prestaged;           // xst already written by the producer (Newton co-state sweep)
+  int gains_in_gst;        // staged: leave the gains in gst (the Newton loop reads no Gamma)
   R* xin_buf;              // workspace for x_in        (nx, 1, B)
   // tree scratch, index l = 1..L, item rows n[l]
   R* vagg[kMaxLevels + 1];

@@ -1596,7 +1596,7 @@ void launch_lqr_wide(const LqrArgs<R>& a0, cudaStream_t s) {
     PTC_WL((kw_value_down0<R, NX, NU, false>), P0 * B, S::kDown0)(a);
   }
   PTC_WL((kw_prop_down0<R, NX, NU>), P0 * B, S::kPropDown0)(a);
-  if (a.staged) launch_gains_out<R, NX, NU>(a, s);
+  if (a.staged && !a.gains_in_gst) launch_gains_out<R, NX, NU>(a, s);
 }
 
 template <typename R, int NX, int NU>
@@ -1643,7 +1643,7 @@ void launch_lqr_block_wide(const LqrArgs<R>& a0, int phase, const void* blocks, 
       for (int l = pl.L - 1; l >= 1; --l) PTC_WL((kw_prop_down<R, NX, NU>), pl.n[l + 1] * B, S::kProp)(a, l);
     }
     PTC_WL((kw_prop_down0<R, NX, NU>), P0 * B, S::kPropDown0)(a);
-    if (a.staged) launch_gains_out<R, NX, NU>(a, s);
+    if (a.staged && !a.gains_in_gst) launch_gains_out<R, NX, NU>(a, s);
   }
 }
 

@@ -972,6 +972,7 @@ struct WideNewton {
     constexpr int kOpsCost = RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4);
     LqrArgs<R> l2 = la;
     l2.prestaged = (la.xst && B == 1) ? 1 : 0;
+    l2.gains_in_gst = l2.prestaged;
     R* o = static_cast<R*>(out);
     const R* gin = static_cast<const R*>(in);
     const double* din = static_cast<const double*>(in);
