@@ -227,7 +227,8 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   constexpr int NX = Dyn::NX, NU = Dyn::NU;
   const long long B = a.B, P0 = a.plan.units0();
   cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
-  k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
+  if constexpr (kWideNewton<Dyn>) WideNewton<R, NX, NU>::cost_partials(a, 0, s);
+  else k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
   bool fused = false;
   if constexpr (NX < 8) {
     if (a.plan.L == 0) {
@@ -271,7 +272,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
       WideNewton<R, NX, NU>::rollout_seq(a, la.dU, s);
       rolled = true;
     }
-    if (rolled) k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+    if (rolled) WideNewton<R, NX, NU>::cost_partials(a, 1, s);
   }
   if (rolled) {
   } else if (a.pr_iters > 0 && a.plan.L >= 1) {

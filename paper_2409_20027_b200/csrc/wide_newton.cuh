@@ -252,6 +252,7 @@ struct NSlab {
   static constexpr int ROLL = CC + NX * NU + 2 * NU;   // [A | c | Bm | u | du]
   static constexpr int kRollUp0 = 2 * CC + ROLL;
   static constexpr int kRollDown0 = 2 * NX + ROLL;
+  static constexpr int kCost = NX + NU + CK;
 };
 
 #define PTC_NW_PROLOGUE(count, gate, ...)        \
@@ -796,6 +797,103 @@ __global__ void __launch_bounds__(64) kwn_blk_carry(NewtonArgs<R> a, const R* g,
   }
 }
 
+// Cost partials of one chunk (k_cost_partials, models.cuh stage_cost /
+// aug_value) with the work spread over the warp: lane i < NX accumulates
+// row i of (x - g)^T Q (x - g) over the chunk's stages, lanes NX..NX+NU-1 the
+// control rows of u^T Rc u, lane k < W constraint row k's barrier log /
+// ADMM residual square and its first infeasible stage; one warp reduction
+// per chunk instead of a serial per-stage sum on one thread.
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(64) kwn_cost_partials(NewtonArgs<R> a, int which) {
+  const int u = warp_unit();
+  if (u >= a.plan.units0() * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (!running(a, b)) return;
+  if (which == 0 && !(a.phase[b] & PH_NEED_COST)) return;
+  using N = NSlab<R, NX, NU>;
+  R* slab = warp_slab<R>(N::kCost);
+  R* xu = slab;                 // [x | u] of the stage
+  R* ck = xu + NX + NU;         // [Q | goal | Rc]
+  const int P0 = a.plan.units0(), T = a.T, B = a.B;
+  const int q = which == 0 ? a.parity[b] : 1 - a.parity[b];
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
+  const ProblemParams& p = *a.pp;
+  const AugArgs<R> g = aug_of(a);
+  const int ln = lane_id();
+  w_cost_consts<R, NX, NU>(p, ck);
+  const R* Qs = ck;
+  const R* gs = ck + NX * NX;
+  const R* Rcs = gs + NX;
+  // this lane's constraint row
+  const int W = p.W;
+  const bool has_row = ln < W && g.kind != AUG_ZERO;
+  int rvar = 0, ridx = 0;
+  R rsgn = R(0), rbnd = R(0);
+  if (has_row) {
+    rvar = p.row_var[ln];
+    ridx = p.row_idx[ln];
+    rsgn = R(p.row_sign[ln]);
+    rbnd = R(p.row_bound[ln]);
+  }
+  const R rho = R(g.rho);
+  double aq = 0.0, ac = 0.0;
+  int first_bad = -1;
+  WGather<R, NX, NU> pf;
+  pf.init(gf_traj(a.X + q * a.xsz, T + 1, B, b), gf_traj(a.U + q * a.usz, T, B, b));
+  if (t0 < t1) pf.load(t0);
+  for (int t = t0; t < t1; ++t) {
+    pf.store(xu);
+    if (t + 1 < t1) pf.load(t + 1);
+    if (ln < NX) {
+      const R ei = xu[ln] - gs[ln];
+      R r = R(0);
+#pragma unroll
+      for (int k = 0; k < NX; ++k) r += ei * Qs[ln * NX + k] * (xu[k] - gs[k]);
+      aq += double(r);
+    } else if (ln < NX + NU) {
+      const int i = ln - NX;
+      R r = R(0);
+#pragma unroll
+      for (int k = 0; k < NU; ++k) r += xu[NX + i] * Rcs[i * NU + k] * xu[NX + k];
+      aq += double(r);
+    }
+    if (has_row) {
+      R var = R(0);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) var = (rvar == 0 && i == ridx) ? xu[i] : var;
+#pragma unroll
+      for (int i = 0; i < NU; ++i) var = (rvar == 1 && i == ridx) ? xu[NX + i] : var;
+      const R w = rsgn > 0 ? var - rbnd : rbnd - var;
+      if (g.kind == AUG_BARRIER) {
+        if (w >= R(0) && first_bad < 0) first_bad = t;
+        ac += double(log(-w));
+      } else {
+        const R res = w - ldf(g.z, ln, t, T, B, b) + ldf(g.v, ln, t, T, B, b) / rho;
+        ac += double(res * res);
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    aq += __shfl_xor_sync(0xffffffffu, aq, off);
+    ac += __shfl_xor_sync(0xffffffffu, ac, off);
+  }
+  // first infeasible (stage, row) in stage-major order
+  int bad = first_bad >= 0 ? first_bad * W + ln : 0x7fffffff;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, off));
+  if (ln == 0) {
+    double sc = 0.0;
+    if (g.kind == AUG_BARRIER) sc = -a.mu[b] * ac;
+    else if (g.kind == AUG_ADMM) sc = 0.5 * double(rho) * ac;
+    double* cp = a.cpart[which];
+    cp[((size_t)0 * P0 + j) * B + b] = 0.5 * aq;
+    cp[((size_t)1 * P0 + j) * B + b] = sc;
+    cp[((size_t)2 * P0 + j) * B + b] = bad == 0x7fffffff ? -1.0 : double(bad);
+  }
+}
+
 #undef PTC_NW_PROLOGUE
 
 // Reduction vectors exchanged between ranks (ptc_solver_block_phase): each
@@ -952,6 +1050,11 @@ struct WideNewton {
     scan<1>(a, dU, s);
   }
 
+  static void cost_partials(const NewtonArgs<R>& a, int which, cudaStream_t s) {
+    kwn_cost_partials<R, NX, NU><<<W::grid((long long)a.plan.units0() * a.B), 32 * kWarpsPerBlock,
+                                   W::smem(N::kCost), s>>>(a, which);
+  }
+
   static void rollout_seq(const NewtonArgs<R>& a, const R* dU, cudaStream_t s) {
     kwn_rollout_seq<R, NX, NU, 1><<<(unsigned)a.B, 32, kSeqSmem, s>>>(a, dU, 0);
   }
@@ -995,7 +1098,7 @@ struct WideNewton {
     switch (phase) {
       case 0:
         cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
-        k_cost_partials<R, NX, NU><<<(unsigned)((P0 * B + 127) / 128), 128, 0, s>>>(a, 0);
+        kwn_cost_partials<R, NX, NU><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kCost), s>>>(a, 0);
         kwn_costate_up0<R, NX, NU><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kCoUp0), s>>>(a);
         up_levels(Rev{}, 1);
         break;
@@ -1022,7 +1125,7 @@ struct WideNewton {
       case 5:
         down_levels(Fwd{}, 2);
         kwn_roll_down0<R, NX, NU, 1><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kRollDown0), s>>>(a, la.dU);
-        k_cost_partials<R, NX, NU><<<(unsigned)((P0 * B + 127) / 128), 128, 0, s>>>(a, 1);
+        kwn_cost_partials<R, NX, NU><<<W::grid(P0 * B), 32 * kWarpsPerBlock, W::smem(N::kCost), s>>>(a, 1);
         if (fold) {
           k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[0], 3, kOpsCost, (int)P0, (int)B);
           k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[1], 3, kOpsCost, (int)P0, (int)B);
