@@ -1402,24 +1402,18 @@ __global__ void __launch_bounds__(128) kw_prop_down0(LqrArgs<R> a) {
       }
     }
     w_st<NU>(a.dU, t, T, B, b, du);
-    // x <- (Fx + Fu Gamma) x + Fu gamma  (F = 0 at global stage 0)
+    // x <- Fx x + Fu du  (= (Fx + Fu Gamma) x + Fu gamma; at global stage 0
+    // the closed-loop map is 0 and x <- Fu gamma)
     const bool head = t + a.t_base == 0;
     for (int i = ln; i < NX; i += 32) {
-      R fgx = R(0);
+      R fu = R(0);
 #pragma unroll
-      for (int k = 0; k < NU; ++k) {
-        R gx = R(0);
-#pragma unroll
-        for (int q = 0; q < NX; ++q) gx = (q == 0) ? Gam[k * NX] * x[0] : fma(Gam[k * NX + q], x[q], gx);
-        fgx = (k == 0) ? Fu[i * NU] * gx : fma(Fu[i * NU + k], gx, fgx);
-      }
+      for (int k = 0; k < NU; ++k)
+        fu = (k == 0) ? Fu[i * NU] * (head ? gam[0] : du[0]) : fma(Fu[i * NU + k], head ? gam[k] : du[k], fu);
       R fx = R(0);
 #pragma unroll
       for (int q = 0; q < NX; ++q) fx = (q == 0) ? Fx[i * NX] * x[0] : fma(Fx[i * NX + q], x[q], fx);
-      R e = R(0);
-#pragma unroll
-      for (int k = 0; k < NU; ++k) e = (k == 0) ? Fu[i * NU] * gam[0] : fma(Fu[i * NU + k], gam[k], e);
-      y[i] = (head ? R(0) : fx + fgx) + e;
+      y[i] = head ? fu : fx + fu;
     }
     __syncwarp();
     w_copy<NX>(y, x);
