@@ -300,6 +300,7 @@ class TimeShardedNewton:
     def __init__(self, blocks, emulate: bool = False, group=None):
         self.blocks = list(blocks)
         self.comm = _Emulated() if emulate else _Distributed(group)
+        self._graph = None      # the captured iteration, reused by later solves
 
     def _round(self, p, outs):
         if p in _RED_SPECS:
@@ -339,10 +340,26 @@ class TimeShardedNewton:
         for bl, g in zip(self.blocks, ins):
             bl.phase(7, g)
 
-    def solve(self, states, controls, z=None, v=None, group_iters: int = 4):
+    def _capture(self):
+        """One iteration (every phase and collective) as a CUDA graph, or None
+        when the stream cannot be captured (the iteration then runs eagerly)."""
+        torch = self.blocks[0].torch
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.iteration()
+            return g
+        except Exception:  # e.g. a backend without graph-capturable collectives
+            torch.cuda.synchronize()
+            return None
+
+    def solve(self, states, controls, z=None, v=None, group_iters: int = 4,
+              graph: bool = True):
         """Load per-block trajectories (B, T_block + 1, nx) / (B, T_block, nu)
         and iterate until every problem is done.  Returns the number of
-        device iterations launched."""
+        device iterations launched.  With ``graph`` the iteration's ~60
+        launches and its collectives are captured once (after a first eager
+        iteration) and replayed as one CUDA graph."""
         for k, bl in enumerate(self.blocks):
             bl.solver.load(states[k], controls[k], None if z is None else z[k],
                            None if v is None else v[k])
@@ -350,12 +367,22 @@ class TimeShardedNewton:
         st = s0.settings
         rounds = max(1, st.max_outer if st.method == N.METHOD_ADMM else 64)
         cap = (st.max_iters + 2) * rounds + 16
-        launched, n = 0, 1
+        self.iteration()                 # eager: lazy kernel attributes, allocator
+        launched = 1
+        if s0.running() == 0:
+            return launched
+        # one process driving every block (no collectives): capture once,
+        # same buffers on every solve.  With a process group the iteration
+        # stays eager (collectives inside a captured graph are left out).
+        if graph and self._graph is None and isinstance(self.comm, _Emulated):
+            self._graph = self._capture()
+        g = self._graph if graph else None
+        step = g.replay if g is not None else self.iteration
+        n = group_iters
         while launched < cap:
             for _ in range(n):
-                self.iteration()
+                step()
             launched += n
             if s0.running() == 0:
                 break
-            n = group_iters
         return launched

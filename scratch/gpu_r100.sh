@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_sharded_newton.py -q -x > gpurun_out/r100_tests.log 2>&1; echo tests rc=$?
+tail -3 gpurun_out/r100_tests.log; grep -E "^E " gpurun_out/r100_tests.log | head
+timeout 900 python bench.py --steps 3 --warmup 3 --no-sweep --no-newton-sweep --no-mpc --no-fp32 --no-e2e --no-solves --no-cpu-baseline --no-long > gpurun_out/r100_bench.json 2> gpurun_out/r100_bench.err; echo bench rc=$?
+python -c "
+import json; d=json.loads(open('gpurun_out/r100_bench.json').read().strip().splitlines()[-1]); print(d['config4_solve']['device_ms'], d['config4_sharded_solve'])"
+timeout 300 python scratch/c4_shard_probe.py 20 2>&1 | tail -4
