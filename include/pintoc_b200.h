@@ -101,6 +101,14 @@ int ptc_lqr_solve(int dtype, int batch, int horizon, int nx, int nu,
                   void* S, void* s, void* Gamma, void* gamma, void* dx, void* du,
                   int* flags, void* workspace, int64_t workspace_bytes,
                   int chunk0, int chunk, void* stream);
+/* The same solve for one long problem (batch 1, nx >= 8, horizon >= 1024)
+ * whose expansion is given as stage rows rows[t * SC + c], row =
+ * [P | R | M | d | Fx | Fu] (the reference StageExpansion's per-stage
+ * arrays side by side): the layout the warp kernels read, no transpose. */
+int ptc_lqr_solve_rows(int dtype, int horizon, int nx, int nu, const void* rows, const void* PT,
+                       const double* alpha, void* S, void* s, void* Gamma, void* gamma, void* dx,
+                       void* du, int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                       int chunk, void* stream);
 /* value_pass + propagation_pass with HOST buffers (the numpy arrays of the
  * reference's StageExpansion, passes.py:291-361): same layouts and outputs
  * (Gamma, gamma, dx, du; flags may be NULL), host->device copies, solve and

@@ -91,6 +91,8 @@ _SIGS = {
                                  + [C.c_void_p] * 2 + [C.c_void_p] * 6
                                  + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int,
                                     C.c_void_p]),
+        "ptc_lqr_solve_rows": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 3 + [C.c_void_p] * 6
+                           + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]),
     "ptc_solver_iterate": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "ptc_solver_block_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_int, C.c_int, C.c_void_p]),

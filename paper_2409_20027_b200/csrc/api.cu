@@ -195,7 +195,7 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
                        const void* M, const void* d, const void* Fx, const void* Fu,
                        const void* PT, const double* alpha, void* S, void* s, void* Gamma,
                        void* gamma, void* dx, void* du, int* flags, void* ws, int64_t ws_bytes,
-                       int chunk0, int chunk, cudaStream_t st) {
+                       int chunk0, int chunk, cudaStream_t st, const void* rows = nullptr) {
   auto it = lqr_registry().find(LqrKey(dtype_code<R>(), nx, nu));
   if (it == lqr_registry().end())
     return fail(PTC_ERR_UNSUPPORTED, "LQR kernels not instantiated for nx=" + std::to_string(nx) +
@@ -226,6 +226,11 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
   if ((int64_t)c.off > ws_bytes) return fail(PTC_ERR_WORKSPACE, "LQR workspace too small");
   if ((S == nullptr) != (s == nullptr)) return fail(PTC_ERR_ARG, "S and s must both be given or both NULL");
   a.red = nullptr;  // trust-region partial sums are a Newton-loop product only
+  if (rows) {  // stage rows: the caller's buffer is the staging buffer
+    if (!a.xst) return fail(PTC_ERR_ARG, "stage-row inputs need batch 1, nx >= 8, horizon >= 1024");
+    a.xst = (R*)rows;
+    a.prestaged = 1;
+  }
   if (a.plan.L >= 1 && !getenv("PTC_NO_GRAPH")) {
     // a tree plan is 4L+4 short launches: replay them as one CUDA graph,
     // cached per argument set (same buffers -> same graph)
@@ -571,6 +576,24 @@ int ptc_lqr_solve_host(int dtype, int batch, int horizon, int nx, int nu, const 
   if (dtype == PTC_F32)
     return lqr_solve_host_t<float>(batch, horizon, nx, nu, hin, alpha, hout, flags, workspace,
                                    workspace_bytes, chunk0, chunk, st);
+  return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
+}
+
+int ptc_lqr_solve_rows(int dtype, int horizon, int nx, int nu, const void* rows, const void* PT,
+                       const double* alpha, void* S, void* s, void* Gamma, void* gamma, void* dx,
+                       void* du, int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                       int chunk, void* stream) {
+  if (horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  if (!rows) return fail(PTC_ERR_ARG, "rows is required");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == PTC_F64)
+    return lqr_solve_t<double>(1, horizon, nx, nu, nullptr, nullptr, nullptr, nullptr, nullptr,
+                               nullptr, PT, alpha, S, s, Gamma, gamma, dx, du, flags, workspace,
+                               workspace_bytes, chunk0, chunk, st, rows);
+  if (dtype == PTC_F32)
+    return lqr_solve_t<float>(1, horizon, nx, nu, nullptr, nullptr, nullptr, nullptr, nullptr,
+                              nullptr, PT, alpha, S, s, Gamma, gamma, dx, du, flags, workspace,
+                              workspace_bytes, chunk0, chunk, st, rows);
   return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
 }
 

@@ -133,6 +133,17 @@ class LqrSolver:
                                       C.byref(k), C.byref(lv)))
         return k0.value, k.value, lv.value
 
+    def solve_rows(self, rows, PT, alpha, stream=None):
+        """One long problem (batch 1, nx >= 8, horizon >= 1024) from stage rows
+        (T, SC): [P | R | M | d | Fx | Fu] per stage (ptc_lqr_solve_rows)."""
+        self.flags.zero_()
+        ptr = lambda t: None if t is None else t.data_ptr()
+        N.check(self.lib.ptc_lqr_solve_rows(
+            self.code, self.T, self.nx, self.nu, ptr(rows), ptr(PT), ptr(alpha), ptr(self.S),
+            ptr(self.s), ptr(self.Gamma), ptr(self.gamma), ptr(self.dx), ptr(self.du),
+            ptr(self.flags), ptr(self.workspace), self.workspace.numel(), self.chunk0,
+            self.chunk, N.stream_ptr(stream)))
+
     def solve(self, P, R, M, d, Fx, Fu, PT, alpha, stream=None):
         self.flags.zero_()
         ptr = lambda t: None if t is None else t.data_ptr()
@@ -200,12 +211,19 @@ def lqr_solve(exp: StageExpansion, executor: str = "auto", dtype=None):
     c0, c1 = plan_chunks(executor, n)
     solver = LqrSolver(1, n, nx, nu, dtype=dtype, chunk0=c0, chunk=c1, with_value=True)
     dev = solver.device
-    args = [_soa(torch, exp.P, dtype, dev, nx * nx), _soa(torch, exp.R, dtype, dev, nu * nu),
-            _soa(torch, exp.M, dtype, dev, nx * nu), _soa(torch, exp.d, dtype, dev, nu),
-            _soa(torch, exp.Fx, dtype, dev, nx * nx), _soa(torch, exp.Fu, dtype, dev, nx * nu),
-            _soa(torch, exp.P_terminal[None], dtype, dev, nx * nx)]
     alpha = torch.full((1,), float(exp.alpha), dtype=torch.float64, device=dev)
-    solver.solve(*args, alpha)
+    PT = _soa(torch, exp.P_terminal[None], dtype, dev, nx * nx)
+    if nx >= 8 and n >= 1024:
+        # the reference's per-stage arrays side by side are the stage rows
+        # the wide kernels read: no transpose on either side
+        rows = np.concatenate([np.asarray(a, float).reshape(n, -1)
+                               for a in (exp.P, exp.R, exp.M, exp.d, exp.Fx, exp.Fu)], axis=1)
+        solver.solve_rows(torch.as_tensor(rows, dtype=dtype).to(dev), PT, alpha)
+    else:
+        args = [_soa(torch, exp.P, dtype, dev, nx * nx), _soa(torch, exp.R, dtype, dev, nu * nu),
+                _soa(torch, exp.M, dtype, dev, nx * nu), _soa(torch, exp.d, dtype, dev, nu),
+                _soa(torch, exp.Fx, dtype, dev, nx * nx), _soa(torch, exp.Fu, dtype, dev, nx * nu)]
+        solver.solve(*args, PT, alpha)
     fl = int(solver.flags[0])
     if fl & (FLAG_DEF_R | FLAG_DEF_Q):
         raise DefinitenessError(-1, "R + alpha*I" if fl & FLAG_DEF_R else "Q")

@@ -199,3 +199,27 @@ def test_block_solve_from_stage_rows_equals_component_layout(world):
     ref = O.lqr_solve(e)
     du = outs[1][2][..., 0].t().cpu().numpy()
     assert rel_gap(du, ref[5]) < 1e-9
+
+
+@pytest.mark.parametrize("nx,nu,T", [(12, 4, 1100), (8, 4, 2048)])
+def test_pass_level_lqr_from_stage_rows(nx, nu, T):
+    """value_pass / propagation_pass on a StageExpansion with nx >= 8 and
+    T >= 1024 hand the reference's per-stage arrays to the device as stage
+    rows (ptc_lqr_solve_rows): bit-identical to the component-major entry,
+    within 1e-9 of the oracle."""
+    import torch
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200 import passes
+    e = O.random_lqr_expansion(np.random.default_rng([nx, T]), T, nx, nu, alpha=0.3)
+    exp = P.StageExpansion.build(e.P, e.R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.3)
+    S, s, law, dxs, dus = passes.lqr_solve(exp)
+    ref = O.lqr_solve(e)
+    assert rel_gap(dus, ref[5]) < 1e-9 and rel_gap(dxs, ref[4]) < 1e-9
+    assert rel_gap(law.Gamma, ref[2]) < 1e-9 and rel_gap(S, ref[0]) < 1e-9
+    sol = passes.LqrSolver(1, T, nx, nu)
+    soa = lambda a, c: passes._soa(torch, a, torch.float64, sol.device, c)
+    sol.solve(soa(e.P, nx * nx), soa(e.R, nu * nu), soa(e.M, nx * nu), soa(e.d, nu),
+              soa(e.Fx, nx * nx), soa(e.Fu, nx * nu), soa(e.PT[None], nx * nx),
+              torch.full((1,), 0.3, dtype=torch.float64, device=sol.device))
+    host = lambda t, shape: t[..., 0].t().reshape(shape).cpu().numpy()
+    assert np.array_equal(host(sol.du, (T, nu)), dus)
