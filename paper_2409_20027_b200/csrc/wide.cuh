@@ -63,6 +63,82 @@ PTC_D void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// acc (fragments of an M x N product, the c/d layout above) += sign op(A) op(B)
+template <int M, int K, int N, bool TA, bool TB, bool NEG, int MB, int NB>
+PTC_D void dmma_accumulate(double (&acc)[MB][NB][2], const double* A, const double* B) {
+  constexpr int KB = (K + 3) / 4;
+  const int ln = lane_id();
+  const int fr = ln >> 2, fc = ln & 3;
+#pragma unroll
+  for (int kb = 0; kb < KB; ++kb) {
+    const int k = kb * 4 + fc;
+    double af[MB], bf[NB];
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+      const int i = mb * 8 + fr;
+      af[mb] = (i < M && k < K) ? (TA ? A[k * M + i] : A[i * K + k]) : 0.0;
+      if (NEG) af[mb] = -af[mb];
+    }
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int j = nb * 8 + fr;
+      bf[nb] = (j < N && k < K) ? (TB ? B[j * K + k] : B[k * N + j]) : 0.0;
+    }
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) dmma_8x8x4(acc[mb][nb], af[mb], bf[nb]);
+  }
+}
+
+// C = sym(D + op(A1) op(B1) + op(A2) op(B2)) for N x N (N <= 16): both
+// products accumulate in the same fragments and the symmetrisation is done
+// there with shuffles (the transposed entry of (i, j) sits in tile (nb, mb)
+// of lane ((j % 8) << 2) | ((i % 8) >> 1)), so the result is stored once,
+// already symmetric -- no separate w_sym pass.  D may be C.
+template <int N, int K1, int K2, bool TA1, bool TB1, bool TA2, bool TB2>
+PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
+                          const double* B2, const double* D, double* C) {
+  constexpr int NB = (N + 7) / 8;
+  const int ln = lane_id();
+  const int fr = ln >> 2, fc = ln & 3;
+  double acc[NB][NB][2];
+#pragma unroll
+  for (int mb = 0; mb < NB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
+        acc[mb][nb][e] = (i < N && j < N) ? D[i * N + j] : 0.0;
+      }
+  dmma_accumulate<N, K1, N, TA1, TB1, false>(acc, A1, B1);
+  dmma_accumulate<N, K2, N, TA2, TB2, false>(acc, A2, B2);
+  double out[NB][NB][2];
+#pragma unroll
+  for (int mb = 0; mb < NB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int src = ((2 * fc + e) << 2) | (fr >> 1);
+        const double v0 = __shfl_sync(0xffffffffu, acc[nb][mb][0], src);
+        const double v1 = __shfl_sync(0xffffffffu, acc[nb][mb][1], src);
+        out[mb][nb][e] = 0.5 * (acc[mb][nb][e] + ((fr & 1) ? v1 : v0));
+      }
+  __syncwarp();  // every lane has read its operands (and D) before C is written
+#pragma unroll
+  for (int mb = 0; mb < NB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
+        if (i < N && j < N) C[i * N + j] = out[mb][nb][e];
+      }
+  __syncwarp();
+}
+
 template <int M, int K, int N, bool TA, bool TB, int MODE>
 PTC_D void w_mm_dmma(const double* A, const double* B, double* C, const double* D = nullptr) {
   constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8, KB = (K + 3) / 4;
@@ -1002,8 +1078,17 @@ PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
   }
   __syncwarp();
   // S' = sym(P + Fx^T SF + Qux^T Gam), eta' = Fx^T eta - Qux^T gam
-  w_mm<NX, NX, NX, true, false, 2>(st + S::sFx, SF, o, st + S::sP);
-  w_mm<NX, NU, NX, true, false, 1>(Qux, Gam, o);
+  const bool fused_sym = sizeof(R) == 8 && NX >= 8 && NX <= 16;
+  if constexpr (sizeof(R) == 8 && NX >= 8 && NX <= 16) {
+    // S' = sym(P + Fx^T SF + Qux^T Gam), symmetrised in the product fragments
+    w_mm2_sym_dmma<NX, NX, NU, true, false, true, false>(
+        reinterpret_cast<const double*>(st + S::sFx), reinterpret_cast<const double*>(SF),
+        reinterpret_cast<const double*>(Qux), reinterpret_cast<const double*>(Gam),
+        reinterpret_cast<const double*>(st + S::sP), reinterpret_cast<double*>(o));
+  } else {
+    w_mm<NX, NX, NX, true, false, 2>(st + S::sFx, SF, o, st + S::sP);
+    w_mm<NX, NU, NX, true, false, 1>(Qux, Gam, o);
+  }
   for (int i = ln; i < NX; i += 32) {
     R s = R(0);
 #pragma unroll
@@ -1014,7 +1099,7 @@ PTC_D int w_riccati(const R* st, const R* c, R* o, R* Gam, R* gam, R* scr) {
     o[NX * NX + i] = s - g;
   }
   __syncwarp();
-  w_sym<NX>(o);
+  if (!fused_sym) w_sym<NX>(o);
   return fl;
 }
 
