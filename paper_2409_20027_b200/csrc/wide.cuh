@@ -963,17 +963,32 @@ PTC_D int w_vcombine_stage(const R* st, const R* r, R* o, R* scr, int* piv) {
     x[i] = bl[i] + fq;
   }
   __syncwarp();
-  w_mm<NX, NX, NX, true, false, 1>(Al, Z1, o + S::eY);
+  constexpr bool kFragSym = sizeof(R) == 8 && NX >= 8 && NX <= 16;
+  if constexpr (kFragSym) {   // Y = sym(Y_l + A_l^T Z1), symmetrised in the fragments
+    w_mm2_sym_dmma<NX, NX, 0, true, false, false, false>(
+        reinterpret_cast<const double*>(Al), reinterpret_cast<const double*>(Z1), nullptr,
+        nullptr, reinterpret_cast<const double*>(o + S::eY), reinterpret_cast<double*>(o + S::eY));
+  } else {
+    w_mm<NX, NX, NX, true, false, 1>(Al, Z1, o + S::eY);
+  }
   w_mv<NX, NX, true, 1>(Al, z, o + S::eEta);
   // A = A_r (A_l - Fu W)   (A_l no longer needed as such)
   w_mm<NX, NU, NX, false, false, -1>(Fu, W, Al);
   w_mm<NX, NX, NX, false, false, 0>(r + S::eA, Al, o + S::eA);
   // C = sym(AF Y2 + C_r) ;  b = A_r x + b_r
-  w_mm<NX, NU, NX, false, false, 2>(AF, Y2, o + S::eC, r + S::eC);
+  if constexpr (kFragSym) {   // C = sym(C_r + AF Y2)
+    w_mm2_sym_dmma<NX, NU, 0, false, false, false, false>(
+        reinterpret_cast<const double*>(AF), reinterpret_cast<const double*>(Y2), nullptr,
+        nullptr, reinterpret_cast<const double*>(r + S::eC), reinterpret_cast<double*>(o + S::eC));
+  } else {
+    w_mm<NX, NU, NX, false, false, 2>(AF, Y2, o + S::eC, r + S::eC);
+  }
   w_copy<NX>(r + S::eB, o + S::eB);
   w_mv<NX, NX, false, 1>(r + S::eA, x, o + S::eB);
-  w_sym<NX>(o + S::eY);
-  w_sym<NX>(o + S::eC);
+  if constexpr (!kFragSym) {
+    w_sym<NX>(o + S::eY);
+    w_sym<NX>(o + S::eC);
+  }
   return fl;
 }
 
