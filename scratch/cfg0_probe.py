@@ -1,0 +1,13 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import bench
+import paper_2409_20027_b200 as P
+pend = bench.models_pkg(P)["pendulum"]
+T0 = 100
+pend = P.ControlProblem(P.PendulumDynamics(T0, P.PendulumParams(damping=0.1, dt=0.05)), pend.cost, pend.constraints)
+rng = np.random.default_rng(20027)
+u0 = np.clip(0.5 * rng.standard_normal((T0, 1)), -4.5, 4.5)
+init0 = P.rollout(pend.dynamics, np.array([np.pi, 0.0]), u0)
+o0 = P.BarrierOptions(mu0=0.1, zeta=0.2, mu_tol=1e-6, newton=P.NewtonOptions(max_iters=int(sys.argv[1]) if len(sys.argv) > 1 else 100))
+P.barrier_solve(pend, init0, o0)
