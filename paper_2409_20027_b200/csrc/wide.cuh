@@ -383,6 +383,38 @@ PTC_D void w_lu_solve(const R* LU, const int* piv, R* B) {
   __syncwarp();
 }
 
+// Solve G^T X = B (B: N x M row-major, in place) with the factors of
+// w_lu(G): G^T = U^T L^T P (as lu_solve_t); lanes own columns.
+template <int N, int M, typename R>
+PTC_D void w_lu_solve_t(const R* LU, const int* piv, R* B) {
+  for (int c = lane_id(); c < M; c += 32) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {  // U^T y = b (lower, reciprocal diagonal)
+      R v = B[i * M + c];
+#pragma unroll
+      for (int k = 0; k < i; ++k) v = fma(-LU[k * N + i], B[k * M + c], v);
+      B[i * M + c] = v * LU[i * N + i];
+    }
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) {  // L^T z = y (upper, unit diagonal)
+      R v = B[i * M + c];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) v = fma(-LU[k * N + i], B[k * M + c], v);
+      B[i * M + c] = v;
+    }
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {  // undo the row interchanges
+      const int p = piv[k];
+      if (p != k) {
+        const R t = B[k * M + c];
+        B[k * M + c] = B[p * M + c];
+        B[p * M + c] = t;
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // Small general matrices (nu <= 6): every lane factors its own register copy
 // with the arithmetic of w_lu (same pivot rule, reciprocal pivots), fully
 // unrolled so rows are swapped by static selects instead of local memory.
@@ -753,7 +785,7 @@ PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* scr, int* piv) {
   R* Z = X + NX * (2 * NX + 1);
   R* T1 = Z + NX * (NX + 1);
   constexpr int WX = 2 * NX + 1, WZ = NX + 1;
-  // G = I + C_l Y_r ; G^T is what the Z solve needs, so factor G^T directly
+  // G = I + C_l Y_r, factored once; Z uses G^T through the same factors
   // Z = G^-T [Y_r A_l | eta_r - Y_r b_l]   X = G^-1 [A_l | C_l | b_l + C_l eta_r]
   w_mm<NX, NX, NX, false, false, 0>(l + S::eC, r + S::eY, G);
   // X rhs, Z rhs (independent of the factorisation)
@@ -785,16 +817,10 @@ PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* scr, int* piv) {
   }
   for (int i = lane_id(); i < NX; i += 32) G[i * NX + i] += R(1);
   __syncwarp();
-  // transposed copy for the G^T solve
-  for (int q = lane_id(); q < NX * NX; q += 32) {
-    const int i = q / NX, j = q - (q / NX) * NX;
-    T1[j * NX + i] = G[q];
-  }
-  __syncwarp();
-  bool ok = w_lu<NX>(G, piv);
+  // one factorisation serves both orientations (G^T = U^T L^T P)
+  const bool ok = w_lu<NX>(G, piv);
   w_lu_solve<NX, WX>(G, piv, X);
-  ok = w_lu<NX>(T1, piv) && ok;
-  w_lu_solve<NX, WZ>(T1, piv, Z);
+  w_lu_solve_t<NX, WZ>(G, piv, Z);
   // Y = sym(A_l^T Z1 + Y_l), eta = A_l^T z + eta_l
   for (int q = lane_id(); q < NX * NX; q += 32) {
     const int i = q / NX, j = q - (q / NX) * NX;
