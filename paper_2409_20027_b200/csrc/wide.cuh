@@ -63,9 +63,12 @@ PTC_D void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// acc (fragments of an M x N product, the c/d layout above) += sign op(A) op(B)
-template <int M, int K, int N, bool TA, bool TB, bool NEG, int MB, int NB>
+// acc (fragments of an M x N product, the c/d layout above) += sign op(A) op(B);
+// LDA / LDB: row strides of the stored A / B (0: dense)
+template <int M, int K, int N, bool TA, bool TB, bool NEG, int MB, int NB, int LDA = 0,
+          int LDB = 0>
 PTC_D void dmma_accumulate(double (&acc)[MB][NB][2], const double* A, const double* B) {
+  constexpr int la = LDA ? LDA : (TA ? M : K), lb = LDB ? LDB : (TB ? K : N);
   constexpr int KB = (K + 3) / 4;
   const int ln = lane_id();
   const int fr = ln >> 2, fc = ln & 3;
@@ -76,13 +79,13 @@ PTC_D void dmma_accumulate(double (&acc)[MB][NB][2], const double* A, const doub
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb) {
       const int i = mb * 8 + fr;
-      af[mb] = (i < M && k < K) ? (TA ? A[k * M + i] : A[i * K + k]) : 0.0;
+      af[mb] = (i < M && k < K) ? (TA ? A[k * la + i] : A[i * la + k]) : 0.0;
       if (NEG) af[mb] = -af[mb];
     }
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
       const int j = nb * 8 + fr;
-      bf[nb] = (j < N && k < K) ? (TB ? B[j * K + k] : B[k * N + j]) : 0.0;
+      bf[nb] = (j < N && k < K) ? (TB ? B[j * lb + k] : B[k * lb + j]) : 0.0;
     }
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb)
@@ -96,7 +99,7 @@ PTC_D void dmma_accumulate(double (&acc)[MB][NB][2], const double* A, const doub
 // there with shuffles (the transposed entry of (i, j) sits in tile (nb, mb)
 // of lane ((j % 8) << 2) | ((i % 8) >> 1)), so the result is stored once,
 // already symmetric -- no separate w_sym pass.  D may be C.
-template <int N, int K1, int K2, bool TA1, bool TB1, bool TA2, bool TB2>
+template <int N, int K1, int K2, bool TA1, bool TB1, bool TA2, bool TB2, int LDB1 = 0>
 PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
                           const double* B2, const double* D, double* C) {
   constexpr int NB = (N + 7) / 8;
@@ -112,7 +115,7 @@ PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
         const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
         acc[mb][nb][e] = (i < N && j < N) ? D[i * N + j] : 0.0;
       }
-  dmma_accumulate<N, K1, N, TA1, TB1, false>(acc, A1, B1);
+  dmma_accumulate<N, K1, N, TA1, TB1, false, NB, NB, 0, LDB1>(acc, A1, B1);
   dmma_accumulate<N, K2, N, TA2, TB2, false>(acc, A2, B2);
   double out[NB][NB][2];
 #pragma unroll
@@ -822,12 +825,19 @@ PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* scr, int* piv) {
   w_lu_solve<NX, WX>(G, piv, X);
   w_lu_solve_t<NX, WZ>(G, piv, Z);
   // Y = sym(A_l^T Z1 + Y_l), eta = A_l^T z + eta_l
-  for (int q = lane_id(); q < NX * NX; q += 32) {
-    const int i = q / NX, j = q - (q / NX) * NX;
-    R s = R(0);
+  constexpr bool kFragSym = sizeof(R) == 8 && NX >= 8 && NX <= 16;
+  if constexpr (kFragSym) {
+    w_mm2_sym_dmma<NX, NX, 0, true, false, false, false, WZ>(
+        reinterpret_cast<const double*>(l + S::eA), reinterpret_cast<const double*>(Z), nullptr,
+        nullptr, reinterpret_cast<const double*>(l + S::eY), reinterpret_cast<double*>(o + S::eY));
+  } else {
+    for (int q = lane_id(); q < NX * NX; q += 32) {
+      const int i = q / NX, j = q - (q / NX) * NX;
+      R s = R(0);
 #pragma unroll
-    for (int k = 0; k < NX; ++k) s = (k == 0) ? l[S::eA + i] * Z[j] : fma(l[S::eA + k * NX + i], Z[k * WZ + j], s);
-    o[S::eY + q] = s + l[S::eY + q];
+      for (int k = 0; k < NX; ++k) s = (k == 0) ? l[S::eA + i] * Z[j] : fma(l[S::eA + k * NX + i], Z[k * WZ + j], s);
+      o[S::eY + q] = s + l[S::eY + q];
+    }
   }
   for (int i = lane_id(); i < NX; i += 32) {
     R s = R(0);
@@ -856,16 +866,22 @@ PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* scr, int* piv) {
   }
   __syncwarp();
   // C = sym(T1 A_r^T + C_r)
-  for (int q = lane_id(); q < NX * NX; q += 32) {
-    const int i = q / NX, j = q - (q / NX) * NX;
-    R s = R(0);
+  if constexpr (kFragSym) {
+    w_mm2_sym_dmma<NX, NX, 0, false, true, false, false>(
+        reinterpret_cast<const double*>(T1), reinterpret_cast<const double*>(r + S::eA), nullptr,
+        nullptr, reinterpret_cast<const double*>(r + S::eC), reinterpret_cast<double*>(o + S::eC));
+  } else {
+    for (int q = lane_id(); q < NX * NX; q += 32) {
+      const int i = q / NX, j = q - (q / NX) * NX;
+      R s = R(0);
 #pragma unroll
-    for (int k = 0; k < NX; ++k) s = (k == 0) ? T1[i * NX] * r[S::eA + j * NX] : fma(T1[i * NX + k], r[S::eA + j * NX + k], s);
-    o[S::eC + q] = s + r[S::eC + q];
+      for (int k = 0; k < NX; ++k) s = (k == 0) ? T1[i * NX] * r[S::eA + j * NX] : fma(T1[i * NX + k], r[S::eA + j * NX + k], s);
+      o[S::eC + q] = s + r[S::eC + q];
+    }
+    __syncwarp();
+    w_sym<NX>(o + S::eY);
+    w_sym<NX>(o + S::eC);
   }
-  __syncwarp();
-  w_sym<NX>(o + S::eY);
-  w_sym<NX>(o + S::eC);
   return ok;
 }
 
@@ -1046,12 +1062,19 @@ PTC_D bool w_vstep(const R* e, const R* c, R* o, R* scr, int* piv) {
   __syncwarp();
   const bool ok = w_lu<NX>(G, piv);
   w_lu_solve<NX, WZ>(G, piv, Z);
-  for (int q = lane_id(); q < NX * NX; q += 32) {
-    const int i = q / NX, j = q - (q / NX) * NX;
-    R s = R(0);
+  constexpr bool kFragSym = sizeof(R) == 8 && NX >= 8 && NX <= 16;
+  if constexpr (kFragSym) {   // Y' = sym(A_e^T Z1 + Y_e) in the DMMA fragments
+    w_mm2_sym_dmma<NX, NX, 0, true, false, false, false, WZ>(
+        reinterpret_cast<const double*>(e + S::eA), reinterpret_cast<const double*>(Z), nullptr,
+        nullptr, reinterpret_cast<const double*>(e + S::eY), reinterpret_cast<double*>(o));
+  } else {
+    for (int q = lane_id(); q < NX * NX; q += 32) {
+      const int i = q / NX, j = q - (q / NX) * NX;
+      R s = R(0);
 #pragma unroll
-    for (int k = 0; k < NX; ++k) s = (k == 0) ? e[S::eA + i] * Z[j] : fma(e[S::eA + k * NX + i], Z[k * WZ + j], s);
-    o[q] = s + e[S::eY + q];
+      for (int k = 0; k < NX; ++k) s = (k == 0) ? e[S::eA + i] * Z[j] : fma(e[S::eA + k * NX + i], Z[k * WZ + j], s);
+      o[q] = s + e[S::eY + q];
+    }
   }
   for (int i = lane_id(); i < NX; i += 32) {
     R s = R(0);
@@ -1060,7 +1083,7 @@ PTC_D bool w_vstep(const R* e, const R* c, R* o, R* scr, int* piv) {
     o[NX * NX + i] = s + e[S::eEta + i];
   }
   __syncwarp();
-  w_sym<NX>(o);
+  if constexpr (!kFragSym) w_sym<NX>(o);
   return ok;
 }
 
