@@ -142,6 +142,32 @@ PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
   __syncwarp();
 }
 
+// C (M x N, dense) = op(A) B with B read at row stride LDB (a column block
+// of a wider matrix), on DMMA
+template <int M, int K, int N, bool TA, int LDB>
+PTC_D void w_mm_ldb_dmma(const double* A, const double* B, double* C) {
+  constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8;
+  const int ln = lane_id();
+  const int fr = ln >> 2, fc = ln & 3;
+  double acc[MB][NB][2];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+  dmma_accumulate<M, K, N, TA, false, false, MB, NB, 0, LDB>(acc, A, B);
+  __syncwarp();
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
+        if (i < M && j < N) C[i * N + j] = acc[mb][nb][e];
+      }
+  __syncwarp();
+}
+
 template <int M, int K, int N, bool TA, bool TB, int MODE>
 PTC_D void w_mm_dmma(const double* A, const double* B, double* C, const double* D = nullptr) {
   constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8, KB = (K + 3) / 4;
@@ -846,17 +872,26 @@ PTC_D bool w_vcombine(const R* l, const R* r, R* o, R* scr, int* piv) {
     o[S::eEta + i] = s + l[S::eEta + i];
   }
   // A = A_r X1, T1 = A_r X2, b = A_r x + b_r
-  for (int q = lane_id(); q < NX * NX; q += 32) {
-    const int i = q / NX, j = q - (q / NX) * NX;
-    R s1 = R(0), s2 = R(0);
+  if constexpr (kFragSym) {
+    w_mm_ldb_dmma<NX, NX, NX, false, WX>(reinterpret_cast<const double*>(r + S::eA),
+                                         reinterpret_cast<const double*>(X),
+                                         reinterpret_cast<double*>(o + S::eA));
+    w_mm_ldb_dmma<NX, NX, NX, false, WX>(reinterpret_cast<const double*>(r + S::eA),
+                                         reinterpret_cast<const double*>(X + NX),
+                                         reinterpret_cast<double*>(T1));
+  } else {
+    for (int q = lane_id(); q < NX * NX; q += 32) {
+      const int i = q / NX, j = q - (q / NX) * NX;
+      R s1 = R(0), s2 = R(0);
 #pragma unroll
-    for (int k = 0; k < NX; ++k) {
-      const R ar = r[S::eA + i * NX + k];
-      s1 = (k == 0) ? ar * X[j] : fma(ar, X[k * WX + j], s1);
-      s2 = (k == 0) ? ar * X[NX + j] : fma(ar, X[k * WX + NX + j], s2);
+      for (int k = 0; k < NX; ++k) {
+        const R ar = r[S::eA + i * NX + k];
+        s1 = (k == 0) ? ar * X[j] : fma(ar, X[k * WX + j], s1);
+        s2 = (k == 0) ? ar * X[NX + j] : fma(ar, X[k * WX + NX + j], s2);
+      }
+      o[S::eA + q] = s1;
+      T1[q] = s2;
     }
-    o[S::eA + q] = s1;
-    T1[q] = s2;
   }
   for (int i = lane_id(); i < NX; i += 32) {
     R s = R(0);
