@@ -63,6 +63,77 @@ PTC_D void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Accumulator fragments to / from a dense M x N row-major matrix.  A 64-bit
+// shared access serves a half-warp (fragment rows fr = 0..3 or 4..7) per
+// wavefront; rows sit 2N words apart, and for N = 12 the c/d layout (lane
+// column group fc holds columns 2fc, 2fc + 1) puts rows fr and fr + 1 on the
+// same banks (2-way conflict, in the merged 128-bit form too).  The fix is
+// to permute the product's columns inside each 8-column tile: MMA column n
+// holds matrix column pi(n) = n ^ 1 for n >= 4 (the b fragment is gathered
+// from column pi(fr) instead of fr; pi is an involution).  A lane's register
+// e then holds column 2fc + (e ^ (fc >> 1)): for every store / load
+// instruction the lane-to-address map changes but the register does not, and
+// the half-warp covers all 32 banks.  The b-operand gathers keep their bank
+// pattern (pi only permutes the columns within each half-warp).  Picked at
+// compile time per N by counting bank multiplicity over a half-warp.
+__host__ __device__ constexpr int frag_pi(int n, bool perm) { return perm ? (n ^ ((n >> 2) & 1)) : n; }
+constexpr int frag_bank_ways(int N, bool perm) {
+  int worst = 1;
+  for (int half = 0; half < 2; ++half)
+    for (int e = 0; e < 2; ++e) {
+      int cnt[32] = {};
+      for (int fr = 4 * half; fr < 4 * half + 4; ++fr)
+        for (int fc = 0; fc < 4; ++fc) {
+          const int j = frag_pi(2 * fc + e, perm);
+          if (fr >= N || j >= N) continue;
+          cnt[(2 * (fr * N + j)) & 31]++;
+        }
+      for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
+    }
+  return worst;
+}
+template <int N>
+struct FragOrder {
+  static constexpr bool perm = frag_bank_ways(N, true) < frag_bank_ways(N, false);
+};
+
+// acc = D (zero outside M x N)
+template <int M, int N, int MB, int NB>
+PTC_D void frag_ld(double (&acc)[MB][NB][2], const double* D) {
+  const int ln = lane_id();
+  const int fr = ln >> 2, fc = ln & 3;
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = mb * 8 + fr, j = nb * 8 + frag_pi(2 * fc + e, FragOrder<N>::perm);
+        acc[mb][nb][e] = (i < M && j < N) ? D[i * N + j] : 0.0;
+      }
+}
+
+// C = acc (MODE 0), C += acc (MODE 1), C -= acc (MODE -1), inside M x N
+template <int M, int N, int MODE, int MB, int NB>
+PTC_D void frag_st(const double (&acc)[MB][NB][2], double* C) {
+  const int ln = lane_id();
+  const int fr = ln >> 2, fc = ln & 3;
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = mb * 8 + fr, j = nb * 8 + frag_pi(2 * fc + e, FragOrder<N>::perm);
+        if (i < M && j < N) {
+          double& c = C[i * N + j];
+          if (MODE == 0) c = acc[mb][nb][e];
+          else if (MODE > 0) c += acc[mb][nb][e];
+          else c -= acc[mb][nb][e];
+        }
+      }
+}
+
 // acc (fragments of an M x N product, the c/d layout above) += sign op(A) op(B);
 // LDA / LDB: row strides of the stored A / B (0: dense)
 template <int M, int K, int N, bool TA, bool TB, bool NEG, int MB, int NB, int LDA = 0,
@@ -84,7 +155,7 @@ PTC_D void dmma_accumulate(double (&acc)[MB][NB][2], const double* A, const doub
     }
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
-      const int j = nb * 8 + fr;
+      const int j = nb * 8 + frag_pi(fr, FragOrder<N>::perm);
       bf[nb] = (j < N && k < K) ? (TB ? B[j * lb + k] : B[k * lb + j]) : 0.0;
     }
 #pragma unroll
@@ -97,7 +168,8 @@ PTC_D void dmma_accumulate(double (&acc)[MB][NB][2], const double* A, const doub
 // C = sym(D + op(A1) op(B1) + op(A2) op(B2)) for N x N (N <= 16): both
 // products accumulate in the same fragments and the symmetrisation is done
 // there with shuffles (the transposed entry of (i, j) sits in tile (nb, mb)
-// of lane ((j % 8) << 2) | ((i % 8) >> 1)), so the result is stored once,
+// of lane ((j % 8) << 2) | (pi(i % 8) >> 1), register pi(i % 8) & 1, pi the
+// column order of frag_ld), so the result is stored once,
 // already symmetric -- no separate w_sym pass.  D may be C.
 template <int N, int K1, int K2, bool TA1, bool TB1, bool TA2, bool TB2, int LDB1 = 0>
 PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
@@ -106,15 +178,7 @@ PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
   const int ln = lane_id();
   const int fr = ln >> 2, fc = ln & 3;
   double acc[NB][NB][2];
-#pragma unroll
-  for (int mb = 0; mb < NB; ++mb)
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
-        acc[mb][nb][e] = (i < N && j < N) ? D[i * N + j] : 0.0;
-      }
+  frag_ld<N, N>(acc, D);
   dmma_accumulate<N, K1, N, TA1, TB1, false, NB, NB, 0, LDB1>(acc, A1, B1);
   dmma_accumulate<N, K2, N, TA2, TB2, false>(acc, A2, B2);
   double out[NB][NB][2];
@@ -124,21 +188,15 @@ PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
     for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int src = ((2 * fc + e) << 2) | (fr >> 1);
+        constexpr bool kP = FragOrder<N>::perm;
+        const int pr = frag_pi(fr, kP);
+        const int src = (frag_pi(2 * fc + e, kP) << 2) | (pr >> 1);
         const double v0 = __shfl_sync(0xffffffffu, acc[nb][mb][0], src);
         const double v1 = __shfl_sync(0xffffffffu, acc[nb][mb][1], src);
-        out[mb][nb][e] = 0.5 * (acc[mb][nb][e] + ((fr & 1) ? v1 : v0));
+        out[mb][nb][e] = 0.5 * (acc[mb][nb][e] + ((pr & 1) ? v1 : v0));
       }
   __syncwarp();  // every lane has read its operands (and D) before C is written
-#pragma unroll
-  for (int mb = 0; mb < NB; ++mb)
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
-        if (i < N && j < N) C[i * N + j] = out[mb][nb][e];
-      }
+  frag_st<N, N, 0>(out, C);
   __syncwarp();
 }
 
@@ -147,8 +205,6 @@ PTC_D void w_mm2_sym_dmma(const double* A1, const double* B1, const double* A2,
 template <int M, int K, int N, bool TA, int LDB>
 PTC_D void w_mm_ldb_dmma(const double* A, const double* B, double* C) {
   constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8;
-  const int ln = lane_id();
-  const int fr = ln >> 2, fc = ln & 3;
   double acc[MB][NB][2];
 #pragma unroll
   for (int mb = 0; mb < MB; ++mb)
@@ -156,15 +212,7 @@ PTC_D void w_mm_ldb_dmma(const double* A, const double* B, double* C) {
     for (int nb = 0; nb < NB; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
   dmma_accumulate<M, K, N, TA, false, false, MB, NB, 0, LDB>(acc, A, B);
   __syncwarp();
-#pragma unroll
-  for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
-        if (i < M && j < N) C[i * N + j] = acc[mb][nb][e];
-      }
+  frag_st<M, N, 0>(acc, C);
   __syncwarp();
 }
 
@@ -174,16 +222,14 @@ PTC_D void w_mm_dmma(const double* A, const double* B, double* C, const double* 
   const int ln = lane_id();
   const int fr = ln >> 2, fc = ln & 3;
   double acc[MB][NB][2];
+  if constexpr (MODE == 2 || MODE == -2) {   // the accumulator starts from D (C = D +- AB)
+    frag_ld<M, N>(acc, D);
+  } else {
 #pragma unroll
-  for (int mb = 0; mb < MB; ++mb)
+    for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        // MODE +-2: the accumulator starts from D (C = D +- AB)
-        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
-        acc[mb][nb][e] = ((MODE == 2 || MODE == -2) && i < M && j < N) ? D[i * N + j] : 0.0;
-      }
+      for (int nb = 0; nb < NB; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+  }
 #pragma unroll
   for (int kb = 0; kb < KB; ++kb) {
     const int k = kb * 4 + fc;
@@ -196,7 +242,7 @@ PTC_D void w_mm_dmma(const double* A, const double* B, double* C, const double* 
     }
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
-      const int j = nb * 8 + fr;
+      const int j = nb * 8 + frag_pi(fr, FragOrder<N>::perm);
       bf[nb] = (j < N && k < K) ? (TB ? B[j * K + k] : B[k * N + j]) : 0.0;
     }
 #pragma unroll
@@ -205,20 +251,7 @@ PTC_D void w_mm_dmma(const double* A, const double* B, double* C, const double* 
       for (int nb = 0; nb < NB; ++nb) dmma_8x8x4(acc[mb][nb], af[mb], bf[nb]);
   }
   __syncwarp();  // every lane has read its operands before C is written
-#pragma unroll
-  for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = mb * 8 + fr, j = nb * 8 + 2 * fc + e;
-        if (i < M && j < N) {
-          double& c = C[i * N + j];
-          if (MODE == 0 || MODE == 2 || MODE == -2) c = acc[mb][nb][e];
-          else if (MODE > 0) c += acc[mb][nb][e];
-          else c -= acc[mb][nb][e];
-        }
-      }
+  frag_st<M, N, (MODE == 1 || MODE == -1) ? MODE : 0>(acc, C);
   __syncwarp();
 }
 
