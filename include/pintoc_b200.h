@@ -149,8 +149,9 @@ int ptc_propagate(int dtype, int batch, int horizon, int nx, int nu,
                   const void* Fx, const void* Fu, const void* Gamma, const void* gamma,
                   const void* d, void* dx, void* du, void* workspace, int64_t workspace_bytes,
                   int chunk0, int chunk, void* stream);
-/* the plan the automatic choice would use (for reporting / depth probes) */
-int ptc_lqr_plan(int batch, int horizon, int chunk0, int chunk, int* out_chunk0,
+/* the plan the automatic choice would use for state size nx (for reporting
+ * / depth probes; the same choice ptc_lqr_workspace_bytes and the solves make) */
+int ptc_lqr_plan(int batch, int horizon, int nx, int chunk0, int chunk, int* out_chunk0,
                  int* out_chunk, int* out_levels);
 
 /* ------------------------------------------------------------------------

@@ -66,7 +66,7 @@ _SIGS = {
     "ptc_lqr_solve": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7 + [C.c_void_p]
                       + [C.c_void_p] * 6 + [C.c_void_p, C.c_void_p, C.c_int64,
                                              C.c_int, C.c_int, C.c_void_p]),
-    "ptc_lqr_plan": (C.c_int, [C.c_int] * 4 + [C.POINTER(C.c_int)] * 3),
+    "ptc_lqr_plan": (C.c_int, [C.c_int] * 5 + [C.POINTER(C.c_int)] * 3),
     "ptc_propagate": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7
                       + [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]),
     "ptc_lqr_block_comps": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

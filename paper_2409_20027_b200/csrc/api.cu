@@ -42,17 +42,22 @@ static int fail(int code, const std::string& msg) {
 // split the horizon into chunks of K0 stages so that ~32K threads are busy,
 // with an 8-ary tree above them (log-depth in the horizon).
 static Plan auto_plan(int B, int T, int K0, int K, int nx = 0) {
-  if (K <= 0) K = 8;
+  const bool wide = nx >= 8;
+  // tree fan-out: each level above the leaves costs K serial combines of
+  // one unit, so the warp kernels' expensive combines (nx >= 8: a 12 x 12
+  // LU per combine) want a narrow tree -- K = 4 measured 4-17% faster than
+  // 8 for nx = 12 at T = 2^10 .. 2^20 (gpurun r119)
+  if (K <= 0) K = wide ? 4 : 8;
   if (K0 <= 0) {
     const long long work = (long long)B * T;
     // thread-per-unit kernels want ~32K units; the warp-per-unit kernels of
-    // nx >= 8 (wide.cuh) ~8K warps, i.e. longer level-0 chunks
-    const long long units = nx >= 8 ? 8192 : 32768;
+    // nx >= 8 (wide.cuh) ~8K warps and level-0 chunks of at least 16 stages
+    const long long units = wide ? 8192 : 32768;
     // one sweep per problem (work-optimal) once the batch alone keeps the
     // GPU busy: measured crossover between 8K (tree 15% faster) and 16K
     // (sweep 25% faster) problems per launch (nx = 2 / 4, T = 256)
     if (B >= 16384) K0 = T;
-    else K0 = (int)std::max<long long>(4, (work + units - 1) / units);
+    else K0 = (int)std::max<long long>(wide ? 16 : 4, (work + units - 1) / units);
   }
   return make_plan(T, K0, K);
 }
@@ -113,10 +118,10 @@ int ptc_supported(int dtype, int model, int nx, int nu) {
   return newton_registry().count(NewtonKey(dtype, model, nx, nu)) ? 1 : 0;
 }
 
-int ptc_lqr_plan(int batch, int horizon, int chunk0, int chunk, int* out_chunk0, int* out_chunk,
-                 int* out_levels) {
+int ptc_lqr_plan(int batch, int horizon, int nx, int chunk0, int chunk, int* out_chunk0,
+                 int* out_chunk, int* out_levels) {
   if (batch < 1 || horizon < 1) return fail(PTC_ERR_ARG, "batch and horizon must be >= 1");
-  Plan p = auto_plan(batch, horizon, chunk0, chunk);
+  Plan p = auto_plan(batch, horizon, chunk0, chunk, nx);
   if (out_chunk0) *out_chunk0 = p.K0;
   if (out_chunk) *out_chunk = p.K;
   if (out_levels) *out_levels = p.L;

@@ -129,7 +129,7 @@ class LqrSolver:
 
     def plan(self):
         k0, k, lv = C.c_int(), C.c_int(), C.c_int()
-        N.check(self.lib.ptc_lqr_plan(self.B, self.T, self.chunk0, self.chunk, C.byref(k0),
+        N.check(self.lib.ptc_lqr_plan(self.B, self.T, self.nx, self.chunk0, self.chunk, C.byref(k0),
                                       C.byref(k), C.byref(lv)))
         return k0.value, k.value, lv.value
 

@@ -60,12 +60,15 @@ def test_workspace_queries_without_gpu():
     assert 0 < small < big
     assert lib.ptc_lqr_workspace_bytes(_native.PTC_F64, 0, 10, 4, 2, 0, 0) < 0
     k0, k, lv = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    assert lib.ptc_lqr_plan(65536, 256, 0, 0, ctypes.byref(k0), ctypes.byref(k),
+    assert lib.ptc_lqr_plan(65536, 256, 4, 0, 0, ctypes.byref(k0), ctypes.byref(k),
                             ctypes.byref(lv)) == 0
     assert k0.value == 256 and lv.value == 0          # big batch: one sweep per problem
-    assert lib.ptc_lqr_plan(1, 1 << 16, 0, 0, ctypes.byref(k0), ctypes.byref(k),
+    assert lib.ptc_lqr_plan(1, 1 << 16, 4, 0, 0, ctypes.byref(k0), ctypes.byref(k),
                             ctypes.byref(lv)) == 0
-    assert lv.value >= 3                              # long horizon: log-depth tree
+    assert lv.value >= 3 and k.value == 8             # long horizon: log-depth tree
+    assert lib.ptc_lqr_plan(1, 1 << 16, 12, 0, 0, ctypes.byref(k0), ctypes.byref(k),
+                            ctypes.byref(lv)) == 0
+    assert (k0.value, k.value) == (16, 4)             # warp kernels: narrow tree
 
 
 def test_solver_path_refuses_without_cuda():
