@@ -40,14 +40,17 @@ static int fail(int code, const std::string& msg) {
 // Automatic scan plan.  Large batches fill the GPU on their own: one thread
 // per problem sweeps its horizon (no tree, work optimal).  Small batches
 // split the horizon into chunks of K0 stages so that ~32K threads are busy,
-// with an 8-ary tree above them (log-depth in the horizon).
+// with a 4-ary tree above them (log-depth in the horizon).
 static Plan auto_plan(int B, int T, int K0, int K, int nx = 0) {
   const bool wide = nx >= 8;
   // tree fan-out: each level above the leaves costs K serial combines of
-  // one unit, so the warp kernels' expensive combines (nx >= 8: a 12 x 12
-  // LU per combine) want a narrow tree -- K = 4 measured 4-17% faster than
-  // 8 for nx = 12 at T = 2^10 .. 2^20 (gpurun r119)
-  if (K <= 0) K = wide ? 4 : 8;
+  // one unit, and the log-depth levels are latency-bound, so a narrow tree
+  // wins: K = 4 measured 4-17% faster than 8 for nx = 12 at T = 2^10 ..
+  // 2^20 and 20-29% faster for nx = 2 / 4 at T = 2^12 .. 2^16, batch 1
+  // (gpurun r119, r121); K = 2 doubles the levels and loses again.  Batched
+  // thread-kernel trees (the strong-scaling shares, 2K-8K problems) keep
+  // K = 8: there the levels are wide and K = 4 measured ~10% slower (r122)
+  if (K <= 0) K = (wide || B < 256) ? 4 : 8;
   if (K0 <= 0) {
     const long long work = (long long)B * T;
     // thread-per-unit kernels want ~32K units; the warp-per-unit kernels of

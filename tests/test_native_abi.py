@@ -65,7 +65,7 @@ def test_workspace_queries_without_gpu():
     assert k0.value == 256 and lv.value == 0          # big batch: one sweep per problem
     assert lib.ptc_lqr_plan(1, 1 << 16, 4, 0, 0, ctypes.byref(k0), ctypes.byref(k),
                             ctypes.byref(lv)) == 0
-    assert lv.value >= 3 and k.value == 8             # long horizon: log-depth tree
+    assert lv.value >= 3 and k.value == 4             # long horizon: log-depth tree
     assert lib.ptc_lqr_plan(1, 1 << 16, 12, 0, 0, ctypes.byref(k0), ctypes.byref(k),
                             ctypes.byref(lv)) == 0
     assert (k0.value, k.value) == (16, 4)             # warp kernels: narrow tree
