@@ -610,6 +610,29 @@ PTC_D void w_ld(const R* f, int t, int rows, int B, int b, R* dst, int c0 = 0) {
   __syncwarp();
 }
 
+// register prefetch of one component-major item (C components of item t,
+// the w_ld layout): issued before the current combine, stored after it
+template <typename R, int C>
+struct WPrefetchItem {
+  static constexpr int PER = (C + 31) / 32;
+  R v[PER];
+  PTC_D void load(const R* f, int t, int rows, int B, int b) {
+    const int ln = lane_id();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int c = ln + 32 * k;
+      v[k] = c < C ? __ldg(f + ((size_t)c * rows + t) * B + b) : R(0);
+    }
+  }
+  PTC_D void store(R* dst) const {
+    const int ln = lane_id();
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (ln + 32 * k < C) dst[ln + 32 * k] = v[k];
+    __syncwarp();
+  }
+};
+
 template <int C, typename R>
 PTC_D void w_st(R* f, int t, int rows, int B, int b, const R* src, int c0 = 0) {
   for (int c = lane_id(); c < C; c += 32) f[((size_t)(c0 + c) * rows + t) * B + b] = src[c];
@@ -1338,10 +1361,16 @@ __global__ void __launch_bounds__(128) kw_value_up(LqrArgs<R> a, int l) {
   R* scr = o + S::VC;
   w_ld<S::VC>(a.vagg[l], last, nl, a.B, b, acc);
   bool okc = true;
+  // the next item loads while the current combine runs; acc / o ping-pong
+  WPrefetchItem<R, S::VC> pf;
+  if (last - 1 >= first) pf.load(a.vagg[l], last - 1, nl, a.B, b);
   for (int i = last - 1; i >= first; --i) {
-    w_ld<S::VC>(a.vagg[l], i, nl, a.B, b, e);
+    pf.store(e);
+    if (i - 1 >= first) pf.load(a.vagg[l], i - 1, nl, a.B, b);
     okc &= w_vcombine<R, NX, NU>(e, acc, o, scr, piv);
-    w_copy<S::VC>(o, acc);
+    R* tmp = acc;
+    acc = o;
+    o = tmp;
   }
   w_st<S::VC>(a.vagg[l + 1], j, nn, a.B, b, acc);
   if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
@@ -1358,11 +1387,16 @@ __global__ void __launch_bounds__(128) kw_value_top(LqrArgs<R> a) {
   if (a.vcarry_in) w_ld<S::CC>(a.vcarry_in, 0, 1, a.B, b, c);
   else w_fill<S::CC>(c, R(0));
   bool okc = true;
+  WPrefetchItem<R, S::VC> pf;
+  pf.load(a.vagg[L], nL - 1, nL, a.B, b);
   for (int i = nL - 1; i >= 0; --i) {
     w_st<S::CC>(a.vcar[L], i, nL, a.B, b, c);
-    w_ld<S::VC>(a.vagg[L], i, nL, a.B, b, e);
+    pf.store(e);
+    if (i > 0) pf.load(a.vagg[L], i - 1, nL, a.B, b);
     okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
-    w_copy<S::CC>(o, c);
+    R* tmp = c;
+    c = o;
+    o = tmp;
   }
   if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
 }
@@ -1378,11 +1412,16 @@ __global__ void __launch_bounds__(128) kw_value_down(LqrArgs<R> a, int l) {
   R* scr = e + S::VC;
   w_ld<S::CC>(a.vcar[l + 1], j, nn, a.B, b, c);
   bool okc = true;
+  WPrefetchItem<R, S::VC> pf;
+  pf.load(a.vagg[l], last, nl, a.B, b);
   for (int i = last; i >= first; --i) {
     w_st<S::CC>(a.vcar[l], i, nl, a.B, b, c);
-    w_ld<S::VC>(a.vagg[l], i, nl, a.B, b, e);
+    pf.store(e);
+    if (i > first) pf.load(a.vagg[l], i - 1, nl, a.B, b);
     okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
-    w_copy<S::CC>(o, c);
+    R* tmp = c;
+    c = o;
+    o = tmp;
   }
   if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
 }
