@@ -1376,6 +1376,62 @@ __global__ void __launch_bounds__(128) kw_value_up(LqrArgs<R> a, int l) {
   if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
 }
 
+// narrow tree levels (few units, latency-bound): one unit per block, its
+// items split between the block's two warps -- each folds its half (the
+// same right-to-left fold as kw_value_up), then warp 0 combines the halves
+// (lower (x) upper).  Depth ceil(K/2) combines instead of K - 1; the
+// association differs from the sequential fold only in rounding.
+static_assert(kWarpsPerBlock == 2, "kw_value_up2 splits a unit over two warps");
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(64) kw_value_up2(LqrArgs<R> a, int l) {
+  using S = WSlab<R, NX, NU>;
+  const int u = blockIdx.x;
+  if (u >= a.plan.n[l + 1] * a.B) return;  // block-uniform exits only
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int w = threadIdx.x >> 5;
+  R* slab = warp_slab<R>(S::kUp);
+  int* piv = warp_piv<R>(slab, S::kUp);
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  const int mid = first + (last - first + 2) / 2;  // warp 0: [first, mid), warp 1: [mid, last]
+  const int lo = w == 0 ? first : mid, hi = w == 0 ? mid - 1 : last;
+  R* acc = slab;
+  R* e = acc + S::VC;
+  R* o = e + S::VC;
+  R* scr = o + S::VC;
+  bool okc = true;
+  if (lo <= hi) {
+    w_ld<S::VC>(a.vagg[l], hi, nl, a.B, b, acc);
+    WPrefetchItem<R, S::VC> pf;
+    if (hi - 1 >= lo) pf.load(a.vagg[l], hi - 1, nl, a.B, b);
+    for (int i = hi - 1; i >= lo; --i) {
+      pf.store(e);
+      if (i - 1 >= lo) pf.load(a.vagg[l], i - 1, nl, a.B, b);
+      okc &= w_vcombine<R, NX, NU>(e, acc, o, scr, piv);
+      R* tmp = acc;
+      acc = o;
+      o = tmp;
+    }
+    if (acc != slab) {  // the half's aggregate at the slab base for the other warp
+      w_copy<S::VC>(acc, slab);
+      o = acc;
+      acc = slab;
+    }
+  }
+  __syncthreads();
+  if (w == 0) {
+    if (mid <= last) {
+      const R* upper = reinterpret_cast<const R*>(reinterpret_cast<const unsigned char*>(slab) +
+                                                  S::bytes_of(S::kUp));
+      okc &= w_vcombine<R, NX, NU>(acc, upper, o, scr, piv);
+      acc = o;
+    }
+    w_st<S::VC>(a.vagg[l + 1], j, nn, a.B, b, acc);
+  }
+  if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
+}
+
 template <typename R, int NX, int NU>
 __global__ void __launch_bounds__(128) kw_value_top(LqrArgs<R> a) {
   PTC_WIDE_PROLOGUE(1, WSlab<R, NX, NU>::kStep)
@@ -1774,6 +1830,7 @@ struct Wide {
     if (done) return;
     allow(kw_value_up0<R, NX, NU>, S::kUp0);
     allow(kw_value_up<R, NX, NU>, S::kUp);
+    allow(kw_value_up2<R, NX, NU>, S::kUp);
     allow(kw_value_top<R, NX, NU>, S::kStep);
     allow(kw_value_down<R, NX, NU>, S::kStep);
     allow(kw_value_down0<R, NX, NU, true>, S::kDown0);
@@ -1792,6 +1849,20 @@ struct Wide {
 };
 
 #define PTC_WL(kernel, units, elems) kernel<<<W::grid(units), 32 * kWarpsPerBlock, W::smem(elems), s>>>
+
+// one up-sweep level: the sequential fold while the level is wide enough to
+// fill the GPU, the two-warp split fold on the narrow (latency-bound) levels
+constexpr long long kUp2MaxUnits = 1024;
+template <typename R, int NX, int NU>
+void kw_value_up_level(const LqrArgs<R>& a, int l, cudaStream_t s) {
+  using W = Wide<R, NX, NU>;
+  using S = WSlab<R, NX, NU>;
+  const long long units = (long long)a.plan.n[l + 1] * a.B;
+  if (units <= kUp2MaxUnits)
+    kw_value_up2<R, NX, NU><<<(unsigned)units, 32 * kWarpsPerBlock, W::smem(S::kUp), s>>>(a, l);
+  else
+    PTC_WL((kw_value_up<R, NX, NU>), units, S::kUp)(a, l);
+}
 
 template <typename R, int NX, int NU>
 void launch_prop_tree_wide(const LqrArgs<R>& a, cudaStream_t s) {
@@ -1838,7 +1909,7 @@ void launch_lqr_wide(const LqrArgs<R>& a0, cudaStream_t s) {
   const long long B = a.B, P0 = pl.units0();
   if (pl.L >= 1) {
     PTC_WL((kw_value_up0<R, NX, NU>), P0 * B, S::kUp0)(a);
-    for (int l = 1; l < pl.L; ++l) PTC_WL((kw_value_up<R, NX, NU>), pl.n[l + 1] * B, S::kUp)(a, l);
+    for (int l = 1; l < pl.L; ++l) kw_value_up_level<R, NX, NU>(a, l, s);
     launch_value_tree_wide<R, NX, NU>(a, s);
     PTC_WL((kw_value_down0<R, NX, NU, true>), P0 * B, S::kDown0)(a);
     launch_prop_tree_wide<R, NX, NU>(a, s);
@@ -1876,7 +1947,7 @@ void launch_lqr_block_wide(const LqrArgs<R>& a0, int phase, const void* blocks, 
   if (phase == 0) {
     if (a.staged && !a.prestaged) launch_stage_in<R, NX, NU>(a, s);
     PTC_WL((kw_value_up0<R, NX, NU>), P0 * B, S::kUp0)(a);
-    for (int l = 1; l < pl.L; ++l) PTC_WL((kw_value_up<R, NX, NU>), pl.n[l + 1] * B, S::kUp)(a, l);
+    for (int l = 1; l < pl.L; ++l) kw_value_up_level<R, NX, NU>(a, l, s);
     PTC_WL((kw_value_block<R, NX, NU>), B, S::kUp)(a, static_cast<R*>(out));
   } else if (phase == 1) {
     PTC_WL((kw_value_carry<R, NX, NU>), B, S::kStep)(a, static_cast<const R*>(blocks), rank, world);
