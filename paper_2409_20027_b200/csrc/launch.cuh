@@ -280,11 +280,16 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     const Plan& pl = a.plan;
     const long long nT = (long long)(a.T + 1) * B;
     k_pr_init<R, NX, NU><<<grid_for(nT), kBlock, 0, s>>>(a, la.dX, la.dU);
-    for (int k = 0; k <= a.pr_iters; ++k) {
+    // affine dynamics: the first guess x + dx already satisfies the
+    // recurrence up to the LQR scan's rounding and one sweep is exact, so two
+    // checks and one sweep replace the nonlinear budget (each unneeded sweep
+    // is ~2(L + 1) early-exit launches in the captured iteration)
+    const int iters = (IsAffine<Dyn>::value && a.pr_iters > 1) ? 1 : a.pr_iters;
+    for (int k = 0; k <= iters; ++k) {
       k_pr_up0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, k);
       if (fold) k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.rres, 1, RED_MAX, (int)P0, (int)B);
       k_pr_check<R><<<grid_for(B), kBlock, 0, s>>>(a, k);
-      if (k == a.pr_iters) break;
+      if (k == iters) break;
       for (int l = 1; l < pl.L; ++l) k_pr_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
       k_pr_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, k);
       for (int l = pl.L - 1; l >= 1; --l)
