@@ -784,7 +784,11 @@ struct Solver final : ptc_solver {
     // candidate rollout: log-depth Newton sweeps for tree plans with long
     // horizons (rollout 0 = auto), the sequential recurrence otherwise
     const bool par = a.plan.L >= 1 && (d.rollout == 2 || (d.rollout == 0 && T >= 1024));
-    a.pr_iters = par ? 8 : 0;
+    // Newton on the recurrence converges quadratically from the LQR's
+    // prediction when it converges at all (non-chaotic stretches): 4 sweeps,
+    // then the sequential recurrence -- a larger budget only adds early-exit
+    // launches to every iteration of the problems that never converge
+    a.pr_iters = par ? 4 : 0;
     a.xr = par ? c.template take<R>(a.xsz) : nullptr;
     a.alpha = db(); a.nu = db(); a.cur_cost = db(); a.cand_cost = db(); a.mu = db();
     a.opt.hist_cap = std::max(0, d.hist_cap);
