@@ -686,7 +686,7 @@ def newton_latency_sweep(torch, P):
                 par += int(int(s.read("rollout_state")[0]) & 2 != 0)
             row = {"ms": round(statistics.median(per), 4), "full": f"{full}/12"}
             if model == "tvlinear12":   # affine nx >= 8: exact affine-scan rollout on tree plans
-                row["rollout"] = "affine scan" if Tn >= 1024 else "sequential (warp)"
+                row["rollout"] = "affine scan"
             else:
                 row["log_depth_rollout_converged"] = f"{par}/3"
             out[str(Tn)] = row

@@ -783,7 +783,12 @@ struct Solver final : ptc_solver {
     a.rres = c.template take<double>(P0 * B);
     // candidate rollout: log-depth Newton sweeps for tree plans with long
     // horizons (rollout 0 = auto), the sequential recurrence otherwise
-    const bool par = a.plan.L >= 1 && (d.rollout == 2 || (d.rollout == 0 && T >= 1024));
+    // (affine dynamics: the log-depth rollout is exact in one scan -- the
+    // wide affine-scan kernels for nx >= 8, one checked sweep otherwise --
+    // and beats the sequential recurrence at any horizon with a tree plan)
+    const bool affine = d.model == PTC_DYN_LINEAR;
+    const bool par = a.plan.L >= 1 &&
+                     (d.rollout == 2 || (d.rollout == 0 && (T >= 1024 || affine)));
     // Newton on the recurrence converges quadratically from the LQR's
     // prediction when it converges at all (non-chaotic stretches): 4 sweeps,
     // then the sequential recurrence -- a larger budget only adds early-exit
