@@ -90,7 +90,8 @@ static void carve_lqr_tree(Carver& c, LqrArgs<R>& a, int nx, int nu) {
     a.xst = c.template take<R>((size_t)a.T * sc);
     a.gst = c.template take<R>((size_t)a.T * (nu * nx + nu));
   }
-  for (int l = 0; l <= kMaxLevels; ++l) a.vagg[l] = a.vcar[l] = a.pagg[l] = a.pcar[l] = nullptr;
+  for (int l = 0; l <= kMaxLevels; ++l)
+    a.vagg[l] = a.vcar[l] = a.pagg[l] = a.pcar[l] = a.vhalf[l] = nullptr;
   a.vcin_buf = a.xin_buf = nullptr;
   if (a.block_mode) {
     a.vcin_buf = c.template take<R>(B * (nx * nx + nx));
@@ -104,6 +105,11 @@ static void carve_lqr_tree(Carver& c, LqrArgs<R>& a, int nx, int nu) {
     a.pagg[l] = c.template take<R>(n * (nx * nx + nx));
     a.pcar[l] = c.template take<R>(n * nx);
   }
+  // split-fold levels of the warp kernels keep their upper-half aggregates
+  if (nx >= 8)
+    for (int l = 1; l < pl.L; ++l)
+      if ((long long)pl.n[l + 1] * a.B <= kUp2MaxUnits)
+        a.vhalf[l] = c.template take<R>((size_t)pl.n[l + 1] * B * (3 * nx * nx + 2 * nx));
 }
 
 }  // namespace ptc

@@ -61,6 +61,9 @@ struct LqrArgs {
   R* vcar[kMaxLevels + 1];
   R* pagg[kMaxLevels + 1];
   R* pcar[kMaxLevels + 1];
+  // wide narrow levels (kw_value_up2 / kw_value_down2): the upper half's
+  // aggregate of each unit of level l (rows n[l + 1]); null where unused
+  R* vhalf[kMaxLevels + 1];
 };
 
 template <typename R>

@@ -1418,6 +1418,8 @@ __global__ void __launch_bounds__(64) kw_value_up2(LqrArgs<R> a, int l) {
       o = acc;
       acc = slab;
     }
+    // ... and, for the down-sweep's split (kw_value_down2), in global memory
+    if (w == 1 && a.vhalf[l]) w_st<S::VC>(a.vhalf[l], j, nn, a.B, b, acc);
   }
   __syncthreads();
   if (w == 0) {
@@ -1474,6 +1476,53 @@ __global__ void __launch_bounds__(128) kw_value_down(LqrArgs<R> a, int l) {
     w_st<S::CC>(a.vcar[l], i, nl, a.B, b, c);
     pf.store(e);
     if (i > first) pf.load(a.vagg[l], i - 1, nl, a.B, b);
+    okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
+    R* tmp = c;
+    c = o;
+    o = tmp;
+  }
+  if (!okc && lane_id() == 0) atomicOr(a.flags + b, FLAG_COND);
+}
+
+// the down-sweep of a split-fold level: warp 1 walks the upper half from
+// the unit's carry; warp 0 first applies the upper half's aggregate (stored
+// by kw_value_up2) to the carry -- vstep(e_mid (x) .. (x) e_last, c) is the
+// carry entering item mid - 1 -- and walks the lower half.  No exchange
+// between the warps; depth ceil(K/2) + 1 steps instead of K.
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(64) kw_value_down2(LqrArgs<R> a, int l) {
+  using S = WSlab<R, NX, NU>;
+  const int u = blockIdx.x;
+  if (u >= a.plan.n[l + 1] * a.B) return;
+  const int b = u % a.B, j = u / a.B;
+  if (lqr_skip(a, b)) return;
+  const int w = threadIdx.x >> 5;
+  R* slab = warp_slab<R>(S::kStep);
+  int* piv = warp_piv<R>(slab, S::kStep);
+  const int nl = a.plan.n[l], nn = a.plan.n[l + 1];
+  const int first = j * a.plan.K, last = min(nl, first + a.plan.K) - 1;
+  const int mid = first + (last - first + 2) / 2;
+  const int lo = w == 0 ? first : mid, hi = w == 0 ? mid - 1 : last;
+  if (lo > hi) return;  // warp-level exit: no block barrier below
+  R* c = slab;
+  R* o = c + S::CC;
+  R* e = o + S::CC;
+  R* scr = e + S::VC;
+  w_ld<S::CC>(a.vcar[l + 1], j, nn, a.B, b, c);
+  bool okc = true;
+  WPrefetchItem<R, S::VC> pf;
+  pf.load(a.vagg[l], hi, nl, a.B, b);
+  if (w == 0 && mid <= last) {
+    w_ld<S::VC>(a.vhalf[l], j, nn, a.B, b, e);
+    okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
+    R* tmp = c;
+    c = o;
+    o = tmp;
+  }
+  for (int i = hi; i >= lo; --i) {
+    w_st<S::CC>(a.vcar[l], i, nl, a.B, b, c);
+    pf.store(e);
+    if (i > lo) pf.load(a.vagg[l], i - 1, nl, a.B, b);
     okc &= w_vstep<R, NX, NU>(e, c, o, scr, piv);
     R* tmp = c;
     c = o;
@@ -1831,6 +1880,7 @@ struct Wide {
     allow(kw_value_up0<R, NX, NU>, S::kUp0);
     allow(kw_value_up<R, NX, NU>, S::kUp);
     allow(kw_value_up2<R, NX, NU>, S::kUp);
+    allow(kw_value_down2<R, NX, NU>, S::kStep);
     allow(kw_value_top<R, NX, NU>, S::kStep);
     allow(kw_value_down<R, NX, NU>, S::kStep);
     allow(kw_value_down0<R, NX, NU, true>, S::kDown0);
@@ -1882,7 +1932,13 @@ void launch_value_tree_wide(const LqrArgs<R>& a, cudaStream_t s) {
   const Plan& pl = a.plan;
   const long long B = a.B;
   PTC_WL((kw_value_top<R, NX, NU>), B, S::kStep)(a);
-  for (int l = pl.L - 1; l >= 1; --l) PTC_WL((kw_value_down<R, NX, NU>), pl.n[l + 1] * B, S::kStep)(a, l);
+  for (int l = pl.L - 1; l >= 1; --l) {
+    const long long units = (long long)pl.n[l + 1] * B;
+    if (a.vhalf[l] && units <= kUp2MaxUnits)
+      kw_value_down2<R, NX, NU><<<(unsigned)units, 32 * kWarpsPerBlock, W::smem(S::kStep), s>>>(a, l);
+    else
+      PTC_WL((kw_value_down<R, NX, NU>), units, S::kStep)(a, l);
+  }
 }
 
 template <typename R, int NX, int NU>
