@@ -377,17 +377,28 @@ template <int N, typename R>
 PTC_D bool w_lu(R* G, int* piv) {
   const int ln = lane_id();
   bool ok = true;
+  // unrolled: the trailing-block extents (N - k - 1) are compile-time
+  // constants, so the rank-1 update's row / column split is shifts and
+  // multiplies instead of integer divisions on the dependent chain
+#pragma unroll
   for (int k = 0; k < N; ++k) {
     R v = (ln >= k && ln < N) ? fabs(G[ln * N + k]) : R(-1);
     int p = (ln >= k && ln < N) ? ln : N;
+    // arg-max over the candidate lanes: N <= 16 fits one half-warp (four
+    // butterfly rounds), then lane 0's answer is broadcast
+    constexpr int kTop = N <= 16 ? 8 : 16;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
+    for (int off = kTop; off > 0; off >>= 1) {
       const R ov = __shfl_xor_sync(0xffffffffu, v, off);
       const int op = __shfl_xor_sync(0xffffffffu, p, off);
       if (ov > v || (ov == v && op < p)) {
         v = ov;
         p = op;
       }
+    }
+    if constexpr (N <= 16) {
+      v = __shfl_sync(0xffffffffu, v, 0);
+      p = __shfl_sync(0xffffffffu, p, 0);
     }
     if (!(v == v)) p = k;  // NaN column: keep the diagonal, as lu_factor does
     if (ln == 0) piv[k] = p;
