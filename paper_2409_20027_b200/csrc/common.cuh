@@ -17,6 +17,13 @@
 #define PTC_D __device__ __forceinline__
 
 namespace ptc {
+// correctly rounded reciprocal (bit-identical to R(1) / x under IEEE
+// division, without the general division's numerator path)
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+}  // namespace ptc
+
+namespace ptc {
 
 constexpr int kMaxLevels = 12;
 

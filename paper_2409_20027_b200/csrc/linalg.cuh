@@ -234,7 +234,7 @@ PTC_D bool lu_factor(R (&A)[N][N], int (&piv)[N]) {
     for (int i = k + 1; i < N; ++i) cswap_rows<N, N>(A, i, k, p == i);
     R pv = A[k][k];
     ok = ok && (pv != R(0));
-    R inv = R(1) / pv;
+    R inv = rcp_rn(pv);
     A[k][k] = inv;  // U's diagonal is kept as reciprocals (solves multiply)
 #pragma unroll
     for (int i = k + 1; i < N; ++i) {

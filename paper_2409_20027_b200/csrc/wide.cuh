@@ -411,7 +411,7 @@ PTC_D bool w_lu(R* G, int* piv) {
     __syncwarp();
     const R pv = G[k * N + k];
     ok = ok && (pv != R(0));
-    const R inv = R(1) / pv;
+    const R inv = rcp_rn(pv);
     __syncwarp();
     if (ln == 0) G[k * N + k] = inv;
     for (int i = k + 1 + ln; i < N; i += 32) G[i * N + k] *= inv;
@@ -519,7 +519,7 @@ PTC_D bool lu_regs(R (&G)[N][N], int (&perm)[N]) {
         }
     const R pv = G[k][k];
     ok = ok && (pv != R(0));
-    const R inv = R(1) / pv;
+    const R inv = rcp_rn(pv);
     G[k][k] = inv;
 #pragma unroll
     for (int i = k + 1; i < N; ++i) G[i][k] *= inv;
