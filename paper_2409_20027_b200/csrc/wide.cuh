@@ -438,20 +438,23 @@ PTC_D void w_lu_solve(const R* LU, const int* piv, R* B) {
         B[p * M + c] = t;
       }
     }
+    // the lane's column in registers: the triangular solves' dependent
+    // chains run without a shared-memory round trip per row
+    R x[N];
 #pragma unroll
-    for (int i = 1; i < N; ++i) {
-      R v = B[i * M + c];
+    for (int i = 0; i < N; ++i) x[i] = B[i * M + c];
 #pragma unroll
-      for (int k = 0; k < i; ++k) v = fma(-LU[i * N + k], B[k * M + c], v);
-      B[i * M + c] = v;
-    }
+    for (int i = 1; i < N; ++i)
+#pragma unroll
+      for (int k = 0; k < i; ++k) x[i] = fma(-LU[i * N + k], x[k], x[i]);
 #pragma unroll
     for (int i = N - 1; i >= 0; --i) {
-      R v = B[i * M + c];
 #pragma unroll
-      for (int k = i + 1; k < N; ++k) v = fma(-LU[i * N + k], B[k * M + c], v);
-      B[i * M + c] = v * LU[i * N + i];
+      for (int k = i + 1; k < N; ++k) x[i] = fma(-LU[i * N + k], x[k], x[i]);
+      x[i] *= LU[i * N + i];
     }
+#pragma unroll
+    for (int i = 0; i < N; ++i) B[i * M + c] = x[i];
   }
   __syncwarp();
 }
@@ -461,20 +464,21 @@ PTC_D void w_lu_solve(const R* LU, const int* piv, R* B) {
 template <int N, int M, typename R>
 PTC_D void w_lu_solve_t(const R* LU, const int* piv, R* B) {
   for (int c = lane_id(); c < M; c += 32) {
+    R x[N];  // the lane's column in registers (as w_lu_solve)
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = B[i * M + c];
 #pragma unroll
     for (int i = 0; i < N; ++i) {  // U^T y = b (lower, reciprocal diagonal)
-      R v = B[i * M + c];
 #pragma unroll
-      for (int k = 0; k < i; ++k) v = fma(-LU[k * N + i], B[k * M + c], v);
-      B[i * M + c] = v * LU[i * N + i];
+      for (int k = 0; k < i; ++k) x[i] = fma(-LU[k * N + i], x[k], x[i]);
+      x[i] *= LU[i * N + i];
     }
 #pragma unroll
-    for (int i = N - 2; i >= 0; --i) {  // L^T z = y (upper, unit diagonal)
-      R v = B[i * M + c];
+    for (int i = N - 2; i >= 0; --i)  // L^T z = y (upper, unit diagonal)
 #pragma unroll
-      for (int k = i + 1; k < N; ++k) v = fma(-LU[k * N + i], B[k * M + c], v);
-      B[i * M + c] = v;
-    }
+      for (int k = i + 1; k < N; ++k) x[i] = fma(-LU[k * N + i], x[k], x[i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) B[i * M + c] = x[i];
 #pragma unroll
     for (int k = N - 1; k >= 0; --k) {  // undo the row interchanges
       const int p = piv[k];
