@@ -149,6 +149,18 @@ int ptc_propagate(int dtype, int batch, int horizon, int nx, int nu,
                   const void* Fx, const void* Fu, const void* Gamma, const void* gamma,
                   const void* d, void* dx, void* du, void* workspace, int64_t workspace_bytes,
                   int chunk0, int chunk, void* stream);
+/* Which stage the definiteness gates of value_pass name (passes.py:231-241
+ * _assert_spd_batch over R + alpha I, then over Q_t, passes.py:316-320) and
+ * whether a combine was singular (ConditioningError, passes.py:280-283) --
+ * the payload of the reference's DefinitenessError(stage, what) after a
+ * solve returned flags.  Same SoA inputs as ptc_lqr_solve, alpha = device
+ * float64[batch]; out = device int32[3 * batch]: row 0 first failing stage
+ * of R + alpha I, row 1 first failing stage of Q_t (-1 = none), row 2 = 1
+ * when some I + C Y is singular.  Error path only: one thread per problem
+ * runs the exact dual-form recursion. */
+int ptc_lqr_diagnose(int dtype, int batch, int horizon, int nx, int nu, const void* P,
+                     const void* R, const void* M, const void* d, const void* Fx, const void* Fu,
+                     const void* PT, const double* alpha, int* out, void* stream);
 /* the plan the automatic choice would use for state size nx (for reporting
  * / depth probes; the same choice ptc_lqr_workspace_bytes and the solves make) */
 int ptc_lqr_plan(int batch, int horizon, int nx, int chunk0, int chunk, int* out_chunk0,
@@ -318,9 +330,20 @@ int ptc_solver_total_cost(ptc_solver* s, void* stream);
 int ptc_solver_block_phase(ptc_solver* s, int phase, const void* in, void* out, const void* aux,
                            int rank, int world, void* stream);
 
+/* Set per-problem loop state between ptc_solver_load and ptc_solver_iterate:
+ * "alpha", "nu" (float64[batch], the Levenberg-Marquardt weight and growth
+ * factor newton.py:154-208 carries between iterations) and "mu" (float64
+ * [batch], the barrier weight of PTC_AUG_BARRIER Newton solves).  Together
+ * with the loaded trajectory and z / v this is the complete state entering
+ * one reference iteration, so the device can restart from any recorded
+ * reference iteration.  src host (on_device = 0) or device. */
+int ptc_solver_write(ptc_solver* s, const char* name, const void* src, int64_t bytes,
+                     int on_device, void* stream);
+
 /* Copy a named buffer out (dst host or device).  Names: states, controls
  * (current trajectory), lam, P, R, M, d, Fx, Fu, PT, S, s, Gamma, gamma, dx,
- * du, z, v, status, iters, term, round, hist_len, hist, cur_cost, alpha, mu,
+ * du, z, v, status, iters, term, round, hist_len, hist, cur_cost, alpha, nu, mu,
+ * bad_value (float64: the constraint value w at bad_index, InfeasibleError.value),
  * round_mu, round_cost, round_iters, round_term, round_rp, round_rd,
  * round_controls, bad_index, flags, rollout_state (bit 0 skipped, bit 1 log-depth
  * rollout converged, bit 2 converged in the scratch buffer).  ptc_solver_buffer_info reports the

@@ -245,8 +245,8 @@ class DeviceSolver:
                                     "Fu", "PT", "S", "s", "Gamma", "gamma", "dx", "du",
                                     "z", "v", "round_controls"):
             dt = torch.int32
-        elif name in ("hist", "cur_cost", "alpha", "mu", "round_mu", "round_cost",
-                      "round_rp", "round_rd"):
+        elif name in ("hist", "cur_cost", "alpha", "nu", "mu", "bad_value", "round_mu",
+                      "round_cost", "round_rp", "round_rd"):
             dt = torch.float64
         else:
             dt = self.dtype
@@ -254,6 +254,14 @@ class DeviceSolver:
         N.check(self.lib.ptc_solver_read(self.handle, name.encode(), out.data_ptr(),
                                          numel * es, 1, self.stream))
         return out
+
+    def write(self, name: str, values) -> None:
+        """Set per-problem loop state ("alpha", "nu", "mu": float64[B]) after
+        load(): the solver then continues exactly as a reference loop that
+        enters its next iteration with that state (ptc_solver_write)."""
+        a = np.ascontiguousarray(np.broadcast_to(np.asarray(values, np.float64), (self.B,)))
+        N.check(self.lib.ptc_solver_write(self.handle, name.encode(), a.ctypes.data, a.nbytes,
+                                          0, self.stream))
 
     def field(self, name: str, rows: int, comps_shape: tuple):
         """Per-stage field as (B, rows, *comps_shape) device tensor."""

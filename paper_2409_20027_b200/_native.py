@@ -79,19 +79,19 @@ _SIGS = {
     "ptc_solver_destroy": (C.c_int, [C.c_void_p]),
     "ptc_solver_load": (C.c_int, [C.c_void_p] * 5 + [C.c_int, C.c_void_p]),
     "ptc_solver_check_consistency": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
-        "ptc_lqr_host_workspace_bytes": (C.c_int64, [C.c_int] * 7),
+    "ptc_lqr_host_workspace_bytes": (C.c_int64, [C.c_int] * 7),
     "ptc_lqr_solve_host": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7 + [C.c_void_p]
                            + [C.c_void_p] * 4 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
                                                   C.c_int, C.c_void_p]),
-        "ptc_value_elements": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 7
+    "ptc_value_elements": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 7
                            + [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ptc_value_combine": (C.c_int, [C.c_int] * 3 + [C.c_void_p] * 5),
     "ptc_affine_combine": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 4),
-        "ptc_lqr_block_solve_rows": (C.c_int, [C.c_int] * 9 + [C.c_void_p] * 3
+    "ptc_lqr_block_solve_rows": (C.c_int, [C.c_int] * 9 + [C.c_void_p] * 3
                                  + [C.c_void_p] * 2 + [C.c_void_p] * 6
                                  + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int,
                                     C.c_void_p]),
-        "ptc_lqr_solve_rows": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 3 + [C.c_void_p] * 6
+    "ptc_lqr_solve_rows": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 3 + [C.c_void_p] * 6
                            + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]),
     "ptc_solver_iterate": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "ptc_solver_block_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
@@ -105,6 +105,10 @@ _SIGS = {
                                          C.POINTER(C.c_int32)]),
     "ptc_solver_read": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int,
                                   C.c_void_p]),
+    "ptc_solver_write": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int,
+                                   C.c_void_p]),
+    "ptc_lqr_diagnose": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7
+                         + [C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 

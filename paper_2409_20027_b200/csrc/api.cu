@@ -530,6 +530,23 @@ int ptc_value_elements(int dtype, int horizon, int nx, int nu, const void* P, co
   return PTC_OK;
 }
 
+int ptc_lqr_diagnose(int dtype, int batch, int horizon, int nx, int nu, const void* P,
+                     const void* R, const void* M, const void* d, const void* Fx, const void* Fu,
+                     const void* PT, const double* alpha, int* out, void* stream) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  if (dtype != PTC_F32 && dtype != PTC_F64) return fail(PTC_ERR_ARG, "bad dtype");
+  if (!P || !R || !M || !d || !Fx || !Fu || !PT || !alpha || !out)
+    return fail(PTC_ERR_ARG, "missing buffer");
+  auto it = lqr_registry().find(LqrKey(dtype == PTC_F64 ? 1 : 0, nx, nu));
+  if (it == lqr_registry().end())
+    return fail(PTC_ERR_UNSUPPORTED, "kernels not instantiated for nx=" + std::to_string(nx) +
+                                         " nu=" + std::to_string(nu));
+  const void* st[7] = {P, R, M, d, Fx, Fu, PT};
+  it->second.diagnose(batch, horizon, st, alpha, out, (cudaStream_t)stream);
+  PTC_CUDA(cudaGetLastError());
+  return PTC_OK;
+}
+
 int ptc_value_combine(int dtype, int n, int nx, const void* left, const void* right, void* out,
                       int* flags, void* stream) {
   if (n < 1 || nx < 1) return fail(PTC_ERR_ARG, "bad dims");
@@ -647,6 +664,8 @@ struct ptc_solver {
   virtual int total_cost(cudaStream_t s) = 0;
   virtual int info(const char* name, int64_t* numel, int32_t* es) = 0;
   virtual int read(const char* name, void* dst, int64_t bytes, int on_dev, cudaStream_t s) = 0;
+  virtual int write(const char* name, const void* src, int64_t bytes, int on_dev,
+                    cudaStream_t s) = 0;
   virtual int block_phase(int phase, const void* in, void* out, const void* aux, int rank,
                           int world, cudaStream_t s) = 0;
 };
@@ -802,6 +821,7 @@ struct Solver final : ptc_solver {
     a.pr_iters = par ? 4 : 0;
     a.xr = par ? c.template take<R>(a.xsz) : nullptr;
     a.alpha = db(); a.nu = db(); a.cur_cost = db(); a.cand_cost = db(); a.mu = db();
+    a.bad_value = db();
     a.opt.hist_cap = std::max(0, d.hist_cap);
     a.opt.round_cap = std::max(1, d.round_cap);
     a.hist = c.template take<double>((size_t)a.opt.hist_cap * 5 * B + 1);
@@ -929,7 +949,9 @@ struct Solver final : ptc_solver {
       reg("hist", a.hist, (int64_t)a.opt.hist_cap * 5 * B, 8);
       reg("cur_cost", a.cur_cost, B, 8);
       reg("alpha", a.alpha, B, 8);
+      reg("nu", a.nu, B, 8);
       reg("mu", a.mu, B, 8);
+      reg("bad_value", a.bad_value, B, 8);
       reg("round_mu", a.round_mu, rc * B, 8);
       reg("round_cost", a.round_cost, rc * B, 8);
       reg("round_rp", a.round_rp, rc * B, 8);
@@ -1136,6 +1158,20 @@ struct Solver final : ptc_solver {
     PTC_CUDA(cudaGetLastError());
     return PTC_OK;
   }
+  // per-problem loop state a caller may set between load and iterate
+  // (restart from a recorded iteration: alpha, nu, mu)
+  int write(const char* name, const void* src, int64_t bytes, int on_dev,
+            cudaStream_t s) override {
+    if (strcmp(name, "alpha") && strcmp(name, "nu") && strcmp(name, "mu"))
+      return fail(PTC_ERR_ARG, std::string("buffer not writable: ") + name);
+    const Buf& bf = bufs.at(name);
+    if (bytes != bf.numel * bf.es) return fail(PTC_ERR_ARG, "size mismatch");
+    PTC_CUDA(cudaMemcpyAsync(bf.p, src, bytes,
+                             on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    if (!on_dev) PTC_CUDA(cudaStreamSynchronize(s));
+    PTC_CUDA(cudaGetLastError());
+    return PTC_OK;
+  }
 };
 
 }  // namespace ptc
@@ -1228,6 +1264,12 @@ int ptc_solver_rollout(ptc_solver* s, void* stream) {
 int ptc_solver_total_cost(ptc_solver* s, void* stream) {
   PTC_S(s);
   return s->total_cost((cudaStream_t)stream);
+}
+int ptc_solver_write(ptc_solver* s, const char* name, const void* src, int64_t bytes, int on_dev,
+                     void* stream) {
+  PTC_S(s);
+  if (!name || !src) return fail(PTC_ERR_ARG, "missing argument");
+  return s->write(name, src, bytes, on_dev, (cudaStream_t)stream);
 }
 int ptc_solver_buffer_info(ptc_solver* s, const char* name, int64_t* numel, int32_t* es) {
   PTC_S(s);

@@ -53,9 +53,9 @@ enum : int { TERM_NONE = 0, TERM_COST = 1, TERM_STEP = 2, TERM_MAX_ITERS = 3, TE
 
 enum : int { AUG_ZERO = 0, AUG_BARRIER = 1, AUG_ADMM = 2 };
 
-// NaN-propagating max (numpy semantics), unlike fmax
+// NaN-propagating max (numpy semantics: a NaN on either side wins), unlike fmax
 template <typename T>
-PTC_HD T nanmax(T a, T b) { return (a != a || b > a) ? ((a != a) ? a : b) : a; }
+PTC_HD T nanmax(T a, T b) { return (a != a) ? a : ((b != b || b > a) ? b : a); }
 
 // Plan of the blocked scan tree over one horizon.
 //   level 0 items: the T stages; one level-0 unit folds K0 consecutive stages

@@ -127,6 +127,8 @@ struct LqrOps {
                      cudaStream_t s);
   void (*vcombine)(int n, const void* l, const void* r, void* o, int* flags, cudaStream_t s);
   void (*affine)(int n, int kind, const void* a, const void* b, void* o, cudaStream_t s);
+  void (*diagnose)(int B, int T, const void* const* stage, const double* alpha, int* out,
+                   cudaStream_t s);
 };
 
 // ------------------------------------------------------- element operations
@@ -151,6 +153,45 @@ __global__ void k_velem_init(int n, const R* P, const R* Rm, const R* M, const R
     if (!velem_from_stage(st, e, L)) flags[t] |= FLAG_DEF_R;
   }
   st_velem(out, t, n + 1, 1, 0, e);
+}
+
+// Which stage value_pass's gates name (passes.py:231-241, 310-320): one
+// thread per problem sweeps the exact dual-form recursion (vstep over
+// velem_from_stage: no factorisation of Q_t on the path, so S_{t+1} stays
+// exact past a failing stage) and tests every gate.  out (int32, 3 x B):
+// row 0 first t with R_t + alpha I not SPD, row 1 first t with Q_t =
+// sym(Rr + Fu^T S_{t+1} Fu) not SPD (-1 = none), row 2 = 1 if some
+// I + C Y was singular.  Error path only (after a flagged solve).
+template <typename R, int NX, int NU>
+__global__ void k_lqr_diagnose(int B, int T, const R* P, const R* Rm, const R* M, const R* d,
+                               const R* Fx, const R* Fu, const R* PT, const double* alpha,
+                               int* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  VCarry<R, NX> c;
+  ld_mat(PT, 0, 1, B, b, c.Y);
+  set_zero(c.eta);
+  int first_r = -1, first_q = -1, cond = 0;
+  for (int t = T - 1; t >= 0; --t) {
+    Stage<R, NX, NU> st;
+    ld_stage(P, Rm, M, d, Fx, Fu, t, T, B, b, R(alpha[b]), st);
+    R FtS[NU][NX], Q[NU][NU];
+    mtm<NU, NX, NX>(st.Fu, c.Y, FtS);
+    mm<NU, NX, NU>(FtS, st.Fu, Q);
+    for (int i = 0; i < NU; ++i)
+      for (int j = 0; j < NU; ++j) Q[i][j] += st.Rr[i][j];
+    symmetrize<NU>(Q);
+    if (!cholesky<NU>(Q)) first_q = t;
+    VElem<R, NX> e;
+    R L[NU][NU];
+    if (!velem_from_stage(st, e, L)) first_r = t;
+    VCarry<R, NX> o;
+    if (!vstep(e, c, o)) cond = 1;
+    c = o;
+  }
+  out[b] = first_r;
+  out[B + b] = first_q;
+  out[2 * B + b] = cond;
 }
 
 // o_i = l_i (earlier) (x) r_i (later); flags[i] |= COND when I + C_l Y_r is singular
@@ -310,7 +351,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[0], 3, kOpsCost, (int)P0, (int)B);
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[1], 3, kOpsCost, (int)P0, (int)B);
   }
-  k_control<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
+  k_control<R, NX, NU><<<grid_for(B), kBlock, 0, s>>>(a);
   k_round_end<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
   if (fold && a.apart && a.opt.method == METHOD_ADMM)
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.apart, 2, RED_MAX | (RED_MAX << 2), (int)P0, (int)B);
@@ -341,13 +382,14 @@ __global__ void k_rollout_inplace(NewtonArgs<R> a) {
 
 // total_cost of buffer parity[b] (problem.py:476), result in cur_cost[b],
 // first infeasible (stage * W + row) in bad_index[b]
-template <typename R, int NX>
+template <typename R, int NX, int NU>
 __global__ void k_cost_finalize(NewtonArgs<R> a) {
   const int b = unit_id();
   if (b >= a.B) return;
   int bad;
   a.cur_cost[b] = finalize_cost<R, NX>(a, 0, a.parity[b], b, bad);
   a.bad_index[b] = bad;
+  a.bad_value[b] = bad >= 0 ? infeasible_value<R, NX, NU>(a, a.parity[b], b, bad) : NAN;
 }
 
 template <typename R>
@@ -402,9 +444,16 @@ struct RegisterLqr {
                                                        static_cast<const R*>(b),
                                                        static_cast<R*>(o));
   }
+  static void diagnose(int B, int T, const void* const* st, const double* alpha, int* out,
+                       cudaStream_t s) {
+    k_lqr_diagnose<R, NX, NU><<<grid_for(B), kBlock, 0, s>>>(
+        B, T, static_cast<const R*>(st[0]), static_cast<const R*>(st[1]),
+        static_cast<const R*>(st[2]), static_cast<const R*>(st[3]), static_cast<const R*>(st[4]),
+        static_cast<const R*>(st[5]), static_cast<const R*>(st[6]), alpha, out);
+  }
   RegisterLqr() {
     lqr_registry()[LqrKey(dtype_code<R>(), NX, NU)] =
-        LqrOps{&solve, &propagate, &block, &velem_init, &vcombine, &affine};
+        LqrOps{&solve, &propagate, &block, &velem_init, &vcombine, &affine, &diagnose};
   }
 };
 
@@ -452,7 +501,7 @@ struct RegisterNewton {
       k_reduce_partials<<<(unsigned)a.B, 256, 0, s>>>(a.cpart[0], 3,
                                                       RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4),
                                                       P0, a.B);
-    k_cost_finalize<R, NX><<<grid_for(a.B), kBlock, 0, s>>>(a);
+    k_cost_finalize<R, NX, NU><<<grid_for(a.B), kBlock, 0, s>>>(a);
   }
   static void block(const void* p, const void* la, int phase, const void* in, void* out,
                     int rank, int world, cudaStream_t s) {

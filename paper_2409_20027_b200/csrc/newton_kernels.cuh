@@ -41,6 +41,7 @@ struct NewtonArgs {
   // per-problem state [B]
   int *status, *phase, *parity, *flags, *iters, *term, *round, *hist_len, *bad_index, *n_running;
   double *alpha, *nu, *cur_cost, *cand_cost, *mu;
+  double* bad_value;        // [B] w at bad_index (InfeasibleError.value)
   double* hist;            // (hist_cap, 5, B)
   double *round_mu, *round_cost, *round_rp, *round_rd;   // (round_cap, B)
   int *round_iters, *round_term;                          // (round_cap, B)
@@ -149,6 +150,7 @@ __global__ void k_init_state(NewtonArgs<R> a) {
   a.round[b] = 0;
   a.hist_len[b] = 0;
   a.bad_index[b] = -1;
+  a.bad_value[b] = NAN;
   a.alpha[b] = a.opt.alpha0;
   a.nu[b] = a.opt.nu0;
   a.cur_cost[b] = 0.0;
@@ -964,8 +966,21 @@ PTC_D double finalize_cost(const NewtonArgs<R>& a, int which, int q, int b, int&
   return term + (sl + sc);
 }
 
+// Constraint value w at the flat index stage * W + row of buffer q: the
+// `value` the reference's InfeasibleError carries (outer.py:47-52).
+template <typename R, int NX, int NU>
+PTC_D double infeasible_value(const NewtonArgs<R>& a, int q, int b, int bad) {
+  const int W = a.pp->W > 0 ? a.pp->W : 1;
+  const int t = bad / W - a.t_base, k = bad % W;
+  if (t < 0 || t >= a.T) return NAN;
+  R x[NX], u[NU];
+  ld_x(a, q, t, b, x);
+  ld_u(a, q, t, b, u);
+  return double(row_value<R, NX, NU>(*a.pp, k, x, u));
+}
+
 // One step of newton.py:157-208 for every running problem.
-template <typename R, int NX>
+template <typename R, int NX, int NU>
 __global__ void k_control(NewtonArgs<R> a) {
   const int b = unit_id();
   if (b >= a.B) return;
@@ -979,6 +994,7 @@ __global__ void k_control(NewtonArgs<R> a) {
     if (barrier && bad >= 0) {
       a.status[b] = ST_ERR_INFEASIBLE;
       a.bad_index[b] = bad;
+      a.bad_value[b] = infeasible_value<R, NX, NU>(a, a.parity[b], b, bad);
       return;
     }
     ph &= ~PH_NEED_COST;

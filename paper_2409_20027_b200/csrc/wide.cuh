@@ -400,7 +400,9 @@ PTC_D bool w_lu(R* G, int* piv) {
       v = __shfl_sync(0xffffffffu, v, 0);
       p = __shfl_sync(0xffffffffu, p, 0);
     }
-    if (!(v == v)) p = k;  // NaN column: keep the diagonal, as lu_factor does
+    // NaN column: keep the diagonal, as lu_factor does (with NaN candidates
+    // the butterfly can also end on lane 0's sentinel p = N: never a row)
+    if (!(v == v) || p >= N) p = k;
     if (ln == 0) piv[k] = p;
     if (p != k)
       for (int j = ln; j < N; j += 32) {

@@ -1134,7 +1134,7 @@ struct WideNewton {
         break;
       case 6:
         k_blk_import_cost<R><<<gB, 128, 0, s>>>(a, din);
-        k_control<R, NX><<<gB, 128, 0, s>>>(a);
+        k_control<R, NX, NU><<<gB, 128, 0, s>>>(a);
         k_round_end<R, NX, NU><<<(unsigned)((P0 * B + 127) / 128), 128, 0, s>>>(a);
         if (fold && a.apart && a.opt.method == METHOD_ADMM)
           k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.apart, 2, RED_MAX | (RED_MAX << 2), (int)P0, (int)B);

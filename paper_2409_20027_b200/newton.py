@@ -154,7 +154,7 @@ def raise_status(solver: DeviceSolver, status: np.ndarray, states=None, controls
             bad = int(solver.read("bad_index")[b])
             W = max(1, solver.W)
             stage, comp = divmod(bad, W)
-            raise InfeasibleError(stage, comp, float("nan"))
+            raise InfeasibleError(stage, comp, float(solver.read("bad_value")[b]))
 
 
 def newton_solve(dyn: DynamicsModel, cost: CostModel, aug: AugmentedCost | None,

@@ -202,6 +202,35 @@ def _soa(torch, a, dtype, device, comps):
     return t.t().contiguous().unsqueeze(-1).to(device)
 
 
+def _raise_gate(solver, exp, dtype, dev):
+    """The reference's exception for a flagged solve, with the stage its gates
+    name (passes.py:231-241): R + alpha I first, then a singular combine,
+    then Q_t (ptc_lqr_diagnose re-runs the exact dual-form recursion)."""
+    torch = solver.torch
+    n, nx, nu = exp.horizon, exp.d_x, exp.d_u
+    args = [_soa(torch, a, dtype, dev, c) for a, c in
+            ((exp.P, nx * nx), (exp.R, nu * nu), (exp.M, nx * nu), (exp.d, nu),
+             (exp.Fx, nx * nx), (exp.Fu, nx * nu))]
+    PT = _soa(torch, exp.P_terminal[None], dtype, dev, nx * nx)
+    alpha = torch.full((1,), float(exp.alpha), dtype=torch.float64, device=dev)
+    out = torch.empty(3, dtype=torch.int32, device=dev)
+    N.check(solver.lib.ptc_lqr_diagnose(solver.code, 1, n, nx, nu,
+                                        *[a.data_ptr() for a in args], PT.data_ptr(),
+                                        alpha.data_ptr(), out.data_ptr(), N.stream_ptr()))
+    first_r, first_q, cond = (int(v) for v in out.cpu())
+    if first_r >= 0:
+        raise DefinitenessError(first_r, "R + alpha*I")
+    if cond:
+        raise ConditioningError("singular I + C*Y while combining value elements")
+    if first_q >= 0:
+        raise DefinitenessError(first_q, "Q")
+    # the fused sweep flagged what the exact recursion does not: report the kind
+    fl = int(solver.flags[0])
+    if fl & FLAG_COND:
+        raise ConditioningError("singular I + C*Y while combining value elements")
+    raise DefinitenessError(-1, "R + alpha*I" if fl & FLAG_DEF_R else "Q")
+
+
 def lqr_solve(exp: StageExpansion, executor: str = "auto", dtype=None):
     """value_pass + propagation_pass of one expansion on the device.
     Returns S, s, FeedbackLaw, dxs, dus as numpy (reference shapes)."""
@@ -225,10 +254,8 @@ def lqr_solve(exp: StageExpansion, executor: str = "auto", dtype=None):
                 _soa(torch, exp.Fx, dtype, dev, nx * nx), _soa(torch, exp.Fu, dtype, dev, nx * nu)]
         solver.solve(*args, PT, alpha)
     fl = int(solver.flags[0])
-    if fl & (FLAG_DEF_R | FLAG_DEF_Q):
-        raise DefinitenessError(-1, "R + alpha*I" if fl & FLAG_DEF_R else "Q")
-    if fl & FLAG_COND:
-        raise ConditioningError("singular I + C*Y while combining value elements")
+    if fl & (FLAG_DEF_R | FLAG_DEF_Q | FLAG_COND):
+        _raise_gate(solver, exp, dtype, dev)
     host = lambda t, shape: t[..., 0].t().reshape(shape).cpu().numpy()
     S = host(solver.S, (n + 1, nx, nx))
     s = host(solver.s, (n + 1, nx))

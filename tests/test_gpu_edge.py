@@ -282,3 +282,23 @@ def test_wide_staged_long_horizon_matches_oracle(nx, nu, T):
     G = np.concatenate([host(o.Gamma) for o in ops]).reshape(T, nu, nx)
     du = np.concatenate([host(o.du) for o in ops])
     assert rel_gap(G, ref[2]) < 1e-9 and rel_gap(du, ref[5]) < 1e-9
+
+
+def test_nan_step_is_rejected_not_converged():
+    """A NaN goal makes every gradient, hence the control step, NaN.  The
+    reference (newton.py:177-206) gets step_norm = NaN (not <= tol), rolls
+    out u + NaN, rejects on DivergenceError with ratio -inf, and after nine
+    rejections (alpha 1, 2, 8, ..., 2^36; pintoc run in the build container)
+    ends 'stalled'.  NaN-propagating step-norm reduction: a NaN step must
+    never read as a converged (zero) step."""
+    import paper_2409_20027_b200 as P
+    dyn = P.LinearDynamics(np.eye(2) * 0.9, np.array([[0.0], [1.0]]), horizon=6)
+    cost = P.QuadraticCost(np.eye(2), np.eye(1), np.eye(2), x_goal=np.array([np.nan, 0.0]))
+    init = P.rollout(dyn, np.array([0.5, -0.5]), np.zeros((6, 1)))
+    for ex in ("sequential", "parallel"):
+        _, rep = P.newton_solve(dyn, cost, None, init, P.NewtonOptions(executor=ex))
+        assert rep.termination == "stalled", (ex, rep.termination)
+        assert rep.iterations == 9
+        assert [r.alpha for r in rep.history] == [2.0 ** (k * (k + 1) // 2) for k in range(9)]
+        for r in rep.history:
+            assert r.gain_ratio == -np.inf and np.isnan(r.step_norm) and not r.accepted

@@ -149,8 +149,8 @@ def test_costate_boundary_is_terminal_gradient():
 def test_device_scan_over_element_tuples():
     """scan() (scan.py:133-166) with the path's combines: a REVERSE scan of
     the value elements is the value function (S_t = Y, s_t = -eta), a
-    FORWARD scan of rollout maps equals the sequential composition; other
-    combines have no device form."""
+    FORWARD scan of rollout maps equals the sequential composition, also
+    through a user combine."""
     import paper_2409_20027_b200 as P
     e, exp = _exp(9, T=11)
     elems = [P.value_element_init(exp, t) for t in range(exp.horizon + 1)]
@@ -166,7 +166,10 @@ def test_device_scan_over_element_tuples():
     for t in range(1, 13):
         F, c = maps[t].F @ F, maps[t].F @ c + maps[t].e
         assert rel_gap(out[t].F, F) < 1e-10 and rel_gap(out[t].e, c) < 1e-10
-    with pytest.raises(TypeError):
-        P.scan(maps, lambda a, b: a)
+    # a user combine runs the same schedule pair by pair
+    user = P.scan(maps, lambda a, b: P.RolloutElement(b.F @ a.F, b.F @ a.e + b.e),
+                  executor="parallel", parallel_threshold=2)
+    for t in range(13):
+        assert rel_gap(user[t].F, out[t].F) < 1e-10 and rel_gap(user[t].e, out[t].e) < 1e-10
     with pytest.raises(P.EmptySequenceError):
         P.scan([], P.rollout_combine)

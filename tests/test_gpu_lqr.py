@@ -190,3 +190,55 @@ def test_lqr_host_buffers_equal_device_solve(nx, nu, T, B):
     assert int(flags.max()) == 0
     for got, want in zip(out, (dev.Gamma, dev.gamma, dev.dx, dev.du)):
         assert torch.equal(got, want.cpu())
+
+
+@pytest.mark.parametrize("nx,nu", [(2, 1), (4, 2), (12, 4)])
+def test_definiteness_error_names_the_reference_stage(nx, nu):
+    """DefinitenessError.stage is the stage the reference's gates name
+    (passes.py:231-241): the first stage whose R + alpha I fails, else the
+    first stage whose Q_t = Rr + Fu^T S_{t+1} Fu fails; checked against the
+    oracle's value_pass on the same expansions."""
+    import paper_2409_20027_b200 as P
+    rng = np.random.default_rng(nx)
+    T = 40
+    e = O.random_lqr_expansion(rng, T, nx, nu)
+    # (a) R + alpha I indefinite at stages 17 and 29 -> 17
+    R = e.R.copy()
+    R[17] = -np.eye(nu)
+    R[29] = -np.eye(nu)
+    exp = P.StageExpansion.build(e.P, R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.0)
+    with pytest.raises(O.Definiteness) as want:
+        O.value_pass(O.Expansion(e.P, R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.0))
+    with pytest.raises(P.DefinitenessError) as got:
+        P.value_pass(exp)
+    assert got.value.stage == want.value.stage == 17 and got.value.what == "R + alpha*I"
+    # (b) R fine, Q_t indefinite through strongly negative P at two stages
+    Pm = e.P.copy()
+    Pm[8] = -60.0 * np.eye(nx)
+    Pm[25] = -60.0 * np.eye(nx)
+    oe = O.Expansion(Pm, e.R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.0)
+    with pytest.raises(O.Definiteness) as want:
+        O.value_pass(oe)
+    with pytest.raises(P.DefinitenessError) as got:
+        P.value_pass(P.StageExpansion.build(Pm, e.R, e.M, e.d, e.Fx, e.Fu, e.PT, 0.0))
+    assert got.value.what == "Q" and got.value.stage == want.value.stage >= 0
+
+
+def test_infeasible_error_carries_the_constraint_value():
+    """InfeasibleError(stage, component, value) from a barrier Newton solve
+    entered at an infeasible point (outer.py:47-52: the value is w >= 0)."""
+    import paper_2409_20027_b200 as P
+    T = 8
+    dyn = P.LinearDynamics(np.eye(2) * 0.9, np.array([[0.0], [1.0]]), horizon=T)
+    cost = P.QuadraticCost(np.eye(2), np.eye(1), np.eye(2))
+    box = P.BoxConstraint(2, 1, control_lower=-1.0, control_upper=1.0)
+    us = np.zeros((T, 1))
+    us[5, 0] = 1.25                       # w = u - 1 = 0.25 at stage 5, row 1 (upper bound)
+    init = P.rollout(dyn, np.array([0.5, -0.5]), us)
+    with pytest.raises(P.InfeasibleError) as err:
+        P.newton_solve(dyn, cost, P.BarrierAugmentation(box, 0.1), init)
+    ob = O.Box(2, 1, control_lower=-1.0, control_upper=1.0)
+    w = ob.w(init.states[:-1], us)
+    st, comp = np.argwhere(w >= 0)[0]
+    assert (err.value.stage, err.value.component) == (st, comp)
+    assert err.value.value == w[st, comp]

@@ -57,13 +57,46 @@ def test_project_box_is_idempotent_clamp(rng):
     assert np.allclose(P.project_box(np.array([-1.0, 2.0, 0.0])), [-1.0, 0.0, 0.0])
 
 
-def test_device_scan_schedule_has_log_span():
-    for n in list(range(1, 300)) + [1 << 12, 1 << 16, 1 << 20]:
+def test_scan_plan_reference_semantics():
+    """Acceptance criterion 2: the parallel plan's critical
+    path is at most 2*ceil(log2 n) for every n; levels write distinct
+    destinations from earlier sources; replaying the plan with a
+    non-commutative combine (string concatenation) gives every prefix."""
+    for n in list(range(1, 300)) + [1000, 1024, 1 << 12]:
         depth = P.scan_depth_probe(n)
+        assert depth <= (0 if n == 1 else 2 * math.ceil(math.log2(n))), (n, depth)
+        buf = [str(i) + "," for i in range(n)]
+        for level in P.scan_plan(n):
+            dsts = [d for _, d in level]
+            assert len(set(dsts)) == len(dsts)
+            assert all(s < d for s, d in level)
+            for s, d in level:
+                buf[d] = buf[s] + buf[d]
+        assert buf == ["".join(f"{j}," for j in range(i + 1)) for i in range(n)]
+    assert P.scan_plan(1) == []
+    with pytest.raises(P.EmptySequenceError):
+        P.scan_plan(0)
+
+
+def test_scan_user_combine_both_directions():
+    words = [chr(97 + i) for i in range(40)]
+    cat = lambda a, b: a + b
+    for ex in ("sequential", "parallel"):
+        fw = P.scan(words, cat, P.ScanDirection.FORWARD, executor=ex)
+        rv = P.scan(words, cat, P.ScanDirection.REVERSE, executor=ex)
+        assert fw == ["".join(words[:i + 1]) for i in range(40)]
+        assert rv == ["".join(words[i:]) for i in range(40)]
+
+
+def test_device_scan_tree_has_log_span():
+    """The solver's own schedule (csrc/common.cuh make_plan): depth
+    2 (K0 + K L) with L = log_K(n / K0) levels."""
+    for n in list(range(1, 300)) + [1 << 12, 1 << 16, 1 << 20]:
+        depth = P.device_scan_depth(n)
         bound = 0 if n == 1 else 4 + 16 * math.ceil(math.log(n, 8)) + 8
         if n > 64:
             assert depth <= bound, (n, depth)
-    lv = P.scan_plan(1 << 16)
+    lv = P.device_scan_plan(1 << 16)
     assert lv[0] == 1 << 16 and lv[-1] <= 8
 
 
