@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "batched LQR-scan solves/sec"
 UNIT = "solves/s"
-B_TOTAL = 65536
+B_TOTAL = 65536      # config 3's batch: the per-GPU unit of the weak-scaling run
 T = 256
 ALPHA = 1.0          # NewtonOptions.alpha0: the regularisation of a first iteration
 
@@ -178,7 +178,7 @@ def run_reference(args) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{2 * per_half} problems per step (half pendulum, half "
@@ -190,13 +190,61 @@ def run_reference(args) -> None:
 
 
 def workload_config(n: int) -> dict:
-    return {"workload": "config 3: 65,536 independent LQR subproblems (32,768 pendulum nx=2 "
-                        "nu=1 + 32,768 cart-pole nx=4 nu=1), T=256, Newton expansions at "
-                        "seeded config-3 trajectories",
+    return {"workload": "config 3: 65,536 independent LQR subproblems per GPU (32,768 pendulum "
+                        "nx=2 nu=1 + 32,768 cart-pole nx=4 nu=1), T=256, Newton expansions at "
+                        "seeded config-3 trajectories (rank-seeded)",
             "alpha": "per problem, first solvable value of the reference LM escalation "
                      "1, 2, 8, 64, ... (newton.py:166-176)",
-            "global_batch": B_TOTAL, "horizon": T, "parallelism": f"problem-sharded x{n}",
+            "per_gpu_batch": B_TOTAL, "global_batch": B_TOTAL * n, "horizon": T,
+            "parallelism": f"problem-sharded x{n}, no data-path collective",
             "l2": "inputs > L2 (no flush needed)"}
+
+
+def launch_ranks(args) -> None:
+    """`--gpus N`: one process per GPU.  Without torchrun (no WORLD_SIZE) and
+    N > 1 this re-executes the script under torch.distributed.run; under
+    torchrun the world must be N and every rank must have its GPU."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None:
+        if args.gpus > 1:
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                   f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            os.execv(sys.executable, cmd)
+        return
+    if int(env_world) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={env_world} but --gpus {args.gpus}")
+
+
+def sum_over_ranks(value: float, world: int, device="cuda") -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return type(value)(float(t))
+
+
+def require_gpus(torch, world: int, local: int) -> None:
+    have = torch.cuda.device_count()
+    if have < world or local >= have:
+        sys.exit(f"bench.py: {world} ranks need {world} GPUs, this node has {have}")
+
+
+def max_over_ranks(value: float, world: int, device) -> float:
+    """Slowest rank's number (timing rule: max over ranks)."""
+    if world == 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t)
 
 
 # ---------------------------------------------------------------------------
@@ -330,10 +378,11 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    require_gpus(torch, world, local)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    b_local = B_TOTAL // world
+    b_local = B_TOTAL           # weak scaling: config 3's batch on every GPU
     bp, bc = half_sizes(b_local)
 
     halves = {}
@@ -389,12 +438,9 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
-    ms = t0.elapsed_time(t1) / args.steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t)
-    value = B_TOTAL / (ms * 1e-3)
+    ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world, "cuda")
+    value = B_TOTAL * world / (ms * 1e-3)
+    strong = strong_leg(torch, P, LqrSolver, args, world, rank) if world > 1 else None
 
     # end-to-end through the C ABI with host buffers: H2D of the step's
     # expansions from pinned memory, solve, D2H of gains and deviations
@@ -446,10 +492,8 @@ def run_ours(args) -> None:
             e2e_step()
         b.record(stream)
         torch.cuda.synchronize()
-        e_ms = torch.tensor([a.elapsed_time(b) / n_e2e], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": B_TOTAL / (float(e_ms) * 1e-3), "unit": UNIT,
+        e_ms = max_over_ranks(a.elapsed_time(b) / n_e2e, world, "cuda")
+        e2e = {"value": B_TOTAL * world / (float(e_ms) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                "ms_per_step": float(e_ms), "sub_batches": len(subs)}
         del subs
@@ -499,12 +543,10 @@ def run_ours(args) -> None:
             step32()
         b32.record(stream)
         torch.cuda.synchronize()
-        ms32 = torch.tensor([a32.elapsed_time(b32) / args.steps], dtype=torch.float64,
-                            device="cuda")
-        if world > 1:
-            dist.all_reduce(ms32, op=dist.ReduceOp.MAX)
+        ms32 = max_over_ranks(a32.elapsed_time(b32) / args.steps, world, "cuda")
         flagged = sum(int((v[0].flags != 0).sum()) for v in h32.values())
-        fp32 = {"value": B_TOTAL / (float(ms32) * 1e-3), "unit": UNIT, "ms_per_step": float(ms32),
+        fp32 = {"value": B_TOTAL * world / (float(ms32) * 1e-3), "unit": UNIT,
+                "ms_per_step": float(ms32),
                 "dtype": "f32", "subproblems_flagged": flagged}
         del h32
 
@@ -551,9 +593,9 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": workload_config(world),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "strong_scaling": strong, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk, "ill_posed_subproblems": ill_posed,
             "lqr_latency_sweep": sweep, "newton_latency_sweep": nsweep,
             "long_horizon": longh, "config4_solve": c4solve, "config4_sharded_solve": c4shard, "single_solves": solves, "mpc_config3": mpc, "fp32": fp32,
@@ -709,7 +751,7 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
     the whole local batch (device-resident loop, host polls every 4
     iterations), Newton iterations, and problem outcomes."""
     from paper_2409_20027_b200 import BatchSolver
-    b_local = B_TOTAL // world
+    b_local = B_TOTAL           # weak scaling, as the headline
     bp, bc = half_sizes(b_local)
     probs = models_pkg(P)
     box = {"pendulum": P.BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0),
@@ -753,7 +795,8 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
     warm = BatchSolver.solve_concurrently([(solvers[k],) + warm_in[k] for k in names])
     ev[3].record()
     torch.cuda.synchronize()
-    cold_ms, warm_ms = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
+    cold_ms = max_over_ranks(ev[0].elapsed_time(ev[1]), world, "cuda")
+    warm_ms = max_over_ranks(ev[2].elapsed_time(ev[3]), world, "cuda")
     for k, rc, rw in zip(names, cold, warm):
         out[k] = {"problems": solvers[k].batch, "cold": outcome(rc, cold_ms),
                   "warm": outcome(rw, warm_ms)}
@@ -763,7 +806,14 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
     out["newton_iterations_per_s_warm"] = sum(out[k]["warm"]["newton_iterations"]
                                               for k in names) / (warm_ms * 1e-3)
     del solvers, cold, warm
-    out["mpc_steps_per_s_warm"] = out["problems"] / (out["warm_ms"] * 1e-3)
+    # only problems that finished their warm solve count as MPC steps; the
+    # stalled ones (SolverStalledError in the reference too, see
+    # tests/test_gpu_restart.py) are reported separately
+    fin = sum_over_ranks(sum(out[k]["warm"]["finished"] for k in names), world)
+    out["warm_finished"] = fin
+    out["warm_stalled"] = sum_over_ranks(sum(out[k]["warm"]["stalled"] for k in names), world)
+    out["problems"] = sum_over_ranks(out["problems"], world)
+    out["mpc_steps_per_s_warm"] = fin / (out["warm_ms"] * 1e-3)
     out["config"] = ("config 3 barrier MPC: pendulum (cfg-0 model/cost) + cart-pole (cfg-2 "
                      "model/cost), control boxes, T=256, fp64, warm start shift %d" % shift)
     return out
@@ -1038,6 +1088,43 @@ def config4_solve_leg(torch, P, logT: int = 20, damp: float = 0.9999):
                     "per-round controls and the reports of the reference-shaped API"}
 
 
+def strong_leg(torch, P, LqrSolver, args, world: int, rank: int) -> dict:
+    """The same metric with config 3's 65,536 problems split over the ranks
+    (strong scaling, B_TOTAL / world per GPU), max over ranks."""
+    bp, bc = half_sizes(B_TOTAL // world)
+    halves = []
+    for system, n in (("pendulum", bp), ("cartpole", bc)):
+        inputs, nx, nu = build_inputs(P, torch, system, n, rank)
+        solver = LqrSolver(n, T, nx, nu, dtype=torch.float64)
+        halves.append((solver, inputs, lm_alpha_device(torch, solver, inputs, n)))
+    stream = torch.cuda.current_stream()
+    side = [torch.cuda.Stream() for _ in halves]
+
+    def step():
+        for st in side:
+            st.wait_stream(stream)
+        for (solver, inputs, alpha), st in zip(halves, side):
+            with torch.cuda.stream(st):
+                solver.solve(*inputs, alpha, stream=st)
+        for st in side:
+            stream.wait_stream(st)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    import torch.distributed as dist
+    dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / args.steps, world, "cuda")
+    return {"value": B_TOTAL / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "per_gpu_batch": B_TOTAL // world, "global_batch": B_TOTAL}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1054,6 +1141,9 @@ def main() -> None:
     ap.add_argument("--no-c4solve", action="store_true")
     ap.add_argument("--no-solves", action="store_true")
     args = ap.parse_args()
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    launch_ranks(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -30,6 +30,8 @@ def test_benchmark_rows_converge_and_respect_bounds(tmp_path):
     assert back == recs
     paths = P.emit_plotdata(recs, tmp_path / "plot")
     assert paths[0].exists()
+    assert paths[0].read_text().splitlines()[0] == (
+        "system,solver,executor,horizon,mean_wall_s,std_wall_s,runs,all_converged")
 
 
 def test_benchmark_deterministic_iteration_counts():
@@ -112,3 +114,26 @@ def test_criterion_6_admm_termination(system, rho):
     assert report.converged
     assert report.state.primal_residual <= 1e-2 and report.state.dual_residual <= 1e-2
     assert problem.constraints.max_violation(traj) <= 1e-2
+
+
+def test_mpc_log_plotdata_and_report_cost(tmp_path):
+    """emit_plotdata(MpcLog) writes the trajectory table (bench.py:403-406);
+    report_cost is the last round's augmented cost (bench.py:212-215)."""
+    import paper_2409_20027_b200 as P
+    log = P.run_mpc(P.RunConfig(system="pendulum", solver="barrier", sim_time=0.05))
+    (path,) = P.emit_plotdata(log, tmp_path)
+    lines = path.read_text().splitlines()
+    assert path.name == "mpc_trajectory.csv"
+    assert lines[0] == "t_s,theta,omega,torque,solve_s" and len(lines) == 1 + log.steps
+    assert float(lines[1].split(",")[1]) == log.states[0, 0]
+    cfg = P.RunConfig(system="pendulum", solver="barrier", horizons=(20,))
+    prob = cfg.build_problem(20, cfg.step_size(20))
+    init = P.rollout(prob.dynamics, P.swingup_start("pendulum"),
+                     P.draw_initial_controls(prob, cfg, 20, 0))
+    traj, rep = P.barrier_solve(prob, init, cfg.barrier_options())
+    assert P.report_cost(rep) == rep.rounds[-1].cost
+    assert P.validate_solution(prob, traj, cfg, rep)
+    xs = traj.states.copy()
+    xs[5, 0] += 1e-3                    # no longer a rollout of its controls
+    bad = P.Trajectory(xs, traj.controls)
+    assert not P.validate_solution(prob, bad, cfg, rep)
