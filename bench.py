@@ -557,9 +557,10 @@ def run_ours(args) -> None:
                  "fp32": lqr_latency_sweep(torch, LqrSolver, torch.float32)}
     if rank == 0 and not args.no_newton_sweep:
         nsweep = newton_latency_sweep(torch, P)
-    mpc = None
+    mpc = mpc32 = None
     if not args.no_mpc:
         mpc = mpc_leg(torch, P, world, rank)
+        mpc32 = mpc_leg(torch, P, world, rank, dtype=torch.float32)
     longh = None
     if not args.no_long:
         del halves
@@ -598,7 +599,8 @@ def run_ours(args) -> None:
             "strong_scaling": strong, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clk, "ill_posed_subproblems": ill_posed,
             "lqr_latency_sweep": sweep, "newton_latency_sweep": nsweep,
-            "long_horizon": longh, "config4_solve": c4solve, "config4_sharded_solve": c4shard, "single_solves": solves, "mpc_config3": mpc, "fp32": fp32,
+            "long_horizon": longh, "config4_solve": c4solve, "config4_sharded_solve": c4shard, "single_solves": solves, "mpc_config3": mpc,
+            "mpc_config3_fp32": mpc32, "fp32": fp32,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -737,7 +739,7 @@ def newton_latency_sweep(torch, P):
     return res
 
 
-def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
+def mpc_leg(torch, P, world: int, rank: int, shift: int = 10, dtype=None):
     """Config 3 end to end: the 65,536 problems (sharded by rank) solved by
     the device-resident barrier method (mu 1e-1 -> 1e-6, zeta 0.2, Newton
     max_iters 50 per round), then one receding-horizon MPC step: start from
@@ -774,7 +776,9 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
         u0 = torch.as_tensor(np.clip(0.1 * bound * rng.standard_normal((n, T, 1)),
                                      -0.9 * bound, 0.9 * bound)).cuda()
         prob = P.ControlProblem(probs[system].dynamics, probs[system].cost, box[system])
-        bs = BatchSolver(prob, n, "barrier", barrier=opts)
+        bs = BatchSolver(prob, n, "barrier", barrier=opts, dtype=dtype)
+        if dtype is not None:
+            u0 = u0.to(dtype)
         solvers[system] = bs
         starts[system] = (bs.rollout(x0, u0), u0)
     names = list(solvers)
@@ -814,8 +818,9 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10):
     out["warm_stalled"] = sum_over_ranks(sum(out[k]["warm"]["stalled"] for k in names), world)
     out["problems"] = sum_over_ranks(out["problems"], world)
     out["mpc_steps_per_s_warm"] = fin / (out["warm_ms"] * 1e-3)
+    prec = "fp32" if dtype is torch.float32 else "fp64"
     out["config"] = ("config 3 barrier MPC: pendulum (cfg-0 model/cost) + cart-pole (cfg-2 "
-                     "model/cost), control boxes, T=256, fp64, warm start shift %d" % shift)
+                     f"model/cost), control boxes, T=256, {prec}, warm start shift {shift}")
     return out
 
 

@@ -268,7 +268,21 @@ typedef struct ptc_problem_desc {
    * (terminal cost and gradient live here).  Iterations then run through
    * ptc_solver_block_phase.  Affine models with nx >= 8, tree plans. */
   int32_t block_mode, t_base, block_last;
+  /* user-defined model (model id from ptc_model_load): its device array of
+   * float64 data (per-stage matrices, tables ...), read by the model's code
+   * as `data`; may be NULL.  Its parameters are dyn_params (`prm`). */
+  const void* user_data;
 } ptc_problem_desc;
+
+/* Register a user-defined dynamics model (reference problem.py:59-112: a
+ * DynamicsModel subclass with f, fx, fu, fxx, fuu, fxu) compiled into its own
+ * shared library from the model's per-stage CUDA code
+ * (paper_2409_20027_b200/usermodel.py, csrc/user_model.cuh).  The library's
+ * fused Newton kernel sets (f64, f32) are registered under a fresh model id
+ * (>= PTC_DYN_USER_BASE) for use as ptc_problem_desc.model; loading the
+ * same path twice returns the same id.  nx / nu receive the model's sizes. */
+#define PTC_DYN_USER_BASE 100
+int ptc_model_load(const char* path, int* model_id, int* nx, int* nu);
 
 int64_t ptc_solver_workspace_bytes(const ptc_problem_desc* desc);
 int ptc_solver_create(const ptc_problem_desc* desc, void* workspace, int64_t workspace_bytes,

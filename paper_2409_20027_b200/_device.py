@@ -114,6 +114,11 @@ class DeviceSolver:
             d.lin_a, d.lin_b, d.lin_c = (t.data_ptr() for t in lin)
             keep.extend(lin)
             d.lin_rows, d.lin_batch = rows, 1
+        if spec.get("user_data") is not None:
+            ud = spec["user_data"]
+            d.user_data = ud.data_ptr()
+            keep.append(ud)
+            self._user_data = ud
         d.Q = dptr(cspec["Q"])
         d.R = dptr(cspec["R"])
         d.Qf = dptr(cspec["Qf"])

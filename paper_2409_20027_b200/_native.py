@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libpintoc_b200.so")
 
 PTC_F32, PTC_F64 = 0, 1
 DYN_PENDULUM, DYN_CARTPOLE, DYN_LINEAR = 0, 1, 2
+DYN_USER_BASE = 100
 AUG_ZERO, AUG_BARRIER, AUG_ADMM = 0, 1, 2
 METHOD_NEWTON, METHOD_BARRIER, METHOD_ADMM = 0, 1, 2
 ST_RUNNING, ST_DONE, ST_ERR_STALLED, ST_ERR_INFEASIBLE = 0, 1, -1, -2
@@ -52,6 +53,7 @@ class ProblemDesc(C.Structure):
         ("chunk0", C.c_int32), ("chunk", C.c_int32),
         ("rollout", C.c_int32),
         ("block_mode", C.c_int32), ("t_base", C.c_int32), ("block_last", C.c_int32),
+        ("user_data", C.c_void_p),
     ]
 
 
@@ -107,6 +109,8 @@ _SIGS = {
                                   C.c_void_p]),
     "ptc_solver_write": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int,
                                    C.c_void_p]),
+    "ptc_model_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                 C.POINTER(C.c_int)]),
     "ptc_lqr_diagnose": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7
                          + [C.c_void_p, C.c_void_p, C.c_void_p]),
 }

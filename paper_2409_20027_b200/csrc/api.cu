@@ -1,9 +1,12 @@
 // C ABI implementation (include/pintoc_b200.h): workspace carving, the
 // batched solver object and dispatch into the instantiated kernel sets.
+#include <dlfcn.h>
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -772,6 +775,7 @@ struct Solver final : ptc_solver {
     p.W = W;
     p.lin_T = std::max(1, d.lin_rows);
     p.lin_B = std::max(1, d.lin_batch);
+    p.user_data = static_cast<const double*>(d.user_data);
   }
 
   static size_t layout(const ptc_problem_desc& d, Carver& c, Solver* self) {
@@ -1265,6 +1269,32 @@ int ptc_solver_total_cost(ptc_solver* s, void* stream) {
   PTC_S(s);
   return s->total_cost((cudaStream_t)stream);
 }
+int ptc_model_load(const char* path, int* model_id, int* nx, int* nu) {
+  static std::mutex mu;
+  static std::map<std::string, int> loaded;
+  static int next_id = PTC_DYN_USER_BASE;
+  if (!path || !model_id || !nx || !nu) return fail(PTC_ERR_ARG, "missing argument");
+  std::lock_guard<std::mutex> lock(mu);
+  void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+  if (!h) return fail(PTC_ERR_ARG, std::string("dlopen failed: ") + dlerror());
+  using OpsFn = int (*)(int, int*, int*, NewtonOps*);
+  auto fn = reinterpret_cast<OpsFn>(dlsym(h, "ptc_user_model_ops"));
+  if (!fn) return fail(PTC_ERR_ARG, std::string(path) + " exports no ptc_user_model_ops");
+  auto it = loaded.find(path);
+  const int id = it != loaded.end() ? it->second : next_id++;
+  int mx = 0, mu_ = 0;
+  for (int dt : {PTC_F64, PTC_F32}) {
+    NewtonOps ops{};
+    if (fn(dt, &mx, &mu_, &ops) == 0) newton_registry()[NewtonKey(dt, id, mx, mu_)] = ops;
+  }
+  if (mx < 1) return fail(PTC_ERR_ARG, std::string(path) + " holds no kernel set");
+  loaded[path] = id;
+  *model_id = id;
+  *nx = mx;
+  *nu = mu_;
+  return PTC_OK;
+}
+
 int ptc_solver_write(ptc_solver* s, const char* name, const void* src, int64_t bytes, int on_dev,
                      void* stream) {
   PTC_S(s);

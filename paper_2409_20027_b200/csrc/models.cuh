@@ -34,6 +34,7 @@ struct ProblemParams {
                             // time-varying models shared by the batch, nx >= 8
                             // (warp kernels: one contiguous row per stage), or null
   double Q[kMaxNX * kMaxNX], Rc[kMaxNU * kMaxNU], Qf[kMaxNX * kMaxNX], goal[kMaxNX];
+  const double* user_data;  // user-defined model (user_model.cuh): its device array or null
   int W, Ws;                // stacked constraint rows, of which Ws are state rows
   int row_var[kMaxRows];    // 0 = state, 1 = control
   int row_idx[kMaxRows];

@@ -643,6 +643,8 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
   p.lin_A = gp.lin_A;
   p.lin_Bm = gp.lin_Bm;
   p.lin_c = gp.lin_c;
+  p.lin_st = gp.lin_st;
+  p.user_data = gp.user_data;
   R* Xc = a.X + c * a.xsz;
   R* Uc = a.U + c * a.usz;
   R x[NX];

@@ -118,6 +118,10 @@ def test_config2_every_outer_step():
     # stable, trajectories within max(1e-9, 10 x the reference's floor)
     floor, stable = g["step_floor"], g["step_stable"]
     within = (gaps <= np.maximum(TOL, 10 * floor)) & (iters_ok | ~stable)
+    bad = np.flatnonzero(~within)
+    print("cfg2 steps outside the floor:", [(int(k), float(gaps[k]), float(floor[k]),
+                                             int(res.iters[k]), int(g["step_iters"][k]))
+                                            for k in bad])
     print(f"cfg2 outer steps: {int(exact.sum())}/{n} identical at 1e-9 with equal counts; "
           f"{int(within.sum())}/{n} within the reference's own floor; count-stable steps "
           f"{int(stable.sum())}, max floor {np.nanmax(floor):.2e}")
@@ -191,9 +195,12 @@ def test_config3_sample_every_round(system, leg):
           f"reference (all stalled on the device); rounds identical at 1e-9 with equal counts "
           f"{int(exact.sum())}/{n_round}, within the reference's own floor "
           f"{int(within.sum())}/{n_round}")
-    bad = [jobs[i] for i in np.flatnonzero(~within) if not (jobs[i][1] == nr[jobs[i][0]] - 1
-                                                          and status[jobs[i][0]] == -1)]
-    assert not bad, bad[:10]
+    bad = [i for i in np.flatnonzero(~within) if not (jobs[i][1] == nr[jobs[i][0]] - 1
+                                                    and status[jobs[i][0]] == -1)]
+    print("rounds outside the floor:", [(jobs[i], int(res.iters[i]),
+                                         int(iters[jobs[i][0], jobs[i][1]]),
+                                         float(g[p + "floor"][jobs[i]])) for i in bad])
+    assert not bad
 
 
 @pytest.mark.parametrize("leg", ["cold", "warm"])

@@ -1,0 +1,92 @@
+"""User-defined dynamics through the device hook (usermodel.DeviceDynamics,
+csrc/user_model.cuh): the reference's user-model pattern -- a
+DynamicsModel subclass such as make_golden.py's TVLinear -- written as
+per-stage CUDA code, compiled into its own kernel library and run by the
+same solver entry points, checked against the reference's own runs."""
+
+import numpy as np
+import pytest
+from conftest import golden, rel_gap
+from restart_util import check_iterations, device_restart
+from user_models import user_pendulum, user_tvlinear
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def test_user_tvlinear_barrier_matches_reference():
+    """make_golden's TVLinear (a user DynamicsModel in pintoc) on the
+    barrier method: counts, histories and trajectories of the reference."""
+    import paper_2409_20027_b200 as P
+    from test_gpu_newton import _check_hist, _hist
+    g = golden("barrier_tvlinear")
+    dyn = user_tvlinear(g["A"], g["B"], g["c"])
+    nu = dyn.d_u
+    cost = P.QuadraticCost(g["Q"], 0.1 * np.eye(nu), g["Q"])
+    box = P.BoxConstraint(dyn.d_x, nu, control_lower=-2.0, control_upper=2.0)
+    init = P.rollout(dyn, g["x0"], g["u0"])
+    for ex in ("sequential", "parallel"):
+        traj, rep = P.barrier_solve(P.ControlProblem(dyn, cost, box), init,
+                                    P.BarrierOptions(newton=P.NewtonOptions(executor=ex)))
+        assert [r.newton.iterations for r in rep.rounds] == list(g["sol_round_iters"])
+        for k, r in enumerate(rep.rounds):
+            _check_hist(_hist(r.newton), g[f"sol_hist{k}"])
+        assert rel_gap(traj.controls, g["sol_us"]) < TOL
+        assert rel_gap(traj.states, g["sol_xs"]) < TOL
+
+
+def test_user_pendulum_converging_swingup_matches_reference():
+    import paper_2409_20027_b200 as P
+    from test_gpu_newton import _check_hist, _hist
+    g = golden("barrier_pendulum_conv")
+    builtin = P.make_swingup_problem("pendulum", 40, 0.05)
+    prm = builtin.dynamics.params
+    dyn = user_pendulum(40, prm.gravity, prm.length, prm.mass, prm.damping, prm.dt)
+    prob = P.ControlProblem(dyn, builtin.cost, builtin.constraints)
+    init = P.rollout(dyn, g["x0"], g["u0"])
+    traj, rep = P.barrier_solve(prob, init, P.BarrierOptions(newton=P.NewtonOptions(max_iters=300)))
+    assert [r.newton.iterations for r in rep.rounds] == list(g["sol_round_iters"])
+    for k, r in enumerate(rep.rounds):
+        _check_hist(_hist(r.newton), g[f"sol_hist{k}"])
+    assert rel_gap(traj.controls, g["sol_us"]) < TOL
+
+
+def test_user_pendulum_config0_every_iteration():
+    """All 600 config-0 iterations restarted from the reference's states
+    with the user-code pendulum (the same restart test as the built-in)."""
+    import paper_2409_20027_b200 as P
+    g = golden("restart_cfg0")
+    cost = P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0]))
+    box = P.BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0)
+    prob = P.ControlProblem(user_pendulum(100), cost, box)
+    tin = g["it_in"]
+    res = device_restart(prob, g["traj_x"][tin], g["traj_u"][tin], g["it_alpha"], g["it_nu"],
+                         mu=g["it_aug"])
+    out = check_iterations(res, g, label="user-pendulum cfg0")
+    assert out["rows"] == 600
+
+
+def test_user_model_batched_and_fp32():
+    """BatchSolver and the fp32 kernel set run the user model too."""
+    import torch
+
+    import paper_2409_20027_b200 as P
+    T, B = 64, 16
+    dyn = user_pendulum(T)
+    prob = P.ControlProblem(dyn, P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]),
+                                                 np.diag([100.0, 10.0])),
+                            P.BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0))
+    rng = np.random.default_rng(3)
+    x0 = np.stack([rng.uniform(-0.3, 0.3, B), rng.normal(0, 0.1, B)], 1)
+    u0 = torch.as_tensor(np.clip(rng.normal(0, 0.5, (B, T, 1)), -4, 4)).cuda()
+    opts = P.BarrierOptions(newton=P.NewtonOptions(max_iters=60))
+    bs = P.BatchSolver(prob, B, "barrier", barrier=opts)
+    res = bs.solve(bs.rollout(x0, u0), u0)
+    for b in range(3):
+        init = P.rollout(dyn, x0[b], u0[b].cpu().numpy())
+        traj, rep = P.barrier_solve(prob, init, opts)
+        assert rel_gap(res.controls[b].cpu().numpy(), traj.controls) < 1e-12
+    bs32 = P.BatchSolver(prob, B, "barrier", barrier=opts, dtype=torch.float32)
+    X32 = bs32.rollout(x0, u0.float())
+    assert torch.isfinite(X32).all()

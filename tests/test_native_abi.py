@@ -131,3 +131,23 @@ def test_solver_descriptor_validation_without_gpu():
     small = lib.ptc_solver_workspace_bytes(ctypes.byref(d))
     d.batch = 400
     assert lib.ptc_solver_workspace_bytes(ctypes.byref(d)) > small > 0
+
+
+def test_user_model_source_and_library():
+    """The user-model hook's generated source (usermodel.model_source) and,
+    when build() has compiled them, the test models' libraries exporting the
+    one hook the main library binds (ptc_user_model_ops)."""
+    import ctypes
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from user_models import PEND_HESS, PEND_JAC, PEND_STEP
+
+    from paper_2409_20027_b200 import usermodel
+    tag, src = usermodel.model_source(2, 1, PEND_STEP, PEND_JAC, PEND_HESS, "pendulum")
+    assert "PTC_USER_MODEL_LIBRARY(2, 1, ptc::UmSrc_" + tag + ")" in src
+    assert "kHess = true" in src and PEND_STEP.strip().splitlines()[0] in src
+    so = os.path.join(usermodel.MODEL_DIR, f"um_{tag}.so")
+    if os.path.exists(so):
+        lib = ctypes.CDLL(so)
+        assert hasattr(lib, "ptc_user_model_ops")
