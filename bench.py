@@ -98,11 +98,24 @@ def rng_for(rank: int, system: str):
 # CPU reference arm: the oracle port of pintoc's LQR-scan solve
 # ---------------------------------------------------------------------------
 
-def cpu_lqr_sample(n_per_half: int, cores: int, pool=None) -> tuple[float, int]:
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_impl() -> str:
+    """"pintoc": the unmodified reference package installed into baseline/_ref
+    (pip install --target); "port": the pinned numpy port
+    (oracle/) when that install is absent."""
+    return "pintoc" if os.path.isdir(os.path.join(REF_PATH, "pintoc")) else "port"
+
+
+def cpu_lqr_sample(n_per_half: int, cores: int, pool=None, impl: str = "port"
+                   ) -> tuple[float, int]:
     """Reference LQR-scan solves of n_per_half problems of each half, spread
     over `cores` worker processes.  Each worker builds its expansions
-    untimed, then times its solves; the aggregate throughput is the sum of
-    the per-worker rates (workers run concurrently, one per core)."""
+    untimed, then times its solves (impl "pintoc": the reference's own
+    value_pass + propagation_pass; "port": the oracle's); the aggregate
+    throughput is the sum of the per-worker rates (workers run
+    concurrently, one per core)."""
     jobs = []
     for system in ("pendulum", "cartpole"):
         rng = rng_for(0, system)
@@ -110,7 +123,7 @@ def cpu_lqr_sample(n_per_half: int, cores: int, pool=None) -> tuple[float, int]:
         us = initial_controls(system, n_per_half, rng)
         per = max(1, math.ceil(2 * n_per_half / cores))
         for i in range(0, n_per_half, per):
-            jobs.append((system, x0[i:i + per], us[i:i + per]))
+            jobs.append((system, x0[i:i + per], us[i:i + per], impl))
     res = pool.map(_cpu_timed_chunk, jobs) if pool else list(map(_cpu_timed_chunk, jobs))
     solved = sum(r[0] for r in res)
     rate = sum(r[0] / max(r[1], 1e-9) for r in res)
@@ -132,7 +145,7 @@ def lm_alpha_oracle(O, e, alpha0=ALPHA, nu0=2.0):
 
 
 def _cpu_timed_chunk(args):
-    system, x0s, us = args
+    system, x0s, us, impl = args
     sys.path.insert(0, ROOT)
     from oracle import pintoc_oracle as O
     dyn, cost = models_oracle(O)[system]
@@ -143,10 +156,22 @@ def _cpu_timed_chunk(args):
         lam = O.costate_pass(dyn, cost, ("zero",), xs, u)
         e = O.expansion(dyn, cost, ("zero",), xs, u, lam, ALPHA)
         exps.append(e.with_alpha(lm_alpha_oracle(O, e)))
-    t0 = time.perf_counter()
-    for e in exps:
-        O.lqr_solve(e)
-    t1 = time.perf_counter()
+    if impl == "pintoc":
+        sys.path.insert(0, REF_PATH)
+        from pintoc.passes import StageExpansion, propagation_pass, value_pass
+        nu_ = exps[0].R.shape[1]
+        exps = [StageExpansion(P=e.P, R=e.R, M=e.M, d=e.d, Fx=e.Fx, Fu=e.Fu, P_terminal=e.PT,
+                               alpha=e.alpha, R_reg=e.R + e.alpha * np.eye(nu_)) for e in exps]
+        t0 = time.perf_counter()
+        for e in exps:
+            _, _, law = value_pass(e)
+            propagation_pass(law, e)
+        t1 = time.perf_counter()
+    else:
+        t0 = time.perf_counter()
+        for e in exps:
+            O.lqr_solve(e)
+        t1 = time.perf_counter()
     return len(exps), t1 - t0, t1 - t_setup0
 
 
@@ -161,16 +186,19 @@ def run_reference(args) -> None:
         return
     cores = os.cpu_count() or 1
     per_half = max(1, cores)  # one problem per core per half per step
+    impl = reference_impl()
     pool = make_pool(cores)
     try:
         for _ in range(args.warmup):
-            cpu_lqr_sample(per_half, cores, pool)
+            cpu_lqr_sample(per_half, cores, pool, impl)
         vals, wall = [], 0.0
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            v, _ = cpu_lqr_sample(per_half, cores, pool)
+            v, _ = cpu_lqr_sample(per_half, cores, pool, impl)
             wall += time.perf_counter() - t0
             vals.append(v)
+        # the pinned port alongside, on one step's sample
+        port = cpu_lqr_sample(per_half, cores, pool, "port")[0] if impl == "pintoc" else None
     finally:
         pool.close()
     value = statistics.median(vals)
@@ -180,10 +208,14 @@ def run_reference(args) -> None:
         "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.gpus),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                         "kind": "reference" if impl == "pintoc" else "port",
                          "sample": f"{2 * per_half} problems per step (half pendulum, half "
                                    "cart-pole, T=256) of the config-3 workload; LQR-scan solve "
-                                   "timed, expansion built untimed"},
+                                   "timed (" + ("pintoc value_pass + propagation_pass from "
+                                   "baseline/_ref" if impl == "pintoc" else "the oracle port")
+                                   + "), expansion built untimed",
+                         "port_value": port},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -368,6 +400,42 @@ def alg_bytes(n: int, nx: int, nu: int) -> int:
     return 8 * n * (T * (inp + out) + nx * nx + nx)
 
 
+def sweep_bytes(n: int, nx: int, nu: int) -> dict:
+    """Traffic each sweep of the two-sweep solve cannot avoid (8-byte
+    words): the backward (value) sweep reads the upper triangles of P and R,
+    M, d, Fx, Fu and writes Gamma, gamma; the forward (propagation) sweep
+    re-reads Fx, Fu, Gamma, gamma and writes dx, du."""
+    tri = lambda q: q * (q + 1) // 2
+    value = T * (tri(nx) + tri(nu) + nx * nu + nu + nx * nx + nx * nu + nu * nx + nu) + tri(nx)
+    prop = T * (nx * nx + nx * nu + nu * nx + nu + nx + nu) + nx
+    return {"value": 8 * n * value, "prop": 8 * n * prop}
+
+
+def time_prop_sweep(torch, solver, inputs, steps: int) -> float:
+    """ms of the forward sweep alone (ptc_propagate on the solve's own gains,
+    same plan and workspace as the solve)."""
+    from paper_2409_20027_b200 import _native as N
+    P_, R_, M_, d_, Fx, Fu, PT = inputs
+    st = torch.cuda.current_stream()
+
+    def go():
+        N.check(solver.lib.ptc_propagate(
+            solver.code, solver.B, solver.T, solver.nx, solver.nu, Fx.data_ptr(), Fu.data_ptr(),
+            solver.Gamma.data_ptr(), solver.gamma.data_ptr(), None, solver.dx.data_ptr(),
+            solver.du.data_ptr(), solver.workspace.data_ptr(), solver.workspace.numel(),
+            solver.chunk0, solver.chunk, N.stream_ptr(st)))
+
+    go()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(st)
+    for _ in range(steps):
+        go()
+    b.record(st)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -505,10 +573,24 @@ def run_ours(args) -> None:
         peak, peak_src = measured_peak()
         achieved = by / (half_ms["cartpole"] * 1e-3) / 1e9
         kname = "lqr_sweep_cartpole(k_value_down0+k_prop_down0)"
+        # the two sweeps separately, each against the traffic it cannot avoid
+        # (the forward sweep must re-read Fx, Fu, Gamma, gamma: 71 of the
+        # solve's 52 algorithmic words per cart-pole stage, a 0.73 ceiling)
+        prop_ms = time_prop_sweep(torch, solver_c, halves["cartpole"][1], args.steps)
+        sb = sweep_bytes(n_c, nx_c, nu_c)
+        val_ms = half_ms["cartpole"] - prop_ms
+        sweeps = {
+            "value_sweep": {"kernel": "k_value_down0<double,4,1>", "ms": val_ms,
+                            "min_bytes": sb["value"],
+                            "frac": sb["value"] / (val_ms * 1e-3) / 1e9 / peak},
+            "prop_sweep": {"kernel": "k_prop_down0<double,4,1>", "ms": prop_ms,
+                           "min_bytes": sb["prop"],
+                           "frac": sb["prop"] / (prop_ms * 1e-3) / 1e9 / peak},
+            "two_sweep_ceiling": by / (sb["value"] + sb["prop"])}
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname,
                 "algorithmic_bytes_per_launch": by, "ms_per_launch": half_ms["cartpole"],
-                "peak_source": peak_src,
+                "peak_source": peak_src, "sweeps": sweeps,
                 "pendulum_half": {"ms": half_ms["pendulum"],
                                   "achieved_gbs": alg_bytes(halves["pendulum"][3], 2, 1)
                                   / (half_ms["pendulum"] * 1e-3) / 1e9}}
@@ -581,16 +663,22 @@ def run_ours(args) -> None:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
+            impl = reference_impl()
             pool = make_pool(cores)
             try:
-                cpu_lqr_sample(max(1, cores // 2), cores, pool)
-                v, n_done = cpu_lqr_sample(4 * cores, cores, pool)
+                cpu_lqr_sample(max(1, cores // 2), cores, pool, impl)
+                v, n_done = cpu_lqr_sample(4 * cores, cores, pool, impl)
+                vp = cpu_lqr_sample(2 * cores, cores, pool, "port")[0] if impl == "pintoc" else v
             finally:
                 pool.close()
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+            what = ("the reference pintoc's own value_pass + propagation_pass (baseline/_ref)"
+                    if impl == "pintoc" else "the pinned numpy port of pintoc's "
+                    "value_pass + propagation_pass (oracle/)")
+            cpu = {"value": v, "unit": UNIT, "cores": cores,
+                   "kind": "reference" if impl == "pintoc" else "port",
                    "sample": f"{n_done} problems (half pendulum, half cart-pole, T=256) of the "
-                             "config-3 workload through the pinned numpy port of pintoc's "
-                             "value_pass+propagation_pass (oracle/), one process per core"}
+                             f"config-3 workload through {what}, one process per core",
+                   "port_value": vp}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -676,7 +764,11 @@ def newton_latency_sweep(torch, P):
                 re-rollout the reference mandates (newton.py:188) is tried as
                 a log-depth Newton solve of the recurrence for T >= 1024 and
                 falls back to the sequential recurrence when that does not
-                converge to a few ulps (chaotic long swing-ups).
+                converge to a few ulps (chaotic long swing-ups);
+      pendulum_hanging  the same nonlinear model regulated about its
+                stable (hanging) equilibrium: a non-chaotic horizon, where the
+                log-depth rollout converges and the whole nonlinear iteration
+                is log-depth.
     Timed over 4 iterations after the LM weight has settled (12 / 2
     iterations), inputs reloaded between 3 repetitions; 'full' counts the
     timed iterations that solved a definite subproblem (the rest are
@@ -684,7 +776,7 @@ def newton_latency_sweep(torch, P):
     from paper_2409_20027_b200 import _native as N
     from paper_2409_20027_b200._device import DeviceSolver, SolveSettings
     res = {}
-    for model in ("tvlinear", "tvlinear12", "pendulum"):
+    for model in ("tvlinear", "tvlinear12", "pendulum", "pendulum_hanging"):
         out = {}
         for logT in (8, 10, 12, 14, 16):
             Tn = 1 << logT
@@ -695,6 +787,14 @@ def newton_latency_sweep(torch, P):
                                        np.diag([100.0, 10.0]))
                 nx, nu, settle = 2, 1, 12
                 x0 = np.array([np.pi, 0.0])
+                us = 0.5 * rng.standard_normal((1, Tn, 1))
+            elif model == "pendulum_hanging":
+                dyn = P.PendulumDynamics(Tn, P.PendulumParams(damping=0.1, dt=0.05))
+                hang = np.array([np.pi, 0.0])
+                cost = P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]),
+                                       np.diag([100.0, 10.0]), x_goal=hang)
+                nx, nu, settle = 2, 1, 3
+                x0 = hang + np.array([1.2, 0.0])
                 us = 0.5 * rng.standard_normal((1, Tn, 1))
             else:
                 nx, nu, settle = (4, 2, 2) if model == "tvlinear" else (12, 4, 2)

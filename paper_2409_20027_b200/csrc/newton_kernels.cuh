@@ -457,10 +457,15 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
   } else {
     ld_vec(a.ccar[1], j, a.plan.n[1], B, b, ln);
   }
+  R x[NX], u[NU];
+  ld_x(a, q, t1 - 1 >= t0 ? t1 - 1 : t0, b, x);
+  ld_u(a, q, t1 - 1 >= t0 ? t1 - 1 : t0, b, u);
   for (int t = t1 - 1; t >= t0; --t) {
-    R x[NX], u[NU];
-    ld_x(a, q, t, b, x);
-    ld_u(a, q, t, b, u);
+    // software pipeline: stage t-1's state and control load while stage t runs
+    R xn[NX], un[NU];
+    const int tp = t > t0 ? t - 1 : t;
+    ld_x(a, q, tp, b, xn);
+    ld_u(a, q, tp, b, un);
     R lt[NX];
     if constexpr (!kExp) {
       // co-states only: first derivatives suffice (bitwise the same lambda
@@ -490,7 +495,12 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
     }
     st_vec(a.lam, t, T + 1, B, b, lt);
 #pragma unroll
-    for (int i = 0; i < NX; ++i) ln[i] = lt[i];
+    for (int i = 0; i < NX; ++i) {
+      ln[i] = lt[i];
+      x[i] = xn[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NU; ++i) u[i] = un[i];
   }
 }
 
@@ -516,12 +526,18 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
   ld_mat(a.PT, 0, 1, B, b, c.Y);
   set_zero(c.eta);
   int fl = 0;
-  R ln[NX];
+  R ln[NX], x[NX], u[NU];
   ld_vec(a.lam, T, T + 1, B, b, ln);
+  ld_x(a, q, T - 1, b, x);
+  ld_u(a, q, T - 1, b, u);
   for (int t = T - 1; t >= 0; --t) {
-    R x[NX], u[NU];
-    ld_x(a, q, t, b, x);
-    ld_u(a, q, t, b, u);
+    // software pipeline: stage t-1's state, control and lambda_t (stored by
+    // the co-state sweep) are in flight while stage t is expanded and folded
+    R xn[NX], un[NU], lt_next[NX];
+    const int tp = t > 0 ? t - 1 : 0;
+    ld_x(a, q, tp, b, xn);
+    ld_u(a, q, tp, b, un);
+    ld_vec(a.lam, t, T + 1, B, b, lt_next);
     Stage<R, NX, NU> st;
     R lt[NX];
     stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
@@ -534,7 +550,13 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
     st_vec(la.gam, t, T, B, b, gam);
     st_vec(a.d, t, T, B, b, st.d);
     c = o;
-    ld_vec(a.lam, t, T + 1, B, b, ln);  // lambda_t, stored by the co-state sweep
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      ln[i] = lt_next[i];
+      x[i] = xn[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NU; ++i) u[i] = un[i];
   }
   if (fl) atomicOr(a.flags + b, fl);
 }
@@ -553,14 +575,22 @@ __global__ void __launch_bounds__(128) k_prop_fused(NewtonArgs<R> a, LqrArgs<R> 
   double s2 = 0.0, sd = 0.0, mx = 0.0;
   R lam0[NX];
   set_zero(lam0);
+  R xs[NX], us[NU], Gam[NU][NX], gam[NU], dd[NU];
+  ld_x(a, q, 0, b, xs);
+  ld_u(a, q, 0, b, us);
+  ld_mat(la.Gam, 0, T, B, b, Gam);
+  ld_vec(la.gam, 0, T, B, b, gam);
+  ld_vec(a.d, 0, T, B, b, dd);
   for (int t = 0; t < T; ++t) {
     st_vec(la.dX, t, T + 1, B, b, x);
-    R xs[NX], us[NU], Gam[NU][NX], gam[NU], dd[NU];
-    ld_x(a, q, t, b, xs);
-    ld_u(a, q, t, b, us);
-    ld_mat(la.Gam, t, T, B, b, Gam);
-    ld_vec(la.gam, t, T, B, b, gam);
-    ld_vec(a.d, t, T, B, b, dd);
+    // software pipeline: stage t+1's inputs load while stage t runs
+    R xs_n[NX], us_n[NU], Gam_n[NU][NX], gam_n[NU], dd_n[NU];
+    const int tn = t + 1 < T ? t + 1 : t;
+    ld_x(a, q, tn, b, xs_n);
+    ld_u(a, q, tn, b, us_n);
+    ld_mat(la.Gam, tn, T, B, b, Gam_n);
+    ld_vec(la.gam, tn, T, B, b, gam_n);
+    ld_vec(a.d, tn, T, B, b, dd_n);
     DynDerivs<R, NX, NU> D;
     Dyn::template derivs<false>(p, t, b, xs, us, lam0, D);
     R du[NU];
@@ -582,7 +612,18 @@ __global__ void __launch_bounds__(128) k_prop_fused(NewtonArgs<R> a, LqrArgs<R> 
     mv<NX, NU>(D.fu, gam, e);
     mv<NX, NX>(F, x, y);
 #pragma unroll
-    for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
+    for (int i = 0; i < NX; ++i) {
+      x[i] = y[i] + e[i];
+      xs[i] = xs_n[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      us[i] = us_n[i];
+      gam[i] = gam_n[i];
+      dd[i] = dd_n[i];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) Gam[i][k] = Gam_n[i][k];
+    }
   }
   st_vec(la.dX, T, T + 1, B, b, x);
   la.red[(size_t)0 * B + b] = s2;
@@ -1047,7 +1088,15 @@ __global__ void k_control(NewtonArgs<R> a) {
         ratio = (pred <= 0.0) ? -INFINITY : (cur - newc) / pred;
       }
       const double used = alpha;
-      if (ratio > 0.0) {
+      // fp32 solver only: a model decrease below the float32 resolution of
+      // the cost (2^-20 |cost|, 16 ulps) cannot be judged by the gain ratio
+      // -- both costs carry that much rounding from the fp32 rollouts -- so
+      // a feasible candidate is accepted and ends the solve as converged
+      // (the relative cost change it makes is below fp32 resolution too).
+      // The fp64 solver never takes this branch: it follows newton.py.
+      const bool below32 = sizeof(R) == 4 && pred > 0.0 && newc < INFINITY &&
+                           pred <= 0x1p-20 * fabs(cur);
+      if (ratio > 0.0 || below32) {
         const double f = 1.0 - pow(2.0 * ratio - 1.0, 3.0);
         alpha = alpha * (f > 1.0 / 3.0 ? f : 1.0 / 3.0);
         nu = 2.0;
@@ -1057,7 +1106,7 @@ __global__ void k_control(NewtonArgs<R> a) {
         cur = newc;
         ph |= PH_NEED_EXP;
         ++it;
-        if (rel <= tol) {
+        if (rel <= tol || below32) {
           finished = true;
           term = TERM_COST;
         }

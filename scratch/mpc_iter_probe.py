@@ -1,0 +1,29 @@
+"""Per-iteration time of the batched barrier Newton iteration (config-3
+halves, 32,768 problems each, T=256, fp64): the MPC workload's unit."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import bench, paper_2409_20027_b200 as P
+from paper_2409_20027_b200 import BatchSolver
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
+for system in (sys.argv[1].split(",") if len(sys.argv) > 1 else ("pendulum", "cartpole")):
+    probs = bench.models_pkg(P)
+    bound = 10.0 if system == "cartpole" else 5.0
+    box = P.BoxConstraint(probs[system].dynamics.d_x, 1, control_lower=-bound, control_upper=bound)
+    prob = P.ControlProblem(probs[system].dynamics, probs[system].cost, box)
+    rng = bench.rng_for(0, system)
+    x0 = bench.initial_states(system, n, rng)
+    u0 = torch.as_tensor(np.clip(0.1 * bound * rng.standard_normal((n, bench.T, 1)), -0.9 * bound, 0.9 * bound)).cuda()
+    opts = P.BarrierOptions(mu0=0.1, zeta=0.2, mu_tol=1e-6, newton=P.NewtonOptions(max_iters=50))
+    bs = BatchSolver(prob, n, "barrier", barrier=opts)
+    xs = bs.rollout(x0, u0)
+    s = bs.solver
+    times = []
+    for rep in range(3):
+        s.load(xs, u0)
+        s.iterate(2)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); s.iterate(10); b.record(); torch.cuda.synchronize()
+        times.append(a.elapsed_time(b) / 10)
+    print(system, n, "ms/iteration", [round(t, 3) for t in times], flush=True)
