@@ -273,9 +273,9 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   bool fused = false;
   if constexpr (NX < 8) {
     if (a.plan.L == 0) {
-      // single-sweep schedule: the LQR sweeps re-derive the expansion in
-      // registers from x, u and the co-states (no stored expansion)
-      k_costate_down0<R, Dyn, false><<<grid_for(B), kBlock, 0, s>>>(a);
+      // single-sweep schedule: the value sweep re-derives every stage's
+      // expansion and its co-state in registers from x, u (no stored
+      // expansion or co-states), the propagation sweep the Jacobians
       k_value_fused<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la);
       k_prop_fused<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la);
       fused = true;

@@ -522,22 +522,33 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
   const ProblemParams& p = *a.pp;
   const AugArgs<R> g = aug_of(a);
   const R alpha = R(a.alpha[b]);
+  // the co-state recursion runs inside this sweep: stage_expansion returns
+  // lambda_t = l_x + f_x^T lambda_{t+1} (passes.py:122-148) next to the
+  // stage's expansion, so the co-states never touch HBM.  Boundary:
+  // lambda_T = terminal gradient, P_T = sym(Qf) (passes.py:140-148).
   VCarry<R, NX> c;
-  ld_mat(a.PT, 0, 1, B, b, c.Y);
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int k = 0; k < NX; ++k) c.Y[i][k] = R(p.Qf[i * NX + k]);
+  symmetrize<NX>(c.Y);
   set_zero(c.eta);
   int fl = 0;
   R ln[NX], x[NX], u[NU];
-  ld_vec(a.lam, T, T + 1, B, b, ln);
+  {
+    R xT[NX];
+    ld_x(a, q, T, b, xT);
+    terminal_grad(p, xT, ln);
+  }
   ld_x(a, q, T - 1, b, x);
   ld_u(a, q, T - 1, b, u);
   for (int t = T - 1; t >= 0; --t) {
-    // software pipeline: stage t-1's state, control and lambda_t (stored by
-    // the co-state sweep) are in flight while stage t is expanded and folded
-    R xn[NX], un[NU], lt_next[NX];
+    // software pipeline: stage t-1's state and control are in flight while
+    // stage t is expanded and folded
+    R xn[NX], un[NU];
     const int tp = t > 0 ? t - 1 : 0;
     ld_x(a, q, tp, b, xn);
     ld_u(a, q, tp, b, un);
-    ld_vec(a.lam, t, T + 1, B, b, lt_next);
     Stage<R, NX, NU> st;
     R lt[NX];
     stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
@@ -552,7 +563,7 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
     c = o;
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
-      ln[i] = lt_next[i];
+      ln[i] = lt[i];
       x[i] = xn[i];
     }
 #pragma unroll
