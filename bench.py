@@ -337,6 +337,26 @@ class Clocks:
         return out
 
 
+def fp64_peak_tflops(torch) -> float:
+    """Measured FP64 peak of this GPU: cuBLAS DGEMM (DMMA tensor path, equal
+    to the FP64 vector peak on B200), 8192^3, best of 5 after warm-up
+    (MEASURED_PEAKS.json carries no FP64 figure)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    best = math.inf
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
 def measured_peak() -> tuple[float, str]:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -981,10 +1001,24 @@ def long_horizon_leg(torch, world: int, rank: int, steps: int = 5, chunk0: int =
     flags = int(ops.flags.max())
     in_bytes = 8 * T_all * (nx * nx * 2 + nu * nu + nx * nu * 2 + nu)
     out_bytes = 8 * T_all * (nu * nx + nu + nx + nu)
+    # FP64 work: the sequential Riccati + forward sweep (the algorithmic
+    # minimum, ~6.5 k FMA per stage at nx 12, nu 4) and the log-depth scan
+    # the kernels run (~18.6 k FMA per stage: Woodbury stage combines,
+    # Riccati steps with affine composition, forward sweep; profiles/r1c)
+    seq_fma = (nu * nx * nx + nu * nx * nu + nu * nx * nx + 2 * nx ** 3 + nx * nu * nx
+               + nu ** 3 + nu * nu * nx + 2 * nx * nx + nx * nx + nu * nx)
+    scan_fma = 18600
+    peak64 = fp64_peak_tflops(torch)
+    sec = float(ms) * 1e-3
     return {"config": "config 4: T=2^20, nx=12, nu=4, fp64, batch 1, time blocks x%d" % world,
             "ms_per_solve": float(ms), "flags": flags,
-            "achieved_gbs": (in_bytes + out_bytes) / (float(ms) * 1e-3) / 1e9,
-            "algorithmic_bytes": in_bytes + out_bytes}
+            "achieved_gbs": (in_bytes + out_bytes) / sec / 1e9,
+            "algorithmic_bytes": in_bytes + out_bytes,
+            "fp64_peak_tflops_measured": peak64,
+            "fp64": {"sequential_gflop": 2 * seq_fma * T_all / 1e9,
+                     "scan_gflop": 2 * scan_fma * T_all / 1e9,
+                     "frac_sequential_work": 2 * seq_fma * T_all / sec / 1e12 / peak64,
+                     "frac_scan_work": 2 * scan_fma * T_all / sec / 1e12 / peak64}}
 
 
 def single_solve_leg(torch, P, cpu: bool = True):

@@ -5,6 +5,7 @@
 #include <map>
 #include <tuple>
 
+#include "bulk_sweeps.cuh"
 #include "newton_kernels.cuh"
 #include "wide.cuh"
 #include "wide_newton.cuh"
@@ -19,6 +20,10 @@ template <typename R, int NX, int NU>
 void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
+  if (bulk_ok<R, NX, NU>(a)) {  // batch-filling single sweep, small stages: TMA-fed rings
+    launch_lqr_bulk<R, NX, NU>(a, s);
+    return;
+  }
   if (pl.L >= 1) {
     k_value_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_value_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
@@ -43,6 +48,10 @@ template <typename R, int NX, int NU>
 void launch_prop(const LqrArgs<R>& a, cudaStream_t s) {
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
+  if (bulk_ok<R, NX, NU>(a)) {
+    launch_prop_bulk<R, NX, NU>(a, s);
+    return;
+  }
   if (pl.L >= 1) {
     k_prop_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);

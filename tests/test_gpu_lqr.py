@@ -242,3 +242,48 @@ def test_infeasible_error_carries_the_constraint_value():
     st, comp = np.argwhere(w >= 0)[0]
     assert (err.value.stage, err.value.component) == (st, comp)
     assert err.value.value == w[st, comp]
+
+
+@pytest.mark.parametrize("nx,nu,B", [(2, 1, 2050), (2, 1, 4096), (1, 2, 2048), (1, 1, 2049),
+                                      (4, 1, 2048)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_bulk_ring_sweeps_match_register_path(nx, nu, B, dtype):
+    """The single-sweep plan at batches >= 2048 with small stages (<= 16
+    component rows) runs the TMA-fed ring kernels (bulk_sweeps.cuh; an odd
+    batch and the cart-pole size keep the register path): same results as
+    the blocked-tree plan and the oracle, S / s included, partial last tile
+    (B % 128 != 0) included."""
+    import torch
+
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200.passes import LqrSolver
+    rng = np.random.default_rng(B + nx)
+    T = 48
+    dt = torch.float64 if dtype == "f64" else torch.float32
+    es = [O.random_lqr_expansion(rng, T, nx, nu) for _ in range(4)]
+    # batch: the four oracle problems repeated, SoA batch-minor
+    def field(name, comps):
+        a = np.stack([getattr(es[b % 4], name).reshape(T, comps) for b in range(B)], -1)
+        return torch.as_tensor(a.transpose(1, 0, 2).copy(), dtype=dt).cuda()
+    ins = [field("P", nx * nx), field("R", nu * nu), field("M", nx * nu), field("d", nu),
+           field("Fx", nx * nx), field("Fu", nx * nu)]
+    PT = torch.as_tensor(np.stack([es[b % 4].PT.reshape(-1) for b in range(B)], -1)[:, None, :],
+                         dtype=dt).cuda()
+    alpha = torch.full((B,), 0.5, dtype=torch.float64, device="cuda")
+    out = {}
+    for plan, (c0, c1) in {"sweep": (T, 0), "tree": (4, 8)}.items():
+        s = LqrSolver(B, T, nx, nu, dtype=dt, chunk0=c0, chunk=c1, with_value=True)
+        s.solve(*ins, PT, alpha)
+        torch.cuda.synchronize()
+        assert int(s.flags.abs().sum()) == 0
+        out[plan] = [t.double().cpu().numpy() for t in (s.Gamma, s.gamma, s.dx, s.du, s.S, s.s)]
+    tol = 1e-9 if dtype == "f64" else 1e-4
+    for a, b in zip(out["sweep"], out["tree"]):
+        assert rel_gap(a, b) < tol
+    for k in range(4):
+        ref = O.lqr_solve(es[k].with_alpha(0.5))   # S, s, Gamma, gamma, dx, du
+        got = out["sweep"]
+        for want, have in zip(ref, (got[4][..., k], got[5][..., k], got[0][..., k],
+                                     got[1][..., k], got[2][..., k], got[3][..., k])):
+            w = np.asarray(want).reshape(T + 1 if have.shape[1] == T + 1 else T, -1)
+            assert rel_gap(have.T.reshape(w.shape), w) < tol
