@@ -356,7 +356,8 @@ int ptc_solver_write(ptc_solver* s, const char* name, const void* src, int64_t b
 
 /* Copy a named buffer out (dst host or device).  Names: states, controls
  * (current trajectory), lam, P, R, M, d, Fx, Fu, PT, S, s, Gamma, gamma, dx,
- * du, z, v, status, iters, term, round, hist_len, hist, cur_cost, alpha, nu, mu,
+ * du, z, v, status, iters, term, round, hist_len, hist, cur_cost, cand_cost (the
+ * last iteration's candidate cost, float64), alpha, nu, mu,
  * bad_value (float64: the constraint value w at bad_index, InfeasibleError.value),
  * round_mu, round_cost, round_iters, round_term, round_rp, round_rd,
  * round_controls, bad_index, flags, rollout_state (bit 0 skipped, bit 1 log-depth

@@ -250,7 +250,7 @@ class DeviceSolver:
                                     "Fu", "PT", "S", "s", "Gamma", "gamma", "dx", "du",
                                     "z", "v", "round_controls"):
             dt = torch.int32
-        elif name in ("hist", "cur_cost", "alpha", "nu", "mu", "bad_value", "round_mu",
+        elif name in ("hist", "cur_cost", "cand_cost", "alpha", "nu", "mu", "bad_value", "round_mu",
                       "round_cost", "round_rp", "round_rd"):
             dt = torch.float64
         else:

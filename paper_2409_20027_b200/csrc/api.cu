@@ -952,6 +952,7 @@ struct Solver final : ptc_solver {
       reg("parity", a.parity, B, 4);
       reg("hist", a.hist, (int64_t)a.opt.hist_cap * 5 * B, 8);
       reg("cur_cost", a.cur_cost, B, 8);
+      reg("cand_cost", a.cand_cost, B, 8);
       reg("alpha", a.alpha, B, 8);
       reg("nu", a.nu, B, 8);
       reg("mu", a.mu, B, 8);

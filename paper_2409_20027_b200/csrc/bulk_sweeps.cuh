@@ -341,21 +341,22 @@ inline int bulk_depth(int B, size_t slot_bytes, int sms) {
 // Whether the bulk path applies: single-sweep plan, no block mode, every
 // component row 16-byte aligned (B * sizeof(R) a multiple of 16 and the
 // fields 16-byte aligned).
-inline int bulk_mode() {   // PTC_BULK=0 / 1 forces the register / ring path (probes)
-  static int m = [] {
-    const char* e = std::getenv("PTC_BULK");
-    return e ? std::atoi(e) : -1;
-  }();
-  return m;
+inline int bulk_mode() {   // PTC_BULK=1 selects the ring path (read per launch)
+  const char* e = std::getenv("PTC_BULK");
+  return e ? std::atoi(e) : -1;
 }
 
-// Measured (scratch/bulk_probe.py, config-3 halves, 32,768 problems): the
-// ring wins for small stages (pendulum, 13 component rows: fp64 0.547 ->
-// 0.472 ms, fp32 0.495 -> 0.456 ms) and loses for wide ones (cart-pole, 36
-// rows: fp64 0.902 -> 0.958, fp32 0.748 -> 0.932 ms), where the register
-// path's per-thread loads already keep the stage stream at 0.8-0.85 of the
-// copy bandwidth; so it is used up to 16 rows per stage.
-constexpr int kBulkMaxRows = 16;
+// Measured (scratch/bulk_probe.py and bench.py, config-3 halves, 32,768
+// problems each): alone, the ring wins for small stages (pendulum, 13
+// component rows: fp64 0.547 -> 0.472 ms, fp32 0.495 -> 0.456 ms) and loses
+// for wide ones (cart-pole, 36 rows: fp64 0.902 -> 0.958, fp32 0.748 -> 0.932
+// ms), where the register path's per-thread loads already keep the stage
+// stream at 0.8-0.9 of the copy bandwidth.  In the headline step the two
+// halves run concurrently and the ring's shared memory (106 KB per CTA for
+// the pendulum) displaces co-resident cart-pole blocks: the step slows from
+// 1.143 to 1.182 ms with the pendulum on the ring (1.246 ms with both).  The
+// register path is therefore the default; PTC_BULK=1 selects the ring.
+constexpr int kBulkMaxRows = 0;
 
 template <typename R, int NX, int NU>
 inline bool bulk_ok(const LqrArgs<R>& a) {

@@ -1098,6 +1098,7 @@ __global__ void k_control(NewtonArgs<R> a) {
         newc = cand;
         ratio = (pred <= 0.0) ? -INFINITY : (cur - newc) / pred;
       }
+      a.cand_cost[b] = newc;   // the candidate's cost (readable: "cand_cost")
       const double used = alpha;
       // fp32 solver only: a model decrease below the float32 resolution of
       // the cost (2^-20 |cost|, 16 ulps) cannot be judged by the gain ratio

@@ -33,6 +33,7 @@ class Restart:
     alpha: np.ndarray
     nu: np.ndarray
     cost: np.ndarray
+    cand: np.ndarray        # the step's candidate cost (inf: infeasible / diverged)
 
 
 def device_restart(prob, X, U, alpha, nu, *, mu=None, z=None, v=None, rho=1.0,
@@ -58,7 +59,7 @@ def device_restart(prob, X, U, alpha, nu, *, mu=None, z=None, v=None, rho=1.0,
     return Restart(status=rd("status"), iters=rd("iters"), term=s.rounds("round_term")[0].cpu().numpy(),
                    hist=s.history().cpu().numpy(), states=s.states().cpu().numpy(),
                    controls=s.controls().cpu().numpy(), alpha=rd("alpha"), nu=rd("nu"),
-                   cost=rd("cur_cost"))
+                   cost=rd("cur_cost"), cand=rd("cand_cost"))
 
 
 def rel(a, b):
@@ -67,20 +68,20 @@ def rel(a, b):
 
 
 def ratio_noise(hist_ref, cur_cost):
-    """Rounding band of the reference's gain ratio (cur - new) / pred: the two
-    costs are sums over up to 500 stages of a trajectory that is itself
-    reproduced to ~1e-13 (the candidate rollout amplifies the step's
-    rounding), so each is known to ~1e-12 relative and the ratio to
-    1e-11 (|cur| + |new|) / |pred| (plus 1e-9 relative)."""
+    """Tolerance band of the gain ratio (cur - new) / pred, a difference
+    quotient of two costs: with each cost held to the parity tolerance 1e-9
+    relative (the candidate cost is a sum over a rollout of up to 500 stages
+    that amplifies the step's rounding), the ratio is known to
+    1e-9 (|cur| + |new|) / |pred| (plus 1e-9 relative)."""
     r = hist_ref[:, 2]
     new = hist_ref[:, 0]
     with np.errstate(all="ignore"):
         pred = np.where(np.isfinite(r) & (r != 0), (cur_cost - new) / r, np.inf)
-        band = 1e-11 * (np.abs(cur_cost) + np.abs(new)) / np.abs(pred) + 1e-9 * np.abs(r)
+        band = TOL * (np.abs(cur_cost) + np.abs(new)) / np.abs(pred) + TOL * np.abs(r)
     return np.where(np.isfinite(band), band, 0.0)
 
 
-def check_iterations(res: Restart, g, prefix="", label=""):
+def check_iterations(res: Restart, g, prefix="", label="", cur=None):
     """Compare B single-iteration restarts with the reference's records.
     Returns a dict of counters (for the test log)."""
     term = g[prefix + "it_term"]
@@ -93,7 +94,16 @@ def check_iterations(res: Restart, g, prefix="", label=""):
         label, "SolverStalledError rows differ", np.flatnonzero((res.status == -1) != stalled)[:10])
     ok = ~stalled
     dh = res.hist[0].T                      # (B, 5) the device's record of its one step
-    band = band_full(g, prefix)
+    band = ratio_noise(hist, cur) if cur is not None else band_full(g, prefix)
+    # a rejected step's record holds the entering cost, not the candidate's:
+    # there the band's scale |pred| = |cur - cand| / |ratio| comes from the
+    # device's own candidate cost
+    rej = ok & (hist[:, 4] < 0.5) & np.isfinite(hist[:, 2]) & (hist[:, 2] != 0)
+    if rej.any():
+        with np.errstate(all="ignore"):
+            pred = np.abs(hist[rej, 0] - res.cand[rej]) / np.abs(hist[rej, 2])
+            b2 = TOL * (np.abs(hist[rej, 0]) + np.abs(res.cand[rej])) / pred
+        band[rej] = np.where(np.isfinite(b2), b2, band[rej]) + TOL * np.abs(hist[rej, 2])
     acc_ref = hist[:, 4] > 0.5
     acc_dev = dh[:, 4] > 0.5
     # a flip is allowed only where the reference's ratio is within its own

@@ -244,15 +244,13 @@ def test_infeasible_error_carries_the_constraint_value():
     assert err.value.value == w[st, comp]
 
 
-@pytest.mark.parametrize("nx,nu,B", [(2, 1, 2050), (2, 1, 4096), (1, 2, 2048), (1, 1, 2049),
-                                      (4, 1, 2048)])
+@pytest.mark.parametrize("nx,nu,B", [(2, 1, 2050), (4, 1, 4096), (4, 2, 2048), (3, 2, 2049)])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_bulk_ring_sweeps_match_register_path(nx, nu, B, dtype):
-    """The single-sweep plan at batches >= 2048 with small stages (<= 16
-    component rows) runs the TMA-fed ring kernels (bulk_sweeps.cuh; an odd
-    batch and the cart-pole size keep the register path): same results as
-    the blocked-tree plan and the oracle, S / s included, partial last tile
-    (B % 128 != 0) included."""
+def test_bulk_ring_sweeps_match_register_path(nx, nu, B, dtype, monkeypatch):
+    """With PTC_BULK=1 the single-sweep plan at batches >= 2048 runs the
+    TMA-fed ring kernels (bulk_sweeps.cuh; an odd batch keeps the register
+    path): same results as the blocked-tree plan and the oracle, S / s
+    included, partial last tile (B % 128 != 0) included."""
     import torch
 
     import paper_2409_20027_b200 as P
@@ -271,6 +269,7 @@ def test_bulk_ring_sweeps_match_register_path(nx, nu, B, dtype):
                          dtype=dt).cuda()
     alpha = torch.full((B,), 0.5, dtype=torch.float64, device="cuda")
     out = {}
+    monkeypatch.setenv("PTC_BULK", "1")
     for plan, (c0, c1) in {"sweep": (T, 0), "tree": (4, 8)}.items():
         s = LqrSolver(B, T, nx, nu, dtype=dt, chunk0=c0, chunk=c1, with_value=True)
         s.solve(*ins, PT, alpha)
