@@ -786,9 +786,9 @@ def newton_latency_sweep(torch, P):
                 falls back to the sequential recurrence when that does not
                 converge to a few ulps (chaotic long swing-ups);
       pendulum_hanging  the same nonlinear model regulated about its
-                stable (hanging) equilibrium: a non-chaotic horizon, where the
-                log-depth rollout converges and the whole nonlinear iteration
-                is log-depth.
+                hanging equilibrium with damping 1 (a contractive Euler map):
+                a non-chaotic horizon, where the log-depth rollout can
+                converge and the whole nonlinear iteration be log-depth.
     Timed over 4 iterations after the LM weight has settled (12 / 2
     iterations), inputs reloaded between 3 repetitions; 'full' counts the
     timed iterations that solved a definite subproblem (the rest are
@@ -809,13 +809,16 @@ def newton_latency_sweep(torch, P):
                 x0 = np.array([np.pi, 0.0])
                 us = 0.5 * rng.standard_normal((1, Tn, 1))
             elif model == "pendulum_hanging":
-                dyn = P.PendulumDynamics(Tn, P.PendulumParams(damping=0.1, dt=0.05))
-                hang = np.array([np.pi, 0.0])
+                # theta'' = -(g/l) sin(theta) - b theta' + ...: theta = 0 is the
+                # hanging equilibrium; with b = 1 the Euler map (dt 0.05) is
+                # contractive there (|eig|^2 = 1 - b dt + dt^2 g/l = 0.97;
+                # config 0's b = 0.1 gives 1.02: energy grows every step)
+                dyn = P.PendulumDynamics(Tn, P.PendulumParams(damping=1.0, dt=0.05))
                 cost = P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]),
-                                       np.diag([100.0, 10.0]), x_goal=hang)
+                                       np.diag([100.0, 10.0]))
                 nx, nu, settle = 2, 1, 3
-                x0 = hang + np.array([1.2, 0.0])
-                us = 0.5 * rng.standard_normal((1, Tn, 1))
+                x0 = np.array([0.5, 0.0])
+                us = 0.05 * rng.standard_normal((1, Tn, 1))
             else:
                 nx, nu, settle = (4, 2, 2) if model == "tvlinear" else (12, 4, 2)
                 A = np.eye(nx)[None] + 0.05 * rng.standard_normal((Tn, nx, nx))
