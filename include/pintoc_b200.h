@@ -272,6 +272,10 @@ typedef struct ptc_problem_desc {
    * float64 data (per-stage matrices, tables ...), read by the model's code
    * as `data`; may be NULL.  Its parameters are dyn_params (`prm`). */
   const void* user_data;
+  /* user-defined cost (a model library built with a cost source): its
+   * parameters (`cprm`) and device float64 array (`cdata`, may be NULL) */
+  double cost_params[8];
+  const void* cost_data;
 } ptc_problem_desc;
 
 /* Register a user-defined dynamics model (reference problem.py:59-112: a

@@ -90,7 +90,14 @@ class DeviceSolver:
         self.nx, self.nu = int(dynamics.d_x), int(dynamics.d_u)
         npdt = np.float64 if self.dtype == torch.float64 else np.float32
 
-        spec = dynamics._device_spec()
+        from .usermodel import DeviceCost, DeviceDynamics
+        if isinstance(cost, DeviceCost):
+            if not isinstance(dynamics, DeviceDynamics):
+                raise ValueError("a DeviceCost is compiled into the model library of a "
+                                 "DeviceDynamics; write the dynamics as one too")
+            spec = dynamics._device_spec(cost)
+        else:
+            spec = dynamics._device_spec()
         cspec = cost._device_spec()
         bspec = constraints._device_spec() if constraints is not None else {}
         keep = []  # host arrays whose pointers the descriptor holds
@@ -119,6 +126,12 @@ class DeviceSolver:
             d.user_data = ud.data_ptr()
             keep.append(ud)
             self._user_data = ud
+        for i, v in enumerate(cspec.get("cost_params", [])):
+            d.cost_params[i] = float(v)
+        if cspec.get("cost_data") is not None:
+            d.cost_data = cspec["cost_data"].data_ptr()
+            keep.append(cspec["cost_data"])
+            self._cost_data = cspec["cost_data"]
         d.Q = dptr(cspec["Q"])
         d.R = dptr(cspec["R"])
         d.Qf = dptr(cspec["Qf"])

@@ -54,6 +54,7 @@ class ProblemDesc(C.Structure):
         ("rollout", C.c_int32),
         ("block_mode", C.c_int32), ("t_base", C.c_int32), ("block_last", C.c_int32),
         ("user_data", C.c_void_p),
+        ("cost_params", C.c_double * 8), ("cost_data", C.c_void_p),
     ]
 
 

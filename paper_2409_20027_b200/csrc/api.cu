@@ -776,6 +776,8 @@ struct Solver final : ptc_solver {
     p.lin_T = std::max(1, d.lin_rows);
     p.lin_B = std::max(1, d.lin_batch);
     p.user_data = static_cast<const double*>(d.user_data);
+    for (int i = 0; i < 8; ++i) p.cost_prm[i] = d.cost_params[i];
+    p.cost_data = static_cast<const double*>(d.cost_data);
   }
 
   static size_t layout(const ptc_problem_desc& d, Carver& c, Solver* self) {
@@ -866,6 +868,7 @@ struct Solver final : ptc_solver {
     l.dX = c.template take<R>(nx * (T + 1) * B);
     l.dU = c.template take<R>(nu * T * B);
     a.blk = d.block_mode ? 1 : 0;
+    a.uterm = 0;
     a.blk_last = d.block_last ? 1 : 0;
     a.t_base = d.block_mode ? d.t_base : 0;
     a.lam_in = a.x_in = nullptr;
@@ -990,6 +993,7 @@ struct Solver final : ptc_solver {
     Carver c{(char*)ws};
     size_t need = layout(d, c, this);
     if ((int64_t)need > bytes) return fail(PTC_ERR_WORKSPACE, "solver workspace too small");
+    na.uterm = ops->user_cost;
     if (d.model == PTC_DYN_LINEAR) {
       const size_t lt = hp.lin_T, lb = hp.lin_B;
       if (!d.lin_a || !d.lin_b) return fail(PTC_ERR_ARG, "linear model needs lin_a and lin_b");

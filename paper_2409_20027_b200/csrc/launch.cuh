@@ -261,6 +261,7 @@ struct NewtonOps {
   // time-block phase (null: the model has no block mode)
   void (*block)(const void* na, const void* la, int phase, const void* in, void* out, int rank,
                 int world, cudaStream_t s);
+  int user_cost;   // the model carries its own cost (NewtonArgs::uterm)
 };
 
 using LqrKey = std::tuple<int, int, int>;            // dtype, nx, nu
@@ -278,7 +279,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   const long long B = a.B, P0 = a.plan.units0();
   cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
   if constexpr (kWideNewton<Dyn>) WideNewton<R, NX, NU>::cost_partials(a, 0, s);
-  else k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
+  else k_cost_partials<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
   bool fused = false;
   if constexpr (NX < 8) {
     if (a.plan.L == 0) {
@@ -348,13 +349,13 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     }
     k_pr_finish<R, NX><<<grid_for(nT), kBlock, 0, s>>>(a);
     k_rollout<R, Dyn, true><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
-    k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+    k_cost_partials<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
   } else if (P0 == 1) {
     // one unit per problem: the rollout also accumulates the candidate cost
     k_rollout<R, Dyn, false, true><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
   } else {
     k_rollout<R, Dyn, false><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
-    k_cost_partials<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+    k_cost_partials<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
   }
   if (fold) {
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[0], 3, kOpsCost, (int)P0, (int)B);
@@ -505,7 +506,7 @@ struct RegisterNewton {
     const NewtonArgs<R>& a = A(p);
     k_force_phase<R><<<grid_for(a.B), kBlock, 0, s>>>(a, PH_NEED_COST);
     const int P0 = a.plan.units0();
-    k_cost_partials<R, NX, NU><<<grid_for((long long)P0 * a.B), kBlock, 0, s>>>(a, 0);
+    k_cost_partials<R, NX, NU, Dyn><<<grid_for((long long)P0 * a.B), kBlock, 0, s>>>(a, 0);
     if (partial_rows(P0) < P0)
       k_reduce_partials<<<(unsigned)a.B, 256, 0, s>>>(a.cpart[0], 3,
                                                       RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4),
@@ -522,7 +523,7 @@ struct RegisterNewton {
   RegisterNewton() {
     newton_registry()[NewtonKey(dtype_code<R>(), DYN, NX, NU)] =
         NewtonOps{&lqr, &init, &check, &iterate, &expand, &rollout, &cost,
-                  kWideNewton<Dyn> ? &block : nullptr};
+                  kWideNewton<Dyn> ? &block : nullptr, kUserCost<Dyn> ? 1 : 0};
   }
 };
 

@@ -10,6 +10,8 @@
 // passes.py:155-185 (expansion).
 #pragma once
 
+#include <type_traits>
+
 #include "elements.cuh"
 
 namespace ptc {
@@ -35,12 +37,25 @@ struct ProblemParams {
                             // (warp kernels: one contiguous row per stage), or null
   double Q[kMaxNX * kMaxNX], Rc[kMaxNU * kMaxNU], Qf[kMaxNX * kMaxNX], goal[kMaxNX];
   const double* user_data;  // user-defined model (user_model.cuh): its device array or null
+  double cost_prm[8];       // user-defined cost: its parameters and device array
+  const double* cost_data;
   int W, Ws;                // stacked constraint rows, of which Ws are state rows
   int row_var[kMaxRows];    // 0 = state, 1 = control
   int row_idx[kMaxRows];
   double row_sign[kMaxRows];
   double row_bound[kMaxRows];
 };
+
+// Models whose cost is user code (user_model.cuh UserModel with a cost
+// source) expose kUserCost and the functions ucost / ucost_derivs / uterm /
+// uterm_grad / uterm_hess; every other model uses the quadratic cost of
+// ProblemParams through the functions below.
+template <class D, class = void>
+struct UserCostOf : std::false_type {};
+template <class D>
+struct UserCostOf<D, std::void_t<decltype(D::kUserCost)>> : std::bool_constant<D::kUserCost> {};
+template <class D>
+constexpr bool kUserCost = UserCostOf<D>::value;
 
 // Augmentation state for one launch (reference AugmentedCost variants)
 template <typename R>

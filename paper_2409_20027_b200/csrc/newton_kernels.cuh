@@ -65,6 +65,7 @@ struct NewtonArgs {
   // time-block mode (ptc_solver_block_phase): stages [t_base, t_base + T) of
   // a longer horizon; blk_last = the block ends it (terminal cost / gradient)
   int blk, blk_last, t_base;
+  int uterm;               // user-defined cost: the terminal cost is in the partials
   R* lam_in;               // (nx, 1, B) co-state entering at the block end
   R* x_in;                 // (nx, 1, B) state at the block start (rollout carry)
   const R* x0g;            // (nx, 1, B) the horizon's initial state (phase argument)
@@ -211,7 +212,7 @@ __global__ void k_admm_init(NewtonArgs<R> a) {
 // ------------------------------------------------------- cost of a trajectory
 
 // which = 0: current trajectory (only when PH_NEED_COST), 1: the candidate
-template <typename R, int NX, int NU>
+template <typename R, int NX, int NU, class Dyn = void>
 __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int which) {
   // cost constants: registers for small states, the block's shared copy for
   // wide ones (loaded before any thread leaves)
@@ -236,11 +237,19 @@ __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int whic
     R x[NX], u[NU];
     ld_x(a, q, t, b, x);
     ld_u(a, q, t, b, u);
-    if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
+    if constexpr (!std::is_void_v<Dyn> && kUserCost<Dyn>) sl += double(Dyn::ucost(p, t, x, u));
+    else if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
     else sl += double(stage_cost<R, NX, NU>(cs_shared, x, u));
     int br;
     sc += double(aug_value<R, NX, NU>(p, g, t, T, B, b, x, u, br));
     if (br >= 0 && bad < 0) bad = t * p.W + br;
+  }
+  if constexpr (!std::is_void_v<Dyn> && kUserCost<Dyn>) {
+    if (j == P0 - 1) {   // the terminal cost rides in the last unit's partial
+      R xT[NX];
+      ld_x(a, q, T, b, xT);
+      sl += double(Dyn::uterm(p, xT));
+    }
   }
   double* cp = a.cpart[which];
   cp[((size_t)0 * P0 + j) * B + b] = sl;
@@ -277,11 +286,17 @@ __global__ void __launch_bounds__(128) k_costate_up0(NewtonArgs<R> a) {
     R cx[NX], cu[NU], cxx[NX], cuu[NU];
     aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
     Aff<R, NX> m;
+    R ulx[NX];
+    if constexpr (kUserCost<Dyn>) Dyn::ucost_grad(p, t, x, u, ulx);
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
       R lx = R(0);
+      if constexpr (kUserCost<Dyn>) {
+        lx = ulx[i];
+      } else {
 #pragma unroll
-      for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+        for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+      }
       m.e[i] = lx + cx[i];
 #pragma unroll
       for (int k = 0; k < NX; ++k) m.F[i][k] = D.fx[k][i];
@@ -289,7 +304,8 @@ __global__ void __launch_bounds__(128) k_costate_up0(NewtonArgs<R> a) {
     if (t == T - 1) {
       R xT[NX], lT[NX], fl[NX];
       ld_x(a, q, T, b, xT);
-      terminal_grad(p, xT, lT);
+      if constexpr (kUserCost<Dyn>) Dyn::uterm_grad(p, xT, lT);
+      else terminal_grad(p, xT, lT);
       mv<NX, NX>(m.F, lT, fl);
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
@@ -380,6 +396,31 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
   Dyn::template derivs<true>(p, t, b, x, u, ln, D);
   R cx[NX], cu[NU], cxx[NX], cuu[NU];
   aug_derivs<R, NX, NU>(p, g, t, a.T, a.B, b, x, u, cx, cu, cxx, cuu);
+  if constexpr (kUserCost<Dyn>) {
+    // user cost: l's derivatives from the model's code (passes.py:171-181
+    // adds lxx + cxx + lambda fxx etc. in this order)
+    R lx[NX], lu[NU], lxx[NX][NX], luu[NU][NU], lxu[NX][NU];
+    Dyn::ucost_derivs(p, t, x, u, lx, lu, lxx, luu, lxu);
+    for (int i = 0; i < NX; ++i)
+      for (int k = 0; k < NX; ++k) st.P[i][k] = (lxx[i][k] + (i == k ? cxx[i] : R(0))) + D.Hxx[i][k];
+    symmetrize<NX>(st.P);
+    for (int i = 0; i < NU; ++i)
+      for (int k = 0; k < NU; ++k) st.Rr[i][k] = (luu[i][k] + (i == k ? cuu[i] : R(0))) + D.Huu[i][k];
+    symmetrize<NU>(st.Rr);
+    R ftl[NU], fxl[NX];
+    mtv<NU, NX>(D.fu, ln, ftl);
+    mtv<NX, NX>(D.fx, ln, fxl);
+    for (int i = 0; i < NU; ++i) st.d[i] = (lu[i] + cu[i]) + ftl[i];
+    for (int i = 0; i < NX; ++i) lt[i] = (lx[i] + cx[i]) + fxl[i];
+    for (int i = 0; i < NX; ++i) {
+      for (int k = 0; k < NU; ++k) {
+        st.M[i][k] = lxu[i][k] + D.Hxu[i][k];
+        st.Fu[i][k] = D.fu[i][k];
+      }
+      for (int k = 0; k < NX; ++k) st.Fx[i][k] = D.fx[i][k];
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < NX; ++i)
 #pragma unroll
@@ -445,13 +486,18 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
   if (j == P0 - 1) {
     R xT[NX];
     ld_x(a, q, T, b, xT);
-    terminal_grad(p, xT, ln);
-    st_vec(a.lam, T, T + 1, B, b, ln);
     R PT[NX][NX];
+    if constexpr (kUserCost<Dyn>) {
+      Dyn::uterm_grad(p, xT, ln);
+      Dyn::uterm_hess(p, xT, PT);
+    } else {
+      terminal_grad(p, xT, ln);
 #pragma unroll
-    for (int i = 0; i < NX; ++i)
+      for (int i = 0; i < NX; ++i)
 #pragma unroll
-      for (int k = 0; k < NX; ++k) PT[i][k] = R(p.Qf[i * NX + k]);
+        for (int k = 0; k < NX; ++k) PT[i][k] = R(p.Qf[i * NX + k]);
+    }
+    st_vec(a.lam, T, T + 1, B, b, ln);
     symmetrize<NX>(PT);
     st_mat(a.PT, 0, 1, B, b, PT);
   } else {
@@ -474,13 +520,18 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
       Dyn::template derivs<false>(p, t, b, x, u, ln, D);
       R cx[NX], cu[NU], cxx[NX], cuu[NU];
       aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
-      R fxl[NX];
+      R fxl[NX], ulx[NX];
       mtv<NX, NX>(D.fx, ln, fxl);
+      if constexpr (kUserCost<Dyn>) Dyn::ucost_grad(p, t, x, u, ulx);
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
         R lx = R(0);
+        if constexpr (kUserCost<Dyn>) {
+          lx = ulx[i];
+        } else {
 #pragma unroll
-        for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+          for (int k = 0; k < NX; ++k) lx += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+        }
         lt[i] = (lx + cx[i]) + fxl[i];
       }
     } else {
@@ -527,19 +578,24 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
   // stage's expansion, so the co-states never touch HBM.  Boundary:
   // lambda_T = terminal gradient, P_T = sym(Qf) (passes.py:140-148).
   VCarry<R, NX> c;
-#pragma unroll
-  for (int i = 0; i < NX; ++i)
-#pragma unroll
-    for (int k = 0; k < NX; ++k) c.Y[i][k] = R(p.Qf[i * NX + k]);
-  symmetrize<NX>(c.Y);
-  set_zero(c.eta);
   int fl = 0;
   R ln[NX], x[NX], u[NU];
   {
     R xT[NX];
     ld_x(a, q, T, b, xT);
-    terminal_grad(p, xT, ln);
+    if constexpr (kUserCost<Dyn>) {
+      Dyn::uterm_grad(p, xT, ln);
+      Dyn::uterm_hess(p, xT, c.Y);
+    } else {
+      terminal_grad(p, xT, ln);
+#pragma unroll
+      for (int i = 0; i < NX; ++i)
+#pragma unroll
+        for (int k = 0; k < NX; ++k) c.Y[i][k] = R(p.Qf[i * NX + k]);
+    }
   }
+  symmetrize<NX>(c.Y);
+  set_zero(c.eta);
   ld_x(a, q, T - 1, b, x);
   ld_u(a, q, T - 1, b, u);
   for (int t = T - 1; t >= 0; --t) {
@@ -735,7 +791,8 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
         fetch(t + kRing, ring[k]);
         if (!kFromUc) st_vec(Uc, t, T, B, b, u);
         if constexpr (kCost) {
-          if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
+          if constexpr (kUserCost<Dyn>) sl += double(Dyn::ucost(gp, t, x, u));
+          else if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
           else sl += double(stage_cost<R, NX, NU>(gp, x, u));
           int br;
           sc += double(aug_value<R, NX, NU>(gp, g, t, T, B, b, x, u, br));
@@ -754,6 +811,7 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
   }
   if (!finite) atomicOr(a.flags + b, FLAG_DIVERGED);
   if constexpr (kCost) {
+    if constexpr (kUserCost<Dyn>) sl += double(Dyn::uterm(gp, x));   // x = x_T
     double* cp = a.cpart[1];  // P0 == 1
     cp[(size_t)0 * B + b] = sl;
     cp[(size_t)1 * B + b] = sc;
@@ -1013,7 +1071,8 @@ PTC_D double finalize_cost(const NewtonArgs<R>& a, int which, int q, int b, int&
     int bj = int(cp[((size_t)2 * P0 + j) * a.B + b]);
     if (bad < 0 && bj >= 0) bad = bj;
   }
-  if (a.blk) return sl + sc;   // block mode: the terminal cost is in the reduced partials
+  // block mode / user cost: the terminal cost is in the (reduced) partials
+  if (a.blk || a.uterm) return sl + sc;
   R xT[NX];
   ld_x(a, q, a.T, b, xT);
   double term = double(terminal_cost(*a.pp, xT));

@@ -71,6 +71,42 @@ class TVLinear(DynamicsModel):
         return self.B[:len(us)]
 
 
+class CosineCost(pintoc.CostModel):
+    """User-defined, non-quadratic cost plugged into the reference API: a
+    periodic angle penalty w0 (1 - cos theta) + w1 omega^2 / 2 + r u^2 / 2,
+    terminal W0 (1 - cos theta) + W1 omega^2 / 2."""
+
+    def __init__(self, w0, w1, r, W0, W1):
+        self.w0, self.w1, self.r, self.W0, self.W1 = w0, w1, r, W0, W1
+
+    def l(self, t, x, u):
+        return self.w0 * (1.0 - np.cos(x[0])) + 0.5 * self.w1 * x[1] ** 2 + 0.5 * self.r * u[0] ** 2
+
+    def lx(self, t, x, u):
+        return np.array([self.w0 * np.sin(x[0]), self.w1 * x[1]])
+
+    def lu(self, t, x, u):
+        return np.array([self.r * u[0]])
+
+    def lxx(self, t, x, u):
+        return np.diag([self.w0 * np.cos(x[0]), self.w1])
+
+    def luu(self, t, x, u):
+        return np.array([[self.r]])
+
+    def lxu(self, t, x, u):
+        return np.zeros((2, 1))
+
+    def terminal(self, x):
+        return self.W0 * (1.0 - np.cos(x[0])) + 0.5 * self.W1 * x[1] ** 2
+
+    def terminal_x(self, x):
+        return np.array([self.W0 * np.sin(x[0]), self.W1 * x[1]])
+
+    def terminal_xx(self, x):
+        return np.diag([self.W0 * np.cos(x[0]), self.W1])
+
+
 def rand_spd(rng, n, scale=1.0):
     a = rng.normal(size=(n, n))
     return scale * (a @ a.T + n * np.eye(n))
@@ -321,6 +357,30 @@ def case_barrier_tvlinear():
     save("barrier_tvlinear", **out)
 
 
+def case_barrier_pendulum_cosine():
+    """A user-defined cost (CosineCost) on the pendulum swing-up (T=40,
+    dt 0.05, reference default barrier, 300 iterations per round)."""
+    T = 40
+    dyn = PendulumDynamics(T, PendulumParams(damping=0.1, dt=0.05))
+    cost = CosineCost(10.0, 0.1, 0.01, 100.0, 10.0)
+    box = BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0)
+    rng = np.random.default_rng(77)
+    u0 = np.clip(rng.standard_normal((T, 1)), -4.5, 4.5)
+    x0 = np.array([math.pi - 0.3, 0.0])
+    opts = BarrierOptions(newton=NewtonOptions(max_iters=300))
+    prob = ControlProblem(dyn, cost, box)
+    traj, rep = barrier_solve(prob, rollout(dyn, x0, u0), opts)
+    out = dict(x0=x0, u0=u0, weights=np.array([10.0, 0.1, 0.01, 100.0, 10.0]))
+    _barrier_record("sol", traj, rep, out)
+
+    def solve(xp, up):
+        t, r = barrier_solve(prob, rollout(dyn, xp, up), opts)
+        return t, [q.newton.iterations for q in r.rounds]
+    out.update({"sol_" + k: v for k, v in noise_floor(
+        solve, x0, u0, traj, [q.newton.iterations for q in rep.rounds]).items()})
+    save("barrier_pendulum_cosine", **out)
+
+
 def _admm_record(prefix, traj, rep, out):
     out[f"{prefix}_xs"], out[f"{prefix}_us"] = traj.states, traj.controls
     out[f"{prefix}_z"], out[f"{prefix}_v"] = rep.state.z, rep.state.v
@@ -450,7 +510,8 @@ def case_criterion5_pendulum():
 
 
 FAST = [case_lqr_small, case_lqr_config1, case_passes_models, case_newton_lq,
-        case_barrier_pendulum_cfg0, case_barrier_pendulum_conv, case_barrier_tvlinear, case_admm_small]
+        case_barrier_pendulum_cfg0, case_barrier_pendulum_conv, case_barrier_tvlinear, case_admm_small,
+        case_barrier_pendulum_cosine]
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()

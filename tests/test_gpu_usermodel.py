@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 from conftest import golden, rel_gap
 from restart_util import check_iterations, device_restart
-from user_models import user_pendulum, user_tvlinear
+from user_models import user_cosine_cost, user_pendulum, user_tvlinear
 
 pytestmark = pytest.mark.gpu
 
@@ -90,3 +90,50 @@ def test_user_model_batched_and_fp32():
     bs32 = P.BatchSolver(prob, B, "barrier", barrier=opts, dtype=torch.float32)
     X32 = bs32.rollout(x0, u0.float())
     assert torch.isfinite(X32).all()
+
+
+def test_user_cost_matches_reference():
+    """make_golden's CosineCost -- a user CostModel with a non-quadratic,
+    indefinite-Hessian stage cost and terminal cost -- written against the
+    device hook (DeviceCost) matches pintoc's barrier run of it: per-round
+    counts, iteration histories, trajectory at 1e-9."""
+    import paper_2409_20027_b200 as P
+    from test_gpu_newton import _check_hist, _hist
+    g = golden("barrier_pendulum_cosine")
+    w = g["weights"]
+    dyn = user_pendulum(40)
+    cost = user_cosine_cost(*w)
+    box = P.BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0)
+    prob = P.ControlProblem(dyn, cost, box)
+    init = P.rollout(dyn, g["x0"], g["u0"])
+    for ex in ("sequential", "parallel"):
+        traj, rep = P.barrier_solve(prob, init, P.BarrierOptions(
+            newton=P.NewtonOptions(max_iters=300, executor=ex)))
+        assert [r.newton.iterations for r in rep.rounds] == list(g["sol_round_iters"]), ex
+        assert [r.newton.termination for r in rep.rounds] == list(g["sol_round_term"])
+        for k, r in enumerate(rep.rounds):
+            _check_hist_band(_hist(r.newton), g[f"sol_hist{k}"])
+        assert rel_gap(traj.controls, g["sol_us"]) < TOL
+        assert rel_gap(traj.states, g["sol_xs"]) < TOL
+        assert rel_gap([r.cost for r in rep.rounds], g["sol_round_cost"]) < TOL
+
+
+def _check_hist_band(hist, ref):
+    """Iteration records equal: accept flags exactly, costs and step norms
+    at 1e-9, the gain ratio -- (cur - new) / pred, a difference quotient of
+    two costs -- within 1e-9 (|cur| + |new|) / |pred| (restart_util), and
+    alpha, which the LM rule derives from the ratios, at 1e-6 (as
+    test_gpu_newton's records)."""
+    assert hist.shape == ref.shape
+    assert np.array_equal(hist[:, 4], ref[:, 4])
+    for col, tol in ((0, TOL), (1, 1e-6), (3, TOL)):
+        fin = np.isfinite(ref[:, col])
+        assert np.array_equal(np.isfinite(hist[:, col]), fin), col
+        gap = np.abs(hist[fin, col] - ref[fin, col]) / np.maximum(1.0, np.abs(ref[fin, col]))
+        assert gap.max(initial=0.0) < tol, col
+    prev = np.concatenate([[np.nan], ref[:-1, 0]])
+    fin = np.isfinite(ref[:, 2]) & (ref[:, 4] > 0.5) & np.isfinite(prev)
+    if fin.any():
+        pred = np.abs(prev[fin] - ref[fin, 0]) / np.abs(ref[fin, 2])
+        band = TOL * (np.abs(prev[fin]) + np.abs(ref[fin, 0])) / pred + TOL * np.abs(ref[fin, 2])
+        assert np.all(np.abs(hist[fin, 2] - ref[fin, 2]) <= band)

@@ -68,8 +68,36 @@ def precompile():
     """Build the test models' libraries (build() does this so GPU runs load
     them without compiling)."""
     import numpy as np
-    paths = [user_pendulum(8).library()]
+    paths = [user_pendulum(8).library(), user_pendulum(8).library(user_cosine_cost())]
     for nx, nu in ((4, 2),):
         z = np.zeros((3, nx, nx)), np.zeros((3, nx, nu)), np.zeros((3, nx))
         paths.append(user_tvlinear(*z).library())
     return paths
+
+
+# make_golden.py's CosineCost (a user CostModel in pintoc) as device code:
+# prm = (w0, w1, r, W0, W1)
+COS_STAGE = "l = R(prm[0]) * (R(1) - cos(x[0])) + R(0.5 * prm[1]) * x[1] * x[1]" \
+            " + R(0.5 * prm[2]) * u[0] * u[0];"
+COS_GRAD = """
+    lx[0] = R(prm[0]) * sin(x[0]);
+    lx[1] = R(prm[1]) * x[1];
+    lu[0] = R(prm[2]) * u[0];
+    lxx[0][0] = R(prm[0]) * cos(x[0]);
+    lxx[1][1] = R(prm[1]);
+    luu[0][0] = R(prm[2]);
+"""
+COS_TERM = "V = R(prm[3]) * (R(1) - cos(x[0])) + R(0.5 * prm[4]) * x[1] * x[1];"
+COS_TERM_GRAD = """
+    Vx[0] = R(prm[3]) * sin(x[0]);
+    Vx[1] = R(prm[4]) * x[1];
+    Vxx[0][0] = R(prm[3]) * cos(x[0]);
+    Vxx[1][1] = R(prm[4]);
+"""
+
+
+def user_cosine_cost(w0=10.0, w1=0.1, r=0.01, W0=100.0, W1=10.0):
+    from paper_2409_20027_b200.usermodel import DeviceCost
+    return DeviceCost(stage=COS_STAGE, gradients=COS_GRAD, terminal=COS_TERM,
+                      terminal_gradients=COS_TERM_GRAD, params=(w0, w1, r, W0, W1),
+                      name="cosine")
