@@ -276,6 +276,12 @@ typedef struct ptc_problem_desc {
    * parameters (`cprm`) and device float64 array (`cdata`, may be NULL) */
   double cost_params[8];
   const void* cost_data;
+  /* user-defined constraints (a model library built with a constraint
+   * source): state / control row counts (the box fields stay NULL), their
+   * parameters and device float64 array */
+  int32_t con_rows_state, con_rows_control;
+  double con_params[8];
+  const void* con_data;
 } ptc_problem_desc;
 
 /* Register a user-defined dynamics model (reference problem.py:59-112: a

@@ -90,12 +90,14 @@ class DeviceSolver:
         self.nx, self.nu = int(dynamics.d_x), int(dynamics.d_u)
         npdt = np.float64 if self.dtype == torch.float64 else np.float32
 
-        from .usermodel import DeviceCost, DeviceDynamics
-        if isinstance(cost, DeviceCost):
+        from .usermodel import DeviceConstraint, DeviceCost, DeviceDynamics
+        ucost = cost if isinstance(cost, DeviceCost) else None
+        ucon = constraints if isinstance(constraints, DeviceConstraint) else None
+        if ucost is not None or ucon is not None:
             if not isinstance(dynamics, DeviceDynamics):
-                raise ValueError("a DeviceCost is compiled into the model library of a "
-                                 "DeviceDynamics; write the dynamics as one too")
-            spec = dynamics._device_spec(cost)
+                raise ValueError("a DeviceCost / DeviceConstraint is compiled into the model "
+                                 "library of a DeviceDynamics; write the dynamics as one too")
+            spec = dynamics._device_spec(ucost, ucon)
         else:
             spec = dynamics._device_spec()
         cspec = cost._device_spec()
@@ -138,6 +140,15 @@ class DeviceSolver:
         d.goal = dptr(cspec["goal"])
         for k in ("state_lower", "state_upper", "control_lower", "control_upper"):
             setattr(d, k, dptr(bspec.get(k)))
+        if "con_rows_state" in bspec:
+            d.con_rows_state = bspec["con_rows_state"]
+            d.con_rows_control = bspec["con_rows_control"]
+            for i, v in enumerate(bspec["con_params"]):
+                d.con_params[i] = float(v)
+            if bspec.get("con_data") is not None:
+                d.con_data = bspec["con_data"].data_ptr()
+                keep.append(bspec["con_data"])
+                self._con_data = bspec["con_data"]
         s = settings
         d.method, d.aug, d.aug_mu = s.method, s.aug, s.aug_mu
         d.alpha0, d.nu0, d.inner_tol, d.max_iters = s.alpha0, s.nu0, s.inner_tol, s.max_iters

@@ -55,6 +55,8 @@ class ProblemDesc(C.Structure):
         ("block_mode", C.c_int32), ("t_base", C.c_int32), ("block_last", C.c_int32),
         ("user_data", C.c_void_p),
         ("cost_params", C.c_double * 8), ("cost_data", C.c_void_p),
+        ("con_rows_state", C.c_int32), ("con_rows_control", C.c_int32),
+        ("con_params", C.c_double * 8), ("con_data", C.c_void_p),
     ]
 
 

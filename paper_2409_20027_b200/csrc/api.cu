@@ -778,6 +778,12 @@ struct Solver final : ptc_solver {
     p.user_data = static_cast<const double*>(d.user_data);
     for (int i = 0; i < 8; ++i) p.cost_prm[i] = d.cost_params[i];
     p.cost_data = static_cast<const double*>(d.cost_data);
+    for (int i = 0; i < 8; ++i) p.con_prm[i] = d.con_params[i];
+    p.con_data = static_cast<const double*>(d.con_data);
+    if (d.con_rows_state + d.con_rows_control > 0) {   // user constraint rows
+      p.Ws = d.con_rows_state;
+      p.W = d.con_rows_state + d.con_rows_control;
+    }
   }
 
   static size_t layout(const ptc_problem_desc& d, Carver& c, Solver* self) {

@@ -362,7 +362,8 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[1], 3, kOpsCost, (int)P0, (int)B);
   }
   k_control<R, NX, NU><<<grid_for(B), kBlock, 0, s>>>(a);
-  k_round_end<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  if constexpr (kUserCon<Dyn>) k_user_bad_value<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a);
+  k_round_end<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
   if (fold && a.apart && a.opt.method == METHOD_ADMM)
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.apart, 2, RED_MAX | (RED_MAX << 2), (int)P0, (int)B);
   k_outer<R><<<grid_for(B), kBlock, 0, s>>>(a);
@@ -478,7 +479,7 @@ struct RegisterNewton {
     const NewtonArgs<R>& a = A(p);
     k_init_state<R><<<grid_for(a.B), kBlock, 0, s>>>(a);
     if (a.opt.method == METHOD_ADMM)
-      k_admm_init<R, NX, NU><<<grid_for((long long)a.T * a.B), kBlock, 0, s>>>(a);
+      k_admm_init<R, NX, NU, Dyn><<<grid_for((long long)a.T * a.B), kBlock, 0, s>>>(a);
   }
   static void check(const void* p, int* bad_t, cudaStream_t s) {
     const NewtonArgs<R>& a = A(p);
@@ -512,6 +513,7 @@ struct RegisterNewton {
                                                       RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4),
                                                       P0, a.B);
     k_cost_finalize<R, NX, NU><<<grid_for(a.B), kBlock, 0, s>>>(a);
+    if constexpr (kUserCon<Dyn>) k_user_bad_value<R, Dyn><<<grid_for(a.B), kBlock, 0, s>>>(a);
   }
   static void block(const void* p, const void* la, int phase, const void* in, void* out,
                     int rank, int world, cudaStream_t s) {

@@ -39,6 +39,8 @@ struct ProblemParams {
   const double* user_data;  // user-defined model (user_model.cuh): its device array or null
   double cost_prm[8];       // user-defined cost: its parameters and device array
   const double* cost_data;
+  double con_prm[8];        // user-defined constraints: parameters and device array
+  const double* con_data;
   int W, Ws;                // stacked constraint rows, of which Ws are state rows
   int row_var[kMaxRows];    // 0 = state, 1 = control
   int row_idx[kMaxRows];
@@ -56,6 +58,14 @@ template <class D>
 struct UserCostOf<D, std::void_t<decltype(D::kUserCost)>> : std::bool_constant<D::kUserCost> {};
 template <class D>
 constexpr bool kUserCost = UserCostOf<D>::value;
+// ... and models whose constraints are user code (kUserCon: kWs state rows
+// g_t(x), kWc control rows h_t(u), functions ucon_w / ucon_derivs)
+template <class D, class = void>
+struct UserConOf : std::false_type {};
+template <class D>
+struct UserConOf<D, std::void_t<decltype(D::kUserCon)>> : std::bool_constant<D::kUserCon> {};
+template <class D>
+constexpr bool kUserCon = UserConOf<D>::value;
 
 // Augmentation state for one launch (reference AugmentedCost variants)
 template <typename R>
@@ -550,6 +560,87 @@ PTC_D void aug_derivs(const ProblemParams& p, const AugArgs<R>& a, int t, int T,
   for (int i = 0; i < NX; ++i) { cx[i] *= rho; cxx[i] *= rho; }
 #pragma unroll
   for (int i = 0; i < NU; ++i) { cu[i] *= rho; cuu[i] *= rho; }
+}
+
+// ------------------------------------------------ user constraint models
+// The augmentations of a model with user constraints w = [g_t(x); h_t(u)]
+// (reference ConstraintModel, problem.py:167-230; barrier outer.py:30-157,
+// ADMM outer.py:252-333), with full Hessians (rows may couple variables).
+
+template <typename R, class Dyn>
+PTC_D R aug_value_user(const ProblemParams& p, const AugArgs<R>& a, int t, int T, int B, int b,
+                       const R (&x)[Dyn::NX], const R (&u)[Dyn::NU], int& bad_row) {
+  constexpr int W = Dyn::kWs + Dyn::kWc;
+  bad_row = -1;
+  if (a.kind == AUG_ZERO) return R(0);
+  R w[W > 0 ? W : 1];
+  Dyn::ucon_w(p, t, x, u, w);
+  if (a.kind == AUG_BARRIER) {
+    R sg = R(0), sh = R(0);
+    for (int k = 0; k < W; ++k) {
+      if (w[k] >= R(0) && bad_row < 0) bad_row = k;
+      const R lg = log(-w[k]);
+      if (k < Dyn::kWs) sg += lg; else sh += lg;
+    }
+    return -R(a.mu[b]) * (sg + sh);
+  }
+  const R rho = R(a.rho);
+  R acc = R(0);
+  for (int k = 0; k < W; ++k) {
+    const R res = w[k] - ldf(a.z, k, t, T, B, b) + ldf(a.v, k, t, T, B, b) / rho;
+    acc += res * res;
+  }
+  return R(0.5) * rho * acc;
+}
+
+// gradients cx, cu and full Hessians Cxx, Cuu (the cross term vanishes:
+// g depends on x, h on u)
+template <typename R, class Dyn>
+PTC_D void aug_derivs_user(const ProblemParams& p, const AugArgs<R>& a, int t, int T, int B,
+                           int b, const R (&x)[Dyn::NX], const R (&u)[Dyn::NU],
+                           R (&cx)[Dyn::NX], R (&cu)[Dyn::NU], R (&Cxx)[Dyn::NX][Dyn::NX],
+                           R (&Cuu)[Dyn::NU][Dyn::NU]) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU, WS = Dyn::kWs, WC = Dyn::kWc;
+  set_zero(cx);
+  set_zero(cu);
+  set_zero(Cxx);
+  set_zero(Cuu);
+  if (a.kind == AUG_ZERO) return;
+  R w[WS + WC > 0 ? WS + WC : 1];
+  R gx[Dyn::kWsA][NX], hu[Dyn::kWcA][NU];
+  R gxx[Dyn::kWsA][NX][NX], huu[Dyn::kWcA][NU][NU];
+  Dyn::ucon_derivs(p, t, x, u, w, gx, hu, gxx, huu);
+  // weights: barrier  cx = -mu gx^T (1/g), Cxx = mu (S^T S - sum_k gxx_k / g_k), S = gx / g
+  //          ADMM     cx = rho gx^T r,     Cxx = rho (gx^T gx + sum_k r_k gxx_k)
+  const bool barrier = a.kind == AUG_BARRIER;
+  const R mu = barrier ? R(a.mu[b]) : R(0), rho = R(a.rho);
+  for (int k = 0; k < WS + WC; ++k) {
+    R c1, c2, c0;   // gradient weight, second-derivative weight, outer-product weight
+    if (barrier) {
+      const R inv = R(1) / w[k];
+      c1 = -mu * inv;
+      c2 = -mu * inv;
+      c0 = mu * inv * inv;
+    } else {
+      const R res = w[k] - ldf(a.z, k, t, T, B, b) + ldf(a.v, k, t, T, B, b) / rho;
+      c1 = rho * res;
+      c2 = rho * res;
+      c0 = rho;
+    }
+    if (k < WS) {
+      const int r = k;
+      for (int i = 0; i < NX; ++i) {
+        cx[i] += c1 * gx[r][i];
+        for (int j = 0; j < NX; ++j) Cxx[i][j] += c0 * gx[r][i] * gx[r][j] + c2 * gxx[r][i][j];
+      }
+    } else {
+      const int r = k - WS;
+      for (int i = 0; i < NU; ++i) {
+        cu[i] += c1 * hu[r][i];
+        for (int j = 0; j < NU; ++j) Cuu[i][j] += c0 * hu[r][i] * hu[r][j] + c2 * huu[r][i][j];
+      }
+    }
+  }
 }
 
 }  // namespace ptc

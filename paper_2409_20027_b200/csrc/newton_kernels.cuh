@@ -193,7 +193,7 @@ __global__ void k_check_consistent(NewtonArgs<R> a, int* bad_t) {
 }
 
 // ADMM start: z = Pi_C(w(x, u)), v = 0   (outer.py:409-410)
-template <typename R, int NX, int NU>
+template <typename R, int NX, int NU, class Dyn = void>
 __global__ void k_admm_init(NewtonArgs<R> a) {
   const int i = unit_id();
   if (i >= a.T * a.B) return;
@@ -202,6 +202,16 @@ __global__ void k_admm_init(NewtonArgs<R> a) {
   R x[NX], u[NU];
   ld_x(a, 0, t, b, x);
   ld_u(a, 0, t, b, u);
+  if constexpr (!std::is_void_v<Dyn> && kUserCon<Dyn>) {
+    constexpr int W = Dyn::kWs + Dyn::kWc;
+    R w[W > 0 ? W : 1];
+    Dyn::ucon_w(p, t, x, u, w);
+    for (int k = 0; k < W; ++k) {
+      stf(a.z, k, t, a.T, a.B, b, w[k] < R(0) ? w[k] : R(0));
+      stf(a.v, k, t, a.T, a.B, b, R(0));
+    }
+    return;
+  }
   for (int k = 0; k < p.W; ++k) {
     R w = row_value<R, NX, NU>(p, k, x, u);
     stf(a.z, k, t, a.T, a.B, b, w < R(0) ? w : R(0));
@@ -241,7 +251,10 @@ __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int whic
     else if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
     else sl += double(stage_cost<R, NX, NU>(cs_shared, x, u));
     int br;
-    sc += double(aug_value<R, NX, NU>(p, g, t, T, B, b, x, u, br));
+    if constexpr (!std::is_void_v<Dyn> && kUserCon<Dyn>)
+      sc += double(aug_value_user<R, Dyn>(p, g, t, T, B, b, x, u, br));
+    else
+      sc += double(aug_value<R, NX, NU>(p, g, t, T, B, b, x, u, br));
     if (br >= 0 && bad < 0) bad = t * p.W + br;
   }
   if constexpr (!std::is_void_v<Dyn> && kUserCost<Dyn>) {
@@ -283,8 +296,14 @@ __global__ void __launch_bounds__(128) k_costate_up0(NewtonArgs<R> a) {
     set_zero(lam0);
     DynDerivs<R, NX, NU> D;
     Dyn::template derivs<false>(p, t, b, x, u, lam0, D);
-    R cx[NX], cu[NU], cxx[NX], cuu[NU];
-    aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
+    R cx[NX], cu[NU];
+    if constexpr (kUserCon<Dyn>) {
+      R Cxx[NX][NX], Cuu[NU][NU];
+      aug_derivs_user<R, Dyn>(p, g, t, T, B, b, x, u, cx, cu, Cxx, Cuu);
+    } else {
+      R cxx[NX], cuu[NU];
+      aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
+    }
     Aff<R, NX> m;
     R ulx[NX];
     if constexpr (kUserCost<Dyn>) Dyn::ucost_grad(p, t, x, u, ulx);
@@ -394,18 +413,48 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
   constexpr int NX = Dyn::NX, NU = Dyn::NU;
   DynDerivs<R, NX, NU> D;
   Dyn::template derivs<true>(p, t, b, x, u, ln, D);
-  R cx[NX], cu[NU], cxx[NX], cuu[NU];
-  aug_derivs<R, NX, NU>(p, g, t, a.T, a.B, b, x, u, cx, cu, cxx, cuu);
-  if constexpr (kUserCost<Dyn>) {
-    // user cost: l's derivatives from the model's code (passes.py:171-181
-    // adds lxx + cxx + lambda fxx etc. in this order)
+  if constexpr (kUserCost<Dyn> || kUserCon<Dyn>) {
+    // a user cost and / or user constraints: l's and the augmentation's
+    // derivatives as full matrices (passes.py:171-181 adds lxx + cxx +
+    // lambda fxx etc. in this order)
     R lx[NX], lu[NU], lxx[NX][NX], luu[NU][NU], lxu[NX][NU];
-    Dyn::ucost_derivs(p, t, x, u, lx, lu, lxx, luu, lxu);
+    if constexpr (kUserCost<Dyn>) {
+      Dyn::ucost_derivs(p, t, x, u, lx, lu, lxx, luu, lxu);
+    } else {
+      set_zero(lxu);
+      for (int i = 0; i < NX; ++i) {
+        R acc = R(0);
+        for (int k = 0; k < NX; ++k) {
+          acc += (x[k] - R(p.goal[k])) * R(p.Q[i * NX + k]);
+          lxx[i][k] = R(p.Q[i * NX + k]);
+        }
+        lx[i] = acc;
+      }
+      for (int i = 0; i < NU; ++i) {
+        R acc = R(0);
+        for (int k = 0; k < NU; ++k) {
+          acc += u[k] * R(p.Rc[i * NU + k]);
+          luu[i][k] = R(p.Rc[i * NU + k]);
+        }
+        lu[i] = acc;
+      }
+    }
+    R cx[NX], cu[NU], Cxx[NX][NX], Cuu[NU][NU];
+    if constexpr (kUserCon<Dyn>) {
+      aug_derivs_user<R, Dyn>(p, g, t, a.T, a.B, b, x, u, cx, cu, Cxx, Cuu);
+    } else {
+      R cxx[NX], cuu[NU];
+      aug_derivs<R, NX, NU>(p, g, t, a.T, a.B, b, x, u, cx, cu, cxx, cuu);
+      set_zero(Cxx);
+      set_zero(Cuu);
+      for (int i = 0; i < NX; ++i) Cxx[i][i] = cxx[i];
+      for (int i = 0; i < NU; ++i) Cuu[i][i] = cuu[i];
+    }
     for (int i = 0; i < NX; ++i)
-      for (int k = 0; k < NX; ++k) st.P[i][k] = (lxx[i][k] + (i == k ? cxx[i] : R(0))) + D.Hxx[i][k];
+      for (int k = 0; k < NX; ++k) st.P[i][k] = (lxx[i][k] + Cxx[i][k]) + D.Hxx[i][k];
     symmetrize<NX>(st.P);
     for (int i = 0; i < NU; ++i)
-      for (int k = 0; k < NU; ++k) st.Rr[i][k] = (luu[i][k] + (i == k ? cuu[i] : R(0))) + D.Huu[i][k];
+      for (int k = 0; k < NU; ++k) st.Rr[i][k] = (luu[i][k] + Cuu[i][k]) + D.Huu[i][k];
     symmetrize<NU>(st.Rr);
     R ftl[NU], fxl[NX];
     mtv<NU, NX>(D.fu, ln, ftl);
@@ -421,6 +470,8 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
     }
     return;
   }
+  R cx[NX], cu[NU], cxx[NX], cuu[NU];
+  aug_derivs<R, NX, NU>(p, g, t, a.T, a.B, b, x, u, cx, cu, cxx, cuu);
 #pragma unroll
   for (int i = 0; i < NX; ++i)
 #pragma unroll
@@ -518,8 +569,14 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
       // as stage_expansion computes)
       DynDerivs<R, NX, NU> D;
       Dyn::template derivs<false>(p, t, b, x, u, ln, D);
-      R cx[NX], cu[NU], cxx[NX], cuu[NU];
-      aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
+      R cx[NX], cu[NU];
+      if constexpr (kUserCon<Dyn>) {
+        R Cxx[NX][NX], Cuu[NU][NU];
+        aug_derivs_user<R, Dyn>(p, g, t, T, B, b, x, u, cx, cu, Cxx, Cuu);
+      } else {
+        R cxx[NX], cuu[NU];
+        aug_derivs<R, NX, NU>(p, g, t, T, B, b, x, u, cx, cu, cxx, cuu);
+      }
       R fxl[NX], ulx[NX];
       mtv<NX, NX>(D.fx, ln, fxl);
       if constexpr (kUserCost<Dyn>) Dyn::ucost_grad(p, t, x, u, ulx);
@@ -795,7 +852,8 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
           else if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, x, u));
           else sl += double(stage_cost<R, NX, NU>(gp, x, u));
           int br;
-          sc += double(aug_value<R, NX, NU>(gp, g, t, T, B, b, x, u, br));
+          if constexpr (kUserCon<Dyn>) sc += double(aug_value_user<R, Dyn>(gp, g, t, T, B, b, x, u, br));
+          else sc += double(aug_value<R, NX, NU>(gp, g, t, T, B, b, x, u, br));
           if (br >= 0 && bad < 0) bad = t * gp.W + br;
         }
         R xn[NX];
@@ -1092,6 +1150,24 @@ PTC_D double infeasible_value(const NewtonArgs<R>& a, int q, int b, int bad) {
   return double(row_value<R, NX, NU>(*a.pp, k, x, u));
 }
 
+// User constraints: the InfeasibleError value k_control could not evaluate
+// (its row tables describe boxes only) from the model's own rows.
+template <typename R, class Dyn>
+__global__ void k_user_bad_value(NewtonArgs<R> a) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU, W = Dyn::kWs + Dyn::kWc;
+  const int b = unit_id();
+  if (b >= a.B) return;
+  const int bad = a.bad_index[b];
+  if (bad < 0 || W == 0) return;
+  const int t = bad / W, k = bad % W;
+  if (t >= a.T) return;
+  R x[NX], u[NU], w[W > 0 ? W : 1];
+  ld_x(a, a.parity[b], t, b, x);
+  ld_u(a, a.parity[b], t, b, u);
+  Dyn::ucon_w(*a.pp, t, x, u, w);
+  a.bad_value[b] = double(w[k]);
+}
+
 // One step of newton.py:157-208 for every running problem.
 template <typename R, int NX, int NU>
 __global__ void k_control(NewtonArgs<R> a) {
@@ -1212,7 +1288,7 @@ __global__ void k_control(NewtonArgs<R> a) {
 
 // per-stage work at the end of a Newton round: copy the round's controls
 // (barrier report) or run the ADMM consensus/dual update with residual maxima
-template <typename R, int NX, int NU>
+template <typename R, int NX, int NU, class Dyn = void>
 __global__ void __launch_bounds__(128) k_round_end(NewtonArgs<R> a) {
   const int P0 = a.plan.units0();
   const int u0 = unit_id();
@@ -1241,8 +1317,17 @@ __global__ void __launch_bounds__(128) k_round_end(NewtonArgs<R> a) {
     R x[NX], u[NU];
     ld_x(a, q, t, b, x);
     ld_u(a, q, t, b, u);
+    R wu[kMaxRows];
+    if constexpr (!std::is_void_v<Dyn> && kUserCon<Dyn>) {
+      constexpr int W = Dyn::kWs + Dyn::kWc;
+      R w_[W > 0 ? W : 1];
+      Dyn::ucon_w(p, t, x, u, w_);
+      for (int k = 0; k < W; ++k) wu[k] = w_[k];
+    }
     for (int k = 0; k < p.W; ++k) {
-      R w = row_value<R, NX, NU>(p, k, x, u);
+      R w;
+      if constexpr (!std::is_void_v<Dyn> && kUserCon<Dyn>) w = wu[k];
+      else w = row_value<R, NX, NU>(p, k, x, u);
       R zp = ldf(a.z, k, t, T, B, b);
       R vv = ldf(a.v, k, t, T, B, b);
       R zs = w + vv / rho;

@@ -62,7 +62,13 @@ def project_box(point, constraints=None):
 
 
 def assert_strictly_feasible(constraints: ConstraintModel, traj: Trajectory) -> None:
-    """Input validation of outer.py:163-177 (host check of the caller's data)."""
+    """Input validation of outer.py:163-177 (host check of the caller's data).
+    Constraints that only evaluate on the device (DeviceConstraint) are
+    checked there instead: the barrier solve's first cost evaluation raises
+    InfeasibleError(stage, component, value) at the first violated row."""
+    from .usermodel import DeviceConstraint
+    if isinstance(constraints, DeviceConstraint):
+        return
     w = constraints.w_batch(traj.states[:-1], traj.controls)
     st, comp = np.nonzero(w >= 0)
     if len(st):

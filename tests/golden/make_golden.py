@@ -107,6 +107,36 @@ class CosineCost(pintoc.CostModel):
         return np.diag([self.W0 * np.cos(x[0]), self.W1])
 
 
+class NormConstraints(pintoc.ConstraintModel):
+    """User-defined, nonlinear constraint rows plugged into the reference API:
+    g(x) = [omega^2 - wmax^2] <= 0, h(u) = [u^2 - umax^2] <= 0 (curved rows,
+    nonzero gxx / huu)."""
+
+    n_state = 1
+    n_control = 1
+
+    def __init__(self, wmax, umax):
+        self.wmax, self.umax = wmax, umax
+
+    def g(self, t, x):
+        return np.array([x[1] ** 2 - self.wmax ** 2])
+
+    def gx(self, t, x):
+        return np.array([[0.0, 2.0 * x[1]]])
+
+    def gxx(self, t, x):
+        return np.array([[[0.0, 0.0], [0.0, 2.0]]])
+
+    def h(self, t, u):
+        return np.array([u[0] ** 2 - self.umax ** 2])
+
+    def hu(self, t, u):
+        return np.array([[2.0 * u[0]]])
+
+    def huu(self, t, u):
+        return np.array([[[2.0]]])
+
+
 def rand_spd(rng, n, scale=1.0):
     a = rng.normal(size=(n, n))
     return scale * (a @ a.T + n * np.eye(n))
@@ -381,6 +411,41 @@ def case_barrier_pendulum_cosine():
     save("barrier_pendulum_cosine", **out)
 
 
+def case_pendulum_norm_constraints():
+    """User-defined constraints (NormConstraints: |omega| < 8, |u| < 5 as
+    curved rows) on the T=40 pendulum swing-up, barrier and ADMM."""
+    T = 40
+    dyn = PendulumDynamics(T, PendulumParams(damping=0.1, dt=0.05))
+    cost = QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0]),
+                         x_goal=np.zeros(2))
+    con = NormConstraints(8.0, 5.0)
+    prob = ControlProblem(dyn, cost, con)
+    rng = np.random.default_rng(91)
+    u0 = np.clip(0.5 * rng.standard_normal((T, 1)), -2.0, 2.0)
+    x0 = np.array([math.pi - 0.2, 0.0])
+    init = rollout(dyn, x0, u0)
+    out = dict(x0=x0, u0=u0, limits=np.array([8.0, 5.0]))
+    bopts = BarrierOptions(newton=NewtonOptions(max_iters=300))
+    traj, rep = barrier_solve(prob, init, bopts)
+    _barrier_record("bar", traj, rep, out)
+
+    def solve(xp, up):
+        t, r = barrier_solve(prob, rollout(dyn, xp, up), bopts)
+        return t, [q.newton.iterations for q in r.rounds]
+    out.update({"bar_" + k: v for k, v in noise_floor(
+        solve, x0, u0, traj, [q.newton.iterations for q in rep.rounds]).items()})
+    aopts = AdmmOptions(rho=1.0, max_outer=40)
+    traj, rep = admm_solve(prob, init, aopts)
+    _admm_record("admm", traj, rep, out)
+
+    def solve2(xp, up):
+        t, r = admm_solve(prob, rollout(dyn, xp, up), aopts)
+        return t, [q.iterations for q in r.newton_reports]
+    out.update({"admm_" + k: v for k, v in noise_floor(
+        solve2, x0, u0, traj, [q.iterations for q in rep.newton_reports]).items()})
+    save("pendulum_norm_constraints", **out)
+
+
 def _admm_record(prefix, traj, rep, out):
     out[f"{prefix}_xs"], out[f"{prefix}_us"] = traj.states, traj.controls
     out[f"{prefix}_z"], out[f"{prefix}_v"] = rep.state.z, rep.state.v
@@ -511,7 +576,7 @@ def case_criterion5_pendulum():
 
 FAST = [case_lqr_small, case_lqr_config1, case_passes_models, case_newton_lq,
         case_barrier_pendulum_cfg0, case_barrier_pendulum_conv, case_barrier_tvlinear, case_admm_small,
-        case_barrier_pendulum_cosine]
+        case_barrier_pendulum_cosine, case_pendulum_norm_constraints]
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()

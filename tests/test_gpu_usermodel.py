@@ -7,8 +7,9 @@ same solver entry points, checked against the reference's own runs."""
 import numpy as np
 import pytest
 from conftest import golden, rel_gap
+from test_gpu_newton import _hist
 from restart_util import check_iterations, device_restart
-from user_models import user_cosine_cost, user_pendulum, user_tvlinear
+from user_models import user_cosine_cost, user_norm_constraints, user_pendulum, user_tvlinear
 
 pytestmark = pytest.mark.gpu
 
@@ -98,7 +99,7 @@ def test_user_cost_matches_reference():
     device hook (DeviceCost) matches pintoc's barrier run of it: per-round
     counts, iteration histories, trajectory at 1e-9."""
     import paper_2409_20027_b200 as P
-    from test_gpu_newton import _check_hist, _hist
+    from test_gpu_newton import _hist
     g = golden("barrier_pendulum_cosine")
     w = g["weights"]
     dyn = user_pendulum(40)
@@ -137,3 +138,50 @@ def _check_hist_band(hist, ref):
         pred = np.abs(prev[fin] - ref[fin, 0]) / np.abs(ref[fin, 2])
         band = TOL * (np.abs(prev[fin]) + np.abs(ref[fin, 0])) / pred + TOL * np.abs(ref[fin, 2])
         assert np.all(np.abs(hist[fin, 2] - ref[fin, 2]) <= band)
+
+
+def _norm_problem(P, g):
+    wmax, umax = g["limits"]
+    dyn = user_pendulum(40)
+    cost = P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]), np.diag([100.0, 10.0]))
+    return dyn, P.ControlProblem(dyn, cost, user_norm_constraints(wmax, umax))
+
+
+def test_user_constraints_barrier_and_admm_match_reference():
+    """make_golden's NormConstraints -- a user ConstraintModel with curved
+    rows (omega^2 <= wmax^2, u^2 <= umax^2: nonzero gxx, huu) -- as a
+    DeviceConstraint: the barrier solve (per-round counts, histories,
+    trajectory 1e-9) and the ADMM solve (per-step counts, residuals, z,
+    trajectory) of pintoc."""
+    import paper_2409_20027_b200 as P
+    g = golden("pendulum_norm_constraints")
+    dyn, prob = _norm_problem(P, g)
+    init = P.rollout(dyn, g["x0"], g["u0"])
+    traj, rep = P.barrier_solve(prob, init, P.BarrierOptions(newton=P.NewtonOptions(max_iters=300)))
+    assert [r.newton.iterations for r in rep.rounds] == list(g["bar_round_iters"])
+    assert [r.newton.termination for r in rep.rounds] == list(g["bar_round_term"])
+    for k, r in enumerate(rep.rounds):
+        _check_hist_band(_hist(r.newton), g[f"bar_hist{k}"])
+    assert rel_gap(traj.controls, g["bar_us"]) < TOL
+    assert rel_gap(traj.states, g["bar_xs"]) < TOL
+    traj, rep = P.admm_solve(prob, init, P.AdmmOptions(rho=1.0, max_outer=40))
+    assert rep.converged == bool(g["admm_converged"])
+    assert [r.iterations for r in rep.newton_reports] == list(g["admm_newton_iters"])
+    assert rel_gap(np.array(rep.residual_history), g["admm_residuals"]) < 1e-8
+    assert rel_gap(rep.state.z, g["admm_z"]) < 1e-8
+    assert rel_gap(traj.controls, g["admm_us"]) < TOL
+
+
+def test_user_constraints_infeasible_start_reports_the_row():
+    """An initial control outside the curved box: the barrier solve raises
+    InfeasibleError(stage, component, value) for the first violated row, as
+    the reference's assert_strictly_feasible does (outer.py:163-177)."""
+    import paper_2409_20027_b200 as P
+    g = golden("pendulum_norm_constraints")
+    dyn, prob = _norm_problem(P, g)
+    u0 = np.array(g["u0"])
+    u0[7, 0] = 5.5                       # h = 5.5^2 - 25 = 5.25 at stage 7
+    with pytest.raises(P.InfeasibleError) as err:
+        P.barrier_solve(prob, P.rollout(dyn, g["x0"], u0), P.BarrierOptions())
+    assert (err.value.stage, err.value.component) == (7, 1)
+    assert abs(err.value.value - 5.25) < 1e-12

@@ -68,7 +68,8 @@ def precompile():
     """Build the test models' libraries (build() does this so GPU runs load
     them without compiling)."""
     import numpy as np
-    paths = [user_pendulum(8).library(), user_pendulum(8).library(user_cosine_cost())]
+    paths = [user_pendulum(8).library(), user_pendulum(8).library(user_cosine_cost()),
+             user_pendulum(8).library(None, user_norm_constraints())]
     for nx, nu in ((4, 2),):
         z = np.zeros((3, nx, nx)), np.zeros((3, nx, nu)), np.zeros((3, nx))
         paths.append(user_tvlinear(*z).library())
@@ -101,3 +102,17 @@ def user_cosine_cost(w0=10.0, w1=0.1, r=0.01, W0=100.0, W1=10.0):
     return DeviceCost(stage=COS_STAGE, gradients=COS_GRAD, terminal=COS_TERM,
                       terminal_gradients=COS_TERM_GRAD, params=(w0, w1, r, W0, W1),
                       name="cosine")
+
+
+# make_golden.py's NormConstraints (a user ConstraintModel in pintoc):
+# g(x) = [omega^2 - wmax^2], h(u) = [u^2 - umax^2]; prm = (wmax, umax)
+NORM_G = "g[0] = x[1] * x[1] - R(prm[0] * prm[0]);"
+NORM_G_D = "gx[0][1] = R(2) * x[1]; gxx[0][1][1] = R(2);"
+NORM_H = "h[0] = u[0] * u[0] - R(prm[1] * prm[1]);"
+NORM_H_D = "hu[0][0] = R(2) * u[0]; huu[0][0][0] = R(2);"
+
+
+def user_norm_constraints(wmax=8.0, umax=5.0):
+    from paper_2409_20027_b200.usermodel import DeviceConstraint
+    return DeviceConstraint(1, 1, g=NORM_G, g_derivs=NORM_G_D, h=NORM_H, h_derivs=NORM_H_D,
+                            params=(wmax, umax), name="norm")
