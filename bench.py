@@ -541,7 +541,7 @@ def run_ours(args) -> None:
         # directions overlap each other and the compute (a user feeding a
         # stream of MPC batches does exactly this).
         from paper_2409_20027_b200.passes import HostLqrSolver
-        nsub = 8
+        nsub = int(os.environ.get("BENCH_E2E_NSUB", "8"))
         subs = []
         h2d = d2h = 0
         for k, (solver, inputs, alpha, n, nx, nu) in halves.items():
