@@ -534,57 +534,10 @@ def run_ours(args) -> None:
     # expansions from pinned memory, solve, D2H of gains and deviations
     e2e = None
     if not args.no_e2e:
-        # The step's 65,536 problems stream through in sub-batches of 4,096
-        # (pinned host buffers per sub-batch), each one ptc_lqr_solve_host
-        # call (host->device copies of what the kernels read, solve,
-        # device->host copies) on one of four streams, so the PCIe
-        # directions overlap each other and the compute (a user feeding a
-        # stream of MPC batches does exactly this).
-        from paper_2409_20027_b200.passes import HostLqrSolver
-        nsub = int(os.environ.get("BENCH_E2E_NSUB", "8"))
-        subs = []
-        h2d = d2h = 0
-        for k, (solver, inputs, alpha, n, nx, nu) in halves.items():
-            step_ = n // nsub
-            for i in range(nsub):
-                sl = slice(i * step_, n if i == nsub - 1 else (i + 1) * step_)
-                m = sl.stop - sl.start
-                h_in = [t[:, :, sl].contiguous().cpu().pin_memory() for t in inputs]
-                h_al = alpha[sl].contiguous().cpu().pin_memory()
-                hs = HostLqrSolver(m, T, nx, nu, dtype=torch.float64)
-                h_out = hs.outputs()
-                subs.append((hs, h_in, h_al, h_out))
-                # bytes that cross PCIe: upper triangles of P and R (nx < 8)
-                tri = lambda q: q * (q + 1) // 2 if nx < 8 else q * q
-                words = T * m * (tri(nx) + tri(nu) + 2 * nx * nu + nu + nx * nx) + m * nx * nx
-                h2d += 8 * words + h_al.numel() * 8
-                d2h += sum(t.numel() * t.element_size() for t in h_out)
-        e_streams = [torch.cuda.Stream() for _ in range(4)]
-
-        def e2e_step():
-            for es in e_streams:
-                es.wait_stream(stream)
-            for k, (hs, h_in, h_al, h_out) in enumerate(subs):
-                hs.solve(*h_in, h_al, h_out, stream=e_streams[k % len(e_streams)])
-            for es in e_streams:
-                stream.wait_stream(es)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        n_e2e = max(2, min(args.steps, 5))
-        if world > 1:
-            dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(n_e2e):
-            e2e_step()
-        b.record(stream)
-        torch.cuda.synchronize()
-        e_ms = max_over_ranks(a.elapsed_time(b) / n_e2e, world, "cuda")
-        e2e = {"value": B_TOTAL * world / (float(e_ms) * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
-               "ms_per_step": float(e_ms), "sub_batches": len(subs)}
-        del subs
+        e2e = e2e_leg(torch, halves, stream, world, args.steps, stacked=False)
+        # the same through ptc_lqr_solve_host_stacked: the reference's own
+        # per-problem arrays (B, T, nx, nx) ..., restacked on the device
+        e2e["stacked"] = e2e_leg(torch, halves, stream, world, args.steps, stacked=True)
 
     roof = None
     if rank == 0:
@@ -1228,6 +1181,70 @@ def config4_solve_leg(torch, P, logT: int = 20, damp: float = 0.9999):
             "final_cost": float(rep.rounds[-1].cost),
             "note": "api_wall_s includes the host copies of the initial trajectory, the "
                     "per-round controls and the reports of the reference-shaped API"}
+
+
+def e2e_leg(torch, halves, stream, world, steps, stacked):
+    """End to end through the C ABI with host buffers: H2D of the step's
+    expansions from pinned memory, solve, D2H of gains and deviations.
+
+    The step's 65,536 problems stream through in sub-batches (pinned host
+    buffers per sub-batch), each one ptc_lqr_solve_host call (host->device
+    copies of what the kernels read, solve, device->host copies) on one of
+    four streams, so the PCIe directions overlap each other and the compute
+    (a user feeding a stream of MPC batches does exactly this).  stacked:
+    the host arrays are the reference's per-problem layout (np.stack of the
+    StageExpansion fields, ptc_lqr_solve_host_stacked): whole P and R cross
+    PCIe and the device restacks them."""
+    from paper_2409_20027_b200.passes import HostLqrSolver
+    nsub = int(os.environ.get("BENCH_E2E_NSUB", "8"))
+    subs = []
+    h2d = d2h = 0
+    for k, (solver, inputs, alpha, n, nx, nu) in halves.items():
+        step_ = n // nsub
+        for i in range(nsub):
+            sl = slice(i * step_, n if i == nsub - 1 else (i + 1) * step_)
+            m = sl.stop - sl.start
+            if stacked:
+                h_in = [t[:, :, sl].permute(2, 1, 0).contiguous().cpu().pin_memory()
+                        for t in inputs]
+            else:
+                h_in = [t[:, :, sl].contiguous().cpu().pin_memory() for t in inputs]
+            h_al = alpha[sl].contiguous().cpu().pin_memory()
+            hs = HostLqrSolver(m, T, nx, nu, dtype=torch.float64, stacked=stacked)
+            h_out = hs.outputs()
+            subs.append((hs, h_in, h_al, h_out))
+            # bytes that cross PCIe: upper triangles of P and R (nx < 8) in
+            # the SoA entry, whole matrices in the stacked one
+            tri = lambda q: q * (q + 1) // 2 if nx < 8 and not stacked else q * q
+            words = T * m * (tri(nx) + tri(nu) + 2 * nx * nu + nu + nx * nx) + m * nx * nx
+            h2d += 8 * words + h_al.numel() * 8
+            d2h += sum(t.numel() * t.element_size() for t in h_out)
+    e_streams = [torch.cuda.Stream() for _ in range(4)]
+
+    def e2e_step():
+        for es in e_streams:
+            es.wait_stream(stream)
+        for k, (hs, h_in, h_al, h_out) in enumerate(subs):
+            hs.solve(*h_in, h_al, h_out, stream=e_streams[k % len(e_streams)])
+        for es in e_streams:
+            stream.wait_stream(es)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    n_e2e = max(2, min(steps, 5))
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n_e2e):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    e_ms = max_over_ranks(a.elapsed_time(b) / n_e2e, world, "cuda")
+    return {"value": B_TOTAL * world / (float(e_ms) * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+            "ms_per_step": float(e_ms), "sub_batches": len(subs),
+            "layout": "stacked (B, T, ...) per-problem" if stacked else "SoA batch-minor"}
 
 
 def strong_leg(torch, P, LqrSolver, args, world: int, rank: int) -> dict:

@@ -124,6 +124,29 @@ int ptc_lqr_solve_host(int dtype, int batch, int horizon, int nx, int nu,
                        void* Gamma, void* gamma, void* dx, void* du, int* flags,
                        void* workspace, int64_t workspace_bytes, int chunk0, int chunk,
                        void* stream);
+/* The same host-buffer solve on the reference's own per-problem arrays
+ * stacked over the batch ("stacked", problem-major: numpy's
+ * np.stack([exp.P for exp in expansions]) of passes.py:291's StageExpansion
+ * fields), so a pintoc caller hands its arrays over without a host
+ * transpose:
+ *   P (batch, horizon, nx, nx), R (batch, horizon, nu, nu),
+ *   M (batch, horizon, nx, nu), d (batch, horizon, nu),
+ *   Fx (batch, horizon, nx, nx), Fu (batch, horizon, nx, nu),
+ *   PT (batch, nx, nx), alpha float64[batch];
+ *   out Gamma (batch, horizon, nu, nx), gamma (batch, horizon, nu),
+ *   dx (batch, horizon + 1, nx), du (batch, horizon, nu).
+ * Each field crosses PCIe whole and is restacked to the SoA layout on the
+ * device (an HBM-bound tiled transpose); results are bit-identical to
+ * ptc_lqr_solve_host.  batch <= 2,097,120.  Workspace (device):
+ * ptc_lqr_host_stacked_workspace_bytes. */
+int64_t ptc_lqr_host_stacked_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
+                                             int chunk0, int chunk);
+int ptc_lqr_solve_host_stacked(int dtype, int batch, int horizon, int nx, int nu,
+                               const void* P, const void* R, const void* M, const void* d,
+                               const void* Fx, const void* Fu, const void* PT,
+                               const double* alpha, void* Gamma, void* gamma, void* dx, void* du,
+                               int* flags, void* workspace, int64_t workspace_bytes, int chunk0,
+                               int chunk, void* stream);
 /* Element-level operations of the three scans, batched over items; item i
  * of a field with C components at f[c * n + i] (device pointers).
  *   ptc_value_elements   value_element_init (passes.py:192-228) of stages

@@ -88,6 +88,10 @@ _SIGS = {
     "ptc_lqr_solve_host": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7 + [C.c_void_p]
                            + [C.c_void_p] * 4 + [C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
                                                   C.c_int, C.c_void_p]),
+    "ptc_lqr_host_stacked_workspace_bytes": (C.c_int64, [C.c_int] * 7),
+    "ptc_lqr_solve_host_stacked": (C.c_int, [C.c_int] * 5 + [C.c_void_p] * 7 + [C.c_void_p]
+                                   + [C.c_void_p] * 4 + [C.c_void_p, C.c_void_p, C.c_int64,
+                                                          C.c_int, C.c_int, C.c_void_p]),
     "ptc_value_elements": (C.c_int, [C.c_int] * 4 + [C.c_void_p] * 7
                            + [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ptc_value_combine": (C.c_int, [C.c_int] * 3 + [C.c_void_p] * 5),

@@ -2,6 +2,7 @@
 // batched solver object and dispatch into the instantiated kernel sets.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -506,7 +507,141 @@ static int lqr_solve_host_t(int batch, int horizon, int nx, int nu, const void* 
   return PTC_OK;
 }
 
+// problem-major <-> SoA batch-minor restack of one field with C components
+// over `rows` stages: stacked[(b * rows + t) * C + c] <-> soa[(c * rows + t) *
+// B + b].  Flattening k = t * C + c makes it a [B][K] <-> [K][B] transpose
+// with the SoA row of k remapped to c * rows + t; 32 x 32 smem tiles keep
+// both sides coalesced (256 B per warp access in fp64).
+template <typename R, bool kToSoa>
+__global__ void __launch_bounds__(256) k_restack(const R* __restrict__ in, R* __restrict__ out,
+                                                 int B, int rows, int C) {
+  __shared__ R tile[32][33];
+  const long long K = (long long)rows * C, k0 = (long long)blockIdx.x * 32;
+  const int b0 = blockIdx.y * 32, tx = threadIdx.x;
+  auto soa = [&](long long k, int b) {
+    return ((long long)(k % C) * rows + k / C) * B + b;
+  };
+#pragma unroll
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    if (kToSoa) {
+      const int b = b0 + j;
+      const long long k = k0 + tx;
+      if (b < B && k < K) tile[j][tx] = in[(long long)b * K + k];
+    } else {
+      const long long k = k0 + j;
+      const int b = b0 + tx;
+      if (b < B && k < K) tile[j][tx] = in[soa(k, b)];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    if (kToSoa) {
+      const long long k = k0 + j;
+      const int b = b0 + tx;
+      if (b < B && k < K) out[soa(k, b)] = tile[tx][j];
+    } else {
+      const int b = b0 + j;
+      const long long k = k0 + tx;
+      if (b < B && k < K) out[(long long)b * K + k] = tile[tx][j];
+    }
+  }
+}
+
+template <typename R>
+static void restack(const R* in, R* out, int B, int rows, int C, bool to_soa, cudaStream_t st) {
+  const dim3 grid((unsigned)(((long long)rows * C + 31) / 32), (unsigned)((B + 31) / 32));
+  if (to_soa) k_restack<R, true><<<grid, dim3(32, 8), 0, st>>>(in, out, B, rows, C);
+  else k_restack<R, false><<<grid, dim3(32, 8), 0, st>>>(in, out, B, rows, C);
+}
+
+// the host entry for the reference's own per-problem arrays stacked over the
+// batch: each field crosses PCIe whole into one device staging buffer and is
+// restacked into the SoA inputs there; the outputs go the other way
+// (every input field side by side: the copies of one call run back to back,
+// then the restacks; the outputs reuse the space)
+static size_t stacked_raw_words(int batch, int horizon, int nx, int nu) {
+  const size_t TB = (size_t)horizon * batch;
+  const size_t in = (size_t)(2 * nx * nx + nu * nu + 2 * nx * nu + nu) * TB + (size_t)nx * nx * batch;
+  const size_t out = (size_t)(nu * nx + 2 * nu) * TB + (size_t)nx * (horizon + 1) * batch;
+  return std::max(in, out);
+}
+
+template <typename R>
+static int lqr_solve_host_stacked_t(int batch, int horizon, int nx, int nu,
+                                    const void* const* hin, const double* alpha,
+                                    void* const* hout, int* flags, void* ws, int64_t ws_bytes,
+                                    int chunk0, int chunk, cudaStream_t st) {
+  if (batch > 65535 * 32) return fail(PTC_ERR_ARG, "stacked layout: batch above 2,097,120");
+  Carver c{(char*)ws};
+  R* in[7];
+  R* out[4];
+  double* al;
+  int* fl;
+  host_staging<R>(c, batch, horizon, nx, nu, in, &al, &fl, out);
+  R* raw = c.template take<R>(stacked_raw_words(batch, horizon, nx, nu));
+  c.off = (c.off + 255) & ~(size_t)255;
+  const int64_t rest = ws_bytes - (int64_t)c.off;
+  if (rest <= 0) return fail(PTC_ERR_WORKSPACE, "LQR host workspace too small");
+  const size_t es = sizeof(R);
+  const int cin[7] = {nx * nx, nu * nu, nx * nu, nu, nx * nx, nx * nu, nx * nx};
+  size_t off[8] = {0};
+  for (int k = 0; k < 7; ++k) off[k + 1] = off[k] + (size_t)cin[k] * (k == 6 ? 1 : horizon) * batch;
+  for (int k = 0; k < 7; ++k)
+    PTC_CUDA(cudaMemcpyAsync(raw + off[k], hin[k], (off[k + 1] - off[k]) * es,
+                             cudaMemcpyHostToDevice, st));
+  for (int k = 0; k < 7; ++k) restack<R>(raw + off[k], in[k], batch, k == 6 ? 1 : horizon, cin[k], true, st);
+  PTC_CUDA(cudaMemcpyAsync(al, alpha, (size_t)batch * sizeof(double), cudaMemcpyHostToDevice, st));
+  PTC_CUDA(cudaMemsetAsync(fl, 0, sizeof(int) * batch, st));
+  int rc = lqr_solve_t<R>(batch, horizon, nx, nu, in[0], in[1], in[2], in[3], in[4], in[5], in[6],
+                          al, nullptr, nullptr, out[0], out[1], out[2], out[3], fl,
+                          (char*)ws + c.off, rest, chunk0, chunk, st);
+  if (rc != PTC_OK) return rc;
+  const int cout_[4] = {nu * nx, nu, nx, nu};
+  size_t oo[5] = {0};
+  for (int k = 0; k < 4; ++k) oo[k + 1] = oo[k] + (size_t)cout_[k] * (k == 2 ? horizon + 1 : horizon) * batch;
+  for (int k = 0; k < 4; ++k)
+    restack<R>(out[k], raw + oo[k], batch, k == 2 ? horizon + 1 : horizon, cout_[k], false, st);
+  for (int k = 0; k < 4; ++k)
+    PTC_CUDA(cudaMemcpyAsync(hout[k], raw + oo[k], (oo[k + 1] - oo[k]) * es,
+                             cudaMemcpyDeviceToHost, st));
+  if (flags) PTC_CUDA(cudaMemcpyAsync(flags, fl, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+  PTC_CUDA(cudaGetLastError());
+  return PTC_OK;
+}
+
 extern "C" {
+
+int64_t ptc_lqr_host_stacked_workspace_bytes(int dtype, int batch, int horizon, int nx, int nu,
+                                             int chunk0, int chunk) {
+  const int64_t hw = ptc_lqr_host_workspace_bytes(dtype, batch, horizon, nx, nu, chunk0, chunk);
+  if (hw < 0) return hw;
+  const size_t es = dtype == PTC_F64 ? 8 : 4;
+  return hw + (int64_t)((stacked_raw_words(batch, horizon, nx, nu) * es + 511) & ~(size_t)255);
+}
+
+int ptc_lqr_solve_host_stacked(int dtype, int batch, int horizon, int nx, int nu, const void* P,
+                               const void* R, const void* M, const void* d, const void* Fx,
+                               const void* Fu, const void* PT, const double* alpha, void* Gamma,
+                               void* gamma, void* dx, void* du, int* flags, void* workspace,
+                               int64_t workspace_bytes, int chunk0, int chunk, void* stream) {
+  if (batch < 1 || horizon < 1 || nx < 1 || nu < 1) return fail(PTC_ERR_ARG, "bad dims");
+  const void* hin[7] = {P, R, M, d, Fx, Fu, PT};
+  for (const void* p : hin)
+    if (!p) return fail(PTC_ERR_ARG, "every input buffer is required");
+  void* hout[4] = {Gamma, gamma, dx, du};
+  for (void* p : hout)
+    if (!p) return fail(PTC_ERR_ARG, "every output buffer is required");
+  if (!alpha) return fail(PTC_ERR_ARG, "alpha is required");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == PTC_F64)
+    return lqr_solve_host_stacked_t<double>(batch, horizon, nx, nu, hin, alpha, hout, flags,
+                                            workspace, workspace_bytes, chunk0, chunk, st);
+  if (dtype == PTC_F32)
+    return lqr_solve_host_stacked_t<float>(batch, horizon, nx, nu, hin, alpha, hout, flags,
+                                           workspace, workspace_bytes, chunk0, chunk, st);
+  return fail(PTC_ERR_ARG, "dtype must be PTC_F32 or PTC_F64");
+}
 
 // element-level entry points: any registered kernel set of this dtype / nx
 static const LqrOps* ops_for_nx(int dtype, int nx) {

@@ -16,6 +16,29 @@ constexpr int kBlock = 128;
 
 inline dim3 grid_for(long long n) { return dim3((unsigned)((n + kBlock - 1) / kBlock)); }
 
+// Sequential-sweep kernels (one thread walks a whole unit of stages) launch
+// in a single wave when the batch is small: then the step time is that of the
+// most loaded SM, and 128-thread CTAs leave it with up to 1.5x the average
+// (32,768 problems = 256 CTAs on 148 SMs: 108 SMs hold two, 40 hold one).
+// Narrower CTAs even it out (1024 CTAs of 32: 6 or 7 per SM).
+struct SeqLaunch {
+  dim3 grid;
+  int block;
+};
+inline SeqLaunch seq_launch(long long n) {
+  const long long sms = sm_count();
+  int best = kBlock;
+  if (n <= sms * 512) {
+    long long load = ((n + kBlock - 1) / kBlock + sms - 1) / sms * kBlock;
+    for (int bs : {64, 32}) {
+      const long long l = ((n + bs - 1) / bs + sms - 1) / sms * bs;
+      if (l < load) load = l, best = bs;
+    }
+  }
+  return {dim3((unsigned)((n + best - 1) / best)), best};
+}
+#define PTC_SEQ(n) seq_launch(n).grid, seq_launch(n).block
+
 template <typename R, int NX, int NU>
 void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
   const Plan& pl = a.plan;
@@ -25,23 +48,23 @@ void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
     return;
   }
   if (pl.L >= 1) {
-    k_value_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_value_up0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_value_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_value_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
     for (int l = pl.L - 1; l >= 1; --l)
       k_value_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
   }
   if (pl.L >= 1 || a.block_mode)
-    k_value_down0<R, NX, NU, true><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_value_down0<R, NX, NU, true><<<PTC_SEQ(P0 * B), 0, s>>>(a);
   else
-    k_value_down0<R, NX, NU, false><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_value_down0<R, NX, NU, false><<<PTC_SEQ(P0 * B), 0, s>>>(a);
   if (pl.L >= 1) {
     for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_prop_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
     for (int l = pl.L - 1; l >= 1; --l)
       k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
   }
-  k_prop_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  k_prop_down0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
 }
 
 template <typename R, int NX, int NU>
@@ -53,13 +76,13 @@ void launch_prop(const LqrArgs<R>& a, cudaStream_t s) {
     return;
   }
   if (pl.L >= 1) {
-    k_prop_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_prop_up0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_prop_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
     for (int l = pl.L - 1; l >= 1; --l)
       k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
   }
-  k_prop_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  k_prop_down0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
 }
 
 // Time-block phases (horizon sharded across ranks; sharded.py drives them
@@ -75,7 +98,7 @@ void launch_lqr_block(const LqrArgs<R>& a0, int phase, const void* blocks, void*
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (phase == 0) {
-    k_value_up0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_value_up0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_value_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_value_block<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, static_cast<R*>(out));
   } else if (phase == 1) {
@@ -86,7 +109,7 @@ void launch_lqr_block(const LqrArgs<R>& a0, int phase, const void* blocks, void*
       for (int l = pl.L - 1; l >= 1; --l)
         k_value_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     }
-    k_value_down0<R, NX, NU, true><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_value_down0<R, NX, NU, true><<<PTC_SEQ(P0 * B), 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_prop_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_prop_block<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, static_cast<R*>(out));
   } else {
@@ -97,7 +120,7 @@ void launch_lqr_block(const LqrArgs<R>& a0, int phase, const void* blocks, void*
       for (int l = pl.L - 1; l >= 1; --l)
         k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     }
-    k_prop_down0<R, NX, NU><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_prop_down0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
   }
 }
 
@@ -111,13 +134,13 @@ void launch_costate(const NewtonArgs<R>& a, cudaStream_t s) {
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (pl.L >= 1) {
-    k_costate_up0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+    k_costate_up0<R, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a);
     for (int l = 1; l < pl.L; ++l) k_costate_up<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     k_costate_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a);
     for (int l = pl.L - 1; l >= 1; --l)
       k_costate_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
   }
-  k_costate_down0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  k_costate_down0<R, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -279,15 +302,15 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   const long long B = a.B, P0 = a.plan.units0();
   cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
   if constexpr (kWideNewton<Dyn>) WideNewton<R, NX, NU>::cost_partials(a, 0, s);
-  else k_cost_partials<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 0);
+  else k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, 0);
   bool fused = false;
   if constexpr (NX < 8) {
     if (a.plan.L == 0) {
       // single-sweep schedule: the value sweep re-derives every stage's
       // expansion and its co-state in registers from x, u (no stored
       // expansion or co-states), the propagation sweep the Jacobians
-      k_value_fused<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la);
-      k_prop_fused<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a, la);
+      k_value_fused<R, Dyn><<<PTC_SEQ(B), 0, s>>>(a, la);
+      k_prop_fused<R, Dyn><<<PTC_SEQ(B), 0, s>>>(a, la);
       fused = true;
     }
   }
@@ -337,7 +360,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     // is ~2(L + 1) early-exit launches in the captured iteration)
     const int iters = (IsAffine<Dyn>::value && a.pr_iters > 1) ? 1 : a.pr_iters;
     for (int k = 0; k <= iters; ++k) {
-      k_pr_up0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, k);
+      k_pr_up0<R, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, k);
       if (fold) k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.rres, 1, RED_MAX, (int)P0, (int)B);
       k_pr_check<R><<<grid_for(B), kBlock, 0, s>>>(a, k);
       if (k == iters) break;
@@ -345,17 +368,17 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
       k_pr_top<R, NX><<<grid_for(B), kBlock, 0, s>>>(a, k);
       for (int l = pl.L - 1; l >= 1; --l)
         k_pr_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
-      k_pr_down0<R, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, k);
+      k_pr_down0<R, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, k);
     }
     k_pr_finish<R, NX><<<grid_for(nT), kBlock, 0, s>>>(a);
-    k_rollout<R, Dyn, true><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
-    k_cost_partials<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+    k_rollout<R, Dyn, true><<<PTC_SEQ(B), 0, s>>>(a, la.dU);
+    k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, 1);
   } else if (P0 == 1) {
     // one unit per problem: the rollout also accumulates the candidate cost
-    k_rollout<R, Dyn, false, true><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
+    k_rollout<R, Dyn, false, true><<<PTC_SEQ(B), 0, s>>>(a, la.dU);
   } else {
-    k_rollout<R, Dyn, false><<<grid_for(B), kBlock, 0, s>>>(a, la.dU);
-    k_cost_partials<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a, 1);
+    k_rollout<R, Dyn, false><<<PTC_SEQ(B), 0, s>>>(a, la.dU);
+    k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, 1);
   }
   if (fold) {
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.cpart[0], 3, kOpsCost, (int)P0, (int)B);
@@ -363,7 +386,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   }
   k_control<R, NX, NU><<<grid_for(B), kBlock, 0, s>>>(a);
   if constexpr (kUserCon<Dyn>) k_user_bad_value<R, Dyn><<<grid_for(B), kBlock, 0, s>>>(a);
-  k_round_end<R, NX, NU, Dyn><<<grid_for(P0 * B), kBlock, 0, s>>>(a);
+  k_round_end<R, NX, NU, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a);
   if (fold && a.apart && a.opt.method == METHOD_ADMM)
     k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.apart, 2, RED_MAX | (RED_MAX << 2), (int)P0, (int)B);
   k_outer<R><<<grid_for(B), kBlock, 0, s>>>(a);
@@ -501,13 +524,13 @@ struct RegisterNewton {
         return;
       }
     }
-    k_rollout_inplace<R, Dyn><<<grid_for(a.B), kBlock, 0, s>>>(a);
+    k_rollout_inplace<R, Dyn><<<PTC_SEQ(a.B), 0, s>>>(a);
   }
   static void cost(const void* p, cudaStream_t s) {
     const NewtonArgs<R>& a = A(p);
     k_force_phase<R><<<grid_for(a.B), kBlock, 0, s>>>(a, PH_NEED_COST);
     const int P0 = a.plan.units0();
-    k_cost_partials<R, NX, NU, Dyn><<<grid_for((long long)P0 * a.B), kBlock, 0, s>>>(a, 0);
+    k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ((long long)P0 * a.B), 0, s>>>(a, 0);
     if (partial_rows(P0) < P0)
       k_reduce_partials<<<(unsigned)a.B, 256, 0, s>>>(a.cpart[0], 3,
                                                       RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4),

@@ -160,9 +160,18 @@ class HostLqrSolver:
     inputs and outputs are CPU tensors in the LqrSolver layouts (pin them
     for asynchronous copies); the host->device copies (only the parts the
     kernels read), the solve and the device->host copies are enqueued on
-    ``stream``, so calls on several streams overlap PCIe with compute."""
+    ``stream``, so calls on several streams overlap PCIe with compute.
 
-    def __init__(self, batch, horizon, nx, nu, dtype=None, chunk0=0, chunk=0, device=None):
+    ``stacked=True`` takes the reference's per-problem arrays stacked over
+    the batch instead (``ptc_lqr_solve_host_stacked``): P (B, T, nx, nx),
+    R (B, T, nu, nu), M (B, T, nx, nu), d (B, T, nu), Fx (B, T, nx, nx),
+    Fu (B, T, nx, nu), PT (B, nx, nx); outputs Gamma (B, T, nu, nx),
+    gamma (B, T, nu), dx (B, T + 1, nx), du (B, T, nu) -- restacked on the
+    device, no host transpose."""
+
+    def __init__(self, batch, horizon, nx, nu, dtype=None, chunk0=0, chunk=0, device=None,
+                 stacked=False):
+        self.stacked = bool(stacked)
         torch = N.require_cuda()
         self.torch = torch
         self.lib = N.load_library()
@@ -172,8 +181,9 @@ class HostLqrSolver:
         if not self.lib.ptc_supported(self.code, -1, self.nx, self.nu):
             raise N.NativeError(f"LQR kernels not compiled for nx={nx} nu={nu}")
         self.chunk0, self.chunk = int(chunk0), int(chunk)
-        nbytes = self.lib.ptc_lqr_host_workspace_bytes(self.code, self.B, self.T, self.nx,
-                                                       self.nu, self.chunk0, self.chunk)
+        wsb = (self.lib.ptc_lqr_host_stacked_workspace_bytes if self.stacked
+               else self.lib.ptc_lqr_host_workspace_bytes)
+        nbytes = wsb(self.code, self.B, self.T, self.nx, self.nu, self.chunk0, self.chunk)
         N.check(0 if nbytes >= 0 else int(nbytes))
         self.workspace = torch.empty(int(nbytes), dtype=torch.uint8,
                                      device=torch.device(device or "cuda"))
@@ -183,14 +193,30 @@ class HostLqrSolver:
         torch = self.torch
         B, T, nx, nu = self.B, self.T, self.nx, self.nu
         mk = lambda *s: torch.empty(*s, dtype=self.dtype, pin_memory=pin)
+        if self.stacked:
+            return mk(B, T, nu, nx), mk(B, T, nu), mk(B, T + 1, nx), mk(B, T, nu)
         return mk(nu * nx, T, B), mk(nu, T, B), mk(nx, T + 1, B), mk(nu, T, B)
 
     def solve(self, P, R, M, d, Fx, Fu, PT, alpha, out, flags=None, stream=None):
         ins = (P, R, M, d, Fx, Fu, PT)
         if any(t.is_cuda for t in ins + tuple(out)) or alpha.is_cuda:
             raise ValueError("HostLqrSolver takes host tensors (use LqrSolver for device ones)")
+        if not all(t.is_contiguous() for t in ins + tuple(out)):
+            raise ValueError("HostLqrSolver takes contiguous tensors")
+        B, T, nx, nu = self.B, self.T, self.nx, self.nu
+        want = (nx * nx * T * B, nu * nu * T * B, nx * nu * T * B, nu * T * B, nx * nx * T * B,
+                nx * nu * T * B, nx * nx * B, nu * nx * T * B, nu * T * B, nx * (T + 1) * B,
+                nu * T * B)
+        for name, t, n in zip(("P", "R", "M", "d", "Fx", "Fu", "PT", "Gamma", "gamma", "dx",
+                               "du"), ins + tuple(out), want):
+            if t.numel() != n or t.dtype != self.dtype:
+                raise ValueError(f"{name}: {t.numel()} {t.dtype} elements, expected {n} "
+                                 f"{self.dtype}")
+        if alpha.numel() != B or alpha.dtype != self.torch.float64:
+            raise ValueError("alpha: float64[batch]")
         ptr = lambda t: None if t is None else t.data_ptr()
-        N.check(self.lib.ptc_lqr_solve_host(
+        fn = self.lib.ptc_lqr_solve_host_stacked if self.stacked else self.lib.ptc_lqr_solve_host
+        N.check(fn(
             self.code, self.B, self.T, self.nx, self.nu, *[ptr(t) for t in ins], ptr(alpha),
             *[ptr(t) for t in out], ptr(flags), ptr(self.workspace), self.workspace.numel(),
             self.chunk0, self.chunk, N.stream_ptr(stream)))

@@ -192,6 +192,49 @@ def test_lqr_host_buffers_equal_device_solve(nx, nu, T, B):
         assert torch.equal(got, want.cpu())
 
 
+@pytest.mark.parametrize("nx,nu,T,B", [(2, 1, 256, 64), (4, 1, 256, 300), (4, 2, 100, 33),
+                                       (12, 4, 1500, 1), (3, 2, 7, 5)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_lqr_host_stacked_equals_soa_solve(nx, nu, T, B, dtype):
+    """ptc_lqr_solve_host_stacked takes the reference's per-problem arrays
+    (np.stack of each StageExpansion field over the batch) and returns the
+    gains and deviations in the same stacking -- bit-identical to the SoA
+    host entry on the same problems, with ragged batch / component counts
+    (not multiples of the 32 x 32 restack tile)."""
+    import torch
+    from paper_2409_20027_b200 import passes
+    td = torch.float64 if dtype == "f64" else torch.float32
+    rng = np.random.default_rng([nx, nu, T, B, 7])
+    exps = [O.random_lqr_expansion(rng, T, nx, nu, alpha=0.2) for _ in range(B)]
+    fields = (lambda e: e.P, lambda e: e.R, lambda e: e.M, lambda e: e.d, lambda e: e.Fx,
+              lambda e: e.Fu, lambda e: e.PT[None])
+    stacked = [torch.as_tensor(np.stack([f(e) for e in exps]), dtype=td) for f in fields]
+    stacked[6] = stacked[6].reshape(B, nx, nx)
+    soa = [t.reshape(B, t.shape[1] if i < 6 else 1, -1).permute(2, 1, 0).contiguous()
+           for i, t in enumerate(stacked)]
+    alpha = torch.full((B,), 0.2, dtype=torch.float64).pin_memory()
+    s = torch.cuda.Stream()
+    ref = passes.HostLqrSolver(B, T, nx, nu, dtype=td)
+    want = ref.outputs()
+    ref.solve(*[t.pin_memory() for t in soa], alpha, want, stream=s)
+    hs = passes.HostLqrSolver(B, T, nx, nu, dtype=td, stacked=True)
+    got = hs.outputs()
+    flags = torch.zeros(B, dtype=torch.int32).pin_memory()
+    hs.solve(*[t.contiguous().pin_memory() for t in stacked], alpha, got, flags=flags, stream=s)
+    s.synchronize()
+    assert int(flags.max()) == 0
+    assert got[0].shape == (B, T, nu, nx) and got[2].shape == (B, T + 1, nx)
+    for g, w in zip(got, want):
+        w = w.reshape(-1, g.shape[1], B).permute(2, 1, 0).reshape(g.shape)
+        assert torch.equal(g, w)
+    if dtype == "f64":  # one problem against the oracle's value + propagation pass
+        k = B // 2
+        _, _, Gam, gam, dxs, dus = O.lqr_solve(exps[k])
+        for g, w in zip(got, (Gam, gam, dxs, dus)):
+            g = g[k].numpy()
+            assert np.max(np.abs(g - w)) <= 1e-9 * max(1.0, np.max(np.abs(w)))
+
+
 @pytest.mark.parametrize("nx,nu", [(2, 1), (4, 2), (12, 4)])
 def test_definiteness_error_names_the_reference_stage(nx, nu):
     """DefinitenessError.stage is the stage the reference's gates name
