@@ -225,9 +225,60 @@ template <typename R>
 struct CartPole {
   static constexpr int NX = 4, NU = 1;
 
-  // cart acc = (F + mp s (l om + g c)) / (mc + mp s^2)
-  // pole acc = (-F c - mp l om^2 c s - (mc + mp) g s) / (l (mc + mp s^2))
-  PTC_D static void accels(const ProblemParams& p, R th, R om, R force, Jet<R>& cart,
+  // Accelerations and their derivatives in the reduced variables (theta,
+  // omega, force), restating the reference's closed forms
+  // (systems.py:262-327 _quotient_derivs / _cartpole_accel): numerator and
+  // denominator derivatives combined by the quotient rule, with only the
+  // entries the model reads (g0..g2; h00, h01, h11, h02, h12 -- the
+  // force-force entry is unused) and none of the identically-zero terms.
+  // One reciprocal of the denominator replaces the quotient rule's
+  // divisions.
+  //   cart acc = (F + mp s (l om + g c)) / (mc + mp s^2)
+  //   pole acc = (-F c - mp l om^2 c s - (mc + mp) g s) / (l (mc + mp s^2))
+  struct Accel {
+    R g0, g1, g2, h00, h01, h11, h02, h12;
+  };
+  // n / den with den depending on theta only (gradient gd0, Hessian hd00)
+  PTC_D static void quotient(R n, R gn0, R gn1, R gn2, R hn00, R hn01, R hn11, R hn02, R den,
+                             R gd0, R hd00, Accel& q) {
+    const R rd = R(1) / den, rd2 = rd * rd;
+    q.g0 = gn0 * rd - n * gd0 * rd2;
+    q.g1 = gn1 * rd;
+    q.g2 = gn2 * rd;
+    q.h00 = hn00 * rd - R(2) * (gn0 * gd0) * rd2 - n * hd00 * rd2 + R(2) * n * (gd0 * gd0) * (rd2 * rd);
+    q.h01 = hn01 * rd - (gn1 * gd0) * rd2;
+    q.h11 = hn11 * rd;
+    q.h02 = hn02 * rd - (gn2 * gd0) * rd2;
+    q.h12 = R(0);
+  }
+
+  PTC_D static void accels(const ProblemParams& p, R th, R om, R force, Accel& cart, Accel& pole) {
+    const R g = R(p.dyn[0]), ln = R(p.dyn[1]), mc = R(p.dyn[2]), mp = R(p.dyn[3]);
+    R s, c;
+    sincos(th, &s, &c);
+    const R c2s2 = c * c - s * s;
+    const R den = mc + mp * s * s;
+    const R gd0 = R(2) * mp * s * c;
+    const R hd00 = R(2) * mp * c2s2;
+    // cart numerator n1 = F + mp s (l om + g c)
+    const R n1 = force + mp * s * (ln * om + g * c);
+    quotient(n1, mp * c * ln * om + mp * g * c2s2, mp * ln * s, R(1),
+             -mp * ln * s * om - R(4) * mp * g * s * c, mp * ln * c, R(0), R(0), den, gd0, hd00,
+             cart);
+    // pole numerator n2 over l den
+    const R om2 = om * om, mg = (mc + mp) * g;
+    const R n2 = -force * c - mp * ln * om2 * c * s - mg * s;
+    quotient(n2, force * s - mp * ln * om2 * c2s2 - mg * c, R(-2) * mp * ln * om * c * s, -c,
+             force * c + R(4) * mp * ln * om2 * s * c + mg * s, R(-2) * mp * ln * om * c2s2,
+             R(-2) * mp * ln * c * s, s, ln * den, ln * gd0, ln * hd00, pole);
+  }
+
+  // fp32 keeps the second-order jet form of the same derivatives (below):
+  // fp32 cart-pole barrier solves are chaotic at the 1e-4 level -- a 1-ulp
+  // change of the controls moves the solution 2e-5..1.2e-3 from the fp64
+  // reference (scratch/fp32_spread.py) -- and the fp32 parity instances are
+  // pinned with this form's rounding.
+  PTC_D static void accels_jet(const ProblemParams& p, R th, R om, R force, Jet<R>& cart,
                            Jet<R>& pole) {
     const R g = R(p.dyn[0]), ln = R(p.dyn[1]), mc = R(p.dyn[2]), mp = R(p.dyn[3]);
     Jet<R> TH = jvar(th, 0), OM = jvar(om, 1), FF = jvar(force, 2);
@@ -246,7 +297,13 @@ struct CartPole {
   PTC_D static void step(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
                          R (&xn)[4]) {
     const R g = R(p.dyn[0]), ln = R(p.dyn[1]), mc = R(p.dyn[2]), mp = R(p.dyn[3]), dt = R(p.dyn[4]);
-    R s = sin(x[1]), c = cos(x[1]);
+    R s, c;
+    if constexpr (sizeof(R) == 4) {
+      s = sin(x[1]);
+      c = cos(x[1]);
+    } else {
+      sincos(x[1], &s, &c);
+    }
     R den = mc + mp * s * s;
     R ca = (u[0] + mp * s * (ln * x[3] + g * c)) / den;
     R pa = (-u[0] * c - mp * ln * x[3] * x[3] * c * s - (mc + mp) * g * s) / (ln * den);
@@ -260,30 +317,37 @@ struct CartPole {
   PTC_D static void derivs(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
                            const R (&lam)[4], DynDerivs<R, 4, 1>& D) {
     const R dt = R(p.dyn[4]);
-    Jet<R> cart, pole;
-    accels(p, x[1], x[3], u[0], cart, pole);
+    Accel cart, pole;
+    if constexpr (sizeof(R) == 4) {
+      Jet<R> jc, jp;
+      accels_jet(p, x[1], x[3], u[0], jc, jp);
+      cart = {jc.g[0], jc.g[1], jc.g[2], jc.h[0][0], jc.h[0][1], jc.h[1][1], jc.h[0][2], jc.h[1][2]};
+      pole = {jp.g[0], jp.g[1], jp.g[2], jp.h[0][0], jp.h[0][1], jp.h[1][1], jp.h[0][2], jp.h[1][2]};
+    } else {
+      accels(p, x[1], x[3], u[0], cart, pole);
+    }
     set_identity(D.fx);
     D.fx[0][2] = dt;
     D.fx[1][3] = dt;
-    D.fx[2][1] = dt * cart.g[0];
-    D.fx[2][3] = dt * cart.g[1];
-    D.fx[3][1] = dt * pole.g[0];
-    D.fx[3][3] = R(1) + dt * pole.g[1];
+    D.fx[2][1] = dt * cart.g0;
+    D.fx[2][3] = dt * cart.g1;
+    D.fx[3][1] = dt * pole.g0;
+    D.fx[3][3] = R(1) + dt * pole.g1;
     D.fu[0][0] = R(0);
     D.fu[1][0] = R(0);
-    D.fu[2][0] = dt * cart.g[2];
-    D.fu[3][0] = dt * pole.g[2];
+    D.fu[2][0] = dt * cart.g2;
+    D.fu[3][0] = dt * pole.g2;
     if (kSecond) {
       set_zero(D.Hxx);
       set_zero(D.Hxu);
       D.Huu[0][0] = R(0);
       // rows 2 (cart) and 3 (pole) carry second derivatives in (theta, omega)
       const R l2 = lam[2] * dt, l3 = lam[3] * dt;
-      D.Hxx[1][1] = l2 * cart.h[0][0] + l3 * pole.h[0][0];
-      D.Hxx[1][3] = D.Hxx[3][1] = l2 * cart.h[0][1] + l3 * pole.h[0][1];
-      D.Hxx[3][3] = l2 * cart.h[1][1] + l3 * pole.h[1][1];
-      D.Hxu[1][0] = l2 * cart.h[0][2] + l3 * pole.h[0][2];
-      D.Hxu[3][0] = l2 * cart.h[1][2] + l3 * pole.h[1][2];
+      D.Hxx[1][1] = l2 * cart.h00 + l3 * pole.h00;
+      D.Hxx[1][3] = D.Hxx[3][1] = l2 * cart.h01 + l3 * pole.h01;
+      D.Hxx[3][3] = l2 * cart.h11 + l3 * pole.h11;
+      D.Hxu[1][0] = l2 * cart.h02 + l3 * pole.h02;
+      D.Hxu[3][0] = l2 * cart.h12 + l3 * pole.h12;
     }
   }
 };
