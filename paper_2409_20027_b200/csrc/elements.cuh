@@ -482,7 +482,9 @@ PTC_D int vcombine_stage(const Stage<R, NX, NU>& st, const VElem<R, NX>& r, VEle
 // Returns FLAG_DEF_R / FLAG_DEF_Q bits.
 // kCheckR: also test R_t + alpha I (DefinitenessError).  Tree and block
 // schedules have already tested every stage in the level-0 up-sweep.
-template <typename R, int NX, int NU, bool kCheckR = true>
+// FxM, FuM: structural zeros of Fx and Fu (linalg.cuh kDense = none).
+template <typename R, int NX, int NU, bool kCheckR = true, uint64_t FxM = kDense,
+          uint64_t FuM = kDense>
 PTC_D int riccati_step(const Stage<R, NX, NU>& st, const VCarry<R, NX>& c, R (&Gam)[NU][NX],
                        R (&gam)[NU], VCarry<R, NX>& o) {
   int fl = 0;
@@ -495,9 +497,9 @@ PTC_D int riccati_step(const Stage<R, NX, NU>& st, const VCarry<R, NX>& c, R (&G
     if (!cholesky<NU>(L)) fl |= FLAG_DEF_R;
   }
   R FtS[NU][NX];
-  mtm<NU, NX, NX>(st.Fu, c.Y, FtS);
+  mtm<NU, NX, NX, R, FuM>(st.Fu, c.Y, FtS);
   R Q[NU][NU];
-  mm<NU, NX, NU>(FtS, st.Fu, Q);
+  mm<NU, NX, NU, R, FuM>(FtS, st.Fu, Q);
 #pragma unroll
   for (int i = 0; i < NU; ++i)
 #pragma unroll
@@ -505,13 +507,13 @@ PTC_D int riccati_step(const Stage<R, NX, NU>& st, const VCarry<R, NX>& c, R (&G
   symmetrize<NU>(Q);
   if (!cholesky<NU>(Q)) fl |= FLAG_DEF_Q;
   R Qux[NU][NX];
-  mm<NU, NX, NX>(FtS, st.Fx, Qux);
+  mm<NU, NX, NX, R, FxM>(FtS, st.Fx, Qux);
 #pragma unroll
   for (int i = 0; i < NU; ++i)
 #pragma unroll
     for (int j = 0; j < NX; ++j) Qux[i][j] += st.M[j][i];
   R Fe[NU];
-  mtv<NU, NX>(st.Fu, c.eta, Fe);  // Fu^T eta = -Fu^T s
+  mtv<NU, NX, R, FuM>(st.Fu, c.eta, Fe);  // Fu^T eta = -Fu^T s
 #pragma unroll
   for (int i = 0; i < NU; ++i) gam[i] = st.d[i] - Fe[i];
 #pragma unroll
@@ -528,8 +530,8 @@ PTC_D int riccati_step(const Stage<R, NX, NU>& st, const VCarry<R, NX>& c, R (&G
   }
   // S' = P + Fx^T (S Fx) + Qux^T Gamma
   R SF[NX][NX];
-  mm<NX, NX, NX>(c.Y, st.Fx, SF);
-  mtm<NX, NX, NX>(st.Fx, SF, o.Y);
+  mm<NX, NX, NX, R, FxM>(c.Y, st.Fx, SF);
+  mtm<NX, NX, NX, R, FxM>(st.Fx, SF, o.Y);
   R QG[NX][NX];
   mtm<NX, NU, NX>(Qux, Gam, QG);
 #pragma unroll
@@ -539,7 +541,7 @@ PTC_D int riccati_step(const Stage<R, NX, NU>& st, const VCarry<R, NX>& c, R (&G
   symmetrize<NX>(o.Y);
   // eta' = -s' = Fx^T eta - Qux^T gamma
   R Fte[NX], Qg[NX];
-  mtv<NX, NX>(st.Fx, c.eta, Fte);
+  mtv<NX, NX, R, FxM>(st.Fx, c.eta, Fte);
   mtv<NX, NU>(Qux, gam, Qg);
 #pragma unroll
   for (int i = 0; i < NX; ++i) o.eta[i] = Fte[i] - Qg[i];

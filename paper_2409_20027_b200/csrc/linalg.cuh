@@ -9,30 +9,62 @@
 
 namespace ptc {
 
-// C = A * B  (A: MxK, B: KxN)
-template <int M, int K, int N, typename R>
+// Structural sparsity: a mask bit (row * cols + col) set = the entry may be
+// nonzero.  A model whose Jacobian has known zeros (the Euler steps' identity
+// blocks) passes its mask, and the products skip those terms: a skipped term
+// fma(a, 0, acc) = acc for finite a, so the result is the dense one up to
+// the sign of an exact zero.  kDense (every entry) is the default.
+constexpr uint64_t kDense = ~0ull;
+PTC_HD constexpr bool may_nz(uint64_t mask, int idx) { return idx >= 64 || ((mask >> idx) & 1ull); }
+// structure of A + B G for A: R x C (mask MA), B: R x K (mask MB), G dense:
+// every row of B with a nonzero fills its whole row
+template <int R_, int C_, int K_>
+PTC_HD constexpr uint64_t plus_rows_mask(uint64_t MA, uint64_t MB) {
+  if (R_ * C_ > 64 || R_ * K_ > 64) return kDense;
+  uint64_t m = MA;
+  for (int i = 0; i < R_; ++i) {
+    bool row = false;
+    for (int k = 0; k < K_; ++k) row = row || may_nz(MB, i * K_ + k);
+    if (row)
+      for (int j = 0; j < C_; ++j) m |= 1ull << (i * C_ + j);
+  }
+  return m;
+}
+
+// C = A * B  (A: MxK, B: KxN; MB, MA = structures of B and A)
+template <int M, int K, int N, typename R, uint64_t MB = kDense, uint64_t MA = kDense>
 PTC_D void mm(const R (&A)[M][K], const R (&B)[K][N], R (&C)[M][N]) {
 #pragma unroll
   for (int i = 0; i < M; ++i)
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      R acc = A[i][0] * B[0][j];
+      R acc = R(0);
+      bool any = false;
 #pragma unroll
-      for (int k = 1; k < K; ++k) acc = fma(A[i][k], B[k][j], acc);
+      for (int k = 0; k < K; ++k) {
+        if (!may_nz(MB, k * N + j) || !may_nz(MA, i * K + k)) continue;
+        acc = any ? fma(A[i][k], B[k][j], acc) : A[i][k] * B[k][j];
+        any = true;
+      }
       C[i][j] = acc;
     }
 }
 
-// C = A^T * B  (A: KxM, B: KxN)
-template <int M, int K, int N, typename R>
+// C = A^T * B  (A: KxM, B: KxN; MA = structure of A)
+template <int M, int K, int N, typename R, uint64_t MA = kDense>
 PTC_D void mtm(const R (&A)[K][M], const R (&B)[K][N], R (&C)[M][N]) {
 #pragma unroll
   for (int i = 0; i < M; ++i)
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      R acc = A[0][i] * B[0][j];
+      R acc = R(0);
+      bool any = false;
 #pragma unroll
-      for (int k = 1; k < K; ++k) acc = fma(A[k][i], B[k][j], acc);
+      for (int k = 0; k < K; ++k) {
+        if (!may_nz(MA, k * M + i)) continue;
+        acc = any ? fma(A[k][i], B[k][j], acc) : A[k][i] * B[k][j];
+        any = true;
+      }
       C[i][j] = acc;
     }
 }
@@ -51,26 +83,36 @@ PTC_D void mmt(const R (&A)[M][K], const R (&B)[N][K], R (&C)[M][N]) {
     }
 }
 
-// y = A x
-template <int M, int K, typename R>
+// y = A x  (MA = structure of A)
+template <int M, int K, typename R, uint64_t MA = kDense>
 PTC_D void mv(const R (&A)[M][K], const R (&x)[K], R (&y)[M]) {
 #pragma unroll
   for (int i = 0; i < M; ++i) {
-    R acc = A[i][0] * x[0];
+    R acc = R(0);
+    bool any = false;
 #pragma unroll
-    for (int k = 1; k < K; ++k) acc = fma(A[i][k], x[k], acc);
+    for (int k = 0; k < K; ++k) {
+      if (!may_nz(MA, i * K + k)) continue;
+      acc = any ? fma(A[i][k], x[k], acc) : A[i][k] * x[k];
+      any = true;
+    }
     y[i] = acc;
   }
 }
 
-// y = A^T x  (A: KxM)
-template <int M, int K, typename R>
+// y = A^T x  (A: KxM; MA = structure of A)
+template <int M, int K, typename R, uint64_t MA = kDense>
 PTC_D void mtv(const R (&A)[K][M], const R (&x)[K], R (&y)[M]) {
 #pragma unroll
   for (int i = 0; i < M; ++i) {
-    R acc = A[0][i] * x[0];
+    R acc = R(0);
+    bool any = false;
 #pragma unroll
-    for (int k = 1; k < K; ++k) acc = fma(A[k][i], x[k], acc);
+    for (int k = 0; k < K; ++k) {
+      if (!may_nz(MA, k * M + i)) continue;
+      acc = any ? fma(A[k][i], x[k], acc) : A[k][i] * x[k];
+      any = true;
+    }
     y[i] = acc;
   }
 }

@@ -91,6 +91,10 @@ struct DynDerivs {
 template <typename R>
 struct Pendulum {
   static constexpr int NX = 2, NU = 1;
+  // fu = [0 dt/I]^T; lambda . fxx only in (theta, theta)
+  static constexpr uint64_t kFxMask = kDense;
+  static constexpr uint64_t kFuMask = 1ull << 1;
+  static constexpr uint64_t kHxxMask = 1ull << 0;
 
   PTC_D static void step(const ProblemParams& p, int, int, const R (&x)[2], const R (&u)[1],
                          R (&xn)[2]) {
@@ -224,6 +228,14 @@ PTC_D void jsincos(const Jet<R>& a, Jet<R>& s, Jet<R>& c) {
 template <typename R>
 struct CartPole {
   static constexpr int NX = 4, NU = 1;
+  // structural nonzeros (bit i * cols + j) of the Euler step's derivatives:
+  // fx = [1 0 dt 0; 0 1 0 dt; 0 * 1 *; 0 * 0 *], fu = [0 0 * *]^T,
+  // lambda . fxx lives in (theta, omega) x (theta, omega)
+  static constexpr uint64_t kFxMask = (1ull << 0) | (1ull << 2) | (1ull << 5) | (1ull << 7) |
+                                      (1ull << 9) | (1ull << 10) | (1ull << 11) | (1ull << 13) |
+                                      (1ull << 15);
+  static constexpr uint64_t kFuMask = (1ull << 2) | (1ull << 3);
+  static constexpr uint64_t kHxxMask = (1ull << 5) | (1ull << 7) | (1ull << 13) | (1ull << 15);
 
   // Accelerations and their derivatives in the reduced variables (theta,
   // omega, force), restating the reference's closed forms
@@ -350,6 +362,16 @@ struct CartPole {
       D.Hxu[3][0] = l2 * cart.h12 + l3 * pole.h12;
     }
   }
+};
+
+// a model's structural zeros (linalg.cuh masks); dense unless it says
+template <class Dyn, class = void>
+struct JacMask {
+  static constexpr uint64_t fx = kDense, fu = kDense, hxx = kDense;
+};
+template <class Dyn>
+struct JacMask<Dyn, std::void_t<decltype(Dyn::kFxMask)>> {
+  static constexpr uint64_t fx = Dyn::kFxMask, fu = Dyn::kFuMask, hxx = Dyn::kHxxMask;
 };
 
 // x' = A_t x + B_t u + c_t with per-stage / per-problem broadcasting

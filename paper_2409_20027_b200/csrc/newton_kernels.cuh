@@ -433,6 +433,7 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
                            const R (&ln)[Dyn::NX], Stage<R, Dyn::NX, Dyn::NU>& st,
                            R (&lt)[Dyn::NX]) {
   constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  constexpr uint64_t FxM = JacMask<Dyn>::fx, FuM = JacMask<Dyn>::fu, HxxM = JacMask<Dyn>::hxx;
   DynDerivs<R, NX, NU> D;
   Dyn::template derivs<true>(p, t, b, x, u, ln, D);
   if constexpr (kUserCost<Dyn> || kUserCon<Dyn>) {
@@ -479,8 +480,8 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
       for (int k = 0; k < NU; ++k) st.Rr[i][k] = (luu[i][k] + Cuu[i][k]) + D.Huu[i][k];
     symmetrize<NU>(st.Rr);
     R ftl[NU], fxl[NX];
-    mtv<NU, NX>(D.fu, ln, ftl);
-    mtv<NX, NX>(D.fx, ln, fxl);
+    mtv<NU, NX, R, FuM>(D.fu, ln, ftl);
+    mtv<NX, NX, R, FxM>(D.fx, ln, fxl);
     for (int i = 0; i < NU; ++i) st.d[i] = (lu[i] + cu[i]) + ftl[i];
     for (int i = 0; i < NX; ++i) lt[i] = (lx[i] + cx[i]) + fxl[i];
     for (int i = 0; i < NX; ++i) {
@@ -494,11 +495,14 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
   }
   R cx[NX], cu[NU], cxx[NX], cuu[NU];
   aug_derivs<R, NX, NU>(p, g, t, a.T, a.B, b, x, u, cx, cu, cxx, cuu);
+  // (terms that are structurally zero are left out: a + 0 = a)
 #pragma unroll
   for (int i = 0; i < NX; ++i)
 #pragma unroll
-    for (int k = 0; k < NX; ++k)
-      st.P[i][k] = (R(p.Q[i * NX + k]) + (i == k ? cxx[i] : R(0))) + D.Hxx[i][k];
+    for (int k = 0; k < NX; ++k) {
+      R v = i == k ? R(p.Q[i * NX + k]) + cxx[i] : R(p.Q[i * NX + k]);
+      st.P[i][k] = may_nz(HxxM, i * NX + k) ? v + D.Hxx[i][k] : v;
+    }
   symmetrize<NX>(st.P);
 #pragma unroll
   for (int i = 0; i < NU; ++i)
@@ -507,7 +511,7 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
       st.Rr[i][k] = (R(p.Rc[i * NU + k]) + (i == k ? cuu[i] : R(0))) + D.Huu[i][k];
   symmetrize<NU>(st.Rr);
   R ftl[NU];
-  mtv<NU, NX>(D.fu, ln, ftl);
+  mtv<NU, NX, R, FuM>(D.fu, ln, ftl);
 #pragma unroll
   for (int i = 0; i < NU; ++i) {
     R ru = R(0);
@@ -516,7 +520,7 @@ PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const
     st.d[i] = (ru + cu[i]) + ftl[i];
   }
   R fxl[NX];
-  mtv<NX, NX>(D.fx, ln, fxl);
+  mtv<NX, NX, R, FxM>(D.fx, ln, fxl);
 #pragma unroll
   for (int i = 0; i < NX; ++i) {
     R lx = R(0);
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
     for (int i = 0; i < NU; ++i) st.Rr[i][i] += alpha;
     R Gam[NU][NX], gam[NU];
     VCarry<R, NX> o;
-    fl |= riccati_step(st, c, Gam, gam, o);
+    fl |= riccati_step<R, NX, NU, true, JacMask<Dyn>::fx, JacMask<Dyn>::fu>(st, c, Gam, gam, o);
     st_mat(la.Gam, t, T, B, b, Gam);
     st_vec(la.gam, t, T, B, b, gam);
     st_vec(a.d, t, T, B, b, st.d);
@@ -749,14 +753,22 @@ __global__ void __launch_bounds__(128) k_prop_fused(NewtonArgs<R> a, LqrArgs<R> 
       mx = nanmax(mx, double(fabs(du[i])));
     }
     st_vec(la.dU, t, T, B, b, du);
+    // closed loop F = fx + fu Gamma (structurally: fx's pattern plus the
+    // rows where fu has entries)
+    constexpr uint64_t FxM = JacMask<Dyn>::fx, FuM = JacMask<Dyn>::fu;
+    constexpr uint64_t FM = plus_rows_mask<NX, NX, NU>(FxM, FuM);
     R F[NX][NX], e[NX], y[NX];
-    mm<NX, NU, NX>(D.fu, Gam, F);
+    mm<NX, NU, NX, R, kDense, FuM>(D.fu, Gam, F);
 #pragma unroll
     for (int i = 0; i < NX; ++i)
 #pragma unroll
-      for (int k = 0; k < NX; ++k) F[i][k] = (t == 0) ? R(0) : F[i][k] + D.fx[i][k];
-    mv<NX, NU>(D.fu, gam, e);
-    mv<NX, NX>(F, x, y);
+      for (int k = 0; k < NX; ++k) {
+        const bool fu_row = may_nz(plus_rows_mask<NX, NX, NU>(0, FuM), i * NX + k);
+        const R v = !fu_row ? D.fx[i][k] : (may_nz(FxM, i * NX + k) ? F[i][k] + D.fx[i][k] : F[i][k]);
+        F[i][k] = (t == 0) ? R(0) : v;
+      }
+    mv<NX, NU, R, FuM>(D.fu, gam, e);
+    mv<NX, NX, R, FM>(F, x, y);
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
       x[i] = y[i] + e[i];
