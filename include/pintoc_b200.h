@@ -339,6 +339,11 @@ int ptc_solver_iterate(ptc_solver* s, int n, void* stream);
 
 /* Number of problems still running (synchronises the stream). */
 int ptc_solver_running(ptc_solver* s, int32_t* n_running, void* stream);
+/* the same count enqueued on `stream` without waiting (n_running: pinned
+ * host memory, valid once the stream reaches the copy -- record an event):
+ * lets a host loop keep the next group of iterations queued while it polls
+ * the previous one */
+int ptc_solver_running_async(ptc_solver* s, int32_t* n_running, void* stream);
 
 /* Pass-level entry points on the loaded trajectory (buffer 0):
  *   expand  = costate_pass + hamiltonian_expansion (passes.py:122, 155)

@@ -241,6 +241,10 @@ class DeviceSolver:
         N.check(self.lib.ptc_solver_running(self.handle, C.byref(out), self.stream))
         return int(out.value)
 
+    def running_async(self, dst) -> None:
+        """Enqueue the running count into dst (pinned int32 host tensor)."""
+        N.check(self.lib.ptc_solver_running_async(self.handle, dst.data_ptr(), self.stream))
+
     def run(self, group: int = 4, max_launch: int | None = None) -> int:
         """Iterate until every problem is done; returns device iterations launched."""
         s = self.settings

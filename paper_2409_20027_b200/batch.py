@@ -116,17 +116,34 @@ class BatchSolver:
         launched = [0] * len(jobs)
         caps = [(bs.settings.max_iters + 2) * max(1, bs.settings.round_cap) + 16
                 for bs, _, _ in jobs]
+        # one group stays queued while the host reads the previous group's
+        # running count (pinned copy + event), so the streams never drain
+        # waiting for the host; a finished batch runs at most one extra
+        # group of early-exit iterations
+        polls = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in jobs]
+        events = [None] * len(jobs)
         active = set(range(len(jobs)))
         n = 1
         while active:
+            pending = []
             for i in sorted(active):
                 with torch.cuda.stream(streams[i]):
                     jobs[i][0].solver.iterate(n)
                 launched[i] += n
-            for i in sorted(active):
+                pending.append((i, events[i]))
+                ev = torch.cuda.Event()
                 with torch.cuda.stream(streams[i]):
-                    if jobs[i][0].solver.running() == 0 or launched[i] >= caps[i]:
-                        active.discard(i)
+                    jobs[i][0].solver.running_async(polls[i])
+                    ev.record(streams[i])
+                # (this copy may land before the previous group's value is
+                # read below: a later count, just as valid -- it only falls)
+                events[i] = ev
+            for i, prev in pending:
+                if prev is None:
+                    continue
+                prev.synchronize()
+                if int(polls[i][0]) == 0 or launched[i] >= caps[i]:
+                    active.discard(i)
             n = group
         out = []
         for (bs, _, _), st, k in zip(jobs, streams, launched):

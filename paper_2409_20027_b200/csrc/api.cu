@@ -796,6 +796,7 @@ struct ptc_solver {
   virtual int check(int32_t* bad, cudaStream_t s) = 0;
   virtual int iterate(int n, cudaStream_t s) = 0;
   virtual int running(int32_t* n, cudaStream_t s) = 0;
+  virtual int running_async(int32_t* n, cudaStream_t s) = 0;
   virtual int expand(cudaStream_t s) = 0;
   virtual int lqr(const double* alpha_host, cudaStream_t s) = 0;
   virtual int rollout(cudaStream_t s) = 0;
@@ -1250,6 +1251,10 @@ struct Solver final : ptc_solver {
     PTC_CUDA(cudaStreamSynchronize(s));
     return PTC_OK;
   }
+  int running_async(int32_t* n, cudaStream_t s) override {
+    PTC_CUDA(cudaMemcpyAsync(n, na.n_running, sizeof(int), cudaMemcpyDeviceToHost, s));
+    return PTC_OK;
+  }
 
   int expand(cudaStream_t s) override {
     ops->expand(&na, s);
@@ -1398,6 +1403,12 @@ int ptc_solver_block_phase(ptc_solver* s, int phase, const void* in, void* out, 
 int ptc_solver_running(ptc_solver* s, int32_t* n, void* stream) {
   PTC_S(s);
   return s->running(n, (cudaStream_t)stream);
+}
+
+int ptc_solver_running_async(ptc_solver* s, int32_t* n, void* stream) {
+  PTC_S(s);
+  if (!n) return fail(PTC_ERR_ARG, "n is required");
+  return s->running_async(n, (cudaStream_t)stream);
 }
 int ptc_solver_expand(ptc_solver* s, void* stream) {
   PTC_S(s);
