@@ -314,15 +314,19 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   else if (P0 == 1 && kSplitCost<Dyn>)
     k_cost_partials<R, NX, NU, Dyn, kCostSplit><<<PTC_SEQ(kCostSplit * B), 0, s>>>(a, 0);
   else k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, 0);
-  bool fused = false;
+  bool fused = false, forward = false;
   if constexpr (NX < 8) {
     if (a.plan.L == 0) {
       // single-sweep schedule: the value sweep re-derives every stage's
       // expansion and its co-state in registers from x, u (no stored
-      // expansion or co-states), the propagation sweep the Jacobians
+      // expansion or co-states); one forward sweep then runs the
+      // propagation (Jacobians re-derived) and the candidate rollout side
+      // by side, with the rollout gate applied at its end
       k_value_fused<R, Dyn><<<PTC_SEQ(B), 0, s>>>(a, la);
-      k_prop_fused<R, Dyn><<<PTC_SEQ(B), 0, s>>>(a, la);
-      fused = true;
+      k_forward_fused<R, Dyn, !kSplitCost<Dyn>><<<PTC_SEQ(B), 0, s>>>(a, la);
+      if constexpr (kSplitCost<Dyn>)
+        k_cost_partials<R, NX, NU, Dyn, kCostSplit><<<PTC_SEQ(kCostSplit * B), 0, s>>>(a, 1);
+      fused = forward = true;
     }
   }
   if constexpr (kWideNewton<Dyn>) {
@@ -345,8 +349,8 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   constexpr int kOpsRed = RED_SUM | (RED_SUM << 2) | (RED_MAX << 4);     // sum du^2, sum du.d, max |du|
   constexpr int kOpsCost = RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4);  // sum l, sum c, first infeasible
   if (fold) k_reduce_partials<<<(unsigned)B, 256, 0, s>>>(a.red, 3, kOpsRed, (int)P0, (int)B);
-  k_roll_gate<R><<<grid_for(B), kBlock, 0, s>>>(a);
-  bool rolled = false;
+  if (!forward) k_roll_gate<R><<<grid_for(B), kBlock, 0, s>>>(a);
+  bool rolled = forward;
   if constexpr (kWideNewton<Dyn>) {
     // affine: the candidate is one exact forward scan (tree plans) or the
     // warp-per-problem recurrence

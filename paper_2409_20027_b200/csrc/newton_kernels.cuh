@@ -711,84 +711,6 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
   if (fl) atomicOr(a.flags + b, fl);
 }
 
-template <typename R, class Dyn>
-__global__ void __launch_bounds__(128) k_prop_fused(NewtonArgs<R> a, LqrArgs<R> la) {
-  constexpr int NX = Dyn::NX, NU = Dyn::NU;
-  const int b = unit_id();
-  if (b >= a.B) return;
-  if (!running(a, b)) return;
-  const int q = a.parity[b];
-  const int T = a.T, B = a.B;
-  const ProblemParams& p = *a.pp;
-  R x[NX];
-  set_zero(x);
-  double s2 = 0.0, sd = 0.0, mx = 0.0;
-  R lam0[NX];
-  set_zero(lam0);
-  R xs[NX], us[NU], Gam[NU][NX], gam[NU], dd[NU];
-  ld_x(a, q, 0, b, xs);
-  ld_u(a, q, 0, b, us);
-  ld_mat(la.Gam, 0, T, B, b, Gam);
-  ld_vec(la.gam, 0, T, B, b, gam);
-  ld_vec(a.d, 0, T, B, b, dd);
-  for (int t = 0; t < T; ++t) {
-    st_vec(la.dX, t, T + 1, B, b, x);
-    // software pipeline: stage t+1's inputs load while stage t runs
-    R xs_n[NX], us_n[NU], Gam_n[NU][NX], gam_n[NU], dd_n[NU];
-    const int tn = t + 1 < T ? t + 1 : t;
-    ld_x(a, q, tn, b, xs_n);
-    ld_u(a, q, tn, b, us_n);
-    ld_mat(la.Gam, tn, T, B, b, Gam_n);
-    ld_vec(la.gam, tn, T, B, b, gam_n);
-    ld_vec(a.d, tn, T, B, b, dd_n);
-    DynDerivs<R, NX, NU> D;
-    Dyn::template derivs<false>(p, t, b, xs, us, lam0, D);
-    R du[NU];
-    mv<NU, NX>(Gam, x, du);
-#pragma unroll
-    for (int i = 0; i < NU; ++i) {
-      du[i] += gam[i];
-      s2 += double(du[i]) * double(du[i]);
-      sd += double(du[i]) * double(dd[i]);
-      mx = nanmax(mx, double(fabs(du[i])));
-    }
-    st_vec(la.dU, t, T, B, b, du);
-    // closed loop F = fx + fu Gamma (structurally: fx's pattern plus the
-    // rows where fu has entries)
-    constexpr uint64_t FxM = JacMask<Dyn>::fx, FuM = JacMask<Dyn>::fu;
-    constexpr uint64_t FM = plus_rows_mask<NX, NX, NU>(FxM, FuM);
-    R F[NX][NX], e[NX], y[NX];
-    mm<NX, NU, NX, R, kDense, FuM>(D.fu, Gam, F);
-#pragma unroll
-    for (int i = 0; i < NX; ++i)
-#pragma unroll
-      for (int k = 0; k < NX; ++k) {
-        const bool fu_row = may_nz(plus_rows_mask<NX, NX, NU>(0, FuM), i * NX + k);
-        const R v = !fu_row ? D.fx[i][k] : (may_nz(FxM, i * NX + k) ? F[i][k] + D.fx[i][k] : F[i][k]);
-        F[i][k] = (t == 0) ? R(0) : v;
-      }
-    mv<NX, NU, R, FuM>(D.fu, gam, e);
-    mv<NX, NX, R, FM>(F, x, y);
-#pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      x[i] = y[i] + e[i];
-      xs[i] = xs_n[i];
-    }
-#pragma unroll
-    for (int i = 0; i < NU; ++i) {
-      us[i] = us_n[i];
-      gam[i] = gam_n[i];
-      dd[i] = dd_n[i];
-#pragma unroll
-      for (int k = 0; k < NX; ++k) Gam[i][k] = Gam_n[i][k];
-    }
-  }
-  st_vec(la.dX, T, T + 1, B, b, x);
-  la.red[(size_t)0 * B + b] = s2;
-  la.red[(size_t)1 * B + b] = sd;
-  la.red[(size_t)2 * B + b] = mx;
-}
-
 // --------------------------------------------------------------- rollout
 
 enum : int { RS_SKIP = 1, RS_CONV = 2, RS_IN_XR = 4 };
@@ -904,6 +826,153 @@ __global__ void __launch_bounds__(128) k_rollout(NewtonArgs<R> a, const R* dU) {
   if (!finite) atomicOr(a.flags + b, FLAG_DIVERGED);
   if constexpr (kCost) {
     if constexpr (kUserCost<Dyn>) sl += double(Dyn::uterm(gp, x));   // x = x_T
+    double* cp = a.cpart[1];  // P0 == 1
+    cp[(size_t)0 * B + b] = sl;
+    cp[(size_t)1 * B + b] = sc;
+    cp[(size_t)2 * B + b] = double(bad);
+  }
+}
+
+// ------------------------------------ fused forward sweep (single-sweep plans)
+//
+// The propagation sweep (passes.py:330-361, Jacobians re-derived from x, u
+// like k_value_fused) and the candidate rollout (k_rollout) both walk the
+// horizon forwards, one thread per problem, and both are
+// latency-bound chains (the 4x4 closed-loop recurrence; the model's step).
+// Here one thread runs them side by side, stage by stage: du_t is formed
+// from the deviation recurrence and at once added to u_t to drive the
+// candidate's step, so the two independent chains fill each other's latency
+// and du, dx never touch HBM.  newton.py:190-197 rolls out only when the
+// step norm exceeds inner_tol; the thread knows its norm only at the end, so
+// the candidate is built speculatively and its outcome (divergence flag)
+// is kept only when the gate passes -- k_control never reads the candidate
+// of a gated problem (same decisions and bits as prop + gate + rollout).
+// kCost: the candidate's stage / augmentation costs accumulate in the same
+// sweep (otherwise k_cost_partials(a, 1) runs after).
+template <typename R, class Dyn, bool kCost>
+__global__ void __launch_bounds__(128) k_forward_fused(NewtonArgs<R> a, LqrArgs<R> la) {
+  constexpr int NX = Dyn::NX, NU = Dyn::NU;
+  const int b = unit_id();
+  if (b >= a.B) return;
+  if (!running(a, b)) return;
+  if (a.flags[b] & (FLAG_DEF_R | FLAG_DEF_Q | FLAG_COND)) {
+    a.rstate[b] = RS_SKIP;  // no law: k_control escalates alpha
+    return;
+  }
+  const int q = a.parity[b], c = 1 - q;
+  const int T = a.T, B = a.B;
+  ProblemParams p;   // model constants in registers (see k_rollout)
+  const ProblemParams& gp = *a.pp;
+  p.dyn_kind = gp.dyn_kind;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p.dyn[i] = gp.dyn[i];
+  p.lin_T = gp.lin_T;
+  p.lin_B = gp.lin_B;
+  p.lin_A = gp.lin_A;
+  p.lin_Bm = gp.lin_Bm;
+  p.lin_c = gp.lin_c;
+  p.lin_st = gp.lin_st;
+  p.user_data = gp.user_data;
+  R* Xc = a.X + c * a.xsz;
+  R* Uc = a.U + c * a.usz;
+  const AugArgs<R> g = aug_of(a);
+  CostRegs<R, NX, NU> cr;
+  if constexpr (kCost && NX < 8) cr.load(gp);
+  R x[NX], xc[NX], lam0[NX];
+  set_zero(x);
+  set_zero(lam0);
+  double s2 = 0.0, sd = 0.0, mx = 0.0, sl = 0.0, sc = 0.0;
+  int bad = -1;
+  bool finite = true;
+  R xs[NX], us[NU], Gam[NU][NX], gam[NU], dd[NU];
+  ld_x(a, q, 0, b, xs);
+  ld_u(a, q, 0, b, us);
+  ld_mat(la.Gam, 0, T, B, b, Gam);
+  ld_vec(la.gam, 0, T, B, b, gam);
+  ld_vec(a.d, 0, T, B, b, dd);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) xc[i] = xs[i];
+  st_vec(Xc, 0, T + 1, B, b, xc);
+  for (int t = 0; t < T; ++t) {
+    // software pipeline: stage t+1's inputs load while stage t runs
+    R xs_n[NX], us_n[NU], Gam_n[NU][NX], gam_n[NU], dd_n[NU];
+    const int tn = t + 1 < T ? t + 1 : t;
+    ld_x(a, q, tn, b, xs_n);
+    ld_u(a, q, tn, b, us_n);
+    ld_mat(la.Gam, tn, T, B, b, Gam_n);
+    ld_vec(la.gam, tn, T, B, b, gam_n);
+    ld_vec(a.d, tn, T, B, b, dd_n);
+    R du[NU], uc[NU];
+    mv<NU, NX>(Gam, x, du);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      du[i] += gam[i];
+      s2 += double(du[i]) * double(du[i]);
+      sd += double(du[i]) * double(dd[i]);
+      mx = nanmax(mx, double(fabs(du[i])));
+      uc[i] = us[i] + du[i];   // the candidate control u + du (problem.py:449)
+    }
+    st_vec(Uc, t, T, B, b, uc);
+    // candidate chain: stage cost at (xc_t, uc_t), then xc_{t+1} = f(xc_t, uc_t)
+    if constexpr (kCost) {
+      if constexpr (kUserCost<Dyn>) sl += double(Dyn::ucost(gp, t, xc, uc));
+      else if constexpr (NX < 8) sl += double(stage_cost<R, NX, NU>(cr, xc, uc));
+      else sl += double(stage_cost<R, NX, NU>(gp, xc, uc));
+      int br;
+      if constexpr (kUserCon<Dyn>) sc += double(aug_value_user<R, Dyn>(gp, g, t, T, B, b, xc, uc, br));
+      else sc += double(aug_value<R, NX, NU>(gp, g, t, T, B, b, xc, uc, br));
+      if (br >= 0 && bad < 0) bad = t * gp.W + br;
+    }
+    R xcn[NX];
+    Dyn::step(p, t, b, xc, uc, xcn);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      finite = finite && isfinite(xcn[i]);
+      xc[i] = xcn[i];
+    }
+    st_vec(Xc, t + 1, T + 1, B, b, xc);
+    // deviation chain: dx_{t+1} = (fx + fu Gamma) dx_t + fu gamma at the
+    // current trajectory
+    DynDerivs<R, NX, NU> D;
+    Dyn::template derivs<false>(p, t, b, xs, us, lam0, D);
+    constexpr uint64_t FxM = JacMask<Dyn>::fx, FuM = JacMask<Dyn>::fu;
+    constexpr uint64_t FM = plus_rows_mask<NX, NX, NU>(FxM, FuM);
+    R F[NX][NX], e[NX], y[NX];
+    mm<NX, NU, NX, R, kDense, FuM>(D.fu, Gam, F);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NX; ++k) {
+        const bool fu_row = may_nz(plus_rows_mask<NX, NX, NU>(0, FuM), i * NX + k);
+        const R v = !fu_row ? D.fx[i][k] : (may_nz(FxM, i * NX + k) ? F[i][k] + D.fx[i][k] : F[i][k]);
+        F[i][k] = (t == 0) ? R(0) : v;
+      }
+    mv<NX, NU, R, FuM>(D.fu, gam, e);
+    mv<NX, NX, R, FM>(F, x, y);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      x[i] = y[i] + e[i];
+      xs[i] = xs_n[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      us[i] = us_n[i];
+      gam[i] = gam_n[i];
+      dd[i] = dd_n[i];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) Gam[i][k] = Gam_n[i][k];
+    }
+  }
+  la.red[(size_t)0 * B + b] = s2;
+  la.red[(size_t)1 * B + b] = sd;
+  la.red[(size_t)2 * B + b] = mx;
+  // the rollout gate of newton.py:181 (k_roll_gate): only a step above
+  // inner_tol is rolled out, so only then does the candidate's outcome count
+  const bool gated = mx <= a.opt.inner_tol;
+  a.rstate[b] = gated ? RS_SKIP : 0;
+  if (!gated && !finite) atomicOr(a.flags + b, FLAG_DIVERGED);
+  if constexpr (kCost) {
+    if constexpr (kUserCost<Dyn>) sl += double(Dyn::uterm(gp, xc));   // xc = x_T
     double* cp = a.cpart[1];  // P0 == 1
     cp[(size_t)0 * B + b] = sl;
     cp[(size_t)1 * B + b] = sc;
