@@ -13,15 +13,11 @@
 namespace ptc {
 
 constexpr int kBlock = 128;
-// Single-unit plans cost the candidate either inside the rollout (the stage
-// costs fill the dynamics recurrence's latency) or, for the smallest models
-// whose recurrence is too short to hide them, with kCostSplit lanes per
-// problem summing horizon ranges (k_cost_partials<.., kCostSplit>).
-// Measured per Newton iteration at 32,768 problems, T = 256: pendulum 1.19
-// -> 1.14 ms split; cart-pole 1.58 fused vs 1.70 ms split.
-constexpr int kCostSplit = 8;
-template <class Dyn>
-constexpr bool kSplitCost = Dyn::NX <= 2;
+// Single-unit plans cost the candidate inside the forward sweep that rolls
+// it out (k_forward_fused; the stage costs fill the recurrences' latency).
+// Round 2 measured, per Newton iteration at 32,768 problems, T = 256: the
+// pendulum's cost on 8 lanes per problem after a separate rollout 1.14 ms,
+// inside the fused forward sweep 0.93 ms.
 
 inline dim3 grid_for(long long n) { return dim3((unsigned)((n + kBlock - 1) / kBlock)); }
 
@@ -311,8 +307,6 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
   const long long B = a.B, P0 = a.plan.units0();
   cudaMemsetAsync(a.n_running, 0, sizeof(int), s);
   if constexpr (kWideNewton<Dyn>) WideNewton<R, NX, NU>::cost_partials(a, 0, s);
-  else if (P0 == 1 && kSplitCost<Dyn>)
-    k_cost_partials<R, NX, NU, Dyn, kCostSplit><<<PTC_SEQ(kCostSplit * B), 0, s>>>(a, 0);
   else k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, 0);
   bool fused = false, forward = false;
   if constexpr (NX < 8) {
@@ -323,9 +317,7 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
       // propagation (Jacobians re-derived) and the candidate rollout side
       // by side, with the rollout gate applied at its end
       k_value_fused<R, Dyn><<<PTC_SEQ(B), 0, s>>>(a, la);
-      k_forward_fused<R, Dyn, !kSplitCost<Dyn>><<<PTC_SEQ(B), 0, s>>>(a, la);
-      if constexpr (kSplitCost<Dyn>)
-        k_cost_partials<R, NX, NU, Dyn, kCostSplit><<<PTC_SEQ(kCostSplit * B), 0, s>>>(a, 1);
+      k_forward_fused<R, Dyn, true><<<PTC_SEQ(B), 0, s>>>(a, la);
       fused = forward = true;
     }
   }
@@ -388,9 +380,6 @@ void launch_newton_iteration(const NewtonArgs<R>& a, const LqrArgs<R>& la, cudaS
     k_pr_finish<R, NX><<<grid_for(nT), kBlock, 0, s>>>(a);
     k_rollout<R, Dyn, true><<<PTC_SEQ(B), 0, s>>>(a, la.dU);
     k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ(P0 * B), 0, s>>>(a, 1);
-  } else if (P0 == 1 && kSplitCost<Dyn>) {
-    k_rollout<R, Dyn, false><<<PTC_SEQ(B), 0, s>>>(a, la.dU);
-    k_cost_partials<R, NX, NU, Dyn, kCostSplit><<<PTC_SEQ(kCostSplit * B), 0, s>>>(a, 1);
   } else if (P0 == 1) {
     // one unit per problem: the rollout also accumulates the candidate cost
     k_rollout<R, Dyn, false, true><<<PTC_SEQ(B), 0, s>>>(a, la.dU);
@@ -548,10 +537,7 @@ struct RegisterNewton {
     const NewtonArgs<R>& a = A(p);
     k_force_phase<R><<<grid_for(a.B), kBlock, 0, s>>>(a, PH_NEED_COST);
     const int P0 = a.plan.units0();
-    if (P0 == 1 && kSplitCost<Dyn>)  // the iteration's summation order
-      k_cost_partials<R, NX, NU, Dyn, kCostSplit><<<PTC_SEQ((long long)kCostSplit * a.B), 0, s>>>(a, 0);
-    else
-      k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ((long long)P0 * a.B), 0, s>>>(a, 0);
+    k_cost_partials<R, NX, NU, Dyn><<<PTC_SEQ((long long)P0 * a.B), 0, s>>>(a, 0);
     if (partial_rows(P0) < P0)
       k_reduce_partials<<<(unsigned)a.B, 256, 0, s>>>(a.cpart[0], 3,
                                                       RED_SUM | (RED_SUM << 2) | (RED_FIRST << 4),

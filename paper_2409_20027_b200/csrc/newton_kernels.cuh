@@ -222,29 +222,21 @@ __global__ void k_admm_init(NewtonArgs<R> a) {
 // ------------------------------------------------------- cost of a trajectory
 
 // which = 0: current trajectory (only when PH_NEED_COST), 1: the candidate.
-// NCH > 1 (single-unit plans only): NCH consecutive lanes split one
-// problem's horizon into NCH ranges and fold their sums with shuffles, so
-// the stage costs (logs of the barrier, the model's cost) run with NCH x
-// the parallelism of one thread per problem; the result lands in row 0.
-template <typename R, int NX, int NU, class Dyn = void, int NCH = 1>
+template <typename R, int NX, int NU, class Dyn = void>
 __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int which) {
-  static_assert(NCH >= 1 && NCH <= 32 && (NCH & (NCH - 1)) == 0, "NCH: power of two <= 32");
   // cost constants: registers for small states, the block's shared copy for
   // wide ones (loaded before any thread leaves)
   __shared__ CostSmem<R, NX, NU> cs_shared;
   if constexpr (NX >= 8) cs_shared.load(*a.pp);
-  const int P0 = NCH > 1 ? 1 : a.plan.units0();
-  const int gid = unit_id();
-  const int u0 = gid / NCH, part = gid % NCH;
+  const int P0 = a.plan.units0();
+  const int u0 = unit_id();
   if (u0 >= P0 * a.B) return;
   const int b = u0 % a.B, j = u0 / a.B;
-  // (the NCH lanes of a problem leave together: same b)
   if (!running(a, b)) return;
   if (which == 0 && !(a.phase[b] & PH_NEED_COST)) return;
   const int q = which == 0 ? a.parity[b] : 1 - a.parity[b];
   const int T = a.T, B = a.B;
-  const int len = NCH > 1 ? (T + NCH - 1) / NCH : a.plan.K0;
-  const int t0 = NCH > 1 ? part * len : j * a.plan.K0, t1 = min(T, t0 + len);
+  const int t0 = j * a.plan.K0, t1 = min(T, t0 + a.plan.K0);
   const ProblemParams& p = *a.pp;
   const AugArgs<R> g = aug_of(a);
   double sl = 0.0, sc = 0.0;
@@ -266,25 +258,11 @@ __global__ void __launch_bounds__(128) k_cost_partials(NewtonArgs<R> a, int whic
     if (br >= 0 && bad < 0) bad = t * p.W + br;
   }
   if constexpr (!std::is_void_v<Dyn> && kUserCost<Dyn>) {
-    if (j == P0 - 1 && part == NCH - 1) {   // the terminal cost rides in the last unit's partial
+    if (j == P0 - 1) {   // the terminal cost rides in the last unit's partial
       R xT[NX];
       ld_x(a, q, T, b, xT);
       sl += double(Dyn::uterm(p, xT));
     }
-  }
-  if constexpr (NCH > 1) {
-    const int lane = threadIdx.x & 31;
-    const unsigned mask = ((NCH == 32) ? 0xffffffffu : ((1u << NCH) - 1)) << (lane & ~(NCH - 1));
-    double fb = double(bad);
-#pragma unroll
-    for (int o = 1; o < NCH; o <<= 1) {
-      sl += __shfl_xor_sync(mask, sl, o);
-      sc += __shfl_xor_sync(mask, sc, o);
-      const double ob = __shfl_xor_sync(mask, fb, o);
-      if (ob >= 0.0 && (fb < 0.0 || ob < fb)) fb = ob;
-    }
-    bad = int(fb);
-    if (part != 0) return;
   }
   double* cp = a.cpart[which];
   cp[((size_t)0 * P0 + j) * B + b] = sl;
