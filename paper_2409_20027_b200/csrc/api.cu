@@ -895,6 +895,14 @@ struct Solver final : ptc_solver {
       p.row_idx[W] = idx;
       p.row_sign[W] = sign;
       p.row_bound[W] = bound;
+      const int v = var == 0 ? idx : kMaxNX + idx;
+      if (sign > 0) {
+        p.box_up |= 1u << v;
+        p.box_ub[v] = bound;
+      } else {
+        p.box_lo |= 1u << v;
+        p.box_lb[v] = bound;
+      }
       ++W;
     };
     // stacking order of BoxConstraint (problem.py:254-260): state upper,

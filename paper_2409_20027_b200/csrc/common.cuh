@@ -17,6 +17,11 @@
 #define PTC_D __device__ __forceinline__
 
 namespace ptc {
+
+// a rounded product the compiler may not contract into a following add
+// (keeps the bits of code that formed the product as a separate value)
+PTC_D double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+PTC_D float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 // correctly rounded reciprocal (bit-identical to R(1) / x under IEEE
 // division, without the general division's numerator path)
 __device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }

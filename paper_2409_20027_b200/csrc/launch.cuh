@@ -44,6 +44,14 @@ inline SeqLaunch seq_launch(long long n) {
 }
 #define PTC_SEQ(n) seq_launch(n).grid, seq_launch(n).block
 
+// Forward (propagation) level-0 sweep: a register ring of kPropRing stages
+// in flight per thread for the thread-per-unit sizes (round 2, config 3,
+// gpurun pf probe: cart-pole sweep 0.380 -> 0.302 ms, pendulum half 0.506
+// -> 0.450 ms; a ring of 4 spills at nx 4 and is slower at nx 2 too).  The
+// backward sweep keeps one stage in flight: its 36-word cart-pole stage
+// spills at two (0.477 -> 0.937 ms).
+template <int NX>
+constexpr int kPropRing = NX <= 4 ? 2 : 1;
 template <typename R, int NX, int NU>
 void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
   const Plan& pl = a.plan;
@@ -69,7 +77,7 @@ void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
     for (int l = pl.L - 1; l >= 1; --l)
       k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
   }
-  k_prop_down0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
+  k_prop_down0<R, NX, NU, kPropRing<NX>><<<PTC_SEQ(P0 * B), 0, s>>>(a);
 }
 
 template <typename R, int NX, int NU>
@@ -87,7 +95,7 @@ void launch_prop(const LqrArgs<R>& a, cudaStream_t s) {
     for (int l = pl.L - 1; l >= 1; --l)
       k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
   }
-  k_prop_down0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
+  k_prop_down0<R, NX, NU, kPropRing<NX>><<<PTC_SEQ(P0 * B), 0, s>>>(a);
 }
 
 // Time-block phases (horizon sharded across ranks; sharded.py drives them
@@ -125,7 +133,7 @@ void launch_lqr_block(const LqrArgs<R>& a0, int phase, const void* blocks, void*
       for (int l = pl.L - 1; l >= 1; --l)
         k_prop_down<R, NX><<<grid_for(pl.n[l + 1] * B), kBlock, 0, s>>>(a, l);
     }
-    k_prop_down0<R, NX, NU><<<PTC_SEQ(P0 * B), 0, s>>>(a);
+    k_prop_down0<R, NX, NU, kPropRing<NX>><<<PTC_SEQ(P0 * B), 0, s>>>(a);
   }
 }
 

@@ -373,7 +373,7 @@ PTC_D void ld_prop_stage(const LqrArgs<R>& a, int t, int b, PropStage<R, NX, NU>
 
 // level-0 forward sweep: dx_t, du_t = Gamma_t dx_t + gamma_t and the
 // per-chunk partial reductions used by the trust-region test
-template <typename R, int NX, int NU>
+template <typename R, int NX, int NU, int D = 1>
 __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
   const int P0 = a.plan.units0();
   const int u = unit_id();
@@ -387,35 +387,42 @@ __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
   else if (a.x_in) ld_vec(a.x_in, 0, 1, B, b, x);
   else set_zero(x);
   double s2 = 0.0, sd = 0.0, mx = 0.0;
-  // software pipeline: stage t+1's law and Jacobians load while stage t runs
-  PropStage<R, NX, NU> ps;
-  if (t0 < t1) ld_prop_stage(a, t0, b, ps);
-  for (int t = t0; t < t1; ++t) {
-    PropStage<R, NX, NU> nps;
-    if (t + 1 < t1) ld_prop_stage(a, t + 1, b, nps);
-    st_vec(a.dX, t, T + 1, B, b, x);
-    R du[NU];
-    mv<NU, NX>(ps.Gam, x, du);
+  // software pipeline: a register ring of D stages, stage t + D's law and
+  // Jacobians loading while stage t runs
+  PropStage<R, NX, NU> ring[D];
 #pragma unroll
-    for (int i = 0; i < NU; ++i) {
-      du[i] += ps.gam[i];
-      s2 += double(du[i]) * double(du[i]);
-      sd += double(du[i]) * double(ps.dd[i]);
-      mx = nanmax(mx, double(fabs(du[i])));
+  for (int k = 0; k < D; ++k)
+    if (t0 + k < t1) ld_prop_stage(a, t0 + k, b, ring[k]);
+  for (int tb = t0; tb < t1; tb += D) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int t = tb + k;
+      if (t >= t1) break;
+      const PropStage<R, NX, NU> ps = ring[k];
+      if (t + D < t1) ld_prop_stage(a, t + D, b, ring[k]);
+      st_vec(a.dX, t, T + 1, B, b, x);
+      R du[NU];
+      mv<NU, NX>(ps.Gam, x, du);
+#pragma unroll
+      for (int i = 0; i < NU; ++i) {
+        du[i] += ps.gam[i];
+        s2 += double(du[i]) * double(du[i]);
+        sd += double(du[i]) * double(ps.dd[i]);
+        mx = nanmax(mx, double(fabs(du[i])));
+      }
+      st_vec(a.dU, t, T, B, b, du);
+      // closed loop: F = Fx + Fu Gamma (F = 0 on the head stage), e = Fu gamma
+      R F[NX][NX], e[NX], y[NX];
+      mm<NX, NU, NX>(ps.Fu, ps.Gam, F);
+#pragma unroll
+      for (int i = 0; i < NX; ++i)
+#pragma unroll
+        for (int k2 = 0; k2 < NX; ++k2) F[i][k2] = (t + a.t_base == 0) ? R(0) : F[i][k2] + ps.Fx[i][k2];
+      mv<NX, NU>(ps.Fu, ps.gam, e);
+      mv<NX, NX>(F, x, y);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
     }
-    st_vec(a.dU, t, T, B, b, du);
-    // closed loop: F = Fx + Fu Gamma (F = 0 on the head stage), e = Fu gamma
-    R F[NX][NX], e[NX], y[NX];
-    mm<NX, NU, NX>(ps.Fu, ps.Gam, F);
-#pragma unroll
-    for (int i = 0; i < NX; ++i)
-#pragma unroll
-      for (int k = 0; k < NX; ++k) F[i][k] = (t + a.t_base == 0) ? R(0) : F[i][k] + ps.Fx[i][k];
-    mv<NX, NU>(ps.Fu, ps.gam, e);
-    mv<NX, NX>(F, x, y);
-#pragma unroll
-    for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
-    if (t + 1 < t1) ps = nps;
   }
   if (j == P0 - 1) st_vec(a.dX, T, T + 1, B, b, x);
   if (a.red) {

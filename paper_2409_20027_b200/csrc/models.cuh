@@ -46,6 +46,10 @@ struct ProblemParams {
   int row_idx[kMaxRows];
   double row_sign[kMaxRows];
   double row_bound[kMaxRows];
+  // the same box rows by variable (bit i: state i, bit kMaxNX + i: control
+  // i), so the barrier sweeps unroll over compile-time variable indices
+  unsigned box_up, box_lo;
+  double box_ub[kMaxNX + kMaxNU], box_lb[kMaxNX + kMaxNU];
 };
 
 // Models whose cost is user code (user_model.cuh UserModel with a cost
@@ -568,13 +572,29 @@ PTC_D R aug_value(const ProblemParams& p, const AugArgs<R>& a, int t, int T, int
   if (a.kind == AUG_ZERO) return R(0);
   const int W = p.W;
   if (a.kind == AUG_BARRIER) {
+    // rows in the stacking order of build_params (api.cu; problem.py:254-260):
+    // state upper, state lower, control upper, control lower -- the same
+    // values and summation order as the row table, unrolled over variables
     R sg = R(0), sh = R(0);
-    for (int k = 0; k < W; ++k) {
-      R w = row_value<R, NX, NU>(p, k, x, u);
+    int k = 0;
+    const unsigned up = p.box_up, lo = p.box_lo;
+    auto row = [&](R w, R& acc) {
       if (w >= R(0) && bad_row < 0) bad_row = k;
-      R lg = log(-w);
-      if (k < p.Ws) sg += lg; else sh += lg;
-    }
+      acc += log(-w);
+      ++k;
+    };
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+      if (up >> i & 1u) row(x[i] - R(p.box_ub[i]), sg);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+      if (lo >> i & 1u) row(R(p.box_lb[i]) - x[i], sg);
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+      if (up >> (kMaxNX + i) & 1u) row(u[i] - R(p.box_ub[kMaxNX + i]), sh);
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+      if (lo >> (kMaxNX + i) & 1u) row(R(p.box_lb[kMaxNX + i]) - u[i], sh);
     return -R(a.mu[b]) * (sg + sh);
   }
   const R rho = R(a.rho);
@@ -602,24 +622,40 @@ PTC_D void aug_derivs(const ProblemParams& p, const AugArgs<R>& a, int t, int T,
   const int W = p.W;
   if (a.kind == AUG_BARRIER) {
     const R mu = R(a.mu[b]);
-    for (int k = 0; k < W; ++k) {
-      R w = row_value<R, NX, NU>(p, k, x, u);
-      R inv = R(1) / w;
-      R sgn = R(p.row_sign[k]);
-      R sc = sgn / w;
-      R g1 = sgn * inv;
-      R h1 = sc * sc;
-      const int idx = p.row_idx[k];
-      if (p.row_var[k] == 0) {
+    // per row w = sign (var - bound): gradient sign / w, Hessian 1 / w^2.
+    // sign = +-1, so sign / w is exactly +-(1 / w): one division per row.
+    // Unrolled over variables (a variable's upper row before its lower one,
+    // as in the row table, the Hessian term rounded before it is summed:
+    // same sums, same bits)
+    const unsigned up = p.box_up, lo = p.box_lo;
 #pragma unroll
-        for (int i = 0; i < NX; ++i)
-          if (i == idx) { cx[i] += g1; cxx[i] += h1; }
-      } else {
-#pragma unroll
-        for (int i = 0; i < NU; ++i)
-          if (i == idx) { cu[i] += g1; cuu[i] += h1; }
+    for (int i = 0; i < NX; ++i)
+      if (up >> i & 1u) {
+        const R inv = R(1) / (x[i] - R(p.box_ub[i]));
+        cx[i] += inv;
+        cxx[i] += mul_rn(inv, inv);
       }
-    }
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+      if (lo >> i & 1u) {
+        const R inv = R(1) / (R(p.box_lb[i]) - x[i]);
+        cx[i] += -inv;
+        cxx[i] += mul_rn(inv, inv);
+      }
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+      if (up >> (kMaxNX + i) & 1u) {
+        const R inv = R(1) / (u[i] - R(p.box_ub[kMaxNX + i]));
+        cu[i] += inv;
+        cuu[i] += mul_rn(inv, inv);
+      }
+#pragma unroll
+    for (int i = 0; i < NU; ++i)
+      if (lo >> (kMaxNX + i) & 1u) {
+        const R inv = R(1) / (R(p.box_lb[kMaxNX + i]) - u[i]);
+        cu[i] += -inv;
+        cuu[i] += mul_rn(inv, inv);
+      }
 #pragma unroll
     for (int i = 0; i < NX; ++i) { cx[i] = -mu * cx[i]; cxx[i] = mu * cxx[i]; }
 #pragma unroll
