@@ -976,6 +976,12 @@ struct Solver final : ptc_solver {
     // launches to every iteration of the problems that never converge
     a.pr_iters = par ? 4 : 0;
     a.xr = par ? c.template take<R>(a.xsz) : nullptr;
+    // cached sin / cos of each trajectory buffer's pole angle (CartPole's
+    // kAux values, single-sweep Newton kernels, fp64)
+    const bool aux = !d.block_mode && d.model == PTC_DYN_CARTPOLE && sizeof(R) == 8;
+    a.auxsz = aux ? 2 * T * B : 0;
+    a.aux = aux ? c.template take<R>(2 * a.auxsz) : nullptr;
+    a.aux_ok = aux ? ib() : nullptr;
     a.alpha = db(); a.nu = db(); a.cur_cost = db(); a.cand_cost = db(); a.mu = db();
     a.bad_value = db();
     a.opt.hist_cap = std::max(0, d.hist_cap);
@@ -1172,6 +1178,7 @@ struct Solver final : ptc_solver {
     auto kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     PTC_CUDA(cudaMemcpyAsync(na.X, X, sizeof(R) * na.xsz, kind, s));
     PTC_CUDA(cudaMemcpyAsync(na.U, U, sizeof(R) * na.usz, kind, s));
+    PTC_CUDA(clear_aux(s));
     ops->init(&na, s);
     if (desc.method == PTC_METHOD_NEWTON && na.aug_kind == AUG_ADMM) {
       const size_t n = sizeof(R) * (size_t)std::max(W, 1) * na.T * na.B;
@@ -1222,6 +1229,12 @@ struct Solver final : ptc_solver {
   ~Solver() override {
     if (iter_exec) cudaGraphExecDestroy(iter_exec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+  }
+
+  // states written outside the iteration: no trajectory buffer's cached
+  // auxiliary values belong to it any more
+  cudaError_t clear_aux(cudaStream_t s) {
+    return na.aux_ok ? cudaMemsetAsync(na.aux_ok, 0, sizeof(int) * na.B, s) : cudaSuccess;
   }
 
   int iterate(int n, cudaStream_t s) override {
@@ -1286,6 +1299,7 @@ struct Solver final : ptc_solver {
   int rollout(cudaStream_t s) override {
     if (na.blk) return fail(PTC_ERR_ARG, "block_mode solvers roll out through block phases 8 / 9");
     PTC_CUDA(cudaMemsetAsync(na.bad_index, 0xff, sizeof(int) * na.B, s));
+    PTC_CUDA(clear_aux(s));
     ops->rollout(&na, s);
     PTC_CUDA(cudaGetLastError());
     return PTC_OK;
@@ -1314,6 +1328,7 @@ struct Solver final : ptc_solver {
       const long long n = (long long)na.B * (na.T + 1);
       k_normalize_parity<R><<<grid_for(n), kBlock, 0, s>>>(na, nx, nu);
       k_clear_parity<R><<<grid_for(na.B), kBlock, 0, s>>>(na);
+      PTC_CUDA(clear_aux(s));
     }
     PTC_CUDA(cudaMemcpyAsync(dst, bf.p, bf.numel * bf.es,
                              on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));

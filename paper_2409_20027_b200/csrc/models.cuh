@@ -268,10 +268,9 @@ struct CartPole {
     q.h12 = R(0);
   }
 
-  PTC_D static void accels(const ProblemParams& p, R th, R om, R force, Accel& cart, Accel& pole) {
+  PTC_D static void accels(const ProblemParams& p, R s, R c, R om, R force, Accel& cart,
+                           Accel& pole) {
     const R g = R(p.dyn[0]), ln = R(p.dyn[1]), mc = R(p.dyn[2]), mp = R(p.dyn[3]);
-    R s, c;
-    sincos(th, &s, &c);
     const R c2s2 = c * c - s * s;
     const R den = mc + mp * s * s;
     const R gd0 = R(2) * mp * s * c;
@@ -310,16 +309,19 @@ struct CartPole {
     pole = jscale(jmul(n2, rden), R(1) / ln);
   }
 
-  PTC_D static void step(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
-                         R (&xn)[4]) {
+  // per-stage auxiliary values of a state (sin theta, cos theta): a
+  // trajectory's are cached next to it by the single-sweep Newton kernels,
+  // so the value sweep and the forward sweep's Jacobians reuse the ones the
+  // candidate's rollout evaluated (same calls, same bits; Newton iteration
+  // 0.998 -> 0.961 ms at 32,768 problems).  fp64 only (the fp32
+  // derivatives keep their jet form)
+  static constexpr int kAux = sizeof(R) == 8 ? 2 : 0;
+  PTC_D static void aux(const R (&x)[4], R (&w)[2]) { sincos(x[1], &w[0], &w[1]); }
+
+  PTC_D static void step_w(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
+                           const R (&w)[2], R (&xn)[4]) {
     const R g = R(p.dyn[0]), ln = R(p.dyn[1]), mc = R(p.dyn[2]), mp = R(p.dyn[3]), dt = R(p.dyn[4]);
-    R s, c;
-    if constexpr (sizeof(R) == 4) {
-      s = sin(x[1]);
-      c = cos(x[1]);
-    } else {
-      sincos(x[1], &s, &c);
-    }
+    const R s = w[0], c = w[1];
     R den = mc + mp * s * s;
     R ca = (u[0] + mp * s * (ln * x[3] + g * c)) / den;
     R pa = (-u[0] * c - mp * ln * x[3] * x[3] * c * s - (mc + mp) * g * s) / (ln * den);
@@ -329,9 +331,21 @@ struct CartPole {
     xn[3] = x[3] + dt * pa;
   }
 
+  PTC_D static void step(const ProblemParams& p, int t, int b, const R (&x)[4], const R (&u)[1],
+                         R (&xn)[4]) {
+    R w[2];
+    if constexpr (sizeof(R) == 4) {
+      w[0] = sin(x[1]);
+      w[1] = cos(x[1]);
+    } else {
+      sincos(x[1], &w[0], &w[1]);
+    }
+    step_w(p, t, b, x, u, w, xn);
+  }
+
   template <bool kSecond>
-  PTC_D static void derivs(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
-                           const R (&lam)[4], DynDerivs<R, 4, 1>& D) {
+  PTC_D static void derivs_w(const ProblemParams& p, int, int, const R (&x)[4], const R (&u)[1],
+                             const R (&w)[2], const R (&lam)[4], DynDerivs<R, 4, 1>& D) {
     const R dt = R(p.dyn[4]);
     Accel cart, pole;
     if constexpr (sizeof(R) == 4) {
@@ -340,7 +354,7 @@ struct CartPole {
       cart = {jc.g[0], jc.g[1], jc.g[2], jc.h[0][0], jc.h[0][1], jc.h[1][1], jc.h[0][2], jc.h[1][2]};
       pole = {jp.g[0], jp.g[1], jp.g[2], jp.h[0][0], jp.h[0][1], jp.h[1][1], jp.h[0][2], jp.h[1][2]};
     } else {
-      accels(p, x[1], x[3], u[0], cart, pole);
+      accels(p, w[0], w[1], x[3], u[0], cart, pole);
     }
     set_identity(D.fx);
     D.fx[0][2] = dt;
@@ -366,6 +380,14 @@ struct CartPole {
       D.Hxu[3][0] = l2 * cart.h12 + l3 * pole.h12;
     }
   }
+
+  template <bool kSecond>
+  PTC_D static void derivs(const ProblemParams& p, int t, int b, const R (&x)[4], const R (&u)[1],
+                           const R (&lam)[4], DynDerivs<R, 4, 1>& D) {
+    R w[2] = {R(0), R(0)};
+    if constexpr (sizeof(R) == 8) sincos(x[1], &w[0], &w[1]);
+    derivs_w<kSecond>(p, t, b, x, u, w, lam, D);
+  }
 };
 
 // a model's structural zeros (linalg.cuh masks); dense unless it says
@@ -377,6 +399,33 @@ template <class Dyn>
 struct JacMask<Dyn, std::void_t<decltype(Dyn::kFxMask)>> {
   static constexpr uint64_t fx = Dyn::kFxMask, fu = Dyn::kFuMask, hxx = Dyn::kHxxMask;
 };
+
+// per-stage auxiliary values a model caches next to a trajectory (kAux,
+// aux, step_w, derivs_w); none unless it says
+template <class Dyn, class = void>
+struct AuxOf {
+  static constexpr int n = 0;
+};
+template <class Dyn>
+struct AuxOf<Dyn, std::void_t<decltype(Dyn::kAux)>> {
+  static constexpr int n = Dyn::kAux;
+};
+template <class Dyn>
+constexpr int kAuxDim = AuxOf<Dyn>::n > 0 ? AuxOf<Dyn>::n : 1;
+
+// the model's derivatives from cached auxiliary values when use_w
+template <bool kSecond, class Dyn, typename R>
+PTC_D void dyn_derivs(const ProblemParams& p, int t, int b, const R (&x)[Dyn::NX],
+                      const R (&u)[Dyn::NU], const R (&w)[kAuxDim<Dyn>], bool use_w,
+                      const R (&lam)[Dyn::NX], DynDerivs<R, Dyn::NX, Dyn::NU>& D) {
+  if constexpr (AuxOf<Dyn>::n > 0) {
+    if (use_w) {
+      Dyn::template derivs_w<kSecond>(p, t, b, x, u, w, lam, D);
+      return;
+    }
+  }
+  Dyn::template derivs<kSecond>(p, t, b, x, u, lam, D);
+}
 
 // x' = A_t x + B_t u + c_t with per-stage / per-problem broadcasting
 template <typename R, int NX_, int NU_>

@@ -69,6 +69,13 @@ struct NewtonArgs {
   R* lam_in;               // (nx, 1, B) co-state entering at the block end
   R* x_in;                 // (nx, 1, B) state at the block start (rollout carry)
   const R* x0g;            // (nx, 1, B) the horizon's initial state (phase argument)
+  // per-stage auxiliary values of each trajectory buffer (models with kAux,
+  // single-sweep plans): buffer q at aux + q * auxsz, (kAux, T, B); aux_ok
+  // [B] bit q = buffer q's values belong to its current states (cleared by
+  // every host entry that writes the states)
+  R* aux;
+  size_t auxsz;
+  int* aux_ok;
 };
 
 template <typename R>
@@ -408,12 +415,13 @@ __global__ void __launch_bounds__(128) k_costate_down(NewtonArgs<R> a, int l) {
 template <typename R, class Dyn>
 PTC_D void stage_expansion(const NewtonArgs<R>& a, const ProblemParams& p, const AugArgs<R>& g,
                            int t, int b, const R (&x)[Dyn::NX], const R (&u)[Dyn::NU],
+                           const R (&w)[kAuxDim<Dyn>], bool use_w,
                            const R (&ln)[Dyn::NX], Stage<R, Dyn::NX, Dyn::NU>& st,
                            R (&lt)[Dyn::NX]) {
   constexpr int NX = Dyn::NX, NU = Dyn::NU;
   constexpr uint64_t FxM = JacMask<Dyn>::fx, FuM = JacMask<Dyn>::fu, HxxM = JacMask<Dyn>::hxx;
   DynDerivs<R, NX, NU> D;
-  Dyn::template derivs<true>(p, t, b, x, u, ln, D);
+  dyn_derivs<true, Dyn>(p, t, b, x, u, w, use_w, ln, D);
   if constexpr (kUserCost<Dyn> || kUserCon<Dyn>) {
     // a user cost and / or user constraints: l's and the augmentation's
     // derivatives as full matrices (passes.py:171-181 adds lxx + cxx +
@@ -597,7 +605,8 @@ __global__ void __launch_bounds__(128) k_costate_down0(NewtonArgs<R> a) {
       }
     } else {
       Stage<R, NX, NU> st;
-      stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
+      const R w0[kAuxDim<Dyn>] = {};
+      stage_expansion<R, Dyn>(a, p, g, t, b, x, u, w0, false, ln, st, lt);
       st_mat(a.P, t, T, B, b, st.P);
       st_mat(a.Rm, t, T, B, b, st.Rr);
       st_mat(a.M, t, T, B, b, st.M);
@@ -657,18 +666,33 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
   }
   symmetrize<NX>(c.Y);
   set_zero(c.eta);
+  // the trajectory's cached auxiliary values (sin / cos of the angle) when
+  // the forward sweep that built it left them, else evaluated and cached
+  constexpr int kA = AuxOf<Dyn>::n;
+  const bool aux_on = kA > 0 && a.aux != nullptr;
+  const bool have = aux_on && ((a.aux_ok[b] >> q) & 1);
+  R* auxq = aux_on ? a.aux + q * a.auxsz : nullptr;
+  R w[kAuxDim<Dyn>] = {};
   ld_x(a, q, T - 1, b, x);
   ld_u(a, q, T - 1, b, u);
+  if (have) ld_vec(auxq, T - 1, T, B, b, w);
   for (int t = T - 1; t >= 0; --t) {
     // software pipeline: stage t-1's state and control are in flight while
     // stage t is expanded and folded
-    R xn[NX], un[NU];
+    R xn[NX], un[NU], wn[kAuxDim<Dyn>];
     const int tp = t > 0 ? t - 1 : 0;
     ld_x(a, q, tp, b, xn);
     ld_u(a, q, tp, b, un);
+    if (have) ld_vec(auxq, tp, T, B, b, wn);
+    if constexpr (kA > 0) {
+      if (aux_on && !have) {
+        Dyn::aux(x, w);
+        st_vec(auxq, t, T, B, b, w);
+      }
+    }
     Stage<R, NX, NU> st;
     R lt[NX];
-    stage_expansion<R, Dyn>(a, p, g, t, b, x, u, ln, st, lt);
+    stage_expansion<R, Dyn>(a, p, g, t, b, x, u, w, aux_on, ln, st, lt);
 #pragma unroll
     for (int i = 0; i < NU; ++i) st.Rr[i][i] += alpha;
     R Gam[NU][NX], gam[NU];
@@ -685,7 +709,12 @@ __global__ void __launch_bounds__(128) k_value_fused(NewtonArgs<R> a, LqrArgs<R>
     }
 #pragma unroll
     for (int i = 0; i < NU; ++i) u[i] = un[i];
+    if (have) {
+#pragma unroll
+      for (int i = 0; i < kAuxDim<Dyn>; ++i) w[i] = wn[i];
+    }
   }
+  if (aux_on && !have) a.aux_ok[b] |= 1 << q;
   if (fl) atomicOr(a.flags + b, fl);
 }
 
@@ -862,24 +891,34 @@ __global__ void __launch_bounds__(128) k_forward_fused(NewtonArgs<R> a, LqrArgs<
   double s2 = 0.0, sd = 0.0, mx = 0.0, sl = 0.0, sc = 0.0;
   int bad = -1;
   bool finite = true;
-  R xs[NX], us[NU], Gam[NU][NX], gam[NU], dd[NU];
+  // cached auxiliary values: the current trajectory's (left by the value
+  // sweep) feed its Jacobians; the candidate's, evaluated for its steps,
+  // are cached next to it
+  constexpr int kA = AuxOf<Dyn>::n;
+  const bool aux_on = kA > 0 && a.aux != nullptr;
+  const bool have = aux_on && ((a.aux_ok[b] >> q) & 1);
+  const R* auxq = aux_on ? a.aux + q * a.auxsz : nullptr;
+  R* auxc = aux_on ? a.aux + c * a.auxsz : nullptr;
+  R xs[NX], us[NU], Gam[NU][NX], gam[NU], dd[NU], ws[kAuxDim<Dyn>] = {};
   ld_x(a, q, 0, b, xs);
   ld_u(a, q, 0, b, us);
   ld_mat(la.Gam, 0, T, B, b, Gam);
   ld_vec(la.gam, 0, T, B, b, gam);
   ld_vec(a.d, 0, T, B, b, dd);
+  if (have) ld_vec(auxq, 0, T, B, b, ws);
 #pragma unroll
   for (int i = 0; i < NX; ++i) xc[i] = xs[i];
   st_vec(Xc, 0, T + 1, B, b, xc);
   for (int t = 0; t < T; ++t) {
     // software pipeline: stage t+1's inputs load while stage t runs
-    R xs_n[NX], us_n[NU], Gam_n[NU][NX], gam_n[NU], dd_n[NU];
+    R xs_n[NX], us_n[NU], Gam_n[NU][NX], gam_n[NU], dd_n[NU], ws_n[kAuxDim<Dyn>];
     const int tn = t + 1 < T ? t + 1 : t;
     ld_x(a, q, tn, b, xs_n);
     ld_u(a, q, tn, b, us_n);
     ld_mat(la.Gam, tn, T, B, b, Gam_n);
     ld_vec(la.gam, tn, T, B, b, gam_n);
     ld_vec(a.d, tn, T, B, b, dd_n);
+    if (have) ld_vec(auxq, tn, T, B, b, ws_n);
     R du[NU], uc[NU];
     mv<NU, NX>(Gam, x, du);
 #pragma unroll
@@ -902,7 +941,18 @@ __global__ void __launch_bounds__(128) k_forward_fused(NewtonArgs<R> a, LqrArgs<
       if (br >= 0 && bad < 0) bad = t * gp.W + br;
     }
     R xcn[NX];
-    Dyn::step(p, t, b, xc, uc, xcn);
+    if constexpr (kA > 0) {
+      if (aux_on) {
+        R wc[kAuxDim<Dyn>];
+        Dyn::aux(xc, wc);
+        st_vec(auxc, t, T, B, b, wc);
+        Dyn::step_w(p, t, b, xc, uc, wc, xcn);
+      } else {
+        Dyn::step(p, t, b, xc, uc, xcn);
+      }
+    } else {
+      Dyn::step(p, t, b, xc, uc, xcn);
+    }
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
       finite = finite && isfinite(xcn[i]);
@@ -912,7 +962,7 @@ __global__ void __launch_bounds__(128) k_forward_fused(NewtonArgs<R> a, LqrArgs<
     // deviation chain: dx_{t+1} = (fx + fu Gamma) dx_t + fu gamma at the
     // current trajectory
     DynDerivs<R, NX, NU> D;
-    Dyn::template derivs<false>(p, t, b, xs, us, lam0, D);
+    dyn_derivs<false, Dyn>(p, t, b, xs, us, ws, have, lam0, D);
     constexpr uint64_t FxM = JacMask<Dyn>::fx, FuM = JacMask<Dyn>::fu;
     constexpr uint64_t FM = plus_rows_mask<NX, NX, NU>(FxM, FuM);
     R F[NX][NX], e[NX], y[NX];
@@ -940,7 +990,12 @@ __global__ void __launch_bounds__(128) k_forward_fused(NewtonArgs<R> a, LqrArgs<
 #pragma unroll
       for (int k = 0; k < NX; ++k) Gam[i][k] = Gam_n[i][k];
     }
+    if (have) {
+#pragma unroll
+      for (int i = 0; i < kAuxDim<Dyn>; ++i) ws[i] = ws_n[i];
+    }
   }
+  if (aux_on) a.aux_ok[b] |= 1 << c;
   la.red[(size_t)0 * B + b] = s2;
   la.red[(size_t)1 * B + b] = sd;
   la.red[(size_t)2 * B + b] = mx;
