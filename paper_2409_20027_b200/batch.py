@@ -101,7 +101,7 @@ class BatchSolver:
             cost=s.read("cur_cost"), launches=launches)
 
     @staticmethod
-    def solve_concurrently(jobs, group: int = 4) -> list:
+    def solve_concurrently(jobs, group: int = 16) -> list:
         """Advance several batches (e.g. the two models of config 3) at once,
         one CUDA stream each: ``jobs`` = [(BatchSolver, states, controls)].
         Every solver keeps its own device-resident loop; the host polls each
@@ -119,7 +119,10 @@ class BatchSolver:
         # one group stays queued while the host reads the previous group's
         # running count (pinned copy + event), so the streams never drain
         # waiting for the host; a finished batch runs at most one extra
-        # group of early-exit iterations
+        # group of early-exit iterations.  16 iterations per group: with 4,
+        # about one config-3 solve in five took ~1.35x as long (a host
+        # hiccup longer than the queued work drains both streams); 16 and
+        # 64 gave no outlier in 24 solves (profiles/r2v_bench.md)
         polls = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in jobs]
         events = [None] * len(jobs)
         active = set(range(len(jobs)))
