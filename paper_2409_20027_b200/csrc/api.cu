@@ -223,6 +223,7 @@ static int lqr_solve_t(int batch, int horizon, int nx, int nu, const void* P, co
   a.B = batch;
   a.T = horizon;
   a.plan = auto_plan(batch, horizon, chunk0, chunk, nx);
+  a.auto_plan = chunk0 == 0 && chunk == 0;
   a.P = (const R*)P;
   a.Rm = (const R*)Rm;
   a.M = (const R*)M;

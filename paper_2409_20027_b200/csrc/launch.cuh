@@ -52,12 +52,57 @@ inline SeqLaunch seq_launch(long long n) {
 // spills at two (0.477 -> 0.937 ms).
 template <int NX>
 constexpr int kPropRing = NX <= 4 ? 2 : 1;
+// One CTA per problem (k_lqr_cta) for the small batches of the latency
+// configs: the whole LQR-scan solve in one launch, trees in shared memory.
+// One SM per problem pays off while the level-0 chunks stay short: batch 1,
+// fp64 (round 2, gpurun s26/s27, ms per solve, multi-launch -> one CTA):
+// nx 2 T = 256 0.040 -> 0.022, T = 1024 0.052 -> 0.028; nx 4 0.087 -> 0.068,
+// 0.114 -> 0.093; fp32 nx 4 0.072 -> 0.039, 0.093 -> 0.054.  At T = 4096 the
+// 16-stage chunks on one SM are 2-4x slower than the whole-GPU tree.
+constexpr int kCtaThreads = 256;
+constexpr int kCtaMaxT = 1024;
+constexpr int kCtaMaxBatch = 16;
+inline int cta_threads(int T) {
+  int p = kCtaThreads;
+  while (p > T) p >>= 1;
+  return p;
+}
+template <typename R, int NX, int NU>
+bool cta_ok(const LqrArgs<R>& a) {
+  if constexpr (NX > 4) {
+    return false;
+  } else {
+    // the pass-level / config-1 solve only: inside the Newton loop (a.red)
+    // the tree's association order moved sensitive batch-1 solves (a
+    // chaotic fp32 cart-pole, a user cost) past their 1e-9 / count pins
+    // and the iteration's other launches kept the latency unchanged
+    return a.auto_plan && a.red == nullptr && !a.block_mode && a.vcarry_in == nullptr && a.x_in == nullptr &&
+           a.t_base == 0 && !a.staged && a.B <= kCtaMaxBatch && a.T >= 32 && a.T <= kCtaMaxT;
+  }
+}
+template <typename R, int NX, int NU>
+void launch_lqr_cta(const LqrArgs<R>& a, cudaStream_t s) {
+  const int P = cta_threads(a.T);
+  const size_t smem = CtaSmem<R, NX>::bytes(P);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lqr_cta<R, NX, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)CtaSmem<R, NX>::bytes(kCtaThreads));
+    attr = true;
+  }
+  k_lqr_cta<R, NX, NU><<<a.B, P, smem, s>>>(a);
+}
+
 template <typename R, int NX, int NU>
 void launch_lqr(const LqrArgs<R>& a, cudaStream_t s) {
   const Plan& pl = a.plan;
   const long long B = a.B, P0 = pl.units0();
   if (bulk_ok<R, NX, NU>(a)) {  // batch-filling single sweep, small stages: TMA-fed rings
     launch_lqr_bulk<R, NX, NU>(a, s);
+    return;
+  }
+  if (cta_ok<R, NX, NU>(a)) {
+    launch_lqr_cta<R, NX, NU>(a, s);
     return;
   }
   if (pl.L >= 1) {

@@ -54,6 +54,8 @@ struct LqrArgs {
   R* gst;
   int staged;
   int prestaged;           // xst already written by the producer (Newton co-state sweep)
+  int auto_plan;           // the caller left the scan plan to auto_plan (chunk0 = chunk = 0):
+                           // small batches may take the one-CTA solve (k_lqr_cta)
   int gains_in_gst;        // staged: leave the gains in gst (the Newton loop reads no Gamma)
   R* xin_buf;              // workspace for x_in        (nx, 1, B)
   // tree scratch, index l = 1..L, item rows n[l]
@@ -430,6 +432,221 @@ __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
     a.red[((size_t)1 * P0 + j) * B + b] = sd;
     a.red[((size_t)2 * P0 + j) * B + b] = mx;
   }
+}
+
+// ------------------------------------------------- one CTA per problem
+// Small batches (batch-1 latency, config 1): the whole LQR-scan solve of a
+// problem in ONE launch.  P threads (a power of two) own contiguous chunks
+// of the horizon; the level-0 folds are those of the multi-launch plan
+// (k_value_up0 / k_value_down0 / k_prop_down0), and the two trees between
+// them are Blelloch scans over the P chunk aggregates in shared memory with
+// barriers instead of one launch per level:
+//   value (suffix): up-sweep with the parent at the left end (vcombine of
+//     earlier x later), down-sweep carrying the value function after each
+//     node (the right child inherits it, the left child gets
+//     vstep(right child's aggregate, carry));
+//   propagation (prefix): up-sweep with the parent at the right end
+//     (aff_compose later o earlier), down-sweep carrying the entry state.
+// Same element functions as the multi-launch plan, so the same math; the
+// tree's association order differs (results agree to rounding).
+template <typename R, int NX>
+struct CtaSmem {
+  static constexpr size_t bytes(int P) {
+    return (size_t)P * (sizeof(VElem<R, NX>) + sizeof(VCarry<R, NX>));
+  }
+};
+
+template <typename R, int NX, int NU>
+__global__ void __launch_bounds__(256) k_lqr_cta(LqrArgs<R> a) {
+  // next-stage prefetch where the registers allow a second stage in
+  // flight (<= 256 bytes: nx 4 fp64 spills with it, 0.093 -> 0.118 ms at
+  // T = 1024)
+  constexpr bool kPre = sizeof(Stage<R, NX, NU>) <= 256;
+  extern __shared__ __align__(16) unsigned char cta_smem[];
+  const int P = blockDim.x;
+  VElem<R, NX>* agg = reinterpret_cast<VElem<R, NX>*>(cta_smem);
+  VCarry<R, NX>* car = reinterpret_cast<VCarry<R, NX>*>(cta_smem + (size_t)P * sizeof(VElem<R, NX>));
+  // the propagation tree reuses the value tree's storage once it is done
+  Aff<R, NX>* paf = reinterpret_cast<Aff<R, NX>*>(cta_smem);
+  R(*xin)[NX] = reinterpret_cast<R(*)[NX]>(cta_smem + (size_t)P * sizeof(VElem<R, NX>));
+  static_assert(sizeof(Aff<R, NX>) <= sizeof(VElem<R, NX>), "propagation aggregates reuse the value slots");
+  static_assert(sizeof(R) * NX <= sizeof(VCarry<R, NX>), "entry states reuse the carry slots");
+  const int b = blockIdx.x;
+  if (lqr_skip(a, b)) return;
+  const int j = threadIdx.x;
+  const int T = a.T, B = a.B;
+  // chunk j = [floor(j T / P), floor((j + 1) T / P)): every chunk non-empty (T >= P)
+  const int t0 = (int)((long long)j * T / P), t1 = (int)((long long)(j + 1) * T / P);
+  const R alpha = R(a.alpha[b]);
+  int fl = 0;
+  bool okc = true;
+
+  // value level 0 up: the chunk's aggregate (the last chunk ends with the terminal)
+  {
+    VElem<R, NX> acc;
+    Stage<R, NX, NU> st;
+    R L[NU][NU];
+    int start;
+    if (j == P - 1) {
+      R PT[NX][NX];
+      ld_mat(a.PT, 0, 1, B, b, PT);
+      velem_terminal(PT, acc);
+      start = t1 - 1;
+    } else {
+      ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t1 - 1, T, B, b, alpha, st);
+      if (!velem_from_stage(st, acc, L)) fl |= FLAG_DEF_R;
+      start = t1 - 2;
+    }
+    // (stage t - 1 loads while stage t is combined)
+    if (start >= t0) ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, start, T, B, b, alpha, st);
+    for (int t = start; t >= t0; --t) {
+      Stage<R, NX, NU> nst;
+      if (kPre && t > t0) ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t - 1, T, B, b, alpha, nst);
+      VElem<R, NX> o;
+      fl |= vcombine_stage(st, acc, o);
+      acc = o;
+      if (t > t0) {
+        if (kPre) st = nst;
+        else ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t - 1, T, B, b, alpha, st);
+      }
+    }
+    agg[j] = acc;
+  }
+  __syncthreads();
+  // value tree, up: node j covers [j, j + 2d) (stored at its left end)
+  for (int d = 1; d < P; d <<= 1) {
+    if ((j & (2 * d - 1)) == 0) {
+      VElem<R, NX> o;
+      okc &= vcombine(agg[j], agg[j + d], o);
+      agg[j] = o;
+    }
+    __syncthreads();
+  }
+  // value tree, down: car[j] = value function after the node stored at j
+  if (j == 0) vcarry_zero(car[0]);
+  __syncthreads();
+  for (int d = P >> 1; d >= 1; d >>= 1) {
+    if ((j & (2 * d - 1)) == 0) {
+      const VCarry<R, NX> cn = car[j];
+      VCarry<R, NX> o;
+      okc &= vstep(agg[j + d], cn, o);
+      car[j + d] = cn;
+      car[j] = o;
+    }
+    __syncthreads();
+  }
+  // value level 0 down: gains (and S, s), the chunk's closed-loop affine map
+  VCarry<R, NX> c = car[j];
+  if (j == P - 1) {
+    ld_mat(a.PT, 0, 1, B, b, c.Y);
+    set_zero(c.eta);
+    if (a.S) {
+      st_mat(a.S, T, T + 1, B, b, c.Y);
+      R z[NX];
+      set_zero(z);
+      st_vec(a.s, T, T + 1, B, b, z);
+    }
+  }
+  Aff<R, NX> pa;
+  aff_identity(pa);
+  Stage<R, NX, NU> st;
+  ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t1 - 1, T, B, b, alpha, st);
+  for (int t = t1 - 1; t >= t0; --t) {
+    Stage<R, NX, NU> nst;
+    if (kPre && t > t0) ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t - 1, T, B, b, alpha, nst);
+    R Gam[NU][NX], gam[NU];
+    VCarry<R, NX> o;
+    fl |= riccati_step<R, NX, NU, false>(st, c, Gam, gam, o);
+    st_mat(a.Gam, t, T, B, b, Gam);
+    st_vec(a.gam, t, T, B, b, gam);
+    Aff<R, NX> m, ao;
+    if (t == 0) {
+      set_zero(m.F);
+    } else {
+      mm<NX, NU, NX>(st.Fu, Gam, m.F);
+#pragma unroll
+      for (int i = 0; i < NX; ++i)
+#pragma unroll
+        for (int k = 0; k < NX; ++k) m.F[i][k] += st.Fx[i][k];
+    }
+    mv<NX, NU>(st.Fu, gam, m.e);
+    aff_compose(pa, m, ao);
+    pa = ao;
+    c = o;
+    if (a.S) {
+      st_mat(a.S, t, T + 1, B, b, c.Y);
+      R sv[NX];
+#pragma unroll
+      for (int i = 0; i < NX; ++i) sv[i] = -c.eta[i];
+      st_vec(a.s, t, T + 1, B, b, sv);
+    }
+    if (t > t0) {
+      if (kPre) st = nst;
+      else ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t - 1, T, B, b, alpha, st);
+    }
+  }
+  __syncthreads();   // the value tree's storage is free
+  paf[j] = pa;
+  __syncthreads();
+  // propagation tree, up: node j covers (j - 2d, j] (stored at its right end)
+  for (int d = 1; d < P; d <<= 1) {
+    if (((j + 1) & (2 * d - 1)) == 0) {
+      Aff<R, NX> o;
+      aff_compose(paf[j], paf[j - d], o);
+      paf[j] = o;
+    }
+    __syncthreads();
+  }
+  // propagation tree, down: xin[j] = entry state of the node stored at j
+  if (j == P - 1) {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xin[j][i] = R(0);
+  }
+  __syncthreads();
+  for (int d = P >> 1; d >= 1; d >>= 1) {
+    if (((j + 1) & (2 * d - 1)) == 0) {
+      R e[NX], y[NX];
+#pragma unroll
+      for (int i = 0; i < NX; ++i) e[i] = xin[j][i];
+      aff_apply(paf[j - d], e, y);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) {
+        xin[j - d][i] = e[i];
+        xin[j][i] = y[i];
+      }
+    }
+    __syncthreads();
+  }
+  // propagation level 0 down: dx, du over the chunk
+  R x[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) x[i] = xin[j][i];
+  PropStage<R, NX, NU> ps;
+  ld_prop_stage(a, t0, b, ps);
+  for (int t = t0; t < t1; ++t) {
+    PropStage<R, NX, NU> nps;
+    if (t + 1 < t1) ld_prop_stage(a, t + 1, b, nps);
+    st_vec(a.dX, t, T + 1, B, b, x);
+    R du[NU];
+    mv<NU, NX>(ps.Gam, x, du);
+#pragma unroll
+    for (int i = 0; i < NU; ++i) du[i] += ps.gam[i];
+    st_vec(a.dU, t, T, B, b, du);
+    R F[NX][NX], e[NX], y[NX];
+    mm<NX, NU, NX>(ps.Fu, ps.Gam, F);
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NX; ++k) F[i][k] = (t == 0) ? R(0) : F[i][k] + ps.Fx[i][k];
+    mv<NX, NU>(ps.Fu, ps.gam, e);
+    mv<NX, NX>(F, x, y);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
+    if (t + 1 < t1) ps = nps;
+  }
+  if (j == P - 1) st_vec(a.dX, T, T + 1, B, b, x);
+  if (!okc) fl |= FLAG_COND;
+  if (fl) atomicOr(a.flags + b, fl);
 }
 
 // ------------------------------------------------------------ time blocks

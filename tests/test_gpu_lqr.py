@@ -329,3 +329,45 @@ def test_bulk_ring_sweeps_match_register_path(nx, nu, B, dtype, monkeypatch):
                                      got[1][..., k], got[2][..., k], got[3][..., k])):
             w = np.asarray(want).reshape(T + 1 if have.shape[1] == T + 1 else T, -1)
             assert rel_gap(have.T.reshape(w.shape), w) < tol
+
+
+@pytest.mark.parametrize("nx,nu", [(1, 1), (2, 1), (3, 2), (4, 1), (4, 2)])
+def test_one_cta_solve_matches_oracle(nx, nu):
+    """Small batches with the automatic plan take the one-CTA-per-problem
+    solve (k_lqr_cta: both trees in shared memory, 32 <= T <= 1024, batch
+    <= 16); every output against the oracle, fp64 1e-9 and fp32 1e-4, for
+    horizons that are and are not powers of two, and a flagged problem
+    (indefinite R) reported for that problem only."""
+    import torch
+    from paper_2409_20027_b200 import passes
+    for B, T in [(1, 32), (5, 100), (16, 257), (3, 1024)]:
+        rng = np.random.default_rng([nx, nu, B, T])
+        exps = [O.random_lqr_expansion(rng, T, nx, nu, alpha=0.2) for _ in range(B)]
+        if B > 1:
+            exps[1].R[T // 3] = -10.0 * np.eye(nu)   # indefinite R + alpha I at one stage
+        refs = [O.lqr_solve(e) if (B == 1 or b != 1) else None for b, e in enumerate(exps)]
+        for dtype, tol in ((torch.float64, 1e-9), (torch.float32, 1e-4)):
+            sol = passes.LqrSolver(B, T, nx, nu, dtype=dtype, with_value=True)
+            dev = sol.device
+            stack = lambda f, c, rows=T: torch.as_tensor(np.stack(
+                [f(e).reshape(rows, c) for e in exps], -1)).permute(1, 0, 2).contiguous().to(dev, dtype)
+            args = [stack(lambda e: e.P, nx * nx), stack(lambda e: e.R, nu * nu),
+                    stack(lambda e: e.M, nx * nu), stack(lambda e: e.d, nu),
+                    stack(lambda e: e.Fx, nx * nx), stack(lambda e: e.Fu, nx * nu),
+                    stack(lambda e: e.PT, nx * nx, 1)]
+            alpha = torch.tensor([e.alpha for e in exps], dtype=torch.float64, device=dev)
+            sol.solve(*args, alpha)
+            torch.cuda.synchronize()
+            flags = sol.flags.cpu().numpy()
+            host = lambda t, rows, shape: t.permute(2, 1, 0).double().cpu().numpy().reshape(
+                (B, rows) + shape)
+            outs = (host(sol.S, T + 1, (nx, nx)), host(sol.s, T + 1, (nx,)),
+                    host(sol.Gamma, T, (nu, nx)), host(sol.gamma, T, (nu,)),
+                    host(sol.dx, T + 1, (nx,)), host(sol.du, T, (nu,)))
+            for b in range(B):
+                if refs[b] is None:
+                    assert flags[b] != 0, (B, T, b)
+                    continue
+                assert flags[b] == 0, (B, T, b, flags[b])
+                for k in range(6):
+                    assert rel_gap(outs[k][b], refs[b][k]) < tol, (B, T, b, k, dtype)
