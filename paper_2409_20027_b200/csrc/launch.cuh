@@ -2,6 +2,7 @@
 // registry that maps (dtype, model, nx, nu) to instantiated sequences.
 #pragma once
 
+#include <algorithm>
 #include <map>
 #include <tuple>
 
@@ -54,17 +55,21 @@ template <int NX>
 constexpr int kPropRing = NX <= 4 ? 2 : 1;
 // One CTA per problem (k_lqr_cta) for the small batches of the latency
 // configs: the whole LQR-scan solve in one launch, trees in shared memory.
-// One SM per problem pays off while the level-0 chunks stay short: batch 1,
+// One CTA per problem pays off while the level-0 chunks stay short: batch 1,
 // fp64 (round 2, gpurun s26/s27, ms per solve, multi-launch -> one CTA):
 // nx 2 T = 256 0.040 -> 0.022, T = 1024 0.052 -> 0.028; nx 4 0.087 -> 0.068,
-// 0.114 -> 0.093; fp32 nx 4 0.072 -> 0.039, 0.093 -> 0.054.  At T = 4096 the
-// 16-stage chunks on one SM are 2-4x slower than the whole-GPU tree.
+// 0.114 -> 0.093; fp32 nx 4 0.072 -> 0.039, 0.093 -> 0.054.  Longer horizons
+// run on a thread-block cluster of up to 16 CTAs (16 SMs, trees crossing
+// CTAs through DSMEM) so the chunks stay short (gpurun s31): nx 2 T = 4096
+// 0.062 -> 0.037, T = 16384 0.074 -> 0.045; nx 4 0.143 -> 0.100, 0.178 ->
+// 0.140; at T = 65536 (16-stage chunks) the whole-GPU tree wins (0.086 vs
+// 0.143 ms), hence kCtaMaxT.
 constexpr int kCtaThreads = 256;
-constexpr int kCtaMaxT = 1024;
 constexpr int kCtaMaxBatch = 16;
-inline int cta_threads(int T) {
-  int p = kCtaThreads;
-  while (p > T) p >>= 1;
+constexpr int kCtaMaxT = 16384;
+inline int pow2_floor(int v) {
+  int p = 1;
+  while (2 * p <= v) p <<= 1;
   return p;
 }
 template <typename R, int NX, int NU>
@@ -76,21 +81,73 @@ bool cta_ok(const LqrArgs<R>& a) {
     // the tree's association order moved sensitive batch-1 solves (a
     // chaotic fp32 cart-pole, a user cost) past their 1e-9 / count pins
     // and the iteration's other launches kept the latency unchanged
-    return a.auto_plan && a.red == nullptr && !a.block_mode && a.vcarry_in == nullptr && a.x_in == nullptr &&
-           a.t_base == 0 && !a.staged && a.B <= kCtaMaxBatch && a.T >= 32 && a.T <= kCtaMaxT;
+    return a.auto_plan && a.red == nullptr && !a.block_mode && a.vcarry_in == nullptr &&
+           a.x_in == nullptr && a.t_base == 0 && !a.staged && a.B <= kCtaMaxBatch && a.T >= 32 &&
+           a.T <= kCtaMaxT;
   }
+}
+// largest cluster (16 non-portable, 8, 4, 2) the device can co-schedule with
+// this kernel's shared memory
+template <typename R, int NX, int NU>
+int cta_max_cluster() {
+  static int best = -1;
+  if (best >= 0) return best;
+  auto k = k_lqr_cta<R, NX, NU, true>;
+  const size_t smem = CtaSmem<R, NX>::bytes(kCtaThreads);
+  cudaFuncSetAttribute(k_lqr_cta<R, NX, NU, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  best = 1;
+  for (int c : {16, 8, 4, 2}) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(c);
+    cfg.blockDim = dim3(kCtaThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) == cudaSuccess && n >= 1) {
+      best = c;
+      break;
+    }
+  }
+  cudaGetLastError();
+  return best;
 }
 template <typename R, int NX, int NU>
 void launch_lqr_cta(const LqrArgs<R>& a, cudaStream_t s) {
-  const int P = cta_threads(a.T);
-  const size_t smem = CtaSmem<R, NX>::bytes(P);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_lqr_cta<R, NX, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)CtaSmem<R, NX>::bytes(kCtaThreads));
-    attr = true;
+  const int maxc = cta_max_cluster<R, NX, NU>();
+  int P, nC;
+  if (a.T <= kCtaThreads * 4) {
+    P = pow2_floor(std::min(a.T, kCtaThreads));
+    nC = 1;
+  } else {
+    P = kCtaThreads;
+    nC = std::min(maxc, pow2_floor(a.T / kCtaThreads));
   }
-  k_lqr_cta<R, NX, NU><<<a.B, P, smem, s>>>(a);
+  if (nC == 1) {   // a plain launch: the implicit one-CTA cluster
+    k_lqr_cta<R, NX, NU, false><<<a.B, P, CtaSmem<R, NX>::bytes(P), s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = nC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(a.B * nC);
+  cfg.blockDim = dim3(P);
+  cfg.dynamicSmemBytes = CtaSmem<R, NX>::bytes(P);
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_lqr_cta<R, NX, NU, true>, a);
 }
 
 template <typename R, int NX, int NU>

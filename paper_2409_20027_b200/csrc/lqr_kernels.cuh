@@ -16,6 +16,8 @@
 // alone fills the GPU.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "elements.cuh"
 
 namespace ptc {
@@ -434,13 +436,16 @@ __global__ void __launch_bounds__(128) k_prop_down0(LqrArgs<R> a) {
   }
 }
 
-// ------------------------------------------------- one CTA per problem
+// ------------------------------------- one CTA (or cluster) per problem
 // Small batches (batch-1 latency, config 1): the whole LQR-scan solve of a
-// problem in ONE launch.  P threads (a power of two) own contiguous chunks
-// of the horizon; the level-0 folds are those of the multi-launch plan
-// (k_value_up0 / k_value_down0 / k_prop_down0), and the two trees between
-// them are Blelloch scans over the P chunk aggregates in shared memory with
-// barriers instead of one launch per level:
+// problem in ONE launch.  One CTA, or a thread-block cluster of nC CTAs on
+// nC SMs for longer horizons, per problem: its N = nC * P threads (powers
+// of two) own contiguous chunks of the horizon; the level-0 folds are those
+// of the multi-launch plan (k_value_up0 / k_value_down0 / k_prop_down0), and
+// the two trees between them are Blelloch scans over the N chunk aggregates
+// in shared memory -- levels that cross CTAs read and write the partner
+// CTA's slots through distributed shared memory (DSMEM) -- with CTA or
+// cluster barriers instead of one launch per level:
 //   value (suffix): up-sweep with the parent at the left end (vcombine of
 //     earlier x later), down-sweep carrying the value function after each
 //     node (the right child inherits it, the left child gets
@@ -456,8 +461,13 @@ struct CtaSmem {
   }
 };
 
-template <typename R, int NX, int NU>
+template <typename R, int NX, int NU, bool kCl>
 __global__ void __launch_bounds__(256) k_lqr_cta(LqrArgs<R> a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  // kCl: launched as a cluster (the single-CTA instantiation carries no
+  // cluster barriers or DSMEM paths: 15-20% of a T = 256 solve)
+  const int nC = kCl ? (int)cl.num_blocks() : 1, rank = kCl ? (int)cl.block_rank() : 0;
   // next-stage prefetch where the registers allow a second stage in
   // flight (<= 256 bytes: nx 4 fp64 spills with it, 0.093 -> 0.118 ms at
   // T = 1024)
@@ -471,12 +481,17 @@ __global__ void __launch_bounds__(256) k_lqr_cta(LqrArgs<R> a) {
   R(*xin)[NX] = reinterpret_cast<R(*)[NX]>(cta_smem + (size_t)P * sizeof(VElem<R, NX>));
   static_assert(sizeof(Aff<R, NX>) <= sizeof(VElem<R, NX>), "propagation aggregates reuse the value slots");
   static_assert(sizeof(R) * NX <= sizeof(VCarry<R, NX>), "entry states reuse the carry slots");
-  const int b = blockIdx.x;
-  if (lqr_skip(a, b)) return;
-  const int j = threadIdx.x;
+  const int b = blockIdx.x / nC;
+  if (lqr_skip(a, b)) return;   // (the whole cluster: same problem)
+  const int j = threadIdx.x, N = nC * P, g = rank * P + j;
   const int T = a.T, B = a.B;
-  // chunk j = [floor(j T / P), floor((j + 1) T / P)): every chunk non-empty (T >= P)
-  const int t0 = (int)((long long)j * T / P), t1 = (int)((long long)(j + 1) * T / P);
+  // chunk g = [floor(g T / N), floor((g + 1) T / N)): every chunk non-empty (T >= N)
+  const int t0 = (int)((long long)g * T / N), t1 = (int)((long long)(g + 1) * T / N);
+  // barrier after a tree level whose partners sit `dist` leaves apart
+  auto level_sync = [&](int dist) {
+    if (kCl && dist >= P) cl.sync();
+    else __syncthreads();
+  };
   const R alpha = R(a.alpha[b]);
   int fl = 0;
   bool okc = true;
@@ -487,7 +502,7 @@ __global__ void __launch_bounds__(256) k_lqr_cta(LqrArgs<R> a) {
     Stage<R, NX, NU> st;
     R L[NU][NU];
     int start;
-    if (j == P - 1) {
+    if (g == N - 1) {
       R PT[NX][NX];
       ld_mat(a.PT, 0, 1, B, b, PT);
       velem_terminal(PT, acc);
@@ -513,31 +528,35 @@ __global__ void __launch_bounds__(256) k_lqr_cta(LqrArgs<R> a) {
     agg[j] = acc;
   }
   __syncthreads();
-  // value tree, up: node j covers [j, j + 2d) (stored at its left end)
-  for (int d = 1; d < P; d <<= 1) {
-    if ((j & (2 * d - 1)) == 0) {
+  // value tree, up: node g covers [g, g + 2d) (stored at its left end); a
+  // partner d >= P leaves away is slot 0 of CTA rank + d / P
+  for (int d = 1; d < N; d <<= 1) {
+    if ((g & (2 * d - 1)) == 0) {
+      const VElem<R, NX>* rp = (!kCl || d < P) ? &agg[j + d] : cl.map_shared_rank(agg, rank + d / P);
       VElem<R, NX> o;
-      okc &= vcombine(agg[j], agg[j + d], o);
+      okc &= vcombine(agg[j], *rp, o);
       agg[j] = o;
     }
-    __syncthreads();
+    level_sync(2 * d);
   }
-  // value tree, down: car[j] = value function after the node stored at j
-  if (j == 0) vcarry_zero(car[0]);
+  // value tree, down: car[g] = value function after the node stored at g
+  if (g == 0) vcarry_zero(car[0]);
   __syncthreads();
-  for (int d = P >> 1; d >= 1; d >>= 1) {
-    if ((j & (2 * d - 1)) == 0) {
+  for (int d = N >> 1; d >= 1; d >>= 1) {
+    if ((g & (2 * d - 1)) == 0) {
       const VCarry<R, NX> cn = car[j];
+      VCarry<R, NX>* rc = (!kCl || d < P) ? &car[j + d] : cl.map_shared_rank(car, rank + d / P);
+      const VElem<R, NX>* ra = (!kCl || d < P) ? &agg[j + d] : cl.map_shared_rank(agg, rank + d / P);
       VCarry<R, NX> o;
-      okc &= vstep(agg[j + d], cn, o);
-      car[j + d] = cn;
+      okc &= vstep(*ra, cn, o);
+      *rc = cn;
       car[j] = o;
     }
-    __syncthreads();
+    level_sync(d);
   }
   // value level 0 down: gains (and S, s), the chunk's closed-loop affine map
   VCarry<R, NX> c = car[j];
-  if (j == P - 1) {
+  if (g == N - 1) {
     ld_mat(a.PT, 0, 1, B, b, c.Y);
     set_zero(c.eta);
     if (a.S) {
@@ -585,37 +604,43 @@ __global__ void __launch_bounds__(256) k_lqr_cta(LqrArgs<R> a) {
       else ld_stage(a.P, a.Rm, a.M, a.d, a.Fx, a.Fu, t - 1, T, B, b, alpha, st);
     }
   }
-  __syncthreads();   // the value tree's storage is free
+  // the value tree's storage is free: remote slots were last touched before
+  // a cluster barrier every thread has passed
+  __syncthreads();
   paf[j] = pa;
   __syncthreads();
-  // propagation tree, up: node j covers (j - 2d, j] (stored at its right end)
-  for (int d = 1; d < P; d <<= 1) {
-    if (((j + 1) & (2 * d - 1)) == 0) {
+  // propagation tree, up: node g covers (g - 2d, g] (stored at its right
+  // end); a partner d >= P leaves back is slot P - 1 of CTA rank - d / P
+  for (int d = 1; d < N; d <<= 1) {
+    if (((g + 1) & (2 * d - 1)) == 0) {
+      const Aff<R, NX>* rp = (!kCl || d < P) ? &paf[j - d] : cl.map_shared_rank(paf, rank - d / P) + (P - 1);
       Aff<R, NX> o;
-      aff_compose(paf[j], paf[j - d], o);
+      aff_compose(paf[j], *rp, o);
       paf[j] = o;
     }
-    __syncthreads();
+    level_sync(2 * d);
   }
-  // propagation tree, down: xin[j] = entry state of the node stored at j
-  if (j == P - 1) {
+  // propagation tree, down: xin[g] = entry state of the node stored at g
+  if (g == N - 1) {
 #pragma unroll
     for (int i = 0; i < NX; ++i) xin[j][i] = R(0);
   }
   __syncthreads();
-  for (int d = P >> 1; d >= 1; d >>= 1) {
-    if (((j + 1) & (2 * d - 1)) == 0) {
+  for (int d = N >> 1; d >= 1; d >>= 1) {
+    if (((g + 1) & (2 * d - 1)) == 0) {
+      const Aff<R, NX>* rp = (!kCl || d < P) ? &paf[j - d] : cl.map_shared_rank(paf, rank - d / P) + (P - 1);
+      R(*rx)[NX] = (!kCl || d < P) ? &xin[j - d] : cl.map_shared_rank(xin, rank - d / P) + (P - 1);
       R e[NX], y[NX];
 #pragma unroll
       for (int i = 0; i < NX; ++i) e[i] = xin[j][i];
-      aff_apply(paf[j - d], e, y);
+      aff_apply(*rp, e, y);
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
-        xin[j - d][i] = e[i];
+        (*rx)[i] = e[i];
         xin[j][i] = y[i];
       }
     }
-    __syncthreads();
+    level_sync(d);
   }
   // propagation level 0 down: dx, du over the chunk
   R x[NX];
@@ -644,7 +669,7 @@ __global__ void __launch_bounds__(256) k_lqr_cta(LqrArgs<R> a) {
     for (int i = 0; i < NX; ++i) x[i] = y[i] + e[i];
     if (t + 1 < t1) ps = nps;
   }
-  if (j == P - 1) st_vec(a.dX, T, T + 1, B, b, x);
+  if (g == N - 1) st_vec(a.dX, T, T + 1, B, b, x);
   if (!okc) fl |= FLAG_COND;
   if (fl) atomicOr(a.flags + b, fl);
 }

@@ -158,9 +158,11 @@ class LqrSolver:
 class HostLqrSolver:
     """The same batched LQR-scan solve on HOST tensors (``ptc_lqr_solve_host``):
     inputs and outputs are CPU tensors in the LqrSolver layouts (pin them
-    for asynchronous copies); the host->device copies (only the parts the
-    kernels read), the solve and the device->host copies are enqueued on
-    ``stream``, so calls on several streams overlap PCIe with compute.
+    for asynchronous copies, and keep them referenced until ``stream`` is
+    synchronised: torch's pinned-memory cache does not see these copies);
+    the host->device copies (only the parts the kernels read), the solve
+    and the device->host copies are enqueued on ``stream``, so calls on
+    several streams overlap PCIe with compute.
 
     ``stacked=True`` takes the reference's per-problem arrays stacked over
     the batch instead (``ptc_lqr_solve_host_stacked``): P (B, T, nx, nx),

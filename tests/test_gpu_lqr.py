@@ -216,12 +216,18 @@ def test_lqr_host_stacked_equals_soa_solve(nx, nu, T, B, dtype):
     s = torch.cuda.Stream()
     ref = passes.HostLqrSolver(B, T, nx, nu, dtype=td)
     want = ref.outputs()
-    ref.solve(*[t.pin_memory() for t in soa], alpha, want, stream=s)
+    # (the pinned inputs stay referenced until the stream is synchronised:
+    # torch's host allocator does not see the C ABI's async copies, so a
+    # dropped buffer could be handed out again before its copy has run)
+    ins_soa = [t.pin_memory() for t in soa]
+    ref.solve(*ins_soa, alpha, want, stream=s)
     hs = passes.HostLqrSolver(B, T, nx, nu, dtype=td, stacked=True)
     got = hs.outputs()
     flags = torch.zeros(B, dtype=torch.int32).pin_memory()
-    hs.solve(*[t.contiguous().pin_memory() for t in stacked], alpha, got, flags=flags, stream=s)
+    ins_st = [t.contiguous().pin_memory() for t in stacked]
+    hs.solve(*ins_st, alpha, got, flags=flags, stream=s)
     s.synchronize()
+    del ins_soa, ins_st
     assert int(flags.max()) == 0
     assert got[0].shape == (B, T, nu, nx) and got[2].shape == (B, T + 1, nx)
     for g, w in zip(got, want):
@@ -335,12 +341,17 @@ def test_bulk_ring_sweeps_match_register_path(nx, nu, B, dtype, monkeypatch):
 def test_one_cta_solve_matches_oracle(nx, nu):
     """Small batches with the automatic plan take the one-CTA-per-problem
     solve (k_lqr_cta: both trees in shared memory, 32 <= T <= 1024, batch
-    <= 16); every output against the oracle, fp64 1e-9 and fp32 1e-4, for
-    horizons that are and are not powers of two, and a flagged problem
-    (indefinite R) reported for that problem only."""
+    <= 16) or, for 1024 < T <= 16384, the same on a thread-block cluster
+    (tree levels across CTAs through DSMEM); every output against the
+    oracle, fp64 1e-9 and fp32 1e-4, for horizons that are and are not
+    powers of two, and a flagged problem (indefinite R) reported for that
+    problem only."""
     import torch
     from paper_2409_20027_b200 import passes
-    for B, T in [(1, 32), (5, 100), (16, 257), (3, 1024)]:
+    cases = [(1, 32), (5, 100), (16, 257), (3, 1024), (2, 2500), (1, 4096)]
+    if nx <= 2:
+        cases.append((1, 16384))
+    for B, T in cases:
         rng = np.random.default_rng([nx, nu, B, T])
         exps = [O.random_lqr_expansion(rng, T, nx, nu, alpha=0.2) for _ in range(B)]
         if B > 1:
