@@ -638,12 +638,36 @@ PTC_D R aug_value(const ProblemParams& p, const AugArgs<R>& a, int t, int T, int
 #pragma unroll
     for (int i = 0; i < NX; ++i)
       if (lo >> i & 1u) row(R(p.box_lb[i]) - x[i], sg);
+    // control rows: a control boxed on both sides evaluates its two logs in
+    // one block (independent chains), summed afterwards in row order
+    R lu[NU], ll[NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      const bool hu = up >> (kMaxNX + i) & 1u, hl = lo >> (kMaxNX + i) & 1u;
+      const R wu = u[i] - R(p.box_ub[kMaxNX + i]), wl = R(p.box_lb[kMaxNX + i]) - u[i];
+      if (hu && hl) {
+        lu[i] = log(-wu);
+        ll[i] = log(-wl);
+      } else if (hu) {
+        lu[i] = log(-wu);
+      } else if (hl) {
+        ll[i] = log(-wl);
+      }
+    }
 #pragma unroll
     for (int i = 0; i < NU; ++i)
-      if (up >> (kMaxNX + i) & 1u) row(u[i] - R(p.box_ub[kMaxNX + i]), sh);
+      if (up >> (kMaxNX + i) & 1u) {
+        if (u[i] - R(p.box_ub[kMaxNX + i]) >= R(0) && bad_row < 0) bad_row = k;
+        sh += lu[i];
+        ++k;
+      }
 #pragma unroll
     for (int i = 0; i < NU; ++i)
-      if (lo >> (kMaxNX + i) & 1u) row(R(p.box_lb[kMaxNX + i]) - u[i], sh);
+      if (lo >> (kMaxNX + i) & 1u) {
+        if (R(p.box_lb[kMaxNX + i]) - u[i] >= R(0) && bad_row < 0) bad_row = k;
+        sh += ll[i];
+        ++k;
+      }
     return -R(a.mu[b]) * (sg + sh);
   }
   const R rho = R(a.rho);
