@@ -828,8 +828,9 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10, dtype=None):
     (systems.py:497) -- config 2's cart-position bound is an ADMM constraint
     and would make most shifted warm starts infeasible for an interior-point
     method.  Reported per system: wall time of the cold and the warm solve of
-    the whole local batch (device-resident loop, host polls every 16
-    iterations; median of 3 timed solves from the same inputs), Newton
+    the whole local batch (each model's whole solve one device-resident
+    graph loop on its own stream, ptc_solver_loop; median of 3 timed solves
+    from the same inputs, after one untimed solve), Newton
     iterations, and problem outcomes."""
     from paper_2409_20027_b200 import BatchSolver
     b_local = B_TOTAL           # weak scaling, as the headline
@@ -861,17 +862,13 @@ def mpc_leg(torch, P, world: int, rank: int, shift: int = 10, dtype=None):
         solvers[system] = bs
         starts[system] = (bs.rollout(x0, u0), u0)
     names = list(solvers)
-    # warm-up (untimed): a small batch of each model through the same kernels,
-    # so module loading and first-launch setup stay out of the cold solve
-    warm_jobs = []
-    for k in names:
-        m = 256
-        prob = P.ControlProblem(probs[k].dynamics, probs[k].cost, box[k])
-        ws = BatchSolver(prob, m, "barrier", barrier=opts, dtype=dtype)
-        X, U = starts[k]
-        warm_jobs.append((ws, X[:m].contiguous(), U[:m].contiguous()))
-    BatchSolver.solve_concurrently(warm_jobs)
-    del warm_jobs
+    # warm-up (untimed): one whole cold solve of the same batches, so module
+    # loading of the single-sweep kernels (a small warm-up batch runs the
+    # tree-plan kernels instead) and the solvers' graph builds stay out of
+    # the timed solves (they cost the first timed solve ~0.27 s otherwise,
+    # scratch/mpc_seq_probe.py)
+    BatchSolver.solve_concurrently([(solvers[k],) + starts[k] for k in names])
+    torch.cuda.synchronize()
     # the two halves advance concurrently (one stream each), as one MPC batch.
     # Each solve is timed `reps` times from the same inputs (deterministic:
     # identical iterations and results every time) and the median reported:

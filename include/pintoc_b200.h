@@ -345,6 +345,15 @@ int ptc_solver_running(ptc_solver* s, int32_t* n_running, void* stream);
  * the previous one */
 int ptc_solver_running_async(ptc_solver* s, int32_t* n_running, void* stream);
 
+/* The whole solve loop enqueued as ONE device-resident CUDA graph (replaces
+ * the host loop of newton.py:157-208 / outer.py:221-245, 392-427 driven by
+ * ptc_solver_iterate + ptc_solver_running): a conditional WHILE node replays
+ * `group` iterations, then the device stops once no problem is running or
+ * max_launch iterations were launched.  launched (pinned host int32, may be
+ * NULL) receives the iteration count once the stream reaches it.  Returns
+ * PTC_ERR_CUDA if the driver cannot build conditional graphs. */
+int ptc_solver_loop(ptc_solver* s, int group, int max_launch, int32_t* launched, void* stream);
+
 /* Pass-level entry points on the loaded trajectory (buffer 0):
  *   expand  = costate_pass + hamiltonian_expansion (passes.py:122, 155)
  *   lqr     = value_pass + propagation_pass on that expansion

@@ -245,6 +245,31 @@ class DeviceSolver:
         """Enqueue the running count into dst (pinned int32 host tensor)."""
         N.check(self.lib.ptc_solver_running_async(self.handle, dst.data_ptr(), self.stream))
 
+    # False once the driver rejected the conditional graph (then the host
+    # polls ptc_solver_running between iteration groups)
+    _device_loop = True
+
+    def device_loop(self, max_launch: int, group: int = 1, launched=None) -> bool:
+        """Enqueue the device-resident loop unless PTC_HOST_LOOP=1 or the
+        driver cannot build it; False = nothing was enqueued."""
+        import os
+        if os.environ.get("PTC_HOST_LOOP") == "1" or not self._device_loop:
+            return False
+        try:
+            self.loop(max_launch, group, launched)   # a failed build enqueues nothing
+        except N.NativeError:
+            self._device_loop = False
+            return False
+        return True
+
+    def loop(self, max_launch: int, group: int = 1, launched=None) -> None:
+        """Enqueue the whole solve as one device-resident graph loop
+        (ptc_solver_loop); ``launched``: pinned int32 host tensor that
+        receives the iteration count once the stream reaches it."""
+        ptr = None if launched is None else launched.data_ptr()
+        N.check(self.lib.ptc_solver_loop(self.handle, int(group), int(max_launch), ptr,
+                                         self.stream))
+
     def run(self, group: int = 4, max_launch: int | None = None) -> int:
         """Iterate until every problem is done; returns device iterations launched."""
         s = self.settings
@@ -252,6 +277,11 @@ class DeviceSolver:
             per_round = s.max_iters + 2
             rounds = max(1, s.max_outer if s.method == N.METHOD_ADMM else 64)
             max_launch = per_round * rounds + 16
+        import torch
+        cnt = torch.zeros(1, dtype=torch.int32).pin_memory()
+        if self.device_loop(max_launch, 1, cnt):
+            torch.cuda.current_stream().synchronize()
+            return int(cnt[0])
         launched = 0
         n = 1
         while launched < max_launch:

@@ -107,6 +107,7 @@ _SIGS = {
                                          C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "ptc_solver_running": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_void_p]),
     "ptc_solver_running_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ptc_solver_loop": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "ptc_solver_expand": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ptc_solver_lqr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "ptc_solver_rollout": (C.c_int, [C.c_void_p, C.c_void_p]),

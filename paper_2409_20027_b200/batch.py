@@ -104,9 +104,11 @@ class BatchSolver:
     def solve_concurrently(jobs, group: int = 16) -> list:
         """Advance several batches (e.g. the two models of config 3) at once,
         one CUDA stream each: ``jobs`` = [(BatchSolver, states, controls)].
-        Every solver keeps its own device-resident loop; the host polls each
-        stream every ``group`` iterations, so one batch's stragglers never
-        serialise the other's iterations."""
+        Every solver runs its whole loop on the device (one graph with a
+        conditional WHILE node per stream, ptc_solver_loop), so one batch's
+        stragglers never serialise the other's iterations and a host stall
+        cannot drain a stream.  Without conditional graphs the host polls
+        each stream every ``group`` iterations instead."""
         import torch
         streams = [torch.cuda.Stream() for _ in jobs]
         for (bs, X, U), st in zip(jobs, streams):
@@ -116,6 +118,22 @@ class BatchSolver:
         launched = [0] * len(jobs)
         caps = [(bs.settings.max_iters + 2) * max(1, bs.settings.round_cap) + 16
                 for bs, _, _ in jobs]
+        # each batch as one device-resident graph loop on its own stream: the
+        # host only waits at the end (ptc_solver_loop)
+        counts = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in jobs]
+        looped = []
+        for i, ((bs, _, _), st) in enumerate(zip(jobs, streams)):
+            with torch.cuda.stream(st):
+                looped.append(bs.solver.device_loop(caps[i], 1, counts[i]))
+        if all(looped):
+            out = []
+            for (bs, _, _), st, cnt in zip(jobs, streams, counts):
+                st.synchronize()
+                with torch.cuda.stream(st):
+                    out.append(bs._result(int(cnt[0])))
+                torch.cuda.current_stream().wait_stream(st)
+            return out
+        assert not any(looped), "device loop available for some solvers only"
         # one group stays queued while the host reads the previous group's
         # running count (pinned copy + event), so the streams never drain
         # waiting for the host; a finished batch runs at most one extra

@@ -798,6 +798,7 @@ struct ptc_solver {
   virtual int iterate(int n, cudaStream_t s) = 0;
   virtual int running(int32_t* n, cudaStream_t s) = 0;
   virtual int running_async(int32_t* n, cudaStream_t s) = 0;
+  virtual int loop(int group, int cap, int32_t* launched, cudaStream_t s) = 0;
   virtual int expand(cudaStream_t s) = 0;
   virtual int lqr(const double* alpha_host, cudaStream_t s) = 0;
   virtual int rollout(cudaStream_t s) = 0;
@@ -811,6 +812,17 @@ struct ptc_solver {
 };
 
 namespace ptc {
+
+// device-resident solve loop (Solver::loop): the launch counter and the
+// WHILE node's condition
+__global__ void k_loop_init(int* count) { *count = 0; }
+
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* n_running, int* count,
+                            int group, int cap) {
+  const int c = *count + group;
+  *count = c;
+  cudaGraphSetConditional(h, (*n_running > 0 && c < cap) ? 1u : 0u);
+}
 
 // component-major affine model (comps x T) -> stage-major rows [t][A | Bm | c]
 template <typename R>
@@ -1227,7 +1239,83 @@ struct Solver final : ptc_solver {
     }
   }
 
+  // The whole solve as one device-resident loop: a CUDA graph whose
+  // conditional WHILE node replays `group` iterations and then lets one
+  // thread decide, from the control kernel's running count, whether to go
+  // round again -- no host round trip between iterations, so a host stall
+  // cannot drain the stream (the host-polled loop's failure mode).
+  cudaGraphExec_t loop_exec = nullptr;
+  int loop_group = 0, loop_cap = 0;
+  int* loop_count = nullptr;
+
+  int build_loop_graph(int group, int cap) {
+    if (loop_exec) cudaGraphExecDestroy(loop_exec);
+    loop_exec = nullptr;
+    if (!loop_count) PTC_CUDA(cudaMalloc(&loop_count, sizeof(int)));
+    if (!cap_stream) PTC_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    PTC_CUDA(cudaGraphCreate(&g, 0));
+    cudaError_t e = add_loop_nodes(g, group, cap);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&loop_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      loop_exec = nullptr;
+      (void)cudaGetLastError();
+      return fail(PTC_ERR_CUDA, std::string("device loop graph: ") + cudaGetErrorString(e));
+    }
+    loop_group = group;
+    loop_cap = cap;
+    return PTC_OK;
+  }
+
+  cudaError_t add_loop_nodes(cudaGraph_t g, int group, int cap) {
+    cudaGraphNode_t init;
+    cudaKernelNodeParams kp = {};
+    void* init_args[] = {&loop_count};
+    kp.func = reinterpret_cast<void*>(ptc::k_loop_init);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = init_args;
+    cudaError_t e = cudaGraphAddKernelNode(&init, g, nullptr, 0, &kp);
+    if (e != cudaSuccess) return e;
+    cudaGraphConditionalHandle h;
+    e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) return e;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop;
+    e = cudaGraphAddNode(&loop, g, &init, 1, &cp);
+    if (e != cudaSuccess) return e;
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    for (int i = 0; i < group; ++i) ops->iterate(&na, &la, cap_stream);
+    ptc::k_loop_cond<<<1, 1, 0, cap_stream>>>(h, na.n_running, loop_count, group, cap);
+    cudaGraph_t out = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cap_stream, &out);
+    return e2 != cudaSuccess ? e2 : cudaGetLastError();
+  }
+
+  int loop(int group, int cap, int32_t* launched, cudaStream_t s) override {
+    if (na.blk) return fail(PTC_ERR_ARG, "block_mode solvers iterate through ptc_solver_block_phase");
+    if (group < 1 || cap < 1) return fail(PTC_ERR_ARG, "group and max_launch must be >= 1");
+    if (!loop_exec || group != loop_group || cap != loop_cap) {
+      int rc = build_loop_graph(group, cap);
+      if (rc) return rc;
+    }
+    PTC_CUDA(cudaGraphLaunch(loop_exec, s));
+    if (launched)
+      PTC_CUDA(cudaMemcpyAsync(launched, loop_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+    return PTC_OK;
+  }
+
   ~Solver() override {
+    if (loop_exec) cudaGraphExecDestroy(loop_exec);
+    if (loop_count) cudaFree(loop_count);
     if (iter_exec) cudaGraphExecDestroy(iter_exec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
   }
@@ -1433,6 +1521,10 @@ int ptc_solver_running_async(ptc_solver* s, int32_t* n, void* stream) {
   PTC_S(s);
   if (!n) return fail(PTC_ERR_ARG, "n is required");
   return s->running_async(n, (cudaStream_t)stream);
+}
+int ptc_solver_loop(ptc_solver* s, int group, int max_launch, int32_t* launched, void* stream) {
+  PTC_S(s);
+  return s->loop(group, max_launch, launched, (cudaStream_t)stream);
 }
 int ptc_solver_expand(ptc_solver* s, void* stream) {
   PTC_S(s);

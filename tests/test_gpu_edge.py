@@ -302,3 +302,59 @@ def test_nan_step_is_rejected_not_converged():
         assert [r.alpha for r in rep.history] == [2.0 ** (k * (k + 1) // 2) for k in range(9)]
         for r in rep.history:
             assert r.gain_ratio == -np.inf and np.isnan(r.step_norm) and not r.accepted
+
+
+@pytest.mark.parametrize("model", ["pendulum", "cartpole", "tvlinear12"])
+def test_device_loop_matches_host_polled_loop(model, monkeypatch):
+    """ptc_solver_loop (the whole solve as one conditional-graph loop on the
+    device) takes exactly the steps of the host-polled iterate / running
+    loop: same status, per-round counts, launches and controls, bitwise."""
+    import torch
+    import paper_2409_20027_b200 as P
+    from paper_2409_20027_b200 import BatchSolver
+    rng = np.random.default_rng(47)
+    if model == "pendulum":
+        T, n, nx = 64, 37, 2
+        prob = P.ControlProblem(P.PendulumDynamics(T, P.PendulumParams(damping=0.1, dt=0.05)),
+                                P.QuadraticCost(np.diag([10.0, 0.1]), np.diag([0.01]),
+                                                np.diag([100.0, 10.0])),
+                                P.BoxConstraint(2, 1, control_lower=-5.0, control_upper=5.0))
+        x0 = np.stack([rng.uniform(-np.pi, np.pi, n), rng.normal(0, 0.5, n)], 1)
+        u0 = torch.as_tensor(np.clip(rng.standard_normal((n, T, 1)), -4.5, 4.5))
+    elif model == "cartpole":
+        T, n, nx = 64, 21, 4
+        Q = np.diag([1.0, 10.0, 0.1, 0.1])
+        prob = P.ControlProblem(
+            P.CartPoleDynamics(T, P.CartPoleParams(cart_mass=1.0, pole_mass=0.1,
+                                                   pole_length=0.5, dt=0.02)),
+            P.QuadraticCost(Q, np.diag([0.01]), 10 * Q, x_goal=np.array([0.0, np.pi, 0.0, 0.0])),
+            P.BoxConstraint(4, 1, control_lower=-10.0, control_upper=10.0))
+        x0 = rng.uniform(-0.5, 0.5, (n, nx))
+        u0 = torch.as_tensor(np.clip(rng.standard_normal((n, T, 1)), -9.0, 9.0))
+    else:
+        T, n, nx, nu = 96, 3, 12, 4
+        A = np.eye(nx) + 0.01 * rng.standard_normal((nx, nx))
+        Bm = 0.1 * rng.standard_normal((nx, nu))
+        prob = P.ControlProblem(P.LinearDynamics(A, Bm, T),
+                                P.QuadraticCost(np.eye(nx), 0.1 * np.eye(nu), np.eye(nx)),
+                                P.BoxConstraint(nx, nu, control_lower=-2.0, control_upper=2.0))
+        x0 = rng.standard_normal((n, nx))
+        u0 = torch.as_tensor(np.clip(0.3 * rng.standard_normal((n, T, nu)), -1.5, 1.5))
+    opts = P.BarrierOptions(mu0=0.1, zeta=0.2, mu_tol=1e-4, newton=P.NewtonOptions(max_iters=30))
+    res = {}
+    for mode in ("device", "host"):
+        if mode == "host":
+            monkeypatch.setenv("PTC_HOST_LOOP", "1")
+        bs = BatchSolver(prob, n, "barrier", barrier=opts)
+        xs = bs.rollout(x0, u0)
+        single = bs.solve(xs, u0)
+        bs2 = BatchSolver(prob, n, "barrier", barrier=opts)
+        conc = BatchSolver.solve_concurrently([(bs2, xs, u0)])[0]
+        if mode == "device":
+            assert bs.solver._device_loop and bs2.solver._device_loop, "device loop not built"
+        res[mode] = (single, conc)
+    for a, b in zip(res["device"], res["host"]):
+        assert torch.equal(a.status, b.status)
+        assert torch.equal(a.round_iters, b.round_iters)
+        assert torch.equal(a.controls, b.controls)
+        assert torch.equal(a.states, b.states)

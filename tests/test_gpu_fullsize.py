@@ -80,6 +80,17 @@ def test_config3_full_size_kkt_and_oracle_sample():
             ref = O.lqr_solve(e)
             assert rel_gap(host(sol.du, b, (T, nu)), ref[5]) < 1e-9, (system, b)
             assert rel_gap(host(sol.dx, b, (T + 1, nx)), ref[4]) < 1e-9, (system, b)
+        # the flagged problems are ones the reference rejects too
+        # (passes.py:231-241: a non-positive-definite R + alpha I or Q)
+        bad = torch.nonzero(~ok).flatten()
+        for b in [int(v) for v in bad[:: max(1, len(bad) // 6)][:6]]:
+            e = O.Expansion(P=host(inputs[0], b, (T, nx, nx)), R=host(inputs[1], b, (T, nu, nu)),
+                            M=host(inputs[2], b, (T, nx, nu)), d=host(inputs[3], b, (T, nu)),
+                            Fx=host(inputs[4], b, (T, nx, nx)), Fu=host(inputs[5], b, (T, nx, nu)),
+                            PT=inputs[6][:, 0, b].reshape(nx, nx).cpu().numpy(),
+                            alpha=float(alpha[b]))
+            with pytest.raises((O.Definiteness, O.Conditioning)):
+                O.lqr_solve(e)
         del inputs, sol
         torch.cuda.empty_cache()
 
