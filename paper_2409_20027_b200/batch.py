@@ -101,16 +101,18 @@ class BatchSolver:
             cost=s.read("cur_cost"), launches=launches)
 
     @staticmethod
-    def solve_concurrently(jobs, group: int = 16) -> list:
+    def solve_concurrently(jobs, group: int = 16, priorities=None) -> list:
         """Advance several batches (e.g. the two models of config 3) at once,
         one CUDA stream each: ``jobs`` = [(BatchSolver, states, controls)].
         Every solver runs its whole loop on the device (one graph with a
         conditional WHILE node per stream, ptc_solver_loop), so one batch's
         stragglers never serialise the other's iterations and a host stall
         cannot drain a stream.  Without conditional graphs the host polls
-        each stream every ``group`` iterations instead."""
+        each stream every ``group`` iterations instead.  ``priorities``:
+        per-job CUDA stream priorities (lower = higher priority)."""
         import torch
-        streams = [torch.cuda.Stream() for _ in jobs]
+        streams = [torch.cuda.Stream(priority=p)
+                   for p in (priorities or [0] * len(jobs))]
         for (bs, X, U), st in zip(jobs, streams):
             st.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(st):
