@@ -127,15 +127,7 @@ class BatchSolver:
         for i, ((bs, _, _), st) in enumerate(zip(jobs, streams)):
             with torch.cuda.stream(st):
                 looped.append(bs.solver.device_loop(caps[i], 1, counts[i]))
-        if all(looped):
-            out = []
-            for (bs, _, _), st, cnt in zip(jobs, streams, counts):
-                st.synchronize()
-                with torch.cuda.stream(st):
-                    out.append(bs._result(int(cnt[0])))
-                torch.cuda.current_stream().wait_stream(st)
-            return out
-        assert not any(looped), "device loop available for some solvers only"
+        # the rest (drivers without conditional graphs): host-polled below
         # one group stays queued while the host reads the previous group's
         # running count (pinned copy + event), so the streams never drain
         # waiting for the host; a finished batch runs at most one extra
@@ -145,7 +137,7 @@ class BatchSolver:
         # 64 gave no outlier in 24 solves (profiles/r2v_bench.md)
         polls = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in jobs]
         events = [None] * len(jobs)
-        active = set(range(len(jobs)))
+        active = {i for i in range(len(jobs)) if not looped[i]}
         n = 1
         while active:
             pending = []
@@ -169,9 +161,12 @@ class BatchSolver:
                     active.discard(i)
             n = group
         out = []
-        for (bs, _, _), st, k in zip(jobs, streams, launched):
+        for i, ((bs, _, _), st) in enumerate(zip(jobs, streams)):
+            if looped[i]:
+                st.synchronize()
+                launched[i] = int(counts[i][0])
             with torch.cuda.stream(st):
-                out.append(bs._result(k))
+                out.append(bs._result(launched[i]))
             torch.cuda.current_stream().wait_stream(st)
         return out
 

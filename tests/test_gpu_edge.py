@@ -358,3 +358,11 @@ def test_device_loop_matches_host_polled_loop(model, monkeypatch):
         assert torch.equal(a.round_iters, b.round_iters)
         assert torch.equal(a.controls, b.controls)
         assert torch.equal(a.states, b.states)
+    # one batch on the device loop, one host-polled, side by side
+    monkeypatch.delenv("PTC_HOST_LOOP")
+    bs3, bs4 = (BatchSolver(prob, n, "barrier", barrier=opts) for _ in range(2))
+    bs4.solver._device_loop = False
+    mixed = BatchSolver.solve_concurrently([(bs3, xs, u0), (bs4, xs, u0)])
+    for r in mixed:
+        assert torch.equal(r.status, res["host"][1].status)
+        assert torch.equal(r.controls, res["host"][1].controls)
