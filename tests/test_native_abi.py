@@ -151,3 +151,13 @@ def test_user_model_source_and_library():
     if os.path.exists(so):
         lib = ctypes.CDLL(so)
         assert hasattr(lib, "ptc_user_model_ops")
+
+
+def test_solver_loop_argument_errors_without_gpu():
+    """ptc_solver_loop validates its handle before touching the device."""
+    from paper_2409_20027_b200 import _native
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    lib = _native.load_library()
+    assert lib.ptc_solver_loop(None, 1, 10, None, None) == -1   # PTC_ERR_ARG
+    assert b"NULL" in lib.ptc_last_error()
