@@ -257,7 +257,10 @@ class DeviceSolver:
             return False
         try:
             self.loop(max_launch, group, launched)   # a failed build enqueues nothing
-        except N.NativeError:
+        except N.NativeError as err:
+            import warnings
+            warnings.warn(f"device-resident solve loop unavailable ({err}); "
+                          "polling from the host instead", RuntimeWarning, stacklevel=2)
             self._device_loop = False
             return False
         return True
