@@ -18,9 +18,9 @@ from .exceptions import DimensionError
 
 
 def _frozen(a) -> np.ndarray:
-    out = np.array(a, dtype=float)
-    out.setflags(write=False)
-    return out
+    arr = np.asarray(a, dtype=np.float64).copy()
+    arr.flags.writeable = False
+    return arr
 
 
 @dataclass(frozen=True)
@@ -32,16 +32,16 @@ class Trajectory:
     controls: np.ndarray  # (N, d_u)
 
     def __post_init__(self):
-        object.__setattr__(self, "states", _frozen(np.atleast_2d(self.states)))
-        object.__setattr__(self, "controls", _frozen(np.atleast_2d(self.controls)))
-        if self.states.shape[0] != self.controls.shape[0] + 1:
+        for name in ("states", "controls"):
+            object.__setattr__(self, name, _frozen(np.atleast_2d(getattr(self, name))))
+        n_x, n_u = len(self.states), len(self.controls)
+        if n_x != n_u + 1:
             raise DimensionError(
-                f"need len(states) == len(controls) + 1, got {self.states.shape[0]} states "
-                f"and {self.controls.shape[0]} controls")
-        if not np.all(np.isfinite(self.states)):
-            raise DimensionError("trajectory states contain non-finite values")
-        if not np.all(np.isfinite(self.controls)):
-            raise DimensionError("trajectory controls contain non-finite values")
+                f"need len(states) == len(controls) + 1, got {n_x} states "
+                f"and {n_u} controls")
+        for name in ("states", "controls"):
+            if not np.isfinite(getattr(self, name)).all():
+                raise DimensionError(f"trajectory {name} contain non-finite values")
 
     @property
     def horizon(self) -> int:
@@ -60,11 +60,9 @@ class DynamicsModel(abc.ABC):
     """Discrete map x_{t+1} = f_t(x_t, u_t) (reference problem.py:59-112)."""
 
     def __init__(self, horizon: int, d_x: int, d_u: int):
-        if horizon < 1 or d_x < 1 or d_u < 1:
+        if min(horizon, d_x, d_u) < 1:
             raise DimensionError("horizon, d_x and d_u must all be positive")
-        self.horizon = horizon
-        self.d_x = d_x
-        self.d_u = d_u
+        self.horizon, self.d_x, self.d_u = horizon, d_x, d_u
 
     @abc.abstractmethod
     def f(self, t: int, x: np.ndarray, u: np.ndarray) -> np.ndarray: ...
@@ -105,12 +103,13 @@ class BoxConstraint(ConstraintModel):
     def __init__(self, d_x: int, d_u: int, control_lower=None, control_upper=None,
                  state_lower=None, state_upper=None):
         self.d_x, self.d_u = d_x, d_u
-        self.control_lower = self._bound(control_lower, d_u, -np.inf)
-        self.control_upper = self._bound(control_upper, d_u, np.inf)
-        self.state_lower = self._bound(state_lower, d_x, -np.inf)
-        self.state_upper = self._bound(state_upper, d_x, np.inf)
-        if np.any(self.control_lower >= self.control_upper) or np.any(
-                self.state_lower >= self.state_upper):
+        for name, given, dim, sign in (("control_lower", control_lower, d_u, -1),
+                                       ("control_upper", control_upper, d_u, 1),
+                                       ("state_lower", state_lower, d_x, -1),
+                                       ("state_upper", state_upper, d_x, 1)):
+            setattr(self, name, self._bound(given, dim, sign * np.inf))
+        if any((lo >= hi).any() for lo, hi in ((self.control_lower, self.control_upper),
+                                               (self.state_lower, self.state_upper))):
             raise DimensionError("box bounds must satisfy lower < upper")
         self._rows = ([(0, i, 1.0, self.state_upper[i]) for i in range(d_x)
                        if np.isfinite(self.state_upper[i])]
@@ -125,9 +124,8 @@ class BoxConstraint(ConstraintModel):
 
     @staticmethod
     def _bound(value, dim, default):
-        if value is None:
-            return _frozen(np.full(dim, default))
-        return _frozen(np.broadcast_to(np.asarray(value, dtype=float), (dim,)))
+        given = default if value is None else np.asarray(value, dtype=float)
+        return _frozen(np.broadcast_to(given, (dim,)))
 
     def w_batch(self, xs: np.ndarray, us: np.ndarray) -> np.ndarray:
         """Stacked constraint values (N, n_total) -- input validation helper."""
@@ -139,17 +137,19 @@ class BoxConstraint(ConstraintModel):
         return out
 
     def max_violation(self, traj: Trajectory) -> float:
-        if self.n_total == 0:
-            return -np.inf
-        return float(self.w_batch(traj.states[:-1], traj.controls).max())
+        w = self.w_batch(traj.states[:-1], traj.controls)
+        return float(w.max()) if w.size else -np.inf
 
     def clamp_controls(self, controls: np.ndarray, margin: float = 0.0) -> np.ndarray:
-        lo, hi = self.control_lower, self.control_upper
+        """Clip to the control box shrunk by `margin` about its centre
+        (problem.py:326-340; one-sided boxes shrink about 0)."""
+        bounds = [self.control_lower, self.control_upper]
         if margin:
-            center = np.where(np.isfinite(lo) & np.isfinite(hi), 0.5 * (lo + hi), 0.0)
-            lo = np.where(np.isfinite(lo), center + (1 - margin) * (lo - center), lo)
-            hi = np.where(np.isfinite(hi), center + (1 - margin) * (hi - center), hi)
-        return np.clip(controls, lo, hi)
+            two_sided = np.isfinite(bounds[0]) & np.isfinite(bounds[1])
+            mid = np.where(two_sided, 0.5 * (bounds[0] + bounds[1]), 0.0)
+            bounds = [np.where(np.isfinite(b), mid + (1 - margin) * (b - mid), b)
+                      for b in bounds]
+        return np.clip(controls, bounds[0], bounds[1])
 
     def _device_spec(self) -> dict:
         return dict(state_lower=self.state_lower, state_upper=self.state_upper,

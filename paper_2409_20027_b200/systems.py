@@ -112,16 +112,15 @@ class LinearDynamics(DynamicsModel):
     """Affine time-invariant map x' = A x + B u + c (systems.py:32-77)."""
 
     def __init__(self, A, B, horizon: int, offset=None):
-        A = np.asarray(A, dtype=float)
-        B = np.asarray(B, dtype=float)
-        super().__init__(horizon, A.shape[0], B.shape[1])
-        if A.shape != (self.d_x, self.d_x) or B.shape != (self.d_x, self.d_u):
+        self.A, self.B = (np.asarray(m, dtype=np.float64) for m in (A, B))
+        super().__init__(horizon, self.A.shape[0], self.B.shape[1])
+        nx, nu = self.d_x, self.d_u
+        if (self.A.shape, self.B.shape) != ((nx, nx), (nx, nu)):
             raise DimensionError("A must be (d_x, d_x) and B (d_x, d_u)")
-        self.A, self.B = A, B
-        self.offset = np.zeros(self.d_x) if offset is None else np.asarray(offset, float)
+        self.offset = np.asarray(np.zeros(nx) if offset is None else offset, dtype=np.float64)
 
     def f(self, t, x, u):
-        return self.A @ x + self.B @ u + self.offset
+        return self.A.dot(x) + self.B.dot(u) + self.offset
 
     def _device_spec(self):
         return dict(model=DYN_LINEAR, lin_a=self.A.reshape(1, -1), lin_b=self.B.reshape(1, -1),
@@ -134,11 +133,9 @@ class TimeVaryingLinearDynamics(DynamicsModel):
     reference)."""
 
     def __init__(self, A, B, offset=None):
-        A = np.asarray(A, dtype=float)
-        B = np.asarray(B, dtype=float)
-        super().__init__(A.shape[0], A.shape[1], B.shape[2])
         # read-only copies: the device keeps a cached transposed upload
         self.A, self.B = _frozen(A), _frozen(B)
+        super().__init__(self.A.shape[0], self.A.shape[1], self.B.shape[2])
         self.offset = _frozen(np.zeros((self.horizon, self.d_x)) if offset is None else offset)
 
     def f(self, t, x, u):
@@ -157,19 +154,20 @@ class QuadraticCost(CostModel):
     (systems.py:80-139)."""
 
     def __init__(self, Q, R, Q_terminal, x_goal=None):
-        self.Q = np.atleast_2d(np.asarray(Q, dtype=float))
-        self.R = np.atleast_2d(np.asarray(R, dtype=float))
-        self.Qf = np.atleast_2d(np.asarray(Q_terminal, dtype=float))
-        d_x = self.Q.shape[0]
-        self.x_goal = np.zeros(d_x) if x_goal is None else np.asarray(x_goal, float)
+        self.Q, self.R, self.Qf = (np.atleast_2d(np.asarray(m, dtype=np.float64))
+                                   for m in (Q, R, Q_terminal))
+        goal = np.zeros(len(self.Q)) if x_goal is None else x_goal
+        self.x_goal = np.asarray(goal, dtype=np.float64)
+
+    @staticmethod
+    def _half_form(M, v) -> float:
+        return 0.5 * float(v @ M @ v)
 
     def l(self, t, x, u):
-        dx = x - self.x_goal
-        return 0.5 * float(dx @ self.Q @ dx) + 0.5 * float(u @ self.R @ u)
+        return self._half_form(self.Q, x - self.x_goal) + self._half_form(self.R, u)
 
     def terminal(self, x):
-        dx = x - self.x_goal
-        return 0.5 * float(dx @ self.Qf @ dx)
+        return self._half_form(self.Qf, x - self.x_goal)
 
     def _device_spec(self):
         return dict(Q=self.Q, R=self.R, Qf=self.Qf, goal=self.x_goal)
@@ -183,19 +181,17 @@ DEFAULT_TERMINAL_SCALE = 10.0
 
 
 def swingup_start(system: str) -> np.ndarray:
-    if system == "pendulum":
-        return np.array([math.pi, 0.0])
-    if system == "cartpole":
-        return np.zeros(4)
-    raise ValueError(f"unknown system {system!r}")
+    starts = {"pendulum": [math.pi, 0.0], "cartpole": [0.0] * 4}
+    if system not in starts:
+        raise ValueError(f"unknown system {system!r}")
+    return np.array(starts[system])
 
 
 def swingup_goal(system: str, target_position: float = 0.0) -> np.ndarray:
-    if system == "pendulum":
-        return np.zeros(2)
-    if system == "cartpole":
-        return np.array([target_position, math.pi, 0.0, 0.0])
-    raise ValueError(f"unknown system {system!r}")
+    goals = {"pendulum": [0.0, 0.0], "cartpole": [target_position, math.pi, 0.0, 0.0]}
+    if system not in goals:
+        raise ValueError(f"unknown system {system!r}")
+    return np.array(goals[system])
 
 
 def make_swingup_problem(system: str, horizon: int, dt: float, q=None, r=None,
@@ -206,17 +202,15 @@ def make_swingup_problem(system: str, horizon: int, dt: float, q=None, r=None,
         raise ValueError(f"unknown system {system!r}; expected one of {SYSTEMS}")
     if horizon < 1:
         raise ValueError("horizon must be >= 1")
-    q_def, r_def = DEFAULT_WEIGHTS[system]
-    Q = np.diag(q_def if q is None else np.asarray(q, dtype=float))
-    R = np.diag(r_def if r is None else np.asarray(r, dtype=float))
-    cost = QuadraticCost(Q, R, terminal_scale * Q, x_goal=swingup_goal(system, target_position))
+    weights = [np.diag(np.asarray(dflt if given is None else given, dtype=np.float64))
+               for given, dflt in zip((q, r), DEFAULT_WEIGHTS[system])]
+    cost = QuadraticCost(weights[0], weights[1], terminal_scale * weights[0],
+                         x_goal=swingup_goal(system, target_position))
     if system == "pendulum":
-        params = PendulumParams(dt=dt)
-        dyn: DynamicsModel = PendulumDynamics(horizon, params)
-        bound = params.torque_limit
+        dyn: DynamicsModel = PendulumDynamics(horizon, PendulumParams(dt=dt))
+        limit = dyn.params.torque_limit
     else:
-        params = CartPoleParams(dt=dt)
-        dyn = CartPoleDynamics(horizon, params)
-        bound = params.force_limit
-    box = BoxConstraint(dyn.d_x, dyn.d_u, control_lower=-bound, control_upper=bound)
-    return ControlProblem(dynamics=dyn, cost=cost, constraints=box)
+        dyn = CartPoleDynamics(horizon, CartPoleParams(dt=dt))
+        limit = dyn.params.force_limit
+    return ControlProblem(dynamics=dyn, cost=cost, constraints=BoxConstraint(
+        dyn.d_x, dyn.d_u, control_lower=-limit, control_upper=limit))
