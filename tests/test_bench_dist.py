@@ -75,3 +75,21 @@ def test_timing_is_max_over_ranks_gloo():
         out = mgr.dict()
         mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
         assert out[0] == out[1] == (2.5, 21)
+
+
+def test_reference_install_is_unmodified_pintoc():
+    """The reference arm's baseline/_ref is pintoc as it lies under
+    /root/reference (installed by __graft_entry__.build()); skipped where the
+    reference tree does not exist (the GPU box)."""
+    import filecmp
+    src = "/root/reference/pkg/src/pintoc"
+    if not os.path.isdir(src):
+        pytest.skip("no reference tree here")
+    import __graft_entry__ as entry
+    entry._install_reference()  # no-op when already installed
+    dst = os.path.join(ROOT, "baseline", "_ref", "pintoc")
+    names = sorted(f for f in os.listdir(src) if f.endswith(".py"))
+    assert names and "passes.py" in names
+    match, mismatch, errors = filecmp.cmpfiles(src, dst, names, shallow=False)
+    assert not mismatch and not errors, (mismatch, errors)
+    assert bench.reference_impl() == "pintoc"
